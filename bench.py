@@ -1,0 +1,390 @@
+#!/usr/bin/env python
+"""bench.py -- frames/s of the moco hot path on B200 (BASELINE.json metric).
+
+Default workload: BASELINE.json configs[2] ("C2"): 10,000 frames of 512x512
+uint16 (12-bit), one 2x2 level to 256x256, w=16 there, +-1 refine at 512x512,
+corrected frames written.  A step = one moco_align_batch over the whole
+(per-rank) stack: every step of the hot path (S1..S7) on every frame.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl moco|reference]
+
+N>1 is launched by torch.distributed.run (one rank per GPU, NCCL): weak
+scaling -- every rank aligns its own contiguous 10,000-frame block of an
+N*10,000-frame stack, the template is broadcast from rank 0 (setup), and each
+timed step ends with an NCCL all_gather of the per-frame results (shifts,
+f_min) to every rank; timing is the max over ranks of CUDA-event time.
+
+Rank 0 prints ONE JSON line (contract in the task statement / DESIGN.md §8).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import config_spec, make_stack  # noqa: E402
+
+METRIC = "frames/sec aligned (512x512 uint16, w=16)"
+UNIT = "frames/s"
+
+
+def read_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]),
+                "sm_max_mhz": float(d.get("sm_max_mhz", 1965.0)), "source": "measured"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0, "source": "fallback"}
+
+
+# ----------------------------------------------------------------- work models
+def fft_model(spec):
+    """SURVEY.md §8(d) minimal algorithmic FLOPs per frame (the roofline model
+    of BASELINE.md §2): FFT correlation + energy + score + downsample + refine."""
+    L = spec.levels
+    mc, nc = spec.m >> L, spec.n >> L
+    P = (mc + spec.w) * (nc + spec.w)
+    W = 2 * spec.w - 1
+    f_fft = 2 * 2.5 * P * math.log2(P) + 3 * P
+    f_energy = 2 * mc * nc
+    f_score = 6 * W * W
+    f_down = 0.75 * sum((spec.m >> l) * (spec.n >> l) for l in range(L))
+    f_refine = sum(20 * (spec.m >> l) * (spec.n >> l) for l in range(L))
+    return {"coarse": f_fft + f_energy + f_score, "downsample": f_down, "refine": f_refine,
+            "total": f_fft + f_energy + f_score + f_down + f_refine}
+
+
+def kernel_models(spec, esz):
+    """Per-frame algorithmic work of each kernel kind -> (bound, amount, unit)."""
+    L = spec.levels
+    m, n = spec.m, spec.n
+    fm = fft_model(spec)
+    down_bytes = sum((m >> l) * (n >> l) * esz + (m >> (l + 1)) * (n >> (l + 1)) * 2 for l in range(L))
+    return {
+        "downsample": ("hbm", down_bytes, "B"),
+        "coarse": ("alu", fm["coarse"], "flop"),
+        "tc_prep": ("hbm", (m >> L) * (n >> L) * 2 * 2, "B"),
+        "tc_score": ("alu", 6 * (2 * spec.w - 1) ** 2, "flop"),
+        "refine": ("alu", fm["refine"], "flop"),
+        "apply": ("hbm", 2 * m * n * esz, "B"),
+    }
+
+
+# ---------------------------------------------------------------- clock sampler
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(smax)) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------- CPU oracle
+def cpu_oracle_rate(frames_np, template_np, spec, nframes):
+    import oracle
+    cores = len(os.sched_getaffinity(0))
+    sel = frames_np[:nframes]
+    t0 = time.perf_counter()
+    oracle.align_stack(sel, template_np, spec.w, spec.levels, workers=cores)
+    dt = time.perf_counter() - t0
+    return len(sel) / dt, cores, dt
+
+
+def reference_arm(args, spec, rank, world):
+    """--impl reference: the CPU oracle (the reference for this tier), timed on
+    the host cores on bounded samples of the same workload."""
+    if rank != 0:
+        return
+    import oracle
+    from concurrent.futures import ProcessPoolExecutor
+    cores = len(os.sched_getaffinity(0))
+    per_step = max(1, min(cores, 64))
+    need = per_step * (args.steps + args.warmup)
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    st = make_stack(spec, 0, min(spec.T, need), device=dev)
+    fr = st.frames.cpu().numpy()
+    tp = st.template.cpu().numpy()
+    ex = ProcessPoolExecutor(max_workers=cores)
+    jobs = lambda k: [(fr[(k * per_step + i) % len(fr)], tp, spec.w, spec.levels) for i in range(per_step)]
+    for k in range(args.warmup):
+        list(ex.map(oracle.moco_oracle._align_one, jobs(k)))
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        list(ex.map(oracle.moco_oracle._align_one, jobs(args.warmup + k)))
+    dt = time.perf_counter() - t0
+    ex.shutdown()
+    value = per_step * args.steps / dt
+    sample = f"{per_step} frames/step of config {spec.index} (of {spec.T}), oracle fp64 numpy, process pool"
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": workload_config(spec, world, None),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def workload_config(spec, world, algo):
+    L = spec.levels
+    return {"workload": f"C{spec.index}: {spec.T} frames/rank of {spec.m}x{spec.n} "
+                        f"{'uint16 12-bit' if spec.dtype == 'u16' else 'float32'}, levels={L}, "
+                        f"w={spec.w} at {spec.m >> L}x{spec.n >> L}, corrected frames written",
+            "config_index": spec.index, "frames_per_rank": spec.T, "m": spec.m, "n": spec.n,
+            "levels": L, "w": spec.w, "coarse_algo": algo,
+            "l2": "no flush needed: per-step input %.2f GB > 126 MB L2" % (spec.T * spec.m * spec.n * (2 if spec.dtype == 'u16' else 4) / 1e9),
+            "parallelism": f"dp{world} (frame blocks)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--frames", type=int, default=None, help="override frames per rank")
+    ap.add_argument("--impl", default="moco", choices=["moco", "reference"])
+    ap.add_argument("--algo", default="auto", choices=["auto", "direct", "tc"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "moco" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    spec = config_spec(args.config)
+    if args.frames:
+        spec = config_spec(args.config, T=args.frames)
+
+    if args.impl == "reference":
+        return reference_arm(args, spec, rank, world)
+
+    import torch.distributed as dist
+    from paper_1506_06039_b200 import Plan
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # per-rank block of an (N * T)-frame stack (weak scaling); chunk-seeded so
+    # every rank regenerates exactly its own frames
+    Tl = spec.T
+    full = config_spec(spec.index, T=Tl * world)
+    st = make_stack(full, rank * Tl, Tl, device=dev)
+    frames = st.frames
+    template = st.template
+    if world > 1:   # template from rank 0 over NCCL (plan setup, untimed)
+        tb = template.view(torch.int16) if template.dtype == torch.uint16 else template
+        dist.broadcast(tb, src=0)
+    esz = frames.element_size()
+    plan = Plan(spec.m, spec.n, spec.w, spec.levels, spec.dtype, 12, device=local)
+    if args.algo != "auto":
+        plan.set_algo(args.algo)
+    plan.set_template(template)
+    shifts = torch.empty((Tl, 2), dtype=torch.int32, device=dev)
+    fmin = torch.empty((Tl,), dtype=torch.float64, device=dev)
+    corrected = torch.empty_like(frames)
+    res = torch.empty((Tl, 4), dtype=torch.int32, device=dev)     # (s, t, fmin as 2 x int32)
+    gathered = torch.empty((world * Tl, 4), dtype=torch.int32, device=dev) if world > 1 else None
+
+    def step():
+        plan.align_into(frames, shifts, fmin, corrected)
+        if world > 1:
+            res[:, :2] = shifts
+            res[:, 2:] = fmin.view(torch.int32).view(Tl, 2)
+            dist.all_gather_into_tensor(gathered, res)
+
+    for _ in range(args.warmup):
+        step()
+    launches_per_step = plan.launches
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    plan.profile(True)
+    plan.profile_read()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    prof = plan.profile_read()
+    plan.profile(False)
+    clocks = clk.stop()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * Tl / (ms_step / 1e3)
+
+    # ---- roofline of the dominant kernel (largest share of the timed region)
+    peaks = read_peaks()
+    models = kernel_models(spec, esz)
+    kind = max((k for k in prof if prof[k][1] > 0), key=lambda k: prof[k][0])
+    kms, klaunch = prof[kind]
+    frames_timed = Tl * args.steps
+    bound, per_frame, _u = models[kind]
+    if bound == "hbm":
+        achieved = per_frame * frames_timed / (kms / 1e3) / 1e9
+        peak, unit = peaks["hbm_gbs"], "GB/s"
+        peak_note = f"MEASURED_PEAKS.json hbm_gbs ({peaks['source']})"
+    else:
+        achieved = per_frame * frames_timed / (kms / 1e3) / 1e12
+        peak = 148 * 128 * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12
+        unit = "TFLOP/s"
+        peak_note = "148 SM x 128 FP32/INT32 lanes x 2 x sm_max_mhz (DESIGN.md §8)"
+    traffic = None
+    try:
+        ncu = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        entry = ncu.get(f"C{spec.index}", {}).get(plan.algo, {}).get(kind)
+        if entry:
+            traffic = entry["bytes_per_launch"]
+    except Exception:
+        pass
+    roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+                "frac": achieved / peak, "traffic": traffic, "kernel": kind,
+                "kernel_share": kms / ms if ms > 0 else None,
+                "per_frame_work": per_frame, "peak_source": peak_note,
+                "kernels_ms": {k: round(v[0], 4) for k, v in prof.items() if v[1]},
+                "kernels_launches": {k: v[1] for k, v in prof.items() if v[1]}}
+    fm = fft_model(spec)
+    hbm_roof_fps = peaks["hbm_gbs"] * 1e9 / (2 * spec.m * spec.n * esz)
+    alu_roof_fps = 148 * 128 * 2 * peaks["sm_max_mhz"] * 1e6 / fm["total"]
+    step_roof = min(hbm_roof_fps, alu_roof_fps)
+
+    # ---- single-frame latency (closed-loop use case), device-resident frame
+    lat = None
+    if rank == 0:
+        one = frames[:1]
+        s1, f1, c1 = shifts[:1], fmin[:1], corrected[:1]
+        for _ in range(20):
+            plan.align_into(one, s1, f1, c1)
+        ts = []
+        for _ in range(200):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            plan.align_into(one, s1, f1, c1)
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        lat = {"p50_ms": float(np.percentile(ts, 50)), "p99_ms": float(np.percentile(ts, 99))}
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        hf = frames.cpu().pin_memory()
+        hc = torch.empty_like(hf).pin_memory()
+        hs = torch.empty((Tl, 2), dtype=torch.int32).pin_memory()
+        hfm = torch.empty((Tl,), dtype=torch.float64).pin_memory()
+        plan.align_host(hf, hs, hfm, hc)
+        if world > 1:
+            dist.barrier()
+        ksteps = 2
+        t0 = time.perf_counter()
+        for _ in range(ksteps):
+            plan.align_host(hf, hs, hfm, hc)
+        dt = torch.tensor([(time.perf_counter() - t0) / ksteps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * Tl / float(dt.item()), "unit": UNIT,
+               "h2d_bytes_per_step": int(hf.numel() * esz * world),
+               "d2h_bytes_per_step": int((hc.numel() * esz + hs.numel() * 4 + hfm.numel() * 8) * world),
+               "api": "moco_align_host (pinned host frames in, shifts/f_min/corrected out)"}
+        del hf, hc
+
+    # ---- CPU oracle baseline (rank 0, N=1 only), bounded sample
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = len(os.sched_getaffinity(0))
+        nfr = int(min(Tl, max(16, min(4 * cores, 256))))
+        rate, cores, dt = cpu_oracle_rate(frames[:nfr].cpu().numpy(), template.cpu().numpy(), spec, nfr)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"first {nfr} frames of the workload, oracle fp64 numpy brute force, "
+                         f"{cores}-process pool, {dt:.1f} s wall"}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": "u16" if spec.dtype == "u16" else "f32", "data": "synthetic",
+               "config": workload_config(spec, world, plan.algo),
+               "roofline": roofline,
+               "step_roofline": {"fps": step_roof, "frac": value / world / step_roof,
+                                 "hbm_fps": hbm_roof_fps, "alu_fps": alu_roof_fps,
+                                 "model": "BASELINE.md §2: slower of (in+out bytes)/HBM and §8(d) FLOPs/FP32"},
+               "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+               "latency_1frame": lat, "clocks": clocks}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

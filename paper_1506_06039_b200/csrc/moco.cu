@@ -1,0 +1,554 @@
+// moco.cu -- host side of libmoco.so: the C-ABI declared in include/moco.h.
+//
+// Plans, workspace, stream-ordered launches of the hot-path kernels
+// (kernels_direct.cuh, kernels_tc.cuh) and the host-buffer end-to-end path.
+// No CPU fallback: every step of the path runs in the kernels; a CUDA failure
+// is reported as MOCO_ECUDA.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <new>
+#include <vector>
+
+#include "moco.h"
+#include "kernels_direct.cuh"
+#include "kernels_tc.cuh"
+
+using namespace moco;
+
+static thread_local char g_err[512] = "";
+
+static int set_cuda_err(cudaError_t e, const char *what) {
+  snprintf(g_err, sizeof(g_err), "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+  return MOCO_ECUDA;
+}
+#define CK(x)                                        \
+  do {                                               \
+    cudaError_t e_ = (x);                            \
+    if (e_ != cudaSuccess) return set_cuda_err(e_, #x); \
+  } while (0)
+#define CKL(name)                                            \
+  do {                                                       \
+    cudaError_t e_ = cudaGetLastError();                     \
+    if (e_ != cudaSuccess) return set_cuda_err(e_, name);    \
+  } while (0)
+
+struct moco_plan {
+  int m, n, w, W, levels, dtype, bits, device;
+  int algo;                   // resolved MOCO_ALGO_*
+  int ml[3], nl[3], pitch[3]; // per level dims and row pitch (elements)
+  size_t esz[3];              // element size per level
+  void *tpl[3];               // template pyramid
+  void *gb;                   // W*W template energies (u64 or double)
+  int64_t cap;                // frames per internal batch
+  void *scratch[3];           // frame pyramid levels 1..L for one batch
+  int32_t *sh[3];             // per-level shifts for one batch
+  bool has_tpl;
+  int64_t launches;
+  // coarse kernel launch geometry
+  int c_threads, c_sc, c_br, c_fpitch;
+  size_t c_smem;
+  // tensor-core path state
+  TcPlan tc;
+  // end-to-end staging
+  bool host_ready;
+  int64_t host_ch;
+  void *slot_in[2], *slot_out[2];
+  int32_t *slot_sh[2];
+  double *slot_f[2];
+  uint8_t *slot_flags[2];
+  cudaStream_t hs[3];
+  cudaEvent_t ev_in[2], ev_done[2], ev_free[2];
+  // live per-kernel timing (moco_profile_*)
+  bool prof_on;
+  struct ProfRec { int kind; cudaEvent_t a, b; };
+  std::vector<ProfRec> prof_live;
+  std::vector<cudaEvent_t> prof_pool;
+};
+
+static cudaEvent_t prof_event(moco_plan *p) {
+  if (!p->prof_pool.empty()) {
+    cudaEvent_t e = p->prof_pool.back();
+    p->prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+// Bracket one launch with events on its stream when profiling is on.
+struct ProfScope {
+  moco_plan *p;
+  cudaStream_t st;
+  int kind;
+  cudaEvent_t a = nullptr;
+  ProfScope(moco_plan *p_, int kind_, cudaStream_t st_) : p(p_), st(st_), kind(kind_) {
+    if (p->prof_on) {
+      a = prof_event(p);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b = prof_event(p);
+      cudaEventRecord(b, st);
+      p->prof_live.push_back({kind, a, b});
+    }
+  }
+};
+
+static int round_up(int x, int a) { return (x + a - 1) / a * a; }
+
+static size_t coarse_smem(const moco_plan *p, int sc, int br, int fpitch) {
+  const int w = p->w, W = p->W, L = p->levels;
+  const size_t acc = 8;
+  const size_t e = p->esz[L];
+  size_t band = std::max((size_t)4 * w * w * acc,
+                         (size_t)br * p->nl[L] * e + (size_t)(br + 2 * (w - 1)) * fpitch * e);
+  size_t sz = (size_t)W * W * acc + (size_t)sc * W * acc + 32 * sizeof(Key) +
+              (size_t)(4 * w + 1 + 32) * acc;
+  sz = (sz + 15) / 16 * 16;
+  return sz + band;
+}
+
+// Exported functions take their C linkage from the declarations in moco.h.
+
+int moco_abi_version(void) { return MOCO_ABI_VERSION; }
+
+const char *moco_strerror(int code) {
+  switch (code) {
+    case MOCO_OK: return "ok";
+    case MOCO_EINVAL: return "invalid argument";
+    case MOCO_ENOMEM: return "out of memory";
+    case MOCO_ECUDA: return "CUDA error";
+    case MOCO_ESTATE: return "invalid call order (template not set)";
+    default: return "unknown moco status";
+  }
+}
+
+const char *moco_last_cuda_error(void) { return g_err; }
+
+int64_t moco_last_launch_count(const moco_plan *p) { return p ? p->launches : 0; }
+
+static void plan_free(moco_plan *p) {
+  if (!p) return;
+  for (int l = 0; l < 3; ++l) {
+    if (p->tpl[l]) cudaFree(p->tpl[l]);
+    if (p->scratch[l]) cudaFree(p->scratch[l]);
+    if (p->sh[l]) cudaFree(p->sh[l]);
+  }
+  if (p->gb) cudaFree(p->gb);
+  tc_free(&p->tc);
+  for (int k = 0; k < 2; ++k) {
+    if (p->slot_in[k]) cudaFree(p->slot_in[k]);
+    if (p->slot_out[k]) cudaFree(p->slot_out[k]);
+    if (p->slot_sh[k]) cudaFree(p->slot_sh[k]);
+    if (p->slot_f[k]) cudaFree(p->slot_f[k]);
+    if (p->slot_flags[k]) cudaFree(p->slot_flags[k]);
+    if (p->ev_in[k]) cudaEventDestroy(p->ev_in[k]);
+    if (p->ev_done[k]) cudaEventDestroy(p->ev_done[k]);
+    if (p->ev_free[k]) cudaEventDestroy(p->ev_free[k]);
+  }
+  for (int k = 0; k < 3; ++k)
+    if (p->hs[k]) cudaStreamDestroy(p->hs[k]);
+  for (auto &r : p->prof_live) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto e : p->prof_pool) cudaEventDestroy(e);
+  delete p;
+}
+
+int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype, int bits,
+                     int device) {
+  if (!out) return MOCO_EINVAL;
+  *out = nullptr;
+  if (levels < 0 || levels > 2) return MOCO_EINVAL;
+  if (dtype != MOCO_U16 && dtype != MOCO_F32) return MOCO_EINVAL;
+  if (dtype == MOCO_U16 && (bits < 1 || bits > 16 || bits + 2 * levels > 16)) return MOCO_EINVAL;
+  if (m < (2 << levels) || n < (2 << levels)) return MOCO_EINVAL;
+  const size_t e0 = dtype == MOCO_U16 ? 2 : 4;
+  if ((n * e0) % 16 != 0) return MOCO_EINVAL;
+  const int mL = m >> levels, nL = n >> levels;
+  if (w < 1 || w >= std::min(mL, nL)) return MOCO_EINVAL;
+  if (w > 64) return MOCO_EINVAL;   // shared-memory lag tables sized for w <= 64
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    snprintf(g_err, sizeof(g_err), "no CUDA device %d (count %d)", device, ndev);
+    return MOCO_ECUDA;
+  }
+  CK(cudaSetDevice(device));
+  moco_plan *p = new (std::nothrow) moco_plan();
+  if (!p) return MOCO_ENOMEM;
+  p->m = m; p->n = n; p->w = w; p->W = 2 * w - 1; p->levels = levels; p->dtype = dtype;
+  p->bits = dtype == MOCO_U16 ? bits : 0; p->device = device;
+  for (int l = 0; l <= levels; ++l) {
+    p->ml[l] = m >> l;
+    p->nl[l] = n >> l;
+    p->pitch[l] = l == 0 ? n : round_up(p->nl[l], 8);
+    p->esz[l] = dtype == MOCO_U16 ? 2 : (l == 0 ? 4 : 8);
+  }
+  // coarse kernel geometry (K3+K4d+K5)
+  const int W = p->W, G = (W + KT - 1) / KT;
+  p->c_sc = std::min(W, std::max(1, 4096 / W));
+  p->c_br = 16;
+  p->c_fpitch = round_up(p->nl[levels] + W + 2 * KT, 8);
+  const int tasks = p->c_sc * G;
+  p->c_threads = std::min(512, std::max(64, round_up(tasks, 32)));
+  p->c_smem = coarse_smem(p, p->c_sc, p->c_br, p->c_fpitch);
+  if (p->c_smem > 227 * 1024) { plan_free(p); return MOCO_EINVAL; }
+  // workspace: template pyramid, tables, one batch of frame pyramid levels
+  int rc = MOCO_OK;
+  auto alloc = [&](void **ptr, size_t bytes) {
+    if (rc != MOCO_OK) return;
+    if (cudaMalloc(ptr, bytes) != cudaSuccess) { cudaGetLastError(); rc = MOCO_ENOMEM; }
+  };
+  for (int l = 0; l <= levels; ++l) alloc(&p->tpl[l], (size_t)p->ml[l] * p->pitch[l] * p->esz[l]);
+  alloc(&p->gb, (size_t)W * W * 8);
+  size_t per_frame = 0;
+  for (int l = 1; l <= levels; ++l) per_frame += (size_t)p->ml[l] * p->pitch[l] * p->esz[l];
+  const size_t budget = (size_t)256 << 20;
+  p->cap = per_frame ? std::max<int64_t>(1, (int64_t)(budget / per_frame)) : (int64_t)1 << 20;
+  p->cap = std::min<int64_t>(p->cap, (int64_t)1 << 20);
+  for (int l = 1; l <= levels; ++l)
+    alloc(&p->scratch[l], (size_t)p->cap * p->ml[l] * p->pitch[l] * p->esz[l]);
+  for (int l = 0; l <= levels; ++l) alloc((void **)&p->sh[l], (size_t)p->cap * 2 * sizeof(int32_t));
+  if (rc != MOCO_OK) { plan_free(p); return rc; }
+  p->algo = MOCO_ALGO_DIRECT;
+  if (tc_supported(p->dtype, p->bits, p->levels, p->w, p->ml[levels], p->nl[levels]) &&
+      tc_auto_prefers(p->w)) {
+    if (tc_init(&p->tc, p->w, p->ml[levels], p->nl[levels], p->cap) == 0) p->algo = MOCO_ALGO_TC;
+    else cudaGetLastError();
+  }
+  *out = p;
+  return MOCO_OK;
+}
+
+int moco_plan_set_algo(moco_plan *p, int algo) {
+  if (!p) return MOCO_EINVAL;
+  if (algo == MOCO_ALGO_DIRECT) { p->algo = algo; return MOCO_OK; }
+  const int L = p->levels;
+  if (algo == MOCO_ALGO_TC || algo == MOCO_ALGO_AUTO) {
+    const bool ok = tc_supported(p->dtype, p->bits, L, p->w, p->ml[L], p->nl[L]);
+    if (algo == MOCO_ALGO_AUTO && !(ok && tc_auto_prefers(p->w))) { p->algo = MOCO_ALGO_DIRECT; return MOCO_OK; }
+    if (!ok) return MOCO_EINVAL;
+    CK(cudaSetDevice(p->device));
+    if (!p->tc.ready && tc_init(&p->tc, p->w, p->ml[L], p->nl[L], p->cap) != 0) return MOCO_ENOMEM;
+    if (p->has_tpl && !p->tc.tpl_ready) {
+      if (tc_set_template(&p->tc, (const uint16_t *)p->tpl[L], p->pitch[L], 0) != 0)
+        return set_cuda_err(cudaGetLastError(), "tc_set_template");
+      CK(cudaDeviceSynchronize());
+    }
+    p->algo = MOCO_ALGO_TC;
+    return MOCO_OK;
+  }
+  return MOCO_EINVAL;
+}
+
+int moco_plan_get_algo(const moco_plan *p) { return p ? p->algo : MOCO_EINVAL; }
+
+int moco_profile_enable(moco_plan *p, int on) {
+  if (!p) return MOCO_EINVAL;
+  p->prof_on = on != 0;
+  return MOCO_OK;
+}
+
+int moco_profile_read(moco_plan *p, double *ms, int64_t *launches, int n) {
+  if (!p || n < 0 || (n > 0 && (!ms || !launches))) return MOCO_EINVAL;
+  for (int k = 0; k < n; ++k) { ms[k] = 0; launches[k] = 0; }
+  for (auto &r : p->prof_live) {
+    CK(cudaEventSynchronize(r.b));
+    float t = 0;
+    CK(cudaEventElapsedTime(&t, r.a, r.b));
+    if (r.kind < n) { ms[r.kind] += t; launches[r.kind] += 1; }
+    p->prof_pool.push_back(r.a);
+    p->prof_pool.push_back(r.b);
+  }
+  p->prof_live.clear();
+  return MOCO_OK;
+}
+
+int moco_plan_destroy(moco_plan *p) {
+  if (!p) return MOCO_OK;
+  cudaSetDevice(p->device);
+  cudaDeviceSynchronize();
+  plan_free(p);
+  return MOCO_OK;
+}
+
+static int grid_for(int64_t work, int threads) {
+  int64_t b = (work + threads - 1) / threads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 32));
+}
+
+// K1: level l -> l+1 for `B` frames.  src/dst are level images with the
+// plan's pitch/fstride conventions.
+static int launch_downsample(moco_plan *p, int l, const void *src, int64_t src_fstride, void *dst,
+                             int64_t B, cudaStream_t st) {
+  const int mi = p->ml[l], ni = p->nl[l], mo = p->ml[l + 1], no = p->nl[l + 1];
+  const int64_t dst_fstride = (int64_t)mo * p->pitch[l + 1];
+  ProfScope ps(p, MOCO_K_DOWNSAMPLE, st);
+  if (p->dtype == MOCO_U16) {
+    const int64_t work = B * mo * ((no + 3) / 4);
+    k_downsample_u16<<<grid_for(work, 256), 256, 0, st>>>(
+        (const uint16_t *)src, src_fstride, p->pitch[l], mi, ni, (uint16_t *)dst, dst_fstride,
+        p->pitch[l + 1], mo, no, (int)B);
+  } else if (l == 0) {
+    k_downsample_mean<float><<<grid_for(B * mo * no, 256), 256, 0, st>>>(
+        (const float *)src, src_fstride, p->pitch[l], mi, ni, (double *)dst, dst_fstride,
+        p->pitch[l + 1], mo, no, (int)B);
+  } else {
+    k_downsample_mean<double><<<grid_for(B * mo * no, 256), 256, 0, st>>>(
+        (const double *)src, src_fstride, p->pitch[l], mi, ni, (double *)dst, dst_fstride,
+        p->pitch[l + 1], mo, no, (int)B);
+  }
+  p->launches++;
+  CKL("k_downsample");
+  return MOCO_OK;
+}
+
+template <class In, bool WIDE>
+static int launch_coarse_t(moco_plan *p, const CoarseArgs &a, cudaStream_t st) {
+  static bool attr_done[8] = {false};   // per-device attribute is set once per process
+  (void)attr_done;
+  CK(cudaFuncSetAttribute(k_coarse<In, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)p->c_smem));
+  ProfScope ps(p, MOCO_K_COARSE, st);
+  k_coarse<In, WIDE><<<a.B, p->c_threads, p->c_smem, st>>>(a);
+  p->launches++;
+  CKL("k_coarse");
+  return MOCO_OK;
+}
+
+static int launch_coarse(moco_plan *p, const void *img, int64_t fstride, int pitch, int64_t B,
+                         int32_t *shift_out, double *f_out, double *grid_out, uint8_t *flags,
+                         cudaStream_t st) {
+  const int L = p->levels;
+  if (p->algo == MOCO_ALGO_TC && grid_out == nullptr) {
+    const int rc = tc_coarse(&p->tc, (const uint16_t *)img, fstride, pitch, (int)B,
+                             (const u64 *)p->gb, (double)(1u << (4 * L)), shift_out, f_out, flags,
+                             st, &p->launches);
+    if (rc != 0) return set_cuda_err(cudaGetLastError(), "tc_coarse");
+    return MOCO_OK;
+  }
+  CoarseArgs a;
+  a.frames = img; a.fstride = fstride; a.pitch = pitch;
+  a.tpl = p->tpl[L]; a.tpitch = p->pitch[L];
+  a.gb = p->gb;
+  a.mc = p->ml[L]; a.nc = p->nl[L]; a.w = p->w;
+  a.scale = p->dtype == MOCO_U16 ? (double)(1u << (4 * L)) : 1.0;
+  a.B = (int)B; a.br = p->c_br; a.sc = p->c_sc; a.fpitch = p->c_fpitch;
+  a.shift_out = shift_out; a.f_out = f_out; a.grid_out = grid_out; a.flags = flags;
+  if (p->dtype == MOCO_U16) {
+    if (p->bits + 2 * L <= 14) return launch_coarse_t<uint16_t, false>(p, a, st);
+    return launch_coarse_t<uint16_t, true>(p, a, st);
+  }
+  if (L == 0) return launch_coarse_t<float, false>(p, a, st);
+  return launch_coarse_t<double, false>(p, a, st);
+}
+
+static int launch_refine(moco_plan *p, int l, const void *img, int64_t fstride, int64_t B,
+                         const int32_t *sin, int32_t *sout, double *fout, cudaStream_t st) {
+  RefineArgs a;
+  a.frames = img; a.fstride = fstride; a.pitch = p->pitch[l];
+  a.tpl = p->tpl[l]; a.tpitch = p->pitch[l];
+  a.ml = p->ml[l]; a.nl = p->nl[l];
+  a.scale = p->dtype == MOCO_U16 ? (double)(1u << (4 * l)) : 1.0;
+  a.B = (int)B; a.shift_in = sin; a.shift_out = sout; a.f_out = fout;
+  ProfScope ps(p, MOCO_K_REFINE, st);
+  if (p->dtype == MOCO_U16) k_refine<uint16_t><<<(unsigned)B, 256, 0, st>>>(a);
+  else if (l == 0) k_refine<float><<<(unsigned)B, 256, 0, st>>>(a);
+  else k_refine<double><<<(unsigned)B, 256, 0, st>>>(a);
+  p->launches++;
+  CKL("k_refine");
+  return MOCO_OK;
+}
+
+static int launch_apply(moco_plan *p, const void *in, void *out, const int32_t *sh, int64_t B,
+                        cudaStream_t st) {
+  ProfScope ps(p, MOCO_K_APPLY, st);
+  if (p->dtype == MOCO_U16) {
+    const int64_t work = B * p->m * (p->n / 8);
+    k_apply<uint16_t><<<grid_for(work, 256), 256, 0, st>>>((const uint16_t *)in, (uint16_t *)out,
+                                                           p->m, p->n, sh, (int)B);
+  } else {
+    const int64_t work = B * p->m * (p->n / 4);
+    k_apply<float><<<grid_for(work, 256), 256, 0, st>>>((const float *)in, (float *)out, p->m,
+                                                        p->n, sh, (int)B);
+  }
+  p->launches++;
+  CKL("k_apply");
+  return MOCO_OK;
+}
+
+int moco_set_template(moco_plan *p, const void *d_template, moco_stream_t stream) {
+  if (!p || !d_template) return MOCO_EINVAL;
+  CK(cudaSetDevice(p->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t bytes0 = (size_t)p->m * p->n * p->esz[0];
+  CK(cudaMemcpyAsync(p->tpl[0], d_template, bytes0, cudaMemcpyDeviceToDevice, st));
+  for (int l = 0; l < p->levels; ++l) {
+    int rc = launch_downsample(p, l, p->tpl[l], 0, p->tpl[l + 1], 1, st);
+    if (rc) return rc;
+  }
+  const int L = p->levels;
+  if (p->dtype == MOCO_U16)
+    k_template_energy<uint16_t><<<p->W * p->W, 256, 0, st>>>(
+        (const uint16_t *)p->tpl[L], p->pitch[L], p->ml[L], p->nl[L], p->w, (u64 *)p->gb);
+  else if (L == 0)
+    k_template_energy<float><<<p->W * p->W, 256, 0, st>>>(
+        (const float *)p->tpl[L], p->pitch[L], p->ml[L], p->nl[L], p->w, (double *)p->gb);
+  else
+    k_template_energy<double><<<p->W * p->W, 256, 0, st>>>(
+        (const double *)p->tpl[L], p->pitch[L], p->ml[L], p->nl[L], p->w, (double *)p->gb);
+  CKL("k_template_energy");
+  if (p->tc.ready) {
+    if (tc_set_template(&p->tc, (const uint16_t *)p->tpl[L], p->pitch[L], st) != 0)
+      return set_cuda_err(cudaGetLastError(), "tc_set_template");
+  }
+  p->has_tpl = true;
+  return MOCO_OK;
+}
+
+static int check_align_args(moco_plan *p, const void *frames, int64_t T) {
+  if (!p || T < 0) return MOCO_EINVAL;
+  if (T > 0 && !frames) return MOCO_EINVAL;
+  if (((uintptr_t)frames & 15) != 0) return MOCO_EINVAL;
+  if (!p->has_tpl) return MOCO_ESTATE;
+  return MOCO_OK;
+}
+
+// One internal batch [f0, f0+B) of device frames.
+static int run_batch(moco_plan *p, const void *frames_b, int64_t B, int32_t *shifts_b,
+                     double *fmin_b, void *corr_b, uint8_t *flags_b, double *grid_b,
+                     cudaStream_t st) {
+  const int L = p->levels;
+  const void *img[3];
+  int64_t fstride[3];
+  img[0] = frames_b;
+  fstride[0] = (int64_t)p->m * p->n;
+  for (int l = 1; l <= L; ++l) {
+    img[l] = p->scratch[l];
+    fstride[l] = (int64_t)p->ml[l] * p->pitch[l];
+  }
+  for (int l = 0; l < L; ++l) {
+    int rc = launch_downsample(p, l, img[l], fstride[l], p->scratch[l + 1], B, st);
+    if (rc) return rc;
+  }
+  if (grid_b) return launch_coarse(p, img[L], fstride[L], p->pitch[L], B, nullptr, nullptr, grid_b,
+                                   nullptr, st);
+  int32_t *sc_out = L == 0 ? shifts_b : p->sh[L];
+  int rc = launch_coarse(p, img[L], fstride[L], p->pitch[L], B, sc_out, L == 0 ? fmin_b : nullptr,
+                         nullptr, flags_b, st);
+  if (rc) return rc;
+  for (int l = L - 1; l >= 0; --l) {
+    int32_t *so = l == 0 ? shifts_b : p->sh[l];
+    rc = launch_refine(p, l, img[l], fstride[l], B, p->sh[l + 1], so, l == 0 ? fmin_b : nullptr, st);
+    if (rc) return rc;
+  }
+  if (corr_b) return launch_apply(p, frames_b, corr_b, shifts_b, B, st);
+  return MOCO_OK;
+}
+
+int moco_align_batch(moco_plan *p, const void *d_frames, int64_t T, int32_t *d_shifts,
+                     double *d_fmin, void *d_corrected, uint8_t *d_flags, moco_stream_t stream) {
+  int rc = check_align_args(p, d_frames, T);
+  if (rc) return rc;
+  if (T > 0 && (!d_shifts || !d_fmin)) return MOCO_EINVAL;
+  if (((uintptr_t)d_corrected & 15) != 0) return MOCO_EINVAL;
+  if (d_corrected && d_corrected == d_frames) return MOCO_EINVAL;
+  CK(cudaSetDevice(p->device));
+  p->launches = 0;
+  const size_t fbytes = (size_t)p->m * p->n * p->esz[0];
+  for (int64_t f0 = 0; f0 < T; f0 += p->cap) {
+    const int64_t B = std::min<int64_t>(p->cap, T - f0);
+    rc = run_batch(p, (const char *)d_frames + f0 * fbytes, B, d_shifts + 2 * f0, d_fmin + f0,
+                   d_corrected ? (char *)d_corrected + f0 * fbytes : nullptr,
+                   d_flags ? d_flags + f0 : nullptr, nullptr, (cudaStream_t)stream);
+    if (rc) return rc;
+  }
+  return MOCO_OK;
+}
+
+int moco_score_grid(moco_plan *p, const void *d_frames, int64_t T, double *d_f,
+                    moco_stream_t stream) {
+  int rc = check_align_args(p, d_frames, T);
+  if (rc) return rc;
+  if (T > 0 && !d_f) return MOCO_EINVAL;
+  CK(cudaSetDevice(p->device));
+  p->launches = 0;
+  const size_t fbytes = (size_t)p->m * p->n * p->esz[0];
+  const int64_t WW = (int64_t)p->W * p->W;
+  for (int64_t f0 = 0; f0 < T; f0 += p->cap) {
+    const int64_t B = std::min<int64_t>(p->cap, T - f0);
+    rc = run_batch(p, (const char *)d_frames + f0 * fbytes, B, nullptr, nullptr, nullptr, nullptr,
+                   d_f + f0 * WW, (cudaStream_t)stream);
+    if (rc) return rc;
+  }
+  return MOCO_OK;
+}
+
+int moco_align_host(moco_plan *p, const void *h_frames, int64_t T, int32_t *h_shifts,
+                    double *h_fmin, void *h_corrected, uint8_t *h_flags) {
+  if (!p || T < 0) return MOCO_EINVAL;
+  if (T == 0) return MOCO_OK;
+  if (!h_frames || !h_shifts || !h_fmin) return MOCO_EINVAL;
+  if (!p->has_tpl) return MOCO_ESTATE;
+  CK(cudaSetDevice(p->device));
+  const size_t fbytes = (size_t)p->m * p->n * p->esz[0];
+  if (!p->host_ready) {
+    // chunks of ~32 MiB of frames, capped by the plan's batch capacity; two
+    // slots so the copy of chunk k+1 in and chunk k-1 out overlap chunk k's
+    // kernels.  Compute stays on ONE stream (the plan's scratch is shared).
+    p->host_ch = std::max<int64_t>(1, std::min<int64_t>(p->cap, ((int64_t)32 << 20) / (int64_t)fbytes));
+    for (int k = 0; k < 2; ++k) {
+      if (cudaMalloc(&p->slot_in[k], p->host_ch * fbytes) != cudaSuccess ||
+          cudaMalloc(&p->slot_out[k], p->host_ch * fbytes) != cudaSuccess ||
+          cudaMalloc((void **)&p->slot_sh[k], p->host_ch * 2 * sizeof(int32_t)) != cudaSuccess ||
+          cudaMalloc((void **)&p->slot_f[k], p->host_ch * sizeof(double)) != cudaSuccess ||
+          cudaMalloc((void **)&p->slot_flags[k], p->host_ch) != cudaSuccess) {
+        cudaGetLastError();
+        return MOCO_ENOMEM;
+      }
+    }
+    for (int k = 0; k < 3; ++k) CK(cudaStreamCreateWithFlags(&p->hs[k], cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+      CK(cudaEventCreateWithFlags(&p->ev_in[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&p->ev_done[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&p->ev_free[k], cudaEventDisableTiming));
+    }
+    p->host_ready = true;
+  }
+  cudaStream_t s_in = p->hs[0], s_comp = p->hs[1], s_out = p->hs[2];
+  int64_t total_launches = 0;
+  int64_t chunk = 0;
+  for (int64_t f0 = 0; f0 < T; f0 += p->host_ch, ++chunk) {
+    const int k = (int)(chunk & 1);
+    const int64_t B = std::min<int64_t>(p->host_ch, T - f0);
+    if (chunk >= 2) CK(cudaStreamWaitEvent(s_in, p->ev_free[k], 0));
+    CK(cudaMemcpyAsync(p->slot_in[k], (const char *)h_frames + f0 * fbytes, B * fbytes,
+                       cudaMemcpyHostToDevice, s_in));
+    CK(cudaEventRecord(p->ev_in[k], s_in));
+    CK(cudaStreamWaitEvent(s_comp, p->ev_in[k], 0));
+    if (chunk >= 2) CK(cudaStreamWaitEvent(s_comp, p->ev_free[k], 0));
+    int rc = moco_align_batch(p, p->slot_in[k], B, p->slot_sh[k], p->slot_f[k],
+                              h_corrected ? p->slot_out[k] : nullptr,
+                              h_flags ? p->slot_flags[k] : nullptr, s_comp);
+    if (rc) return rc;
+    total_launches += p->launches;
+    CK(cudaEventRecord(p->ev_done[k], s_comp));
+    CK(cudaStreamWaitEvent(s_out, p->ev_done[k], 0));
+    CK(cudaMemcpyAsync(h_shifts + 2 * f0, p->slot_sh[k], B * 2 * sizeof(int32_t),
+                       cudaMemcpyDeviceToHost, s_out));
+    CK(cudaMemcpyAsync(h_fmin + f0, p->slot_f[k], B * sizeof(double), cudaMemcpyDeviceToHost, s_out));
+    if (h_corrected)
+      CK(cudaMemcpyAsync((char *)h_corrected + f0 * fbytes, p->slot_out[k], B * fbytes,
+                         cudaMemcpyDeviceToHost, s_out));
+    if (h_flags) CK(cudaMemcpyAsync(h_flags + f0, p->slot_flags[k], B, cudaMemcpyDeviceToHost, s_out));
+    CK(cudaEventRecord(p->ev_free[k], s_out));
+  }
+  CK(cudaStreamSynchronize(s_out));
+  p->launches = total_launches;
+  return MOCO_OK;
+}
+

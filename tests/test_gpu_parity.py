@@ -1,0 +1,204 @@
+"""GPU parity: the CUDA path through the C-ABI (paper_1506_06039_b200.Plan ->
+libmoco.so) against the CPU oracle on the same seeded inputs."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1506_06039_b200 import MocoError, Plan
+from synth import config_spec, make_stack
+from tests import paper_forms as pf
+from tests.parity import check_frame
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda", 0)
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _plan_for(spec, algo=None):
+    p = Plan(spec.m, spec.n, spec.w, spec.levels, spec.dtype, 12, device=0)
+    if algo:
+        p.set_algo(algo)
+    return p
+
+
+# ------------------------------------------------------------- score grid (S1-S4)
+@pytest.mark.parametrize("m,n,levels,w,hi", [
+    (80, 72, 1, 9, 4096),      # coarse 40x36: ragged bands (16-row) and ragged t-groups
+    (64, 48, 0, 11, 4096),
+    (96, 104, 2, 5, 4096),     # two levels, coarse 24x26
+    (40, 40, 0, 20, 65536),    # 16-bit samples: the wide-accumulation kernel
+])
+def test_score_grid_u16_bit_exact(m, n, levels, w, hi):
+    """Every coarse-level f_{s,t} equals the oracle's objective_grid bit for bit."""
+    rng = np.random.default_rng(m * 1000 + n + levels)
+    T = 3
+    bits = 16 if hi > 4096 else 12
+    fr = rng.integers(0, hi, size=(T, m, n)).astype(np.uint16)
+    tp = rng.integers(0, hi, size=(m, n)).astype(np.uint16)
+    fr[1] = pf.translate_zero_fill(tp, 3, -2)
+    if bits + 2 * levels > 16:
+        pytest.skip("plan rejects bits + 2*levels > 16")
+    p = Plan(m, n, w, levels, "u16", bits, device=0)
+    p.set_template(torch.from_numpy(tp).to(DEV))
+    g = _np(p.score_grid(torch.from_numpy(fr).to(DEV)))
+    B = oracle.pyramid(tp, levels)[levels]
+    for k in range(T):
+        A = oracle.pyramid(fr[k], levels)[levels]
+        ref = oracle.objective_grid(A, B, w)
+        assert np.array_equal(g[k], ref), np.argwhere(g[k] != ref)[:5]
+
+
+def test_score_grid_f32():
+    spec = config_spec(0, T=4)
+    st = make_stack(spec, 0, 4)
+    p = _plan_for(spec)
+    p.set_template(st.template.to(DEV))
+    g = _np(p.score_grid(st.frames.to(DEV)))
+    for k in range(4):
+        ref = oracle.objective_grid(st.frames[k].numpy(), st.template.numpy(), spec.w)
+        np.testing.assert_allclose(g[k], ref, rtol=1e-9, atol=1e-12)
+
+
+# --------------------------------------------------------------- end to end, C0-C4
+def _run_config(c, T, sample, device_gen=True, algo=None, **over):
+    spec = config_spec(c, T=T, **over)
+    st = make_stack(spec, 0, T, device=DEV if device_gen else "cpu")
+    frames = st.frames.to(DEV)
+    p = _plan_for(spec, algo)
+    p.set_template(st.template.to(DEV))
+    sh, fm, co, fl = p.align(frames, corrected=True, flags=True)
+    torch.cuda.synchronize()
+    sh, fm, fl = _np(sh), _np(fm), _np(fl)
+    tp = _np(st.template)
+    kinds = []
+    for k in sample:
+        kinds.append(check_frame(_np(frames[k]), tp, spec.w, spec.levels, sh[k], fm[k], _np(co[k]),
+                                 exact=spec.dtype == "u16"))
+    return spec, st, sh, fm, fl, kinds, p
+
+
+def test_config0_all_frames():
+    spec, st, sh, fm, fl, kinds, _ = _run_config(0, 20, range(20), device_gen=False)
+    # clean-ish translates: the recovered shift is the ground truth
+    assert (sh == st.shifts).all()
+
+
+def test_config1_sampled():
+    _, st, sh, *_ = _run_config(1, 96, [0, 1, 47, 95])
+    assert (sh == st.shifts).mean() > 0.9
+
+
+def test_config2_full_stack_sampled():
+    """C2 as bench.py runs it: all 10,000 frames in one moco_align_batch call
+    (internal batches of the plan's capacity), sampled frames across internal
+    batch boundaries checked bit-exactly against the oracle."""
+    spec = config_spec(2)
+    p = _plan_for(spec)
+    sample = [0, 1, 2047, 2048, 5000, 8191, 8192, 9999]
+    spec, st, sh, fm, fl, kinds, p = _run_config(2, spec.T, sample)
+    assert kinds == ["exact"] * len(sample)
+    assert (sh == st.shifts).mean() > 0.95
+
+
+def test_config3_stripes_sampled():
+    spec = config_spec(3, T=64)
+    st = make_stack(spec, 0, 64, device=DEV)
+    stripe = np.nonzero(st.stripe)[0]
+    sample = [0, 63] + ([int(stripe[0])] if len(stripe) else [])
+    _run_config(3, 64, sample)
+
+
+def test_config4_sampled():
+    _run_config(4, 6, [0, 5])
+
+
+# --------------------------------------------------------------------- edge cases
+def test_exact_translates_give_zero():
+    spec = config_spec(1, T=1)
+    tp = make_stack(spec, 0, 1).template.numpy()
+    shifts = [(0, 0), (19, -19), (-19, 7), (5, 19), (-3, -11)]
+    fr = np.stack([pf.translate_zero_fill(tp, dy, dx) for dy, dx in shifts]).astype(np.uint16)
+    p = Plan(256, 256, 20, 0, "u16", 12, device=0)
+    p.set_template(torch.from_numpy(tp).to(DEV))
+    sh, fm, co, _ = p.align(torch.from_numpy(fr).to(DEV))
+    assert _np(sh).tolist() == [list(x) for x in shifts]
+    assert (_np(fm) == 0).all()
+
+
+def test_exact_translates_levels2():
+    spec = config_spec(4, T=1)
+    tp = make_stack(spec, 0, 1).template.numpy()
+    shifts = [(84, -48), (-92, 4), (0, 93)]
+    fr = np.stack([pf.translate_zero_fill(tp, dy, dx) for dy, dx in shifts]).astype(np.uint16)
+    p = Plan(1024, 1024, 24, 2, "u16", 12, device=0)
+    p.set_template(torch.from_numpy(tp).to(DEV))
+    sh, fm, _, _ = p.align(torch.from_numpy(fr).to(DEV), corrected=False)
+    assert _np(sh).tolist() == [list(x) for x in shifts]
+    assert (_np(fm) == 0).all()
+
+
+def test_constant_frames_tie_break():
+    """All f equal -> smallest (s,t) lexicographically (reading R4)."""
+    m = n = 64
+    c = torch.full((2, m, n), 9, dtype=torch.int32).to(torch.uint16).to(DEV)
+    p = Plan(m, n, 6, 1, "u16", 12, device=0)
+    p.set_template(c[0])
+    sh, fm, _, _ = p.align(c, corrected=False)
+    r = oracle.align_frame(_np(c[0]), _np(c[0]), 6, 1)
+    assert _np(sh).tolist() == [[r.s, r.t]] * 2 and (_np(fm) == 0).all()
+
+
+def test_T_zero_and_one():
+    spec = config_spec(2, T=1)
+    st = make_stack(spec, 0, 1, device=DEV)
+    p = _plan_for(spec)
+    p.set_template(st.template)
+    empty = torch.empty((0, 512, 512), dtype=torch.uint16, device=DEV)
+    sh, fm, co, _ = p.align(empty)
+    assert sh.shape == (0, 2)
+    sh, fm, co, _ = p.align(st.frames)
+    check_frame(_np(st.frames[0]), _np(st.template), 16, 1, _np(sh)[0], _np(fm)[0], _np(co[0]))
+
+
+def test_batch_split_and_host_path_identical():
+    """Results independent of batch split; moco_align_host == moco_align_batch."""
+    spec = config_spec(1, T=40)
+    st = make_stack(spec, 0, 40, device=DEV)
+    p = _plan_for(spec)
+    p.set_template(st.template)
+    sh, fm, co, _ = p.align(st.frames)
+    sh2 = torch.cat([p.align(st.frames[:13])[0], p.align(st.frames[13:])[0]])
+    assert torch.equal(sh, sh2)
+    hf = st.frames.cpu().pin_memory()
+    hco = torch.empty_like(hf).pin_memory()
+    hs, hfm, _, _ = p.align_host(hf, corrected=hco)
+    assert torch.equal(hs, sh.cpu()) and torch.equal(hfm, fm.cpu())
+    assert torch.equal(hco.view(torch.int16), co.cpu().view(torch.int16))
+
+
+def test_flags_edge():
+    spec = config_spec(1, T=1)
+    tp = make_stack(spec, 0, 1).template.numpy()
+    fr = pf.translate_zero_fill(tp, 19, 0)[None]
+    p = Plan(256, 256, 20, 0, "u16", 12, device=0)
+    p.set_template(torch.from_numpy(tp).to(DEV))
+    _, _, _, fl = p.align(torch.from_numpy(fr).to(DEV), corrected=False, flags=True)
+    assert int(_np(fl)[0]) & 1
+
+
+def test_errors():
+    with pytest.raises(MocoError):
+        Plan(512, 512, 16, 3, "u16", 12, device=0)          # levels >= 3
+    with pytest.raises(MocoError):
+        Plan(64, 64, 32, 1, "u16", 12, device=0)            # w >= coarse size
+    with pytest.raises(MocoError):
+        Plan(64, 60, 8, 0, "u16", 12, device=0)             # row pitch not 16-byte multiple
+    p = Plan(64, 64, 8, 0, "u16", 12, device=0)
+    fr = torch.zeros((1, 64, 64), dtype=torch.int32).to(torch.uint16).to(DEV)
+    with pytest.raises(MocoError) as e:
+        p.align(fr)                                         # before set_template
+    assert e.value.code == -4
