@@ -562,3 +562,201 @@ __global__ void k_apply(const E *__restrict__ in, E *__restrict__ out, int m, in
 }
 
 }  // namespace moco
+
+namespace moco {
+
+// ------------------------------------------------------------- K6+K7 fused (u16)
+// One CTA per frame at level l: the nine candidates (2s+u, 2t+v) by exact direct
+// sums N = sum_D (a - b)^2, argmin with key (f, s, t), and -- at level 0 when
+// requested -- the corrected frame c[i][j] = a[i+s][j+t] or 0 written
+// right after, while the frame is still in L2 (one HBM read for both steps).
+// Each thread owns 8 consecutive template columns of a row; the 3 frame rows it
+// needs are read as aligned 16-byte vectors and shifted in registers.  The
+// misalignment (T-1) mod 8 is the same for the whole CTA, so the loop is
+// specialised on it (template OFFA).
+struct RefineApplyArgs {
+  const uint16_t *frames;   // level-l images
+  int64_t fstride;
+  int pitch;
+  const uint16_t *tpl;      // level-l template
+  int tpitch;
+  int ml, nl;
+  double scale;             // 16^l
+  int B;
+  const int32_t *shift_in;  // [B][2] at level l+1
+  int32_t *shift_out;       // [B][2] at level l
+  double *f_out;            // [B] or null
+  uint16_t *corrected;      // [B][m][n] or null (level 0 only; fstride/pitch of the frames)
+  int flush;                // products summed in 32 bits before widening
+};
+
+template <int OFF>
+__device__ __forceinline__ void extract10(const uint4 &lo, const uint4 &hi, uint32_t (&v)[10]) {
+  const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+  for (int x = 0; x < 10; ++x) {
+    const int e = OFF + x;   // element within the 16 (e == 16 only for OFF == 7: set by caller)
+    if (e < 16) v[x] = (w[e >> 1] >> (16 * (e & 1))) & 0xffffu;
+  }
+}
+
+template <int OFFA>
+__device__ __forceinline__ void refine_rows(const RefineApplyArgs &a, const uint16_t *A, int S, int T,
+                                            u64 (&acc64)[9]) {
+  const int ml = a.ml, nl = a.nl;
+  const int groups = (nl + 7) >> 3;
+  const int ilo = max(0, -S - 1), ihi = min(ml, ml - S + 1);
+  const int items = (ihi - ilo) * groups;
+  uint32_t acc[9];
+#pragma unroll
+  for (int c = 0; c < 9; ++c) acc[c] = 0;
+  int cnt = 0;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int i = ilo + it / groups;
+    const int j0 = (it % groups) * 8;
+    const uint4 bq = *reinterpret_cast<const uint4 *>(a.tpl + (int64_t)i * a.tpitch + j0);
+    const uint32_t bw[4] = {bq.x, bq.y, bq.z, bq.w};
+    uint32_t bv[8];
+#pragma unroll
+    for (int x = 0; x < 8; ++x) bv[x] = (bw[x >> 1] >> (16 * (x & 1))) & 0xffffu;
+    const int base = j0 + T - 1;              // frame column of (x=0, v=-1)
+    const int ab = base - OFFA;               // 8-aligned
+    // 10 columns from an 8-aligned start: two vectors, plus one sample when OFFA == 7
+    const bool fast = ab >= 0 && ab + 16 + (OFFA == 7) <= a.pitch && base + 10 <= nl && j0 + 8 <= nl;
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const int r = i + S + u - 1;
+      if (r < 0 || r >= ml) continue;
+      const uint16_t *arow = A + (int64_t)r * a.pitch;
+      uint32_t av[10];
+      if (fast) {
+        const uint4 lo = *reinterpret_cast<const uint4 *>(arow + ab);
+        const uint4 hi = *reinterpret_cast<const uint4 *>(arow + ab + 8);
+        extract10<OFFA>(lo, hi, av);
+        if (OFFA == 7) av[9] = arow[ab + 16];
+#pragma unroll
+        for (int v = 0; v < 3; ++v)
+#pragma unroll
+          for (int x = 0; x < 8; ++x) {
+            const int d = (int)av[x + v] - (int)bv[x];
+            acc[u * 3 + v] += (uint32_t)(d * d);
+          }
+      } else {
+#pragma unroll
+        for (int x = 0; x < 10; ++x) {
+          const int c = base + x;
+          av[x] = (c >= 0 && c < nl) ? arow[c] : 0u;
+        }
+#pragma unroll
+        for (int v = 0; v < 3; ++v)
+#pragma unroll
+          for (int x = 0; x < 8; ++x) {
+            const int c = base + x + v;   // frame column of template column j0+x, candidate v
+            if (c < 0 || c >= nl || j0 + x >= nl) continue;
+            const int d = (int)av[x + v] - (int)bv[x];
+            acc[u * 3 + v] += (uint32_t)(d * d);
+          }
+      }
+    }
+    if (++cnt == a.flush) {
+#pragma unroll
+      for (int c = 0; c < 9; ++c) {
+        acc64[c] += acc[c];
+        acc[c] = 0;
+      }
+      cnt = 0;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 9; ++c) acc64[c] += acc[c];
+}
+
+template <int OFFT>
+__device__ __forceinline__ void apply_rows(const RefineApplyArgs &a, const uint16_t *A, uint16_t *O, int s,
+                                           int t, int m, int n) {
+  const int groups = n >> 3;   // n % 8 == 0 at level 0
+  for (int it = threadIdx.x; it < m * groups; it += blockDim.x) {
+    const int i = it / groups, j0 = (it % groups) * 8;
+    const int r = i + s;
+    uint4 outv = make_uint4(0, 0, 0, 0);
+    if (r >= 0 && r < m) {
+      const uint16_t *arow = A + (int64_t)r * a.pitch;
+      const int base = j0 + t, ab = base - OFFT;
+      if (ab >= 0 && ab + 16 <= n) {
+        const uint4 lo = __ldg(reinterpret_cast<const uint4 *>(arow + ab));
+        const uint4 hi = OFFT ? __ldg(reinterpret_cast<const uint4 *>(arow + ab + 8)) : lo;
+        uint32_t v[10];
+        extract10<OFFT>(lo, hi, v);
+        outv = make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16), v[6] | (v[7] << 16));
+      } else {
+        uint32_t v[8];
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+          const int c = base + x;
+          v[x] = (c >= 0 && c < n) ? arow[c] : 0u;
+        }
+        outv = make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16), v[6] | (v[7] << 16));
+      }
+    }
+    __stcs(reinterpret_cast<uint4 *>(O + (int64_t)i * n + j0), outv);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_refine_apply(RefineApplyArgs a) {
+  const int64_t f = blockIdx.x;
+  const uint16_t *A = a.frames + f * a.fstride;
+  const int S = 2 * a.shift_in[2 * f], T = 2 * a.shift_in[2 * f + 1];
+  u64 acc[9];
+#pragma unroll
+  for (int c = 0; c < 9; ++c) acc[c] = 0;
+  switch ((T - 1) & 7) {
+    case 0: refine_rows<0>(a, A, S, T, acc); break;
+    case 1: refine_rows<1>(a, A, S, T, acc); break;
+    case 2: refine_rows<2>(a, A, S, T, acc); break;
+    case 3: refine_rows<3>(a, A, S, T, acc); break;
+    case 4: refine_rows<4>(a, A, S, T, acc); break;
+    case 5: refine_rows<5>(a, A, S, T, acc); break;
+    case 6: refine_rows<6>(a, A, S, T, acc); break;
+    default: refine_rows<7>(a, A, S, T, acc); break;
+  }
+  __shared__ u64 part[9][32];
+  __shared__ Key red[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int c = 0; c < 9; ++c) {
+    const u64 v = warp_sum(acc[c]);
+    if (lane == 0) part[c][wid] = v;
+  }
+  __syncthreads();
+  Key k{~0ull, ~0u};
+  if (threadIdx.x < 9) {
+    u64 N = 0;
+    for (int q = 0; q < nw; ++q) N += part[threadIdx.x][q];
+    const int u = threadIdx.x / 3 - 1, v = threadIdx.x % 3 - 1;
+    const int s = S + u, t = T + v;
+    const double area = (double)((a.ml - abs(s)) * (a.nl - abs(t)));
+    const double fv = (double)N / (a.scale * area);
+    k = Key{(u64)__double_as_longlong(fv), (unsigned)threadIdx.x};   // rank == (s,t) order
+  }
+  k = block_min_key(k, red);
+  const int s = S + (int)(k.idx / 3) - 1, t = T + (int)(k.idx % 3) - 1;
+  if (threadIdx.x == 0) {
+    a.shift_out[2 * f] = s;
+    a.shift_out[2 * f + 1] = t;
+    if (a.f_out) a.f_out[f] = __longlong_as_double((long long)k.f);
+  }
+  if (!a.corrected) return;
+  uint16_t *O = a.corrected + f * a.fstride;
+  switch (t & 7) {
+    case 0: apply_rows<0>(a, A, O, s, t, a.ml, a.nl); break;
+    case 1: apply_rows<1>(a, A, O, s, t, a.ml, a.nl); break;
+    case 2: apply_rows<2>(a, A, O, s, t, a.ml, a.nl); break;
+    case 3: apply_rows<3>(a, A, O, s, t, a.ml, a.nl); break;
+    case 4: apply_rows<4>(a, A, O, s, t, a.ml, a.nl); break;
+    case 5: apply_rows<5>(a, A, O, s, t, a.ml, a.nl); break;
+    case 6: apply_rows<6>(a, A, O, s, t, a.ml, a.nl); break;
+    default: apply_rows<7>(a, A, O, s, t, a.ml, a.nl); break;
+  }
+}
+
+}  // namespace moco

@@ -7,9 +7,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <new>
 #include <vector>
 
@@ -47,6 +49,7 @@ struct moco_plan {
   void *scratch[3];           // frame pyramid levels 1..L for one batch
   int32_t *sh[3];             // per-level shifts for one batch
   bool has_tpl;
+  bool simple_refine;         // MOCO_REFINE=simple: unfused K6/K7 (cross-check in tests)
   int64_t launches;
   // coarse kernel launch geometry
   int c_threads, c_sc, c_br, c_fpitch;
@@ -182,6 +185,10 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
   if (!p) return MOCO_ENOMEM;
   p->m = m; p->n = n; p->w = w; p->W = 2 * w - 1; p->levels = levels; p->dtype = dtype;
   p->bits = dtype == MOCO_U16 ? bits : 0; p->device = device;
+  {
+    const char *e = getenv("MOCO_REFINE");
+    p->simple_refine = e && strcmp(e, "simple") == 0;
+  }
   for (int l = 0; l <= levels; ++l) {
     p->ml[l] = m >> l;
     p->nl[l] = n >> l;
@@ -217,7 +224,7 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
   p->algo = MOCO_ALGO_DIRECT;
   if (tc_supported(p->dtype, p->bits, p->levels, p->w, p->ml[levels], p->nl[levels]) &&
       tc_auto_prefers(p->w)) {
-    if (tc_init(&p->tc, p->w, p->ml[levels], p->nl[levels], p->cap) == 0) p->algo = MOCO_ALGO_TC;
+    if (tc_init(&p->tc, p->w, p->ml[levels], p->nl[levels], levels, p->cap) == 0) p->algo = MOCO_ALGO_TC;
     else cudaGetLastError();
   }
   *out = p;
@@ -233,7 +240,7 @@ int moco_plan_set_algo(moco_plan *p, int algo) {
     if (algo == MOCO_ALGO_AUTO && !(ok && tc_auto_prefers(p->w))) { p->algo = MOCO_ALGO_DIRECT; return MOCO_OK; }
     if (!ok) return MOCO_EINVAL;
     CK(cudaSetDevice(p->device));
-    if (!p->tc.ready && tc_init(&p->tc, p->w, p->ml[L], p->nl[L], p->cap) != 0) return MOCO_ENOMEM;
+    if (!p->tc.ready && tc_init(&p->tc, p->w, p->ml[L], p->nl[L], L, p->cap) != 0) return MOCO_ENOMEM;
     if (p->has_tpl && !p->tc.tpl_ready) {
       if (tc_set_template(&p->tc, (const uint16_t *)p->tpl[L], p->pitch[L], 0) != 0)
         return set_cuda_err(cudaGetLastError(), "tc_set_template");
@@ -324,13 +331,6 @@ static int launch_coarse(moco_plan *p, const void *img, int64_t fstride, int pit
                          int32_t *shift_out, double *f_out, double *grid_out, uint8_t *flags,
                          cudaStream_t st) {
   const int L = p->levels;
-  if (p->algo == MOCO_ALGO_TC && grid_out == nullptr) {
-    const int rc = tc_coarse(&p->tc, (const uint16_t *)img, fstride, pitch, (int)B,
-                             (const u64 *)p->gb, (double)(1u << (4 * L)), shift_out, f_out, flags,
-                             st, &p->launches);
-    if (rc != 0) return set_cuda_err(cudaGetLastError(), "tc_coarse");
-    return MOCO_OK;
-  }
   CoarseArgs a;
   a.frames = img; a.fstride = fstride; a.pitch = pitch;
   a.tpl = p->tpl[L]; a.tpitch = p->pitch[L];
@@ -362,6 +362,33 @@ static int launch_refine(moco_plan *p, int l, const void *img, int64_t fstride, 
   p->launches++;
   CKL("k_refine");
   return MOCO_OK;
+}
+
+// K6 (+K7 at level 0): fused u16 kernel when 32-bit partial sums are safe.
+static int launch_refine_apply(moco_plan *p, int l, const void *img, int64_t fstride, int64_t B,
+                               const int32_t *sin, int32_t *sout, double *fout, void *corr,
+                               cudaStream_t st) {
+  const int vb = p->bits + 2 * l;
+  RefineApplyArgs a;
+  a.frames = (const uint16_t *)img; a.fstride = fstride; a.pitch = p->pitch[l];
+  a.tpl = (const uint16_t *)p->tpl[l]; a.tpitch = p->pitch[l];
+  a.ml = p->ml[l]; a.nl = p->nl[l];
+  a.scale = (double)(1u << (4 * l));
+  a.B = (int)B; a.shift_in = sin; a.shift_out = sout; a.f_out = fout;
+  a.corrected = (uint16_t *)corr;
+  const double dmax = (double)((1u << vb) - 1);
+  a.flush = (int)std::min(1024.0, std::floor(4294967295.0 / (8.0 * dmax * dmax)));
+  {
+    ProfScope ps(p, MOCO_K_REFINE, st);
+    k_refine_apply<<<(unsigned)B, 256, 0, st>>>(a);
+  }
+  p->launches++;
+  CKL("k_refine_apply");
+  return MOCO_OK;
+}
+
+static bool fused_ok(const moco_plan *p, int l) {
+  return !p->simple_refine && p->dtype == MOCO_U16 && p->bits + 2 * l <= 14;
 }
 
 static int launch_apply(moco_plan *p, const void *in, void *out, const int32_t *sh, int64_t B,
@@ -418,6 +445,54 @@ static int check_align_args(moco_plan *p, const void *frames, int64_t T) {
   return MOCO_OK;
 }
 
+// Tensor-core coarse search (kernels_tc.cuh) straight from the level-0 frames.
+static int launch_tc(moco_plan *p, const void *frames_b, int64_t B, int32_t *shift_out, double *f_out,
+                     uint8_t *flags, double *grid_out, cudaStream_t st) {
+  const TcGeom &g = p->tc.g;
+  const int64_t groups = (B + g.F - 1) / g.F;
+  TcPrepArgs pa;
+  pa.frames = (const uint16_t *)frames_b; pa.fstride = (int64_t)p->m * p->n; pa.n = p->n;
+  pa.B = (int)B; pa.g = g; pa.G = p->tc.G; pa.ga = p->tc.ga;
+  {
+    ProfScope ps(p, MOCO_K_PREP, st);
+    if (p->levels == 0) k_tc_prep<0><<<(unsigned)groups, 256, g.prep_smem, st>>>(pa);
+    else if (p->levels == 1) k_tc_prep<1><<<(unsigned)groups, 256, g.prep_smem, st>>>(pa);
+    else k_tc_prep<2><<<(unsigned)groups, 256, g.prep_smem, st>>>(pa);
+  }
+  p->launches++;
+  CKL("k_tc_prep");
+  TcArgs ta;
+  ta.G = p->tc.G; ta.T8 = p->tc.T8; ta.ga = p->tc.ga; ta.gb = (const u64 *)p->gb; ta.g = g;
+  ta.scale = (double)(1u << (4 * p->levels)); ta.B = (int)B;
+  ta.shift_out = shift_out; ta.f_out = f_out; ta.flags = flags; ta.grid_out = grid_out;
+  {
+    ProfScope ps(p, MOCO_K_COARSE, st);
+    k_tc_coarse<<<(unsigned)((groups + g.GG - 1) / g.GG), 256, g.smem, st>>>(ta);
+  }
+  p->launches++;
+  CKL("k_tc_coarse");
+  return MOCO_OK;
+}
+
+// S5 refine at levels L-1..0, then S6 apply (fused into the level-0 refine when possible).
+static int refine_levels(moco_plan *p, const void *const *img, const int64_t *fstride, int64_t B,
+                         int32_t *shifts_b, double *fmin_b, void *corr_b, cudaStream_t st) {
+  const int L = p->levels;
+  if (L == 0) return corr_b ? launch_apply(p, img[0], corr_b, shifts_b, B, st) : MOCO_OK;
+  for (int l = L - 1; l >= 0; --l) {
+    int32_t *so = l == 0 ? shifts_b : p->sh[l];
+    double *fo = l == 0 ? fmin_b : nullptr;
+    int rc;
+    if (fused_ok(p, l))
+      rc = launch_refine_apply(p, l, img[l], fstride[l], B, p->sh[l + 1], so, fo, l == 0 ? corr_b : nullptr, st);
+    else
+      rc = launch_refine(p, l, img[l], fstride[l], B, p->sh[l + 1], so, fo, st);
+    if (rc) return rc;
+  }
+  if (corr_b && !fused_ok(p, 0)) return launch_apply(p, img[0], corr_b, shifts_b, B, st);
+  return MOCO_OK;
+}
+
 // One internal batch [f0, f0+B) of device frames.
 static int run_batch(moco_plan *p, const void *frames_b, int64_t B, int32_t *shifts_b,
                      double *fmin_b, void *corr_b, uint8_t *flags_b, double *grid_b,
@@ -431,9 +506,19 @@ static int run_batch(moco_plan *p, const void *frames_b, int64_t B, int32_t *shi
     img[l] = p->scratch[l];
     fstride[l] = (int64_t)p->ml[l] * p->pitch[l];
   }
-  for (int l = 0; l < L; ++l) {
+  const bool tc = p->algo == MOCO_ALGO_TC;
+  // the tensor-core search block-sums the level-0 frames itself; only the levels the
+  // refine steps read (1..L-1) are materialised
+  for (int l = 0; l < (tc ? L - 1 : L); ++l) {
     int rc = launch_downsample(p, l, img[l], fstride[l], p->scratch[l + 1], B, st);
     if (rc) return rc;
+  }
+  if (tc) {
+    int rc = grid_b ? launch_tc(p, frames_b, B, nullptr, nullptr, nullptr, grid_b, st)
+                    : launch_tc(p, frames_b, B, L == 0 ? shifts_b : p->sh[L], L == 0 ? fmin_b : nullptr,
+                                flags_b, nullptr, st);
+    if (rc || grid_b) return rc;
+    return refine_levels(p, img, fstride, B, shifts_b, fmin_b, corr_b, st);
   }
   if (grid_b) return launch_coarse(p, img[L], fstride[L], p->pitch[L], B, nullptr, nullptr, grid_b,
                                    nullptr, st);
@@ -441,13 +526,7 @@ static int run_batch(moco_plan *p, const void *frames_b, int64_t B, int32_t *shi
   int rc = launch_coarse(p, img[L], fstride[L], p->pitch[L], B, sc_out, L == 0 ? fmin_b : nullptr,
                          nullptr, flags_b, st);
   if (rc) return rc;
-  for (int l = L - 1; l >= 0; --l) {
-    int32_t *so = l == 0 ? shifts_b : p->sh[l];
-    rc = launch_refine(p, l, img[l], fstride[l], B, p->sh[l + 1], so, l == 0 ? fmin_b : nullptr, st);
-    if (rc) return rc;
-  }
-  if (corr_b) return launch_apply(p, frames_b, corr_b, shifts_b, B, st);
-  return MOCO_OK;
+  return refine_levels(p, img, fstride, B, shifts_b, fmin_b, corr_b, st);
 }
 
 int moco_align_batch(moco_plan *p, const void *d_frames, int64_t T, int32_t *d_shifts,

@@ -26,23 +26,33 @@ def _plan_for(spec, algo=None):
 
 
 # ------------------------------------------------------------- score grid (S1-S4)
-@pytest.mark.parametrize("m,n,levels,w,hi", [
-    (80, 72, 1, 9, 4096),      # coarse 40x36: ragged bands (16-row) and ragged t-groups
-    (64, 48, 0, 11, 4096),
-    (96, 104, 2, 5, 4096),     # two levels, coarse 24x26
-    (40, 40, 0, 20, 65536),    # 16-bit samples: the wide-accumulation kernel
-])
-def test_score_grid_u16_bit_exact(m, n, levels, w, hi):
-    """Every coarse-level f_{s,t} equals the oracle's objective_grid bit for bit."""
-    rng = np.random.default_rng(m * 1000 + n + levels)
+GRID_CASES = [
+    (80, 72, 1, 9, 4096, "direct"),     # coarse 40x36: ragged bands (16-row) and ragged t-groups
+    (64, 48, 0, 11, 4096, "direct"),
+    (96, 104, 2, 5, 4096, "direct"),    # two levels, coarse 24x26
+    (40, 40, 0, 20, 65536, "direct"),   # 16-bit samples: the wide-accumulation kernel
+    (128, 64, 1, 9, 4096, "tc"),        # tensor cores: coarse 64x32, F=4 groups, 3 frames (ragged group)
+    (96, 64, 0, 20, 4096, "tc"),        # W=39 -> 3 M tiles, Wt=48
+    (80, 96, 0, 32, 4096, "tc"),        # W=63, N=128
+    (64, 64, 1, 16, 4096, "tc"),        # C2 geometry (W=31) on a 32x32 coarse image
+    (128, 128, 0, 30, 16384, "tc"),     # 14-bit samples: largest exact int8 split
+]
+
+
+@pytest.mark.parametrize("m,n,levels,w,hi,algo", GRID_CASES)
+def test_score_grid_u16_bit_exact(m, n, levels, w, hi, algo):
+    """Every coarse-level f_{s,t} equals the oracle's objective_grid bit for bit,
+    boundary lags |s|,|t| = w-1 included."""
+    rng = np.random.default_rng(m * 1000 + n + levels + w)
     T = 3
-    bits = 16 if hi > 4096 else 12
+    bits = 16 if hi > 16384 else (14 if hi > 4096 else 12)
     fr = rng.integers(0, hi, size=(T, m, n)).astype(np.uint16)
     tp = rng.integers(0, hi, size=(m, n)).astype(np.uint16)
     fr[1] = pf.translate_zero_fill(tp, 3, -2)
     if bits + 2 * levels > 16:
         pytest.skip("plan rejects bits + 2*levels > 16")
-    p = Plan(m, n, w, levels, "u16", bits, device=0)
+    p = Plan(m, n, w, levels, "u16", bits, device=0, algo=algo)
+    assert p.algo == algo
     p.set_template(torch.from_numpy(tp).to(DEV))
     g = _np(p.score_grid(torch.from_numpy(fr).to(DEV)))
     B = oracle.pyramid(tp, levels)[levels]
@@ -79,6 +89,58 @@ def _run_config(c, T, sample, device_gen=True, algo=None, **over):
         kinds.append(check_frame(_np(frames[k]), tp, spec.w, spec.levels, sh[k], fm[k], _np(co[k]),
                                  exact=spec.dtype == "u16"))
     return spec, st, sh, fm, fl, kinds, p
+
+
+@pytest.mark.parametrize("c,T", [(1, 1000), (2, 2100), (3, 300)])
+def test_tc_equals_direct_whole_stack(c, T):
+    """Tensor-core and CUDA-core coarse searches agree bit for bit on every frame
+    (both are exact integer evaluations of the same N_{s,t})."""
+    spec = config_spec(c, T=T)
+    st = make_stack(spec, 0, T, device=DEV)
+    out = {}
+    for algo in ("tc", "direct"):
+        p = _plan_for(spec, algo)
+        p.set_template(st.template)
+        sh, fm, _, fl = p.align(st.frames, corrected=False, flags=True)
+        out[algo] = (sh, fm, fl)
+    assert torch.equal(out["tc"][0], out["direct"][0])
+    assert torch.equal(out["tc"][1], out["direct"][1])
+    assert torch.equal(out["tc"][2], out["direct"][2])
+
+
+@pytest.mark.parametrize("c,T", [(2, 2100), (4, 24)])
+def test_fused_refine_equals_simple_refine(c, T, monkeypatch):
+    """The fused, register-blocked refine+apply kernel and the simple one-candidate-
+    per-load kernel agree bit for bit on every frame (shifts, f_min, corrected)."""
+    spec = config_spec(c, T=T)
+    st = make_stack(spec, 0, T, device=DEV)
+    out = {}
+    for mode in ("fused", "simple"):
+        if mode == "simple":
+            monkeypatch.setenv("MOCO_REFINE", "simple")
+        p = _plan_for(spec)
+        p.set_template(st.template)
+        sh, fm, co, _ = p.align(st.frames, corrected=True)
+        out[mode] = (sh, fm, co.view(torch.int16))
+    for a, b in zip(out["fused"], out["simple"]):
+        assert torch.equal(a, b)
+
+
+def test_refine_all_alignments():
+    """Refine+apply at every column misalignment of the doubled shift (the fused
+    kernel specialises on (T-1) mod 8): exact translates with dx = -9..9."""
+    spec = config_spec(2, T=1)
+    tp = make_stack(spec, 0, 1).template.numpy()
+    shifts = [(dy, dx) for dx in range(-9, 10) for dy in (-3, 4)]
+    fr = np.stack([pf.translate_zero_fill(tp, dy, dx) for dy, dx in shifts]).astype(np.uint16)
+    rng = np.random.default_rng(3)
+    fr = np.clip(fr.astype(np.int64) + rng.integers(0, 3, fr.shape), 0, 4095).astype(np.uint16)
+    p = Plan(512, 512, 16, 1, "u16", 12, device=0)
+    p.set_template(torch.from_numpy(tp).to(DEV))
+    sh, fm, co, _ = p.align(torch.from_numpy(fr).to(DEV))
+    sh, fm = _np(sh), _np(fm)
+    for k in range(len(shifts)):
+        check_frame(fr[k], tp, 16, 1, sh[k], fm[k], _np(co[k]))
 
 
 def test_config0_all_frames():
