@@ -600,89 +600,145 @@ __device__ __forceinline__ void extract10(const uint4 &lo, const uint4 &hi, uint
   }
 }
 
+// One item = template row i, columns j0..j0+7: all 7 vector loads (b, and the two
+// vectors of each of the 3 frame rows i+S-1..i+S+1, clamped to a valid row when out
+// of range) are issued before any arithmetic; `ITEMS` items per iteration.
+template <int OFFA>
+struct RefineItem {
+  uint4 b, lo[3], hi[3];
+  uint32_t e16[3];
+  int i, j0, base;
+  bool live, fast, rv[3];
+};
+
+template <int OFFA>
+__device__ __forceinline__ void refine_load(const RefineApplyArgs &a, const uint16_t *A, int S, int T, int it,
+                                            int items, int ng, int g0, int ilo, RefineItem<OFFA> &x) {
+  const int ml = a.ml, nl = a.nl;
+  x.live = it < items;
+  const int itc = x.live ? it : 0;
+  x.i = ilo + itc / ng;
+  x.j0 = (g0 + itc % ng) * 8;
+  x.base = x.j0 + T - 1;
+  const int ab = x.base - OFFA;
+  x.fast = ab >= 0 && ab + 16 + (OFFA == 7) <= a.pitch && x.base + 10 <= nl && x.j0 + 8 <= nl;
+  x.b = *reinterpret_cast<const uint4 *>(a.tpl + (int64_t)x.i * a.tpitch + x.j0);
+#pragma unroll
+  for (int u = 0; u < 3; ++u) {
+    const int r = x.i + S + u - 1;
+    x.rv[u] = x.live && r >= 0 && r < ml;
+    if (x.fast) {
+      const uint16_t *arow = A + (int64_t)(x.rv[u] ? r : 0) * a.pitch;
+      x.lo[u] = *reinterpret_cast<const uint4 *>(arow + ab);
+      x.hi[u] = *reinterpret_cast<const uint4 *>(arow + ab + 8);
+      if (OFFA == 7) x.e16[u] = arow[ab + 16];
+    }
+  }
+}
+
+template <int OFFA>
+__device__ __forceinline__ void refine_compute(const RefineApplyArgs &a, const uint16_t *A, int S,
+                                               const RefineItem<OFFA> &x, uint32_t (&acc)[9]) {
+  if (!x.live) return;
+  const int nl = a.nl;
+  const uint32_t bw[4] = {x.b.x, x.b.y, x.b.z, x.b.w};
+  uint32_t bv[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) bv[q] = (bw[q >> 1] >> (16 * (q & 1))) & 0xffffu;
+#pragma unroll
+  for (int u = 0; u < 3; ++u) {
+    if (!x.rv[u]) continue;
+    uint32_t av[10];
+    if (x.fast) {
+      extract10<OFFA>(x.lo[u], x.hi[u], av);
+      if (OFFA == 7) av[9] = x.e16[u];
+#pragma unroll
+      for (int v = 0; v < 3; ++v)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int d = (int)av[q + v] - (int)bv[q];
+          acc[u * 3 + v] += (uint32_t)(d * d);
+        }
+    } else {
+      const uint16_t *arow = A + (int64_t)(x.i + S + u - 1) * a.pitch;
+#pragma unroll
+      for (int q = 0; q < 10; ++q) {
+        const int c = x.base + q;
+        av[q] = (c >= 0 && c < nl) ? arow[c] : 0u;
+      }
+#pragma unroll
+      for (int v = 0; v < 3; ++v)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int c = x.base + q + v;   // frame column of template column j0+q, candidate v
+          if (c < 0 || c >= nl || x.j0 + q >= nl) continue;
+          const int d = (int)av[q + v] - (int)bv[q];
+          acc[u * 3 + v] += (uint32_t)(d * d);
+        }
+    }
+  }
+}
+
+// Items (row, column group) over column groups [g0, g0+ng), two per iteration.
+template <int OFFA>
+__device__ __forceinline__ void refine_span(const RefineApplyArgs &a, const uint16_t *A, int S, int T, int g0,
+                                            int ng, int ilo, int rows, uint32_t (&acc)[9], u64 (&acc64)[9],
+                                            int &cnt) {
+  if (ng <= 0) return;
+  const int items = rows * ng;
+  const int nth = blockDim.x;
+  for (int it = threadIdx.x; it < items; it += 2 * nth) {
+    RefineItem<OFFA> x0, x1;
+    refine_load<OFFA>(a, A, S, T, it, items, ng, g0, ilo, x0);
+    refine_load<OFFA>(a, A, S, T, it + nth, items, ng, g0, ilo, x1);
+    refine_compute<OFFA>(a, A, S, x0, acc);
+    refine_compute<OFFA>(a, A, S, x1, acc);
+    cnt += 2;
+    if (cnt >= a.flush) {
+#pragma unroll
+      for (int c = 0; c < 9; ++c) { acc64[c] += acc[c]; acc[c] = 0; }
+      cnt = 0;
+    }
+  }
+}
+
 template <int OFFA>
 __device__ __forceinline__ void refine_rows(const RefineApplyArgs &a, const uint16_t *A, int S, int T,
                                             u64 (&acc64)[9]) {
   const int ml = a.ml, nl = a.nl;
   const int groups = (nl + 7) >> 3;
   const int ilo = max(0, -S - 1), ihi = min(ml, ml - S + 1);
-  const int items = (ihi - ilo) * groups;
+  // column groups whose fast-path condition holds (it depends on j0 only): warps
+  // stay uniform on the fast path; the few edge groups run in their own loop
+  const int jlo = max(0, OFFA + 1 - T);
+  const int jhi = min(min(a.pitch - 16 - (OFFA == 7) + OFFA + 1 - T, nl - 9 - T), nl - 8);
+  int g_lo = (jlo + 7) >> 3, g_hi = jhi >= 0 ? (jhi >> 3) + 1 : 0;
+  g_lo = min(g_lo, groups);
+  g_hi = max(g_lo, min(g_hi, groups));
   uint32_t acc[9];
 #pragma unroll
   for (int c = 0; c < 9; ++c) acc[c] = 0;
   int cnt = 0;
-  for (int it = threadIdx.x; it < items; it += blockDim.x) {
-    const int i = ilo + it / groups;
-    const int j0 = (it % groups) * 8;
-    const uint4 bq = *reinterpret_cast<const uint4 *>(a.tpl + (int64_t)i * a.tpitch + j0);
-    const uint32_t bw[4] = {bq.x, bq.y, bq.z, bq.w};
-    uint32_t bv[8];
-#pragma unroll
-    for (int x = 0; x < 8; ++x) bv[x] = (bw[x >> 1] >> (16 * (x & 1))) & 0xffffu;
-    const int base = j0 + T - 1;              // frame column of (x=0, v=-1)
-    const int ab = base - OFFA;               // 8-aligned
-    // 10 columns from an 8-aligned start: two vectors, plus one sample when OFFA == 7
-    const bool fast = ab >= 0 && ab + 16 + (OFFA == 7) <= a.pitch && base + 10 <= nl && j0 + 8 <= nl;
-#pragma unroll
-    for (int u = 0; u < 3; ++u) {
-      const int r = i + S + u - 1;
-      if (r < 0 || r >= ml) continue;
-      const uint16_t *arow = A + (int64_t)r * a.pitch;
-      uint32_t av[10];
-      if (fast) {
-        const uint4 lo = *reinterpret_cast<const uint4 *>(arow + ab);
-        const uint4 hi = *reinterpret_cast<const uint4 *>(arow + ab + 8);
-        extract10<OFFA>(lo, hi, av);
-        if (OFFA == 7) av[9] = arow[ab + 16];
-#pragma unroll
-        for (int v = 0; v < 3; ++v)
-#pragma unroll
-          for (int x = 0; x < 8; ++x) {
-            const int d = (int)av[x + v] - (int)bv[x];
-            acc[u * 3 + v] += (uint32_t)(d * d);
-          }
-      } else {
-#pragma unroll
-        for (int x = 0; x < 10; ++x) {
-          const int c = base + x;
-          av[x] = (c >= 0 && c < nl) ? arow[c] : 0u;
-        }
-#pragma unroll
-        for (int v = 0; v < 3; ++v)
-#pragma unroll
-          for (int x = 0; x < 8; ++x) {
-            const int c = base + x + v;   // frame column of template column j0+x, candidate v
-            if (c < 0 || c >= nl || j0 + x >= nl) continue;
-            const int d = (int)av[x + v] - (int)bv[x];
-            acc[u * 3 + v] += (uint32_t)(d * d);
-          }
-      }
-    }
-    if (++cnt == a.flush) {
-#pragma unroll
-      for (int c = 0; c < 9; ++c) {
-        acc64[c] += acc[c];
-        acc[c] = 0;
-      }
-      cnt = 0;
-    }
-  }
+  // flush threshold counts items of 8 pixels; a.flush items fit 32 bits
+  refine_span<OFFA>(a, A, S, T, g_lo, g_hi - g_lo, ilo, ihi - ilo, acc, acc64, cnt);
+  refine_span<OFFA>(a, A, S, T, 0, g_lo, ilo, ihi - ilo, acc, acc64, cnt);
+  refine_span<OFFA>(a, A, S, T, g_hi, groups - g_hi, ilo, ihi - ilo, acc, acc64, cnt);
 #pragma unroll
   for (int c = 0; c < 9; ++c) acc64[c] += acc[c];
 }
 
-template <int OFFT>
-__device__ __forceinline__ void apply_rows(const RefineApplyArgs &a, const uint16_t *A, uint16_t *O, int s,
-                                           int t, int m, int n) {
-  const int groups = n >> 3;   // n % 8 == 0 at level 0
-  for (int it = threadIdx.x; it < m * groups; it += blockDim.x) {
-    const int i = it / groups, j0 = (it % groups) * 8;
+template <int OFFT, bool EDGE>
+__device__ __forceinline__ void apply_span(const RefineApplyArgs &a, const uint16_t *A, uint16_t *O, int s,
+                                           int t, int m, int n, int g0, int ng) {
+  if (ng <= 0) return;
+  for (int it = threadIdx.x; it < m * ng; it += blockDim.x) {
+    const int i = it / ng, j0 = (g0 + it % ng) * 8;
     const int r = i + s;
     uint4 outv = make_uint4(0, 0, 0, 0);
     if (r >= 0 && r < m) {
       const uint16_t *arow = A + (int64_t)r * a.pitch;
       const int base = j0 + t, ab = base - OFFT;
-      if (ab >= 0 && ab + 16 <= n) {
+      if (!EDGE) {
         const uint4 lo = __ldg(reinterpret_cast<const uint4 *>(arow + ab));
         const uint4 hi = OFFT ? __ldg(reinterpret_cast<const uint4 *>(arow + ab + 8)) : lo;
         uint32_t v[10];
@@ -700,6 +756,19 @@ __device__ __forceinline__ void apply_rows(const RefineApplyArgs &a, const uint1
     }
     __stcs(reinterpret_cast<uint4 *>(O + (int64_t)i * n + j0), outv);
   }
+}
+
+template <int OFFT>
+__device__ __forceinline__ void apply_rows(const RefineApplyArgs &a, const uint16_t *A, uint16_t *O, int s,
+                                           int t, int m, int n) {
+  const int groups = n >> 3;   // n % 8 == 0 at level 0
+  // interior chunks: both aligned vectors inside the row
+  const int jlo = max(0, OFFT - t), jhi = n - 16 + OFFT - t;
+  int g_lo = min((jlo + 7) >> 3, groups), g_hi = jhi >= 0 ? (jhi >> 3) + 1 : 0;
+  g_hi = max(g_lo, min(g_hi, groups));
+  apply_span<OFFT, false>(a, A, O, s, t, m, n, g_lo, g_hi - g_lo);
+  apply_span<OFFT, true>(a, A, O, s, t, m, n, 0, g_lo);
+  apply_span<OFFT, true>(a, A, O, s, t, m, n, g_hi, groups - g_hi);
 }
 
 __global__ void __launch_bounds__(256) k_refine_apply(RefineApplyArgs a) {

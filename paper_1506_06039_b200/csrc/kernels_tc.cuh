@@ -43,8 +43,8 @@ struct TcGeom {
   int nstrips;  // 32-column strips of j'
   int planeB;   // bytes per 16-column plane = R * 32 * F
   int stripB;   // 2 planes
-  int OFF, TSW; // template strip: columns [J0-OFF, J0-OFF+TSW)
-  int NS;       // B ring stages (2 batches of NS/2 template rows)
+  int TPAD, TP; // padded template parts: TP = nc + 2*TPAD bytes per row, zeros in the pads
+  int ICH;      // template rows per super-stage (one ring slot per producer warp)
   int GG;       // operand groups per CTA
   int tmem_cols;
   int smem;     // dynamic shared memory bytes
@@ -76,6 +76,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
@@ -313,115 +316,179 @@ struct TcArgs {
   double *grid_out;      // [B][W*W] or null: f for every coarse lag
 };
 
-// One CTA = GG operand groups (GG*F frames) sharing every generated B tile.
-// 256 threads: all generate B tiles for ICH template rows at a time into a ring of
-// NS = 2*ICH stages, thread 0 issues the MMAs of the batch and commits each stage to
-// its `empty` mbarrier, so generation of batch b+1 overlaps the MMAs of batch b.
-__global__ void __launch_bounds__(256, 1) k_tc_coarse(TcArgs a) {
+// One CTA = GG operand groups (GG*F frames), warp-specialised, no block barrier in
+// the main loop.  Work is handed over in super-stages of ICH consecutive template
+// rows (ICH B tiles): one full/empty mbarrier handshake per super-stage.  Super-stage
+// u is built by producer p = u mod 7 into ITS OWN ring slot p: every barrier is then
+// waited on in phase order by exactly one producer and by the MMA warp, so a parity
+// wait can never alias a phase two completions away.
+//   warp 0           MMA issuer (warp-uniform loop, one elected lane issues): per
+//                    32-column strip one bulk copy per group, then per super-stage
+//                    wait full[ss], issue ICH*GG*NT MMAs, commit to empty[ss];
+//   warps 1..7       producers: warp p builds super-stages u == p-1 (mod 7) straight
+//                    from the zero-padded template parts in global memory (L1/L2
+//                    resident), then arrives on full[ss].
+// Producers depend only on the template, so they run up to NSS super-stages ahead,
+// across strip boundaries; the strip reload stall is covered by the second CTA on
+// the SM.
+constexpr int TC_THREADS = 256;
+constexpr int TC_PRODUCERS = 7;
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+template <int CPL>   // B chunks (16 bytes) per producer lane per tile = 2N/32
+__global__ void __launch_bounds__(TC_THREADS, 2) k_tc_coarse(TcArgs a) {
   const TcGeom &g = a.g;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char *smem = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nth = blockDim.x;
-  const int F = g.F, hw = g.hw, mc = g.mc, nc = g.nc, N = g.N, NT = g.NT, NS = g.NS, GG = g.GG;
-  const int ICH = NS / 2;
+  unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int F = g.F, hw = g.hw, mc = g.mc, nc = g.nc, N = g.N, NT = g.NT, GG = g.GG;
+  constexpr int NSS = TC_PRODUCERS;                            // one ring slot per producer warp
+  const int ICH = g.ICH;
   unsigned char *As = smem;                                   // [GG] strips of 2 planes
-  unsigned char *TS = As + GG * g.stripB;                     // [2][mc][TSW]
-  unsigned char *Bring = TS + 2 * mc * g.TSW;                 // [NS][N*32]
-  uint64_t *bars = reinterpret_cast<uint64_t *>(Bring + NS * N * 32);   // empty[NS], aload
-  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + NS + 1);
+  unsigned char *Bring = As + GG * g.stripB;                  // [NSS][ICH][N*32]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(Bring + NSS * ICH * N * 32);
+  uint64_t *full = bars, *empty = bars + NSS, *aload = bars + 2 * NSS;
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * NSS + 1);
   Key *keys = reinterpret_cast<Key *>(smem);                 // epilogue: aliases the strips
   const int grp0 = blockIdx.x * GG;
   const int ngroups = (a.B + F - 1) / F;
   const int gcount = min(GG, ngroups - grp0);
+  const int nsuper = g.nstrips * (mc / ICH);
 
   if (warp == 0) tmem_alloc(tmem_holder, g.tmem_cols);
   if (tid == 0) {
-    for (int s = 0; s < NS + 1; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < NSS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(aload, 1);
     fence_mbar_init();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t taddr = *tmem_holder;
-  const uint32_t idesc = idesc_i8(128, N);
-  const uint32_t As_u = smem_u32(As);
-  const uint32_t B_u = smem_u32(Bring);
-  uint64_t *aload = &bars[NS];
 
-  int it = 0;
-  for (int st = 0; st < g.nstrips; ++st) {
-    const int J0 = st * 32;
-    if (tid == 0) {
-      mbar_arrive_expect_tx(aload, (uint32_t)(gcount * g.stripB));
-      for (int gg = 0; gg < gcount; ++gg)
-        bulk_g2s(As + gg * g.stripB, a.G + ((int64_t)(grp0 + gg) * g.nstrips + st) * g.stripB,
-                 (uint32_t)g.stripB, aload);
-    }
-    // template strip: TS[pb][i][x] = b_pb[i][J0 - OFF + x] (0 outside the image)
-    {
-      const int vec = g.TSW / 16;
-      const int total = 2 * mc * vec;
-      for (int e = tid; e < total; e += nth) {
-        const int x16 = e % vec;
-        const int row = e / vec;   // pb*mc + i
-        const int col = J0 - g.OFF + x16 * 16;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (col >= 0 && col + 16 <= nc) v = *reinterpret_cast<const uint4 *>(a.T8 + (int64_t)row * nc + col);
-        *reinterpret_cast<uint4 *>(TS + row * g.TSW + x16 * 16) = v;
+  if (warp == 0) {
+    // ---------------- MMA issuer (whole warp walks the loop; one lane issues)
+    const uint32_t idesc = idesc_i8(128, N);
+    const uint64_t bdesc0 = umma_desc(smem_u32(Bring), 128, 256);
+    const uint64_t adesc0 = umma_desc(smem_u32(As), g.planeB, 128);
+    const uint32_t rowstep = (32 * F) >> 4;          // descriptor units per plane row
+    const uint32_t tilestep = (N * 32) >> 4;         // descriptor units per B tile
+    const uint32_t groupstep = g.stripB >> 4;
+    int su = 0, ss = 0, round = 0;      // super-stage, its slot (= producer), slot use
+    int pss = NSS - 1, pround = -1;      // slot/round of the previous super-stage
+    for (int st = 0; st < g.nstrips; ++st) {
+      if (st > 0) {   // all MMAs of the previous strip done -> strip buffers free
+        mbar_wait(&empty[pss], pround & 1);
       }
-    }
-    mbar_wait(aload, st & 1);
-    __syncthreads();
-    for (int i0 = 0; i0 < mc; i0 += ICH) {
-      const int nI = min(ICH, mc - i0);
-      // ring slots of this batch must have been consumed by the MMAs of batch-2
-      for (int q = 0; q < nI; ++q) {
-        const int j = it + q;
-        if (j >= NS) mbar_wait(&bars[j % NS], ((j / NS) - 1) & 1);
+      if (elect_one()) {
+        mbar_arrive_expect_tx(aload, (uint32_t)(gcount * g.stripB));
+        for (int gg = 0; gg < gcount; ++gg)
+          bulk_g2s(As + gg * g.stripB, a.G + ((int64_t)(grp0 + gg) * g.nstrips + st) * g.stripB,
+                   (uint32_t)g.stripB, aload);
       }
-      // B tiles: N rows (pb, t) x 32 bytes: B[(pb,t)][k] = b_pb[i][J0 + k - t]
-      for (int c = tid; c < nI * 2 * N; c += nth) {
-        const int q = c / (2 * N), cc = c % (2 * N);
-        const int n = cc >> 1, h = cc & 1;
-        const int pb = n / g.Wt, ti = n % g.Wt;
-        unsigned char *Bt = Bring + ((it + q) % NS) * N * 32;
-        uint4 outv = make_uint4(0, 0, 0, 0);
-        if (ti < g.W) {
-          const int o = 16 * h - (ti - hw) + g.OFF;
-          const uint32_t *wp =
-              reinterpret_cast<const uint32_t *>(TS + (pb * mc + i0 + q) * g.TSW + (o & ~3));
-          const uint32_t sh = (o & 3) * 8;
-          const uint32_t w0 = wp[0], w1 = wp[1], w2 = wp[2], w3 = wp[3], w4 = wp[4];
-          outv.x = __funnelshift_r(w0, w1, sh);
-          outv.y = __funnelshift_r(w1, w2, sh);
-          outv.z = __funnelshift_r(w2, w3, sh);
-          outv.w = __funnelshift_r(w3, w4, sh);
+      __syncwarp();
+      mbar_wait(aload, st & 1);
+      tc_fence_after();
+      for (int i0 = 0; i0 < mc; i0 += ICH, ++su) {
+        mbar_wait(&full[ss], round & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          uint64_t bdesc = bdesc0 + (uint64_t)(ss * ICH) * tilestep;
+          for (int q = 0; q < ICH; ++q, bdesc += tilestep) {
+            const uint32_t acc = (st | (i0 + q)) != 0 ? 1u : 0u;
+            uint64_t adesc_g = adesc0 + (uint64_t)(i0 + q) * rowstep;
+            uint32_t tcol = taddr;
+            for (int gg = 0; gg < gcount; ++gg, adesc_g += groupstep) {
+              uint64_t adesc = adesc_g;
+              for (int k = 0; k < NT; ++k, adesc += (uint64_t)g.ST * rowstep, tcol += N)
+                mma_i8(tcol, adesc, bdesc, idesc, acc);
+            }
+          }
+          mma_commit(&empty[ss]);
         }
-        *reinterpret_cast<uint4 *>(Bt + (n >> 3) * 256 + h * 128 + (n & 7) * 16) = outv;
+        __syncwarp();
+        pss = ss;
+        pround = round;
+        if (++ss == NSS) { ss = 0; ++round; }
+      }
+    }
+  } else {
+    // ---------------- B producers
+    const int p = warp - 1;
+    // per-lane chunk geometry is the same for every tile: chunk cc = lane + 32q ->
+    // B row n = cc/2 = (pb, t), 16-byte half h = cc%2
+    int srcoff[CPL], dstoff[CPL];
+    bool live[CPL];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      const int cc = lane + 32 * q;
+      const int n = cc >> 1, h = cc & 1;
+      const int pb = n >= g.Wt ? 1 : 0, ti = n - pb * g.Wt;
+      live[q] = ti < g.W;
+      // bytes b_pb[i][J0 + 16h - t + x], x = 0..15, from the 4-aligned word below
+      const int col = 16 * h - (ti - hw) + g.TPAD;          // + J0, in the padded row
+      srcoff[q] = pb * mc * g.TP + col;
+      dstoff[q] = (n >> 3) * 256 + h * 128 + (n & 7) * 16;
+    }
+    const int per_strip = mc / ICH;
+    int st = p / per_strip, i0 = (p % per_strip) * ICH;
+    const int ss = p;
+    int round = 0;
+    for (int u = p; u < nsuper; u += TC_PRODUCERS, ++round) {
+      if (round > 0) mbar_wait(&empty[ss], (round - 1) & 1);
+      unsigned char *Bs = Bring + ss * ICH * N * 32;
+      for (int q = 0; q < ICH; ++q) {
+        const uint8_t *rowbase = a.T8 + (int64_t)(i0 + q) * g.TP + st * 32;
+        uint32_t wv[CPL][5];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const uint32_t *wp = reinterpret_cast<const uint32_t *>(rowbase + (srcoff[c] & ~3));
+#pragma unroll
+          for (int e = 0; e < 5; ++e) wv[c][e] = __ldg(wp + e);
+        }
+        unsigned char *Bt = Bs + q * N * 32;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const uint32_t sh = (srcoff[c] & 3) * 8;
+          uint4 outv = make_uint4(0, 0, 0, 0);
+          if (live[c]) {
+            outv.x = __funnelshift_r(wv[c][0], wv[c][1], sh);
+            outv.y = __funnelshift_r(wv[c][1], wv[c][2], sh);
+            outv.z = __funnelshift_r(wv[c][2], wv[c][3], sh);
+            outv.w = __funnelshift_r(wv[c][3], wv[c][4], sh);
+          }
+          *reinterpret_cast<uint4 *>(Bt + dstoff[c]) = outv;
+        }
       }
       fence_proxy_async();
-      __syncthreads();
-      if (tid == 0) {
-        tc_fence_after();
-        for (int q = 0; q < nI; ++q) {
-          const int stage = (it + q) % NS;
-          const int i = i0 + q;
-          const uint64_t bdesc = umma_desc(B_u + stage * N * 32, 128, 256);
-          for (int gg = 0; gg < gcount; ++gg)
-            for (int k = 0; k < NT; ++k) {
-              const uint64_t adesc =
-                  umma_desc(As_u + gg * g.stripB + (i + k * g.ST) * 32 * F, g.planeB, 128);
-              mma_i8(taddr + (gg * NT + k) * N, adesc, bdesc, idesc, (st | i) != 0 ? 1u : 0u);
-            }
-          mma_commit(&bars[stage]);
-        }
-      }
-      it += nI;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[ss]);
+      // next super-stage of this warp: TC_PRODUCERS super-stages later
+      i0 += TC_PRODUCERS * ICH;
+      while (i0 >= mc) { i0 -= mc; ++st; }
     }
-    // every MMA of this strip has completed before the strip buffers are reused
-    const int last = it - 1;
-    mbar_wait(&bars[last % NS], (last / NS) & 1);
   }
+  // all MMAs done -> accumulators final.  Every warp must be converged before the
+  // .sync.aligned TMEM loads (threads can leave the mbarrier spin at different times).
+  {
+    const int last = nsuper - 1;
+    mbar_wait(&empty[last % NSS], (last / NSS) & 1);
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
   tc_fence_after();
 
   // ---- epilogue: h -> N -> f -> argmin (S4), per frame.  Warp w reads TMEM lanes
@@ -448,12 +515,12 @@ __global__ void __launch_bounds__(256, 1) k_tc_coarse(TcArgs a) {
         tmem_ld16(tbase + g.Wt + c, xl);      // pb = lo
         tmem_wait_ld();
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const uint32_t ph = __shfl_xor_sync(0xffffffffu, xh[q], 1);   // partner row: pa = lo
-          const uint32_t pl = __shfl_xor_sync(0xffffffffu, xl[q], 1);
-          const int ti = c + q;
+        for (int qq = 0; qq < 16; ++qq) {
+          const uint32_t ph = __shfl_xor_sync(0xffffffffu, xh[qq], 1);   // partner row: pa = lo
+          const uint32_t pl = __shfl_xor_sync(0xffffffffu, xl[qq], 1);
+          const int ti = c + qq;
           if (!valid || ti >= W) continue;
-          const u64 h = ((u64)xh[q] << 14) + (((u64)xl[q] + (u64)ph) << 7) + (u64)pl;
+          const u64 h = ((u64)xh[qq] << 14) + (((u64)xl[qq] + (u64)ph) << 7) + (u64)pl;
           const int lag = (s + hw) * W + ti;
           const u64 Nn = a.ga[(int64_t)fi * W * W + lag] + a.gb[lag] - 2 * h;
           const int t = ti - hw;
@@ -494,13 +561,19 @@ __global__ void __launch_bounds__(256, 1) k_tc_coarse(TcArgs a) {
   if (warp == 0) tmem_dealloc(taddr, g.tmem_cols);
 }
 
-// template parts for the B operand: T8[0] = b >> 7, T8[1] = b & 127 (coarse template)
-__global__ void k_tc_template(const uint16_t *__restrict__ b, int pitch, int mc, int nc, uint8_t *T8) {
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < mc * nc; e += gridDim.x * blockDim.x) {
-    const int i = e / nc, j = e % nc;
-    const uint32_t v = b[(int64_t)i * pitch + j];
-    T8[e] = (uint8_t)(v >> 7);
-    T8[mc * nc + e] = (uint8_t)(v & 127u);
+// template parts for the B operand, zero-padded rows: T8[pb][i][TPAD + j] =
+// (b >> 7, b & 127)[pb] for j in [0, nc), 0 in the pads
+__global__ void k_tc_template(const uint16_t *__restrict__ b, int pitch, int mc, int nc, int TPAD, int TP,
+                              uint8_t *T8) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 2 * mc * TP; e += gridDim.x * blockDim.x) {
+    const int pb = e / (mc * TP), r = e % (mc * TP);
+    const int i = r / TP, j = r % TP - TPAD;
+    uint8_t v = 0;
+    if (j >= 0 && j < nc) {
+      const uint32_t x = b[(int64_t)i * pitch + j];
+      v = (uint8_t)(pb == 0 ? (x >> 7) : (x & 127u));
+    }
+    T8[e] = v;
   }
 }
 
@@ -524,20 +597,21 @@ inline bool tc_make_geom(TcGeom *gp, int w, int mc, int nc, int L) {
   g.nstrips = (nc + 31) / 32;
   g.planeB = g.R * 32 * g.F;
   g.stripB = 2 * g.planeB;
-  g.OFF = (g.hw + 15) / 16 * 16;
-  g.TSW = (16 + g.hw + g.OFF + 20 + 15) / 16 * 16;
-  auto smem_for = [&](int GG, int NS) {
-    return 1024 + GG * g.stripB + 2 * mc * g.TSW + NS * g.N * 32 + (NS + 1) * 8 + 16;
+  g.TPAD = (g.hw + 8 + 15) / 16 * 16;
+  g.TP = nc + 2 * g.TPAD;
+  auto smem_for = [&](int GG, int ICH) {
+    return 1024 + GG * g.stripB + TC_PRODUCERS * ICH * g.N * 32 + (2 * TC_PRODUCERS + 1) * 8 + 16;
   };
-  // as many groups per CTA as shared memory (227 KB) and TMEM (512 columns) allow
-  g.NS = 16;
+  // two CTAs per SM (one loads its next strip while the other computes): as many
+  // groups per CTA as half of shared memory and half of TMEM allow, then the
+  // largest super-stage (ICH | mc) that still fits
   g.GG = 0;
-  for (int GG = 8; GG >= 1 && !g.GG; --GG) {
-    if (GG * g.NT * g.N > 512) continue;
-    for (int NS = 16; NS >= 4; NS -= 4)
-      if (smem_for(GG, NS) <= 227 * 1024 && GG * 128 * 16 <= GG * g.stripB) {
+  for (int GG = 4; GG >= 1 && !g.GG; --GG) {
+    if (GG * g.NT * g.N > 256) continue;
+    for (int ICH = 4; ICH >= 1; ICH /= 2)
+      if (mc % ICH == 0 && smem_for(GG, ICH) <= 113 * 1024 && GG * 128 * 16 <= GG * g.stripB) {
         g.GG = GG;
-        g.NS = NS;
+        g.ICH = ICH;
         break;
       }
   }
@@ -545,7 +619,7 @@ inline bool tc_make_geom(TcGeom *gp, int w, int mc, int nc, int L) {
   int cols = 32;
   while (cols < g.GG * g.NT * g.N) cols <<= 1;
   g.tmem_cols = cols;
-  g.smem = smem_for(g.GG, g.NS);
+  g.smem = smem_for(g.GG, g.ICH);
   g.prep_smem = (g.F * (4 * g.hw + 4 * w * w + 1)) * 8;
   *gp = g;
   return true;
@@ -567,8 +641,15 @@ inline int tc_init(TcPlan *tc, int w, int mc, int nc, int L, int64_t cap) {
   const int64_t groups = (cap + g.F - 1) / g.F;
   if (cudaMalloc(&tc->G, (size_t)groups * g.nstrips * g.stripB) != cudaSuccess) return -1;
   if (cudaMalloc(&tc->ga, (size_t)cap * g.W * g.W * sizeof(u64)) != cudaSuccess) return -1;
-  if (cudaMalloc(&tc->T8, (size_t)2 * mc * nc) != cudaSuccess) return -1;
-  if (cudaFuncSetAttribute(k_tc_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess)
+  if (cudaMalloc(&tc->T8, (size_t)2 * mc * g.TP) != cudaSuccess) return -1;
+  if (cudaFuncSetAttribute(k_tc_coarse<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
+      cudaFuncSetAttribute(k_tc_coarse<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
+      cudaFuncSetAttribute(k_tc_coarse<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
+      cudaFuncSetAttribute(k_tc_coarse<14>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
+      cudaFuncSetAttribute(k_tc_coarse<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
+      cudaFuncSetAttribute(k_tc_coarse<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
+      cudaFuncSetAttribute(k_tc_coarse<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
+      cudaFuncSetAttribute(k_tc_coarse<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess)
     return -1;
   if (cudaFuncSetAttribute(k_tc_prep<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.prep_smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_tc_prep<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.prep_smem) != cudaSuccess ||
@@ -580,7 +661,7 @@ inline int tc_init(TcPlan *tc, int w, int mc, int nc, int L, int64_t cap) {
 
 inline int tc_set_template(TcPlan *tc, const uint16_t *tpl_coarse, int pitch, cudaStream_t st) {
   const TcGeom &g = tc->g;
-  k_tc_template<<<64, 256, 0, st>>>(tpl_coarse, pitch, g.mc, g.nc, tc->T8);
+  k_tc_template<<<128, 256, 0, st>>>(tpl_coarse, pitch, g.mc, g.nc, g.TPAD, g.TP, tc->T8);
   if (cudaGetLastError() != cudaSuccess) return -1;
   tc->tpl_ready = true;
   return 0;

@@ -467,7 +467,17 @@ static int launch_tc(moco_plan *p, const void *frames_b, int64_t B, int32_t *shi
   ta.shift_out = shift_out; ta.f_out = f_out; ta.flags = flags; ta.grid_out = grid_out;
   {
     ProfScope ps(p, MOCO_K_COARSE, st);
-    k_tc_coarse<<<(unsigned)((groups + g.GG - 1) / g.GG), 256, g.smem, st>>>(ta);
+    const unsigned grid = (unsigned)((groups + g.GG - 1) / g.GG);
+    switch (g.N / 16) {   // chunks per producer lane = 2N/32
+      case 2: k_tc_coarse<2><<<grid, TC_THREADS, g.smem, st>>>(ta); break;
+      case 4: k_tc_coarse<4><<<grid, TC_THREADS, g.smem, st>>>(ta); break;
+      case 10: k_tc_coarse<10><<<grid, TC_THREADS, g.smem, st>>>(ta); break;
+      case 14: k_tc_coarse<14><<<grid, TC_THREADS, g.smem, st>>>(ta); break;
+      case 6: k_tc_coarse<6><<<grid, TC_THREADS, g.smem, st>>>(ta); break;
+      case 8: k_tc_coarse<8><<<grid, TC_THREADS, g.smem, st>>>(ta); break;
+      case 12: k_tc_coarse<12><<<grid, TC_THREADS, g.smem, st>>>(ta); break;
+      default: k_tc_coarse<16><<<grid, TC_THREADS, g.smem, st>>>(ta); break;
+    }
   }
   p->launches++;
   CKL("k_tc_coarse");
