@@ -122,6 +122,29 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Warp-uniform variants: every lane executes the asm, one elected lane issues.
+// Descriptors are passed as (low word, high word); only the low word (start
+// address) changes inside the main loop.
+__device__ __forceinline__ void mma_i8_elect(uint32_t tmem_d, uint32_t alo, uint32_t ahi, uint32_t blo,
+                                             uint32_t bhi, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 da, db;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %7, 0;\n\t"
+      "mov.b64 da, {%1, %2};\n\t"
+      "mov.b64 db, {%3, %4};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], da, db, %5, p;\n\t}" ::"r"(tmem_d),
+      "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "r"(0), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_elect(uint64_t *bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -379,45 +402,52 @@ __global__ void __launch_bounds__(TC_THREADS, 2) k_tc_coarse(TcArgs a) {
   const uint32_t taddr = *tmem_holder;
 
   if (warp == 0) {
-    // ---------------- MMA issuer (whole warp walks the loop; one lane issues)
+    // ---------------- MMA issuer (whole warp walks the loop, warp-uniform; the
+    // elect is inside the asm so no per-instruction ELECT loop is generated)
     const uint32_t idesc = idesc_i8(128, N);
-    const uint64_t bdesc0 = umma_desc(smem_u32(Bring), 128, 256);
-    const uint64_t adesc0 = umma_desc(smem_u32(As), g.planeB, 128);
-    const uint32_t rowstep = (32 * F) >> 4;          // descriptor units per plane row
-    const uint32_t tilestep = (N * 32) >> 4;         // descriptor units per B tile
-    const uint32_t groupstep = g.stripB >> 4;
-    int su = 0, ss = 0, round = 0;      // super-stage, its slot (= producer), slot use
-    int pss = NSS - 1, pround = -1;      // slot/round of the previous super-stage
-    for (int st = 0; st < g.nstrips; ++st) {
-      if (st > 0) {   // all MMAs of the previous strip done -> strip buffers free
-        mbar_wait(&empty[pss], pround & 1);
-      }
+    const uint64_t bd0 = umma_desc(smem_u32(Bring), 128, 256);
+    const uint64_t ad0 = umma_desc(smem_u32(As), g.planeB, 128);
+    const uint32_t blo0 = (uint32_t)bd0, bhi = (uint32_t)(bd0 >> 32);
+    const uint32_t alo0 = (uint32_t)ad0, ahi = (uint32_t)(ad0 >> 32);
+    const uint32_t rowstep = (32u * F) >> 4;         // descriptor units per plane row
+    const uint32_t tilestep = (uint32_t)(N * 32) >> 4;
+    const uint32_t sstep = (uint32_t)ICH * tilestep;
+    // per-MMA (group gg, M tile k) A offsets and TMEM columns, j = gg*NT + k < 4
+    const int ntg = gcount * NT;
+    uint32_t aoff[4], tcol[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gg = j / NT, k = j % NT;
+      aoff[j] = (uint32_t)(gg * g.stripB >> 4) + (uint32_t)(k * g.ST) * rowstep;
+      tcol[j] = taddr + (uint32_t)(j * N);
+    }
+    const int nst = g.nstrips;
+    const int per_strip = mc / ICH;
+    int ss = 0, round = 0;              // slot (= producer) and slot use of the super-stage
+    int pss = NSS - 1, pround = -1;     // of the previous super-stage
+    for (int st = 0; st < nst; ++st) {
+      if (st > 0) mbar_wait(&empty[pss], pround & 1);   // strip buffers free
       if (elect_one()) {
         mbar_arrive_expect_tx(aload, (uint32_t)(gcount * g.stripB));
         for (int gg = 0; gg < gcount; ++gg)
-          bulk_g2s(As + gg * g.stripB, a.G + ((int64_t)(grp0 + gg) * g.nstrips + st) * g.stripB,
+          bulk_g2s(As + gg * g.stripB, a.G + ((int64_t)(grp0 + gg) * nst + st) * g.stripB,
                    (uint32_t)g.stripB, aload);
       }
       __syncwarp();
       mbar_wait(aload, st & 1);
       tc_fence_after();
-      for (int i0 = 0; i0 < mc; i0 += ICH, ++su) {
+      uint32_t arow = alo0;             // A descriptor low word at template row i
+      for (int u = 0; u < per_strip; ++u) {
         mbar_wait(&full[ss], round & 1);
         tc_fence_after();
-        if (elect_one()) {
-          uint64_t bdesc = bdesc0 + (uint64_t)(ss * ICH) * tilestep;
-          for (int q = 0; q < ICH; ++q, bdesc += tilestep) {
-            const uint32_t acc = (st | (i0 + q)) != 0 ? 1u : 0u;
-            uint64_t adesc_g = adesc0 + (uint64_t)(i0 + q) * rowstep;
-            uint32_t tcol = taddr;
-            for (int gg = 0; gg < gcount; ++gg, adesc_g += groupstep) {
-              uint64_t adesc = adesc_g;
-              for (int k = 0; k < NT; ++k, adesc += (uint64_t)g.ST * rowstep, tcol += N)
-                mma_i8(tcol, adesc, bdesc, idesc, acc);
-            }
-          }
-          mma_commit(&empty[ss]);
+        uint32_t blo = blo0 + (uint32_t)ss * sstep;
+        for (int q = 0; q < ICH; ++q, blo += tilestep, arow += rowstep) {
+          const uint32_t acc = (st | u | q) != 0 ? 1u : 0u;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (j < ntg) mma_i8_elect(tcol[j], arow + aoff[j], ahi, blo, bhi, idesc, acc);
         }
+        mma_commit_elect(&empty[ss]);
         __syncwarp();
         pss = ss;
         pround = round;
@@ -607,7 +637,7 @@ inline bool tc_make_geom(TcGeom *gp, int w, int mc, int nc, int L) {
   // largest super-stage (ICH | mc) that still fits
   g.GG = 0;
   for (int GG = 4; GG >= 1 && !g.GG; --GG) {
-    if (GG * g.NT * g.N > 256) continue;
+    if (GG * g.NT * g.N > 256 || GG * g.NT > 4) continue;
     for (int ICH = 4; ICH >= 1; ICH /= 2)
       if (mc % ICH == 0 && smem_for(GG, ICH) <= 113 * 1024 && GG * 128 * 16 <= GG * g.stripB) {
         g.GG = GG;
