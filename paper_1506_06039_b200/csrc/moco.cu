@@ -45,6 +45,8 @@ struct moco_plan {
   size_t esz[3];              // element size per level
   void *tpl[3];               // template pyramid
   void *gb;                   // W*W template energies (u64 or double)
+  u64 *cb[3];                 // refine levels: template column prefix of b^2 [(ml+1)][nl]
+  int rpad[3];                // refine levels: zero columns staged each side of a frame row
   int64_t cap;                // frames per internal batch
   void *scratch[3];           // frame pyramid levels 1..L for one batch
   int32_t *sh[3];             // per-level shifts for one batch
@@ -144,6 +146,8 @@ static void plan_free(moco_plan *p) {
     if (p->sh[l]) cudaFree(p->sh[l]);
   }
   if (p->gb) cudaFree(p->gb);
+  for (int l = 0; l < 3; ++l)
+    if (p->cb[l]) cudaFree(p->cb[l]);
   tc_free(&p->tc);
   for (int k = 0; k < 2; ++k) {
     if (p->slot_in[k]) cudaFree(p->slot_in[k]);
@@ -220,6 +224,12 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
   for (int l = 1; l <= levels; ++l)
     alloc(&p->scratch[l], (size_t)p->cap * p->ml[l] * p->pitch[l] * p->esz[l]);
   for (int l = 0; l <= levels; ++l) alloc((void **)&p->sh[l], (size_t)p->cap * 2 * sizeof(int32_t));
+  if (dtype == MOCO_U16)
+    for (int l = 0; l < levels; ++l) {
+      alloc((void **)&p->cb[l], (size_t)(p->ml[l] + 1) * p->nl[l] * sizeof(u64));
+      // |T| at level l <= 2^(L-l) * w (doubled shift from the level above)
+      p->rpad[l] = ((w << (levels - l)) + 10 + 7) / 8 * 8;
+    }
   if (rc != MOCO_OK) { plan_free(p); return rc; }
   p->algo = MOCO_ALGO_DIRECT;
   if (tc_supported(p->dtype, p->bits, p->levels, p->w, p->ml[levels], p->nl[levels]) &&
@@ -376,11 +386,19 @@ static int launch_refine_apply(moco_plan *p, int l, const void *img, int64_t fst
   a.scale = (double)(1u << (4 * l));
   a.B = (int)B; a.shift_in = sin; a.shift_out = sout; a.f_out = fout;
   a.corrected = (uint16_t *)corr;
+  a.pad = p->rpad[l];
+  a.cb = p->cb[l];
   const double dmax = (double)((1u << vb) - 1);
   a.flush = (int)std::min(1024.0, std::floor(4294967295.0 / (8.0 * dmax * dmax)));
   {
     ProfScope ps(p, MOCO_K_REFINE, st);
-    k_refine_apply<<<(unsigned)B, 256, 0, st>>>(a);
+    const int smem = 2 * (2 * REF_RB + 2) * (p->nl[l] + 2 * p->rpad[l] + 8) * 2;
+    static int attr_smem = 0;
+    if (smem > attr_smem) {
+      CK(cudaFuncSetAttribute(k_refine_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr_smem = smem;
+    }
+    k_refine_apply<<<(unsigned)B, 256, smem, st>>>(a);
   }
   p->launches++;
   CKL("k_refine_apply");
@@ -388,7 +406,13 @@ static int launch_refine_apply(moco_plan *p, int l, const void *img, int64_t fst
 }
 
 static bool fused_ok(const moco_plan *p, int l) {
-  return !p->simple_refine && p->dtype == MOCO_U16 && p->bits + 2 * l <= 14;
+  if (p->simple_refine || p->dtype != MOCO_U16 || p->bits + 2 * l > 14) return false;
+  // 32-bit partial sums must hold one band's items per thread (see refine_rows)
+  const double dmax = (double)((1u << (p->bits + 2 * l)) - 1);
+  const double flush = std::floor(4294967295.0 / (8.0 * dmax * dmax));
+  const int per_band = ((p->nl[l] + 7) / 8 + 31) / 32;
+  const size_t smem = 2 * (2 * REF_RB + 2) * (size_t)(p->nl[l] + 2 * p->rpad[l] + 8) * 2;
+  return flush >= per_band && p->nl[l] % 8 == 0 && smem <= 200 * 1024;
 }
 
 static int launch_apply(moco_plan *p, const void *in, void *out, const int32_t *sh, int64_t B,
@@ -429,6 +453,12 @@ int moco_set_template(moco_plan *p, const void *d_template, moco_stream_t stream
     k_template_energy<double><<<p->W * p->W, 256, 0, st>>>(
         (const double *)p->tpl[L], p->pitch[L], p->ml[L], p->nl[L], p->w, (double *)p->gb);
   CKL("k_template_energy");
+  if (p->dtype == MOCO_U16)
+    for (int l = 0; l < L; ++l) {
+      k_colprefix_u16<<<(p->nl[l] + 127) / 128, 128, 0, st>>>((const uint16_t *)p->tpl[l], p->pitch[l],
+                                                                p->ml[l], p->nl[l], p->cb[l]);
+      CKL("k_colprefix_u16");
+    }
   if (p->tc.ready) {
     if (tc_set_template(&p->tc, (const uint16_t *)p->tpl[L], p->pitch[L], st) != 0)
       return set_cuda_err(cudaGetLastError(), "tc_set_template");
