@@ -186,6 +186,48 @@ struct TcPrepArgs {
 
 // One CTA per operand group of F frames.  Shared: per frame, edge-row and edge-column
 // sums of a^2, the four (hw+1)^2 corner tables and the total.
+// Coarse values of 16 consecutive coarse columns as 8 pair-words P[k] = v[2k] | v[2k+1]<<16.
+// L=0: the raw words are the pairs.  L=1: rows 2r and 2r+1 are added word-wise (each
+// 16-bit half < 2^13, no carry), then the two halves of each word (raw columns 2c,
+// 2c+1 of coarse column c) are folded with two byte-permutes and one add.
+template <int L>
+__device__ __forceinline__ void coarse_pairs(const uint16_t *base, int n, uint32_t (&P)[8]) {
+  if constexpr (L == 0) {
+    const uint4 u0 = *reinterpret_cast<const uint4 *>(base);
+    const uint4 u1 = *reinterpret_cast<const uint4 *>(base + 8);
+    P[0] = u0.x; P[1] = u0.y; P[2] = u0.z; P[3] = u0.w;
+    P[4] = u1.x; P[5] = u1.y; P[6] = u1.z; P[7] = u1.w;
+  } else if constexpr (L == 1) {
+    uint32_t s[16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 x = *reinterpret_cast<const uint4 *>(base + q * 8);
+      const uint4 y = *reinterpret_cast<const uint4 *>(base + n + q * 8);
+      s[4 * q + 0] = x.x + y.x; s[4 * q + 1] = x.y + y.y;
+      s[4 * q + 2] = x.z + y.z; s[4 * q + 3] = x.w + y.w;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      P[k] = __byte_perm(s[2 * k], s[2 * k + 1], 0x5410) + __byte_perm(s[2 * k], s[2 * k + 1], 0x7632);
+  } else {
+    uint32_t v[16];
+#pragma unroll
+    for (int x = 0; x < 16; ++x) v[x] = 0;
+    constexpr int bs = 1 << L;
+#pragma unroll
+    for (int dy = 0; dy < bs; ++dy)
+#pragma unroll
+      for (int q = 0; q < 2 * bs; ++q) {
+        const uint4 u = *reinterpret_cast<const uint4 *>(base + (int64_t)dy * n + q * 8);
+        const uint32_t ws[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[(q * 8 + e) / bs] += (ws[e >> 1] >> (16 * (e & 1))) & 0xffffu;
+      }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) P[k] = v[2 * k] | (v[2 * k + 1] << 16);
+  }
+}
+
 template <int L>
 __global__ void __launch_bounds__(256) k_tc_prep(TcPrepArgs a) {
   const TcGeom &g = a.g;
@@ -200,93 +242,82 @@ __global__ void __launch_bounds__(256) k_tc_prep(TcPrepArgs a) {
   for (int k = tid; k < F * (4 * hw + 4 * CS + 1); k += nth) rowE[k] = 0;
   __syncthreads();
   const int grp = blockIdx.x;
-  const int items = g.nstrips * 2 * g.R * F;
   constexpr int bs = 1 << L;
-  u64 mytot[4] = {0, 0, 0, 0};
-  for (int it = tid; it < items; it += nth) {
-    const int f = it % F;
-    int rest = it / F;
-    const int r = rest % g.R;
-    rest /= g.R;
-    const int kc = rest & 1, st = rest >> 1;
-    const int fi = grp * F + f;
-    const int cr = r - hw;
+  // thread -> fixed frame f of the group; rows r = tid/F, + nth/F, ...
+  const int f = tid % F, rstep = nth / F;
+  const int fi = grp * F + f;
+  const bool fvalid = fi < a.B;
+  const uint16_t *frame = a.frames + (int64_t)(fvalid ? fi : 0) * a.fstride;
+  u64 mytot = 0;
+  for (int sk = 0; sk < 2 * g.nstrips; ++sk) {
+    const int st = sk >> 1, kc = sk & 1;
     const int c0 = st * 32 + kc * 16;
-    uint32_t v[16];
+    uint8_t *dbase = a.G + (((int64_t)grp * g.nstrips + st) * 2 + kc) * g.R * (32 * F) + f * 32;
+    for (int r = tid / F; r < g.R; r += rstep) {
+      const int cr = r - hw;
+      const bool live = fvalid && cr >= 0 && cr < mc;   // c0 < nc always (nc % 32 == 0)
+      uint32_t P[8];
+      if (live) {
+        coarse_pairs<L>(frame + (int64_t)(cr * bs) * a.n + c0 * bs, a.n, P);
+      } else {
 #pragma unroll
-    for (int x = 0; x < 16; ++x) v[x] = 0;
-    const bool live = fi < a.B && cr >= 0 && cr < mc && c0 < nc;
-    if (live) {
-      const uint16_t *base = a.frames + (int64_t)fi * a.fstride + (int64_t)(cr * bs) * a.n + c0 * bs;
-#pragma unroll
-      for (int dy = 0; dy < bs; ++dy) {
-        const uint16_t *row = base + (int64_t)dy * a.n;
-        // 16 coarse columns = 16*bs raw samples = 2*bs 16-byte vectors (nc % 32 == 0)
-#pragma unroll
-        for (int q = 0; q < 2 * bs; ++q) {
-          const uint4 u = *reinterpret_cast<const uint4 *>(row + q * 8);
-          const uint32_t ws[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const uint32_t s = (ws[e >> 1] >> (16 * (e & 1))) & 0xffffu;
-            const int x = (q * 8 + e) / bs;   // coarse column within the 16
-            v[x] += s;
-          }
-        }
+        for (int k = 0; k < 8; ++k) P[k] = 0;
       }
+      // int8 parts: hi = v >> 7, lo = v & 127, two coarse values per word, four per byte-word
+      uint32_t hi[4], lo[4];
 #pragma unroll
-      for (int x = 0; x < 16; ++x)
-        if (c0 + x >= nc) v[x] = 0;
-    }
-    // int8 parts, 16 bytes each
-    uint32_t hi[4], lo[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      hi[q] = lo[q] = 0;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        hi[q] |= (v[4 * q + e] >> 7) << (8 * e);
-        lo[q] |= (v[4 * q + e] & 127u) << (8 * e);
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t h0 = (P[2 * q] >> 7) & 0x007F007Fu, h1 = (P[2 * q + 1] >> 7) & 0x007F007Fu;
+        const uint32_t l0 = P[2 * q] & 0x007F007Fu, l1 = P[2 * q + 1] & 0x007F007Fu;
+        hi[q] = __byte_perm(h0, h1, 0x6420);
+        lo[q] = __byte_perm(l0, l1, 0x6420);
       }
-    }
-    uint8_t *dst = a.G + ((((int64_t)grp * g.nstrips + st) * 2 + kc) * g.R + r) * (32 * F) + f * 32;
-    *reinterpret_cast<uint4 *>(dst) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-    *reinterpret_cast<uint4 *>(dst + 16) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-    if (!live) continue;
-    // energies (S2): totals, edge strips, corners
-    uint32_t rs = 0;
+      uint8_t *dst = dbase + r * (32 * F);
+      *reinterpret_cast<uint4 *>(dst) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<uint4 *>(dst + 16) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      if (!live) continue;
+      // energies (S2): totals, edge strips, corners
+      uint32_t rs = 0;
 #pragma unroll
-    for (int x = 0; x < 16; ++x) rs += v[x] * v[x];   // < 16 * 2^28 = 2^32
-    mytot[f] += rs;
-    const bool top = cr < hw, bot = cr >= mc - hw;
-    if (top) atomicAdd(&rowE[f * 2 * hw + cr], (u64)rs);
-    if (bot) atomicAdd(&rowE[f * 2 * hw + hw + (mc - 1 - cr)], (u64)rs);
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t v0 = P[k] & 0xffffu, v1 = P[k] >> 16;
+        rs += v0 * v0 + v1 * v1;   // 16 terms < 2^28 each: < 2^32
+      }
+      mytot += rs;
+      const bool top = cr < hw, bot = cr >= mc - hw;
+      if (top) atomicAdd(&rowE[f * 2 * hw + cr], (u64)rs);
+      if (bot) atomicAdd(&rowE[f * 2 * hw + hw + (mc - 1 - cr)], (u64)rs);
+      if (c0 >= hw && c0 + 16 <= nc - hw) continue;   // no edge column in this item
+      uint32_t v[16];
 #pragma unroll
-    for (int x = 0; x < 16; ++x) {
-      const int c = c0 + x;
-      if (c >= nc) break;
-      const bool lf = c < hw, rt = c >= nc - hw;
-      if (!(lf || rt)) continue;
-      const u64 v2 = (u64)(v[x] * v[x]);
-      if (lf) atomicAdd(&colE[f * 2 * hw + c], v2);
-      if (rt) atomicAdd(&colE[f * 2 * hw + hw + (nc - 1 - c)], v2);
-      if (top || bot) {
-        for (int qb = 0; qb < 2; ++qb) {
-          if (!(qb ? bot : top)) continue;
-          const int p = qb ? mc - cr : cr + 1;
-          for (int qr = 0; qr < 2; ++qr) {
-            if (!(qr ? rt : lf)) continue;
-            const int qq = qr ? nc - c : c + 1;
-            cor[((f * 4) + (qb * 2 + qr)) * CS + p * w + qq] = v2;
+      for (int k = 0; k < 8; ++k) { v[2 * k] = P[k] & 0xffffu; v[2 * k + 1] = P[k] >> 16; }
+#pragma unroll
+      for (int x = 0; x < 16; ++x) {
+        const int c = c0 + x;
+        const bool lf = c < hw, rt = c >= nc - hw;
+        if (!(lf || rt)) continue;
+        const u64 v2 = (u64)(v[x] * v[x]);
+        if (lf) atomicAdd(&colE[f * 2 * hw + c], v2);
+        if (rt) atomicAdd(&colE[f * 2 * hw + hw + (nc - 1 - c)], v2);
+        if (top || bot) {
+          for (int qb = 0; qb < 2; ++qb) {
+            if (!(qb ? bot : top)) continue;
+            const int p = qb ? mc - cr : cr + 1;
+            for (int qr = 0; qr < 2; ++qr) {
+              if (!(qr ? rt : lf)) continue;
+              const int qq = qr ? nc - c : c + 1;
+              cor[((f * 4) + (qb * 2 + qr)) * CS + p * w + qq] = v2;
+            }
           }
         }
       }
     }
   }
-  // totals
-  for (int f = 0; f < F; ++f) {
-    const u64 s = warp_sum(mytot[f]);
-    if ((tid & 31) == 0) atomicAdd(&tot[f], s);
+  // totals: a warp's lanes cover all F frames (F | 32), so reduce within lanes of equal f
+  {
+    u64 sum = mytot;
+    for (int o = 16; o >= F; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if ((tid & 31) < F) atomicAdd(&tot[f], sum);
   }
   __syncthreads();
   // prefix sums: edge strips (1-D), corners (2-D, the DP of P:35 in each corner)
@@ -309,6 +340,7 @@ __global__ void __launch_bounds__(256) k_tc_prep(TcPrepArgs a) {
     const int f = k / (W * W), lag = k % (W * W);
     const int fi = grp * F + f;
     if (fi >= a.B) continue;
+    (void)fvalid;
     const int s = lag / W - hw, t = lag % W - hw;
     const u64 *re = rowE + f * 2 * hw, *ce = colE + f * 2 * hw;
     // rows of the frame outside the frame-side rectangle of D_{s,t}:
