@@ -229,8 +229,8 @@ def main():
     frames = st.frames
     template = st.template
     if world > 1:   # template from rank 0 over NCCL (plan setup, untimed)
-        tb = template.view(torch.int16) if template.dtype == torch.uint16 else template
-        dist.broadcast(tb, src=0)
+        from paper_1506_06039_b200.dist import broadcast_template
+        broadcast_template(template, src=0)
     esz = frames.element_size()
     plan = Plan(spec.m, spec.n, spec.w, spec.levels, spec.dtype, 12, device=local)
     if args.algo != "auto":
@@ -239,15 +239,12 @@ def main():
     shifts = torch.empty((Tl, 2), dtype=torch.int32, device=dev)
     fmin = torch.empty((Tl,), dtype=torch.float64, device=dev)
     corrected = torch.empty_like(frames)
-    res = torch.empty((Tl, 4), dtype=torch.int32, device=dev)     # (s, t, fmin as 2 x int32)
-    gathered = torch.empty((world * Tl, 4), dtype=torch.int32, device=dev) if world > 1 else None
+    from paper_1506_06039_b200.dist import gather_results
 
     def step():
         plan.align_into(frames, shifts, fmin, corrected)
-        if world > 1:
-            res[:, :2] = shifts
-            res[:, 2:] = fmin.view(torch.int32).view(Tl, 2)
-            dist.all_gather_into_tensor(gathered, res)
+        if world > 1:   # per-frame results of every rank to every rank (16 B/frame)
+            gather_results(shifts, fmin, world * Tl)
 
     for _ in range(args.warmup):
         step()
