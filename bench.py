@@ -96,7 +96,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200",
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "50",
                  "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -301,8 +301,8 @@ def main():
     try:
         ncu = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
         entry = ncu.get(f"C{spec.index}", {}).get(plan.algo, {}).get(kind)
-        if entry:
-            traffic = entry["bytes_per_launch"]
+        if entry:   # per-frame DRAM bytes from the committed ncu capture x frames per launch
+            traffic = entry["bytes_per_frame"] * frames_timed / klaunch
     except Exception:
         pass
     roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
