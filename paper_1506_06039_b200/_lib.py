@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmoco.so")
+LIB_PATH = os.environ.get("MOCO_LIB") or os.path.join(_HERE, "libmoco.so")
 
 MOCO_U16, MOCO_F32 = 1, 2
 MOCO_ALGO_AUTO, MOCO_ALGO_DIRECT, MOCO_ALGO_TC = 0, 1, 2

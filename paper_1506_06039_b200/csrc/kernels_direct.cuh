@@ -177,19 +177,6 @@ __global__ void k_template_energy(const In *__restrict__ b, int pitch, int mc, i
   }
 }
 
-// Template column prefix of b^2 (refine padding correction): cb[i][j] = sum_{i'<i} b[i'][j]^2.
-__global__ void k_colprefix_u16(const uint16_t *__restrict__ b, int pitch, int m, int n, u64 *__restrict__ cb) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    u64 acc = 0;
-    cb[j] = 0;
-    for (int i = 0; i < m; ++i) {
-      const u64 v = b[(int64_t)i * pitch + j];
-      acc += v * v;
-      cb[(int64_t)(i + 1) * n + j] = acc;
-    }
-  }
-}
-
 // ---------------------------------------------------------------- K3+K4d+K5
 // One CTA per frame.  Shared memory:
 //   ga[W*W]      frame energy per lag (strip/corner form of the DP)
@@ -571,309 +558,6 @@ __global__ void k_apply(const E *__restrict__ in, E *__restrict__ out, int m, in
     }
     *reinterpret_cast<uint4 *>(out + f * (int64_t)m * n + (int64_t)i * n + cg * V) =
         *reinterpret_cast<const uint4 *>(o);
-  }
-}
-
-}  // namespace moco
-
-namespace moco {
-
-// ------------------------------------------------------------- K6+K7 fused (u16)
-// One CTA per frame at level l: the nine candidates (2s+u, 2t+v) by exact direct
-// sums N = sum_D (a - b)^2, argmin with key (f, s, t), and -- at level 0 when
-// requested -- the corrected frame c[i][j] = a[i+s][j+t] or 0 written
-// right after, while the frame is still in L2 (one HBM read for both steps).
-// Each thread owns 8 consecutive template columns of a row; the 3 frame rows it
-// needs are read as aligned 16-byte vectors and shifted in registers.  The
-// misalignment (T-1) mod 8 is the same for the whole CTA, so the loop is
-// specialised on it (template OFFA).
-struct RefineApplyArgs {
-  const uint16_t *frames;   // level-l images
-  int64_t fstride;
-  int pitch;
-  const uint16_t *tpl;      // level-l template
-  int tpitch;
-  int ml, nl;
-  double scale;             // 16^l
-  int B;
-  const int32_t *shift_in;  // [B][2] at level l+1
-  int32_t *shift_out;       // [B][2] at level l
-  double *f_out;            // [B] or null
-  uint16_t *corrected;      // [B][m][n] or null (level 0 only; fstride/pitch of the frames)
-  int flush;                // products summed in 32 bits before widening
-  int pad;                  // zero columns staged on each side of a frame row (>= max|T| + 10)
-  const u64 *cb;            // [ml+1][nl]: cb[i][j] = sum_{i' < i} b[i'][j]^2 (template column prefix)
-};
-
-template <int OFF>
-__device__ __forceinline__ void extract10(const uint4 &lo, const uint4 &hi, uint32_t (&v)[10]) {
-  const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-#pragma unroll
-  for (int x = 0; x < 10; ++x) {
-    const int e = OFF + x;   // element within the 16 (e == 16 only for OFF == 7: set by caller)
-    if (e < 16) v[x] = (w[e >> 1] >> (16 * (e & 1))) & 0xffffu;
-  }
-}
-
-// Rows are staged in shared memory by cp.async in bands of RB template rows (and the
-// RB+2 frame rows they pair with), double-buffered: the next band streams in from
-// HBM/L2 while the current one is scored from shared memory.  One item = template
-// row, 8 columns; the 3 frame rows are read as two aligned 16-byte vectors each.
-constexpr int REF_RB = 8;
-
-__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-               "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// One item: template row (smem row r of the band, global row r0 + r), 8 columns at
-// j0; smem frame row r + u holds frame row r0 + r + S + u - 1, zero-padded by `pad`
-// columns on each side, so every item takes the same aligned path.  Out-of-frame
-// columns then contribute b^2 instead of nothing; refine_rows subtracts that exactly.
-template <int OFFA>
-__device__ __forceinline__ void band_item(const uint16_t *Ts, const uint16_t *Fs, int ps, int pad, int r, int j0,
-                                          int r0, int S, int T, int ml, uint32_t (&acc)[9]) {
-  const uint4 bq = *reinterpret_cast<const uint4 *>(Ts + r * ps + j0);
-  const uint32_t bw[4] = {bq.x, bq.y, bq.z, bq.w};
-  uint32_t bv[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) bv[q] = (bw[q >> 1] >> (16 * (q & 1))) & 0xffffu;
-  const int ab = j0 + T - 1 - OFFA + pad;          // 8-aligned, inside the padded row
-#pragma unroll
-  for (int u = 0; u < 3; ++u) {
-    const int fr = r0 + r + S + u - 1;
-    if (fr < 0 || fr >= ml) continue;
-    const uint16_t *arow = Fs + (r + u) * ps;
-    uint32_t av[10];
-    const uint4 lo = *reinterpret_cast<const uint4 *>(arow + ab);
-    const uint4 hi = *reinterpret_cast<const uint4 *>(arow + ab + 8);
-    extract10<OFFA>(lo, hi, av);
-    if (OFFA == 7) av[9] = arow[ab + 16];
-#pragma unroll
-    for (int v = 0; v < 3; ++v)
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int d = (int)av[q + v] - (int)bv[q];
-        acc[u * 3 + v] += (uint32_t)(d * d);
-      }
-  }
-}
-
-template <int OFFA>
-__device__ __forceinline__ void refine_rows(const RefineApplyArgs &a, const uint16_t *A, int S, int T,
-                                            u64 (&acc64)[9]) {
-  extern __shared__ __align__(16) unsigned char rsm[];
-  const int ml = a.ml, nl = a.nl, pitch = a.pitch, pad = a.pad;
-  const int ps = nl + 2 * pad + 8;                      // padded smem row (+16 B: bank spread)
-  const int groups = nl >> 3;                           // nl % 8 == 0 (host check)
-  const int ilo = max(0, -S - 1), ihi = min(ml, ml - S + 1);
-  const int nb = (ihi - ilo + REF_RB - 1) / REF_RB;
-  const int stageE = (2 * REF_RB + 2) * ps;             // elements per stage
-  uint16_t *stg0 = reinterpret_cast<uint16_t *>(rsm);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
-  const int vec = nl >> 3;                              // 16-byte chunks per row
-  // zero the pads of the frame rows once (cp.async never writes them)
-  for (int e = threadIdx.x; e < 2 * (REF_RB + 2) * (2 * pad + 8); e += blockDim.x) {
-    const int st = e / ((REF_RB + 2) * (2 * pad + 8)), rem = e % ((REF_RB + 2) * (2 * pad + 8));
-    const int row = rem / (2 * pad + 8), c = rem % (2 * pad + 8);
-    const int col = c < pad ? c : nl + c;               // [0,pad) and [pad+nl, ps)
-    stg0[st * stageE + (REF_RB + row) * ps + col] = 0;
-  }
-  auto load_band = [&](int b, uint16_t *dst) {
-    const int r0 = ilo + b * REF_RB;
-    const int nr = min(REF_RB, ihi - r0);
-    for (int row = warp; row < 2 * REF_RB + 2; row += nwarp) {
-      const uint16_t *src = nullptr;
-      uint16_t *d = dst + row * ps;
-      if (row < REF_RB) {
-        if (row < nr) src = a.tpl + (int64_t)(r0 + row) * a.tpitch;
-      } else {
-        const int k = row - REF_RB, fr = r0 + S - 1 + k;
-        if (k < nr + 2 && fr >= 0 && fr < ml) src = A + (int64_t)fr * pitch;
-        d += pad;
-      }
-      if (!src) continue;
-      for (int c = lane; c < vec; c += 32) cp_async16(d + 8 * c, src + 8 * c);
-    }
-    cp_async_commit();
-  };
-  uint32_t acc[9];
-#pragma unroll
-  for (int c = 0; c < 9; ++c) acc[c] = 0;
-  // 32-bit partials: per band a lane adds <= ceil(groups/32) items (8 px) per candidate
-  // (one template row per warp: REF_RB == blockDim/32)
-  const int per_band = (groups + 31) >> 5;
-  const int flush_bands = max(1, a.flush / per_band);
-  __syncthreads();
-  if (nb > 0) load_band(0, stg0);
-  for (int b = 0; b < nb; ++b) {
-    if (b + 1 < nb) {
-      load_band(b + 1, stg0 + ((b + 1) & 1) * stageE);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const uint16_t *Ts = stg0 + (b & 1) * stageE, *Fs = Ts + REF_RB * ps;
-    const int r0 = ilo + b * REF_RB;
-    const int nr = min(REF_RB, ihi - r0);
-    for (int r = warp; r < nr; r += nwarp)
-      for (int g = lane; g < groups; g += 32)
-        band_item<OFFA>(Ts, Fs, ps, pad, r, g * 8, r0, S, T, ml, acc);
-    if ((b + 1) % flush_bands == 0) {
-#pragma unroll
-      for (int c = 0; c < 9; ++c) { acc64[c] += acc[c]; acc[c] = 0; }
-    }
-    __syncthreads();   // stage b&1 is reloaded by the next iteration
-  }
-#pragma unroll
-  for (int c = 0; c < 9; ++c) acc64[c] += acc[c];
-}
-
-// Exact correction for the zero-padded columns: candidate (s,t) counted b[i][j]^2 at
-// every template column j whose frame column j+t is outside [0,nl), for the template
-// rows i whose frame row i+s is inside [0,ml).  Sum over those columns of the
-// column-prefix table cb (computed once per plan).  Warp w < 9 handles candidate w.
-__device__ __forceinline__ u64 pad_correction(const RefineApplyArgs &a, int s, int t) {
-  const int ml = a.ml, nl = a.nl;
-  const int i0 = max(0, -s), i1 = min(ml, ml - s);
-  int j0, j1;   // invalid template columns [j0, j1)
-  if (t < 0) { j0 = 0; j1 = min(nl, -t); }
-  else if (t > 0) { j0 = max(0, nl - t); j1 = nl; }
-  else return 0;
-  u64 c = 0;
-  for (int j = j0 + (threadIdx.x & 31); j < j1; j += 32)
-    c += a.cb[(int64_t)i1 * nl + j] - a.cb[(int64_t)i0 * nl + j];
-  return warp_sum(c);
-}
-
-template <int OFFT, bool EDGE>
-__device__ __forceinline__ void apply_span(const RefineApplyArgs &a, const uint16_t *A, uint16_t *O, int s,
-                                           int t, int m, int n, int g0, int ng) {
-  if (ng <= 0) return;
-  constexpr int UNROLL = EDGE ? 1 : 4;
-  const int total = m * ng;
-  const int nth = blockDim.x;
-  for (int it0 = threadIdx.x; it0 < total; it0 += UNROLL * nth) {
-    uint4 lo[UNROLL], hi[UNROLL];
-    int ii[UNROLL], jj[UNROLL];
-    bool ok[UNROLL];
-#pragma unroll
-    for (int k = 0; k < UNROLL; ++k) {
-      const int it = it0 + k * nth;
-      const int itc = it < total ? it : 0;
-      ii[k] = itc / ng;
-      jj[k] = (g0 + itc % ng) * 8;
-      const int r = ii[k] + s;
-      ok[k] = it < total;
-      const bool inrow = r >= 0 && r < m;
-      if (!EDGE) {
-        const uint16_t *arow = A + (int64_t)(inrow ? r : 0) * a.pitch;
-        const int ab = jj[k] + t - OFFT;
-        lo[k] = __ldg(reinterpret_cast<const uint4 *>(arow + ab));
-        hi[k] = OFFT ? __ldg(reinterpret_cast<const uint4 *>(arow + ab + 8)) : lo[k];
-        if (!inrow) lo[k] = hi[k] = make_uint4(0, 0, 0, 0);
-      } else {
-        uint32_t v[8];
-#pragma unroll
-        for (int x = 0; x < 8; ++x) {
-          const int c = jj[k] + t + x;
-          v[x] = (inrow && c >= 0 && c < n) ? A[(int64_t)r * a.pitch + c] : 0u;
-        }
-        lo[k] = make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16), v[6] | (v[7] << 16));
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < UNROLL; ++k) {
-      if (!ok[k]) continue;
-      uint4 outv = lo[k];
-      if (!EDGE) {
-        uint32_t v[10];
-        extract10<OFFT>(lo[k], hi[k], v);
-        outv = make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16), v[6] | (v[7] << 16));
-      }
-      __stcs(reinterpret_cast<uint4 *>(O + (int64_t)ii[k] * n + jj[k]), outv);
-    }
-  }
-}
-
-template <int OFFT>
-__device__ __forceinline__ void apply_rows(const RefineApplyArgs &a, const uint16_t *A, uint16_t *O, int s,
-                                           int t, int m, int n) {
-  const int groups = n >> 3;   // n % 8 == 0 at level 0
-  // interior chunks: both aligned vectors inside the row
-  const int jlo = max(0, OFFT - t), jhi = n - 16 + OFFT - t;
-  int g_lo = min((jlo + 7) >> 3, groups), g_hi = jhi >= 0 ? (jhi >> 3) + 1 : 0;
-  g_hi = max(g_lo, min(g_hi, groups));
-  apply_span<OFFT, false>(a, A, O, s, t, m, n, g_lo, g_hi - g_lo);
-  apply_span<OFFT, true>(a, A, O, s, t, m, n, 0, g_lo);
-  apply_span<OFFT, true>(a, A, O, s, t, m, n, g_hi, groups - g_hi);
-}
-
-__global__ void __launch_bounds__(256) k_refine_apply(RefineApplyArgs a) {
-  const int64_t f = blockIdx.x;
-  const uint16_t *A = a.frames + f * a.fstride;
-  const int S = 2 * a.shift_in[2 * f], T = 2 * a.shift_in[2 * f + 1];
-  u64 acc[9];
-#pragma unroll
-  for (int c = 0; c < 9; ++c) acc[c] = 0;
-  switch ((T - 1) & 7) {
-    case 0: refine_rows<0>(a, A, S, T, acc); break;
-    case 1: refine_rows<1>(a, A, S, T, acc); break;
-    case 2: refine_rows<2>(a, A, S, T, acc); break;
-    case 3: refine_rows<3>(a, A, S, T, acc); break;
-    case 4: refine_rows<4>(a, A, S, T, acc); break;
-    case 5: refine_rows<5>(a, A, S, T, acc); break;
-    case 6: refine_rows<6>(a, A, S, T, acc); break;
-    default: refine_rows<7>(a, A, S, T, acc); break;
-  }
-  __shared__ u64 part[9][32];
-  __shared__ u64 corr[9];
-  __shared__ Key red[32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-  for (int c = 0; c < 9; ++c) {
-    const u64 v = warp_sum(acc[c]);
-    if (lane == 0) part[c][wid] = v;
-  }
-  for (int c = wid; c < 9; c += nw) {
-    const u64 v = pad_correction(a, S + c / 3 - 1, T + c % 3 - 1);
-    if (lane == 0) corr[c] = v;
-  }
-  __syncthreads();
-  Key k{~0ull, ~0u};
-  if (threadIdx.x < 9) {
-    u64 N = 0;
-    for (int q = 0; q < nw; ++q) N += part[threadIdx.x][q];
-    N -= corr[threadIdx.x];
-    const int u = threadIdx.x / 3 - 1, v = threadIdx.x % 3 - 1;
-    const int s = S + u, t = T + v;
-    const double area = (double)((a.ml - abs(s)) * (a.nl - abs(t)));
-    const double fv = (double)N / (a.scale * area);
-    k = Key{(u64)__double_as_longlong(fv), (unsigned)threadIdx.x};   // rank == (s,t) order
-  }
-  k = block_min_key(k, red);
-  const int s = S + (int)(k.idx / 3) - 1, t = T + (int)(k.idx % 3) - 1;
-  if (threadIdx.x == 0) {
-    a.shift_out[2 * f] = s;
-    a.shift_out[2 * f + 1] = t;
-    if (a.f_out) a.f_out[f] = __longlong_as_double((long long)k.f);
-  }
-  if (!a.corrected) return;
-  uint16_t *O = a.corrected + f * a.fstride;
-  switch (t & 7) {
-    case 0: apply_rows<0>(a, A, O, s, t, a.ml, a.nl); break;
-    case 1: apply_rows<1>(a, A, O, s, t, a.ml, a.nl); break;
-    case 2: apply_rows<2>(a, A, O, s, t, a.ml, a.nl); break;
-    case 3: apply_rows<3>(a, A, O, s, t, a.ml, a.nl); break;
-    case 4: apply_rows<4>(a, A, O, s, t, a.ml, a.nl); break;
-    case 5: apply_rows<5>(a, A, O, s, t, a.ml, a.nl); break;
-    case 6: apply_rows<6>(a, A, O, s, t, a.ml, a.nl); break;
-    default: apply_rows<7>(a, A, O, s, t, a.ml, a.nl); break;
   }
 }
 

@@ -1,0 +1,494 @@
+// kernels_refine.cuh -- S5 refine (+ S6 apply) for MOCO_U16.
+//
+// At each finer level l the nine candidates (s,t) = (S+u, T+v), u,v in {-1,0,1},
+// with (S,T) = 2 x the shift of level l+1 ("multiply the optimal (s,t) by 2 and
+// do a local search"), are scored exactly through the decomposition of P:31:
+//
+//     N(s,t) = GA(s,t) + GB(s,t) - 2 H(s,t)
+//     H(s,t)  = sum_{(i,j) in D_{s,t}} a[i+s][j+t] b[i][j]       (cross term)
+//     GA(s,t) = sum_{(i,j) in D_{s,t}} a[i+s][j+t]^2             (frame energy)
+//     GB(s,t) = sum_{(i,j) in D_{s,t}} b[i][j]^2                 (template energy)
+//
+// Template-stationary design: the template is read ONCE per plan call, not once per
+// frame.  K_sum (k_refine_sums) gives each CTA a fixed tile of template rows
+// [r0, r1) x 256 columns in shared memory; a producer warp streams, frame after frame,
+// the matching frame rows [r0+S-1, r1+S+1) into a TMA ring, and each consumer warp
+// takes one frame at a time (lane = 8 template columns, all rows of the tile, frame
+// rows kept in registers).  TMA tensor boxes start at the 16-byte aligned column
+// x0 <= T-1 and are zero-filled outside the frame, so with a_pad = 0 outside
+//     H(s,t)  = sum_{tile (i,j)} a_pad[i+s][j+t] b[i][j]
+//     GA(s,t) = sum_{tile (i,j)} a_pad[i+s][j+t]^2
+// -- one uniform loop (specialised on the misalignment T-1-x0).  The warp's 18 sums
+// go to the frame's 64-bit accumulators with one atomic add each.
+// K_pick (k_refine_pick) then forms N = GA + GB - 2H per candidate (GB from the
+// plan's 2-D prefix table of b^2), takes the argmin with key (f, s, t), re-zeroes the
+// accumulators and, at level 0, writes the corrected frame c[i][j] = a[i+s][j+t]
+// (0 outside) with 16-byte streaming stores.
+// Everything is exact in integers, so f = fl(N / (16^l A)) is the oracle's value.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "kernels_tc.cuh"
+
+namespace moco {
+
+// 2-D prefix of b^2: P[i][j] = sum_{i' < i, j' < j} b[i'][j']^2, (m+1) x (n+1), once per plan.
+// Pass 1 (rows) then pass 2 (columns), one thread per row / column.
+__global__ void k_prefix2d_rows(const uint16_t *__restrict__ b, int pitch, int m, int n, u64 *__restrict__ P) {
+  const int n1 = n + 1;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= m; i += gridDim.x * blockDim.x) {
+    u64 *row = P + (int64_t)i * n1;
+    row[0] = 0;
+    u64 acc = 0;
+    for (int j = 0; j < n; ++j) {
+      if (i > 0) {
+        const u64 v = b[(int64_t)(i - 1) * pitch + j];
+        acc += v * v;
+      }
+      row[j + 1] = acc;
+    }
+  }
+}
+__global__ void k_prefix2d_cols(int m, int n, u64 *__restrict__ P) {
+  const int n1 = n + 1;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= n; j += gridDim.x * blockDim.x) {
+    u64 acc = 0;
+    for (int i = 0; i <= m; ++i) {
+      acc += P[(int64_t)i * n1 + j];
+      P[(int64_t)i * n1 + j] = acc;
+    }
+  }
+}
+
+struct RefineSumArgs {
+  const uint16_t *tpl;      // level-l template
+  int tpitch;
+  int ml, nl;
+  int B;
+  const int32_t *shift_in;  // [B][2] at level l+1
+  u64 *acc;                 // [B][18]: H for the 9 candidates, then GA
+  int rt;                   // template rows per tile (<= RS_MAXRT)
+  int nrt;                  // row tiles
+  int stages;               // ring depth
+  int wide;                 // 1: flush 32-bit partials after every row (values >= 2^13)
+};
+
+constexpr int RS_CT = 512;            // template columns per tile (a warp walks it in 256-column halves)
+constexpr int RS_BOX = 176;           // frame box columns (3 boxes cover CT + 9)
+constexpr int RS_NBOX = 3;
+constexpr int RS_MAXRT = 8;
+constexpr int RS_CW = 12;             // consumer warps (frames in flight per CTA)
+constexpr int RS_THREADS = 32 * (1 + RS_CW);
+
+// staged frame box: (rt+2) rows x RS_BOX columns, padded to 128 bytes (TMA destination alignment)
+__host__ __device__ inline int rs_box_elems(int rt) { return ((rt + 2) * RS_BOX * 2 + 127) / 128 * 64; }
+__host__ __device__ inline int rs_stage_bytes(int rt) { return RS_NBOX * rs_box_elems(rt) * 2; }
+inline int rs_smem_bytes(int rt, int stages) { return 1024 + RS_MAXRT * RS_CT * 2 + stages * rs_stage_bytes(rt) + RS_CW * 32 * 19 * 4; }
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+// TMA tensor load of a 3-D box (x = column, y = row, z = frame), zero fill out of bounds.
+__device__ __forceinline__ void tma_load3(void *dst, const CUtensorMap *tm, int x, int y, int z, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store3(const CUtensorMap *tm, int x, int y, int z, const void *src) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                   reinterpret_cast<uint64_t>(tm)),
+               "r"(x), "r"(y), "r"(z), "r"(smem_u32(src))
+               : "memory");
+}
+// L2 eviction-priority policies (createpolicy) and the hinted copies that use them.
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load3_hint(void *dst, const CUtensorMap *tm, int x, int y, int z, uint64_t *bar,
+                                               uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, "
+      "{%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void st_global_hint(void *p, const uint4 &v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// 10 consecutive samples starting OFF elements into the 16 held by (lo, hi).
+template <int OFF>
+__device__ __forceinline__ void extract10(const uint4 &lo, const uint4 &hi, uint32_t (&v)[10]) {
+  const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+  for (int x = 0; x < 10; ++x) {
+    const int e = OFF + x;   // e == 16 only for OFF == 7: set by the caller
+    if (e < 16) v[x] = (e & 1) ? (w[e >> 1] >> 16) : (w[e >> 1] & 0xffffu);
+  }
+}
+
+// Frame row window for template columns j0..j0+7: the 10 samples at frame columns
+// j0+T-1 .. j0+T+8 (staged columns j0+OFFA .. j0+OFFA+9), plus the three 8-wide sums
+// of their squares for v = -1, 0, +1.
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+// Frame row window for template columns j0..j0+7: the 10 samples at frame columns
+// j0+T-1 .. j0+T+8, i.e. staged columns c+OFFA .. c+OFFA+9.  Six 32-bit words from the
+// word offset OFFA/2 (per-word shared addresses: the window may cross a box), then
+// one runtime funnel shift per word pair for odd OFFA -- the same code for every
+// misalignment, so concurrently running warps share one instruction stream.
+__device__ __forceinline__ void rs_frame10(const uint32_t (&wa)[6], uint32_t roff, uint32_t sh, uint32_t (&v)[10],
+                                           uint32_t (&wsum)[3]) {
+  uint32_t w[6];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) w[q] = lds32(wa[q] + roff);
+#pragma unroll
+  for (int m = 0; m < 5; ++m) {
+    const uint32_t u = __funnelshift_r(w[m], w[m + 1], sh);
+    v[2 * m] = u & 0xffffu;
+    v[2 * m + 1] = u >> 16;
+  }
+  uint32_t sq[10];
+#pragma unroll
+  for (int x = 0; x < 10; ++x) sq[x] = v[x] * v[x];
+  uint32_t mid = 0;
+#pragma unroll
+  for (int x = 1; x < 9; ++x) mid += sq[x];
+  wsum[0] = mid - sq[8] + sq[0];   // v = -1
+  wsum[1] = mid;                   // v =  0
+  wsum[2] = mid - sq[1] + sq[9];   // v = +1
+}
+
+__device__ __forceinline__ void load_tpl8(const uint16_t *p, uint32_t (&bv)[8]) {
+  const uint4 bq = *reinterpret_cast<const uint4 *>(p);
+  const uint32_t bw[4] = {bq.x, bq.y, bq.z, bq.w};
+#pragma unroll
+  for (int x = 0; x < 8; ++x) bv[x] = (x & 1) ? (bw[x >> 1] >> 16) : (bw[x >> 1] & 0xffffu);
+}
+
+// One template row against the three frame rows (u = -1, 0, +1).
+__device__ __forceinline__ void h_row(const uint32_t (&bv)[8], const uint32_t (&f0)[10], const uint32_t (&f1)[10],
+                                      const uint32_t (&f2)[10], const uint32_t (&w0)[3], const uint32_t (&w1)[3],
+                                      const uint32_t (&w2)[3], uint32_t (&H)[9], uint32_t (&GA)[9]) {
+#pragma unroll
+  for (int v = 0; v < 3; ++v) {
+    uint32_t h0 = H[v], h1 = H[3 + v], h2 = H[6 + v];
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+      h0 += f0[x + v] * bv[x];
+      h1 += f1[x + v] * bv[x];
+      h2 += f2[x + v] * bv[x];
+    }
+    H[v] = h0; H[3 + v] = h1; H[6 + v] = h2;
+    GA[v] += w0[v]; GA[3 + v] += w1[v]; GA[6 + v] += w2[v];
+  }
+}
+
+// One frame on one warp: rows 0..nr-1 of the tile against staged frame rows 0..nr+1,
+// the tile's columns walked in halves of 256 (lane = 8 columns of a half).
+// Staged row k of box b starts at Fs + b*rs_box_elems(rt) + k*RS_BOX.
+template <bool WIDE>
+__device__ __forceinline__ void rs_frame(const uint16_t *Tt, const uint16_t *Fs, int rt, int nr, int ncols, int offa,
+                                         uint32_t (&H)[9], uint32_t (&GA)[9], u64 (&H64)[9], u64 (&G64)[9]) {
+  const int lane = threadIdx.x & 31;
+  const int be = rs_box_elems(rt);
+  const uint32_t fbase = (uint32_t)__cvta_generic_to_shared(Fs);
+  const uint32_t sh = (uint32_t)(offa & 1) * 16;
+  auto fl = [&]() {
+    if (WIDE) {
+#pragma unroll
+      for (int q = 0; q < 9; ++q) { H64[q] += H[q]; G64[q] += GA[q]; H[q] = 0; GA[q] = 0; }
+    }
+  };
+  for (int c = lane * 8; c < ncols; c += 256) {   // ncols % 8 == 0: a lane's 8 columns are all in or all out
+    uint32_t wa[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const int col = c + (offa & ~1) + 2 * q;
+      wa[q] = fbase + (uint32_t)(((col / RS_BOX) * be + (col % RS_BOX)) * 2);
+    }
+    const uint16_t *tp = Tt + c;
+    uint32_t fa[10], fb[10], fc[10], wa0[3], wb[3], wc[3], bv[8];
+    auto ld = [&](int k, uint32_t (&v)[10], uint32_t (&w)[3]) { rs_frame10(wa, (uint32_t)(k * RS_BOX * 2), sh, v, w); };
+    ld(0, fa, wa0);
+    ld(1, fb, wb);
+    int q = 0;
+    for (; q + 3 <= nr; q += 3) {
+      ld(q + 2, fc, wc); load_tpl8(tp + q * RS_CT, bv); h_row(bv, fa, fb, fc, wa0, wb, wc, H, GA); fl();
+      ld(q + 3, fa, wa0); load_tpl8(tp + (q + 1) * RS_CT, bv); h_row(bv, fb, fc, fa, wb, wc, wa0, H, GA); fl();
+      ld(q + 4, fb, wb); load_tpl8(tp + (q + 2) * RS_CT, bv); h_row(bv, fc, fa, fb, wc, wa0, wb, H, GA); fl();
+    }
+    if (q < nr) { ld(q + 2, fc, wc); load_tpl8(tp + q * RS_CT, bv); h_row(bv, fa, fb, fc, wa0, wb, wc, H, GA); fl(); ++q; }
+    if (q < nr) { ld(q + 2, fa, wa0); load_tpl8(tp + q * RS_CT, bv); h_row(bv, fb, fc, fa, wb, wc, wa0, H, GA); fl(); }
+  }
+}
+
+template <bool WIDE>
+__global__ void __launch_bounds__(RS_THREADS, 1)
+    k_refine_sums(const __grid_constant__ CUtensorMap tmF, RefineSumArgs a) {
+  extern __shared__ __align__(1024) unsigned char rs_smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(rs_smem);   // [32]
+  uint64_t *empty = full + 32;                               // [32], then int[32] stage misalignments
+  uint16_t *Tt = reinterpret_cast<uint16_t *>(rs_smem + 1024);
+  unsigned char *ring = rs_smem + 1024 + RS_MAXRT * RS_CT * 2;
+  const int RT = a.rt, NS = a.stages, SB = rs_stage_bytes(RT);
+  uint32_t *red = reinterpret_cast<uint32_t *>(ring + NS * SB);   // [RS_CW][32][19]
+  const int ml = a.ml, nl = a.nl;
+  const int rtile = blockIdx.x % a.nrt, ctile = blockIdx.x / a.nrt;
+  const int r0 = (int)((int64_t)rtile * ml / a.nrt), nr = (int)((int64_t)(rtile + 1) * ml / a.nrt) - r0;
+  const int c0 = ctile * RS_CT;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // the template tile, zero outside the template
+  for (int e = tid; e < RS_MAXRT * RS_CT; e += blockDim.x) {
+    const int r = e / RS_CT, c = e % RS_CT;
+    Tt[e] = (r < nr && c0 + c < nl) ? a.tpl[(int64_t)(r0 + r) * a.tpitch + c0 + c] : (uint16_t)0;
+  }
+  if (tid == 0) {
+    for (int k = 0; k < NS; ++k) {
+      mbar_init(&full[k], 1);
+      mbar_init(&empty[k], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (nr <= 0) return;
+  int *stg_offa = reinterpret_cast<int *>(empty + 32);   // [32] misalignment of the frame in each stage
+  if (warp == 0) {
+    // ---------------- producer: frame f's rows [r0+S-1, r0+nr+S+1) into stage f % NS.
+    // Lanes 0..7 each own every 8th frame (independent stages), so eight frames are
+    // waited for and issued per pass; shifts are read 32 frames at a time.
+    const uint32_t bytes = (uint32_t)(RS_NBOX * (RT + 2) * RS_BOX * 2);   // full boxes
+    for (int f32 = 0; f32 < a.B; f32 += 32) {
+      int2 sv = make_int2(0, 0);
+      if (f32 + lane < a.B) sv = reinterpret_cast<const int2 *>(a.shift_in)[f32 + lane];
+      for (int k0 = 0; k0 < 32; k0 += 8) {
+        const int sx = __shfl_sync(0xffffffffu, sv.x, k0 + (lane & 7));
+        const int sy = __shfl_sync(0xffffffffu, sv.y, k0 + (lane & 7));
+        const int f = f32 + k0 + lane;
+        if (lane < 8 && f < a.B) {
+          const int S = 2 * sx, T = 2 * sy;
+          const int stg = f % NS;
+          if (f >= NS) mbar_wait(&empty[stg], ((f / NS) - 1) & 1);
+          const int x0 = c0 + (T - 1) - ((T - 1) & 7);
+          uint16_t *Fs = reinterpret_cast<uint16_t *>(ring + stg * SB);
+          stg_offa[stg] = (T - 1) & 7;
+          mbar_arrive_expect_tx(&full[stg], bytes);
+#pragma unroll
+          for (int bx = 0; bx < RS_NBOX; ++bx)
+            tma_load3(Fs + bx * rs_box_elems(RT), &tmF, x0 + bx * RS_BOX, r0 + S - 1, f, &full[stg]);
+        }
+        __syncwarp();
+      }
+    }
+    return;
+  }
+  // ---------------- consumers: warp w takes frames w-1, w-1+RS_CW, ...
+  const int cw = warp - 1;
+  uint32_t *rw = red + cw * 32 * 19;
+  for (int f = cw; f < a.B; f += RS_CW) {
+    const int stg = f % NS;
+    mbar_wait(&full[stg], (f / NS) & 1);
+    const int offa = stg_offa[stg];
+    const uint16_t *Fs = reinterpret_cast<const uint16_t *>(ring + stg * SB);
+    uint32_t H[9], GA[9];
+    u64 H64[9], G64[9];   // 64-bit flush targets, live only when WIDE
+#pragma unroll
+    for (int q = 0; q < 9; ++q) { H[q] = 0; GA[q] = 0; }
+    if (WIDE) {
+#pragma unroll
+      for (int q = 0; q < 9; ++q) { H64[q] = 0; G64[q] = 0; }
+    }
+#ifndef RS_NOCOMPUTE
+    rs_frame<WIDE>(Tt, Fs, RT, nr, min(RS_CT, nl - c0), offa, H, GA, H64, G64);
+#else
+    H[0] += Fs[lane] + offa;
+#endif
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stg]);   // the staged rows are no longer read
+    u64 *acc = a.acc + (int64_t)f * 18;
+    if (!WIDE) {
+      // lane sums < 2^31 (<= 64 products < 2^24 each): transpose through shared memory,
+      // lanes 0..17 add one column of 32 in 64 bits
+#pragma unroll
+      for (int q = 0; q < 9; ++q) { rw[lane * 19 + q] = H[q]; rw[lane * 19 + 9 + q] = GA[q]; }
+      __syncwarp();
+      if (lane < 18) {
+        u64 sum = 0;
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k) sum += rw[k * 19 + lane];
+        atomicAdd(acc + lane, sum);
+      }
+      __syncwarp();
+    } else {
+#pragma unroll
+      for (int q = 0; q < 9; ++q) {
+        const u64 h = warp_sum(H64[q]), g = warp_sum(G64[q]);
+        if (lane == 0) { atomicAdd(acc + q, h); atomicAdd(acc + 9 + q, g); }
+      }
+    }
+  }
+}
+
+struct RefinePickArgs {
+  const uint16_t *frames;   // level-l images (apply source at level 0)
+  int64_t fstride;
+  int pitch;
+  const u64 *pb2;           // [(ml+1)][(nl+1)] prefix of b^2
+  int ml, nl;
+  double scale;             // 16^l
+  int B;
+  const int32_t *shift_in;  // [B][2] at level l+1
+  u64 *acc;                 // [B][18], re-zeroed here
+  int32_t *shift_out;       // [B][2] at level l
+  double *f_out;            // [B] or null
+  uint16_t *corrected;      // [B][ml][nl] or null (level 0)
+};
+
+template <int SH>
+__device__ __forceinline__ void pick_apply_rows(const uint16_t *A, uint16_t *O, int pitch, int s, int t, int ml,
+                                                int nl) {
+  // output chunk (i, 8-column group j0): source samples a[i+s][j0+t .. j0+t+7]; the two
+  // aligned vectors at ab = j0 + t - SH cover them; out-of-frame samples are 0
+  const int groups = nl >> 3, total = ml * groups;
+  constexpr int U = 4;
+  for (int e0 = threadIdx.x; e0 < total; e0 += U * blockDim.x) {
+    uint4 lo[U], hi[U];
+    int ii[U], jj[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int e = e0 + k * blockDim.x;
+      const int ec = e < total ? e : 0;
+      ii[k] = ec / groups;
+      jj[k] = (ec % groups) * 8;
+      const int r = ii[k] + s, ab = jj[k] + t - SH;
+      const bool rok = e < total && r >= 0 && r < ml;
+      const uint16_t *row = A + (int64_t)(rok ? r : 0) * pitch;
+      lo[k] = (rok && ab >= 0 && ab + 8 <= nl) ? __ldcs(reinterpret_cast<const uint4 *>(row + ab)) : make_uint4(0, 0, 0, 0);
+      hi[k] = (SH && rok && ab + 8 >= 0 && ab + 16 <= nl) ? __ldcs(reinterpret_cast<const uint4 *>(row + ab + 8))
+                                                          : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int e = e0 + k * blockDim.x;
+      if (e >= total) continue;
+      const uint32_t w[8] = {lo[k].x, lo[k].y, lo[k].z, lo[k].w, hi[k].x, hi[k].y, hi[k].z, hi[k].w};
+      uint32_t o[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e2 = SH + 2 * q;
+        o[q] = (e2 & 1) ? __funnelshift_r(w[e2 >> 1], w[(e2 >> 1) + 1], 16) : w[e2 >> 1];
+      }
+      __stcs(reinterpret_cast<uint4 *>(O + (int64_t)ii[k] * nl + jj[k]), make_uint4(o[0], o[1], o[2], o[3]));
+    }
+  }
+}
+
+// One CTA per frame: argmin of the nine candidates, then (level 0) the corrected frame.
+__global__ void __launch_bounds__(256) k_refine_pick(RefinePickArgs a) {
+  __shared__ int res[2];
+  const int64_t f = blockIdx.x;
+  const int S = 2 * a.shift_in[2 * f], T = 2 * a.shift_in[2 * f + 1];
+  const int ml = a.ml, nl = a.nl;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    u64 *acc = a.acc + f * 18;
+    Key k{~0ull, ~0u};
+    if (lane < 9) {
+      const int c = lane;
+      const u64 h = acc[c], ga = acc[9 + c];
+      const int s = S + c / 3 - 1, t = T + c % 3 - 1, n1 = nl + 1;
+      const int i0 = max(0, -s), i1 = ml - max(0, s), j0 = max(0, -t), j1 = nl - max(0, t);
+      const u64 gb = a.pb2[(int64_t)i1 * n1 + j1] - a.pb2[(int64_t)i0 * n1 + j1] -
+                     a.pb2[(int64_t)i1 * n1 + j0] + a.pb2[(int64_t)i0 * n1 + j0];
+      const u64 N = ga + gb - 2 * h;
+      const double area = (double)((ml - abs(s)) * (nl - abs(t)));
+      const double fv = (double)N / (a.scale * area);
+      k = Key{(u64)__double_as_longlong(fv), (unsigned)c};   // rank == (s,t) lexicographic order
+    }
+    k = warp_min_key(k);
+    if (lane < 18) acc[lane] = 0;   // ready for the next call
+    if (lane == 0) {
+      const int s = S + (int)(k.idx / 3) - 1, t = T + (int)(k.idx % 3) - 1;
+      a.shift_out[2 * f] = s;
+      a.shift_out[2 * f + 1] = t;
+      if (a.f_out) a.f_out[f] = __longlong_as_double((long long)k.f);
+      res[0] = s;
+      res[1] = t;
+    }
+  }
+  if (!a.corrected) return;
+  __syncthreads();
+  const int s = res[0], t = res[1];
+  const uint16_t *A = a.frames + f * a.fstride;
+  uint16_t *O = a.corrected + f * (int64_t)ml * nl;
+  switch (t & 7) {
+    case 0: pick_apply_rows<0>(A, O, a.pitch, s, t, ml, nl); break;
+    case 1: pick_apply_rows<1>(A, O, a.pitch, s, t, ml, nl); break;
+    case 2: pick_apply_rows<2>(A, O, a.pitch, s, t, ml, nl); break;
+    case 3: pick_apply_rows<3>(A, O, a.pitch, s, t, ml, nl); break;
+    case 4: pick_apply_rows<4>(A, O, a.pitch, s, t, ml, nl); break;
+    case 5: pick_apply_rows<5>(A, O, a.pitch, s, t, ml, nl); break;
+    case 6: pick_apply_rows<6>(A, O, a.pitch, s, t, ml, nl); break;
+    default: pick_apply_rows<7>(A, O, a.pitch, s, t, ml, nl); break;
+  }
+}
+
+// -------------------------------------------------------------- host helpers
+// Tensor maps (driver entry point fetched through the runtime: no -lcuda).
+inline PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+// 3-D u16 tensor [frames][rows][cols] with row pitch `pitch` and frame stride `fstride`
+// (elements); box = bw columns x bh rows x 1 frame; out-of-bounds elements read as 0.
+inline bool tmap_u16_3d(CUtensorMap *tm, const void *base, int cols, int rows, int64_t frames, int pitch,
+                        int64_t fstride, int bw, int bh) {
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)frames};
+  const cuuint64_t strides[2] = {(cuuint64_t)pitch * 2, (cuuint64_t)fstride * 2};
+  const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void *>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace moco

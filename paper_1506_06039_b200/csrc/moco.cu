@@ -18,6 +18,7 @@
 #include "moco.h"
 #include "kernels_direct.cuh"
 #include "kernels_tc.cuh"
+#include "kernels_refine.cuh"
 
 using namespace moco;
 
@@ -45,13 +46,17 @@ struct moco_plan {
   size_t esz[3];              // element size per level
   void *tpl[3];               // template pyramid
   void *gb;                   // W*W template energies (u64 or double)
-  u64 *cb[3];                 // refine levels: template column prefix of b^2 [(ml+1)][nl]
-  int rpad[3];                // refine levels: zero columns staged each side of a frame row
+  u64 *pb2[3];                // refine levels: 2-D prefix of b^2 [(ml+1)][(nl+1)]
+  int rstages[3];             // refine levels: bulk-copy ring depth
+  int rrt[3], rnrt[3];        // refine levels: template rows per tile, row tiles
+  u64 *racc;                  // refine accumulators [cap][18] (kept zero between calls)
+  int nsm;                    // multiprocessors of the plan's device
   int64_t cap;                // frames per internal batch
   void *scratch[3];           // frame pyramid levels 1..L for one batch
   int32_t *sh[3];             // per-level shifts for one batch
   bool has_tpl;
   bool simple_refine;         // MOCO_REFINE=simple: unfused K6/K7 (cross-check in tests)
+  int simple_level;           // MOCO_REFINE=simpleN: simple K6 at level N only (debug)
   int64_t launches;
   // coarse kernel launch geometry
   int c_threads, c_sc, c_br, c_fpitch;
@@ -146,8 +151,9 @@ static void plan_free(moco_plan *p) {
     if (p->sh[l]) cudaFree(p->sh[l]);
   }
   if (p->gb) cudaFree(p->gb);
+  if (p->racc) cudaFree(p->racc);
   for (int l = 0; l < 3; ++l)
-    if (p->cb[l]) cudaFree(p->cb[l]);
+    if (p->pb2[l]) cudaFree(p->pb2[l]);
   tc_free(&p->tc);
   for (int k = 0; k < 2; ++k) {
     if (p->slot_in[k]) cudaFree(p->slot_in[k]);
@@ -185,13 +191,17 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
     return MOCO_ECUDA;
   }
   CK(cudaSetDevice(device));
+  int nsm = 0;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
   moco_plan *p = new (std::nothrow) moco_plan();
   if (!p) return MOCO_ENOMEM;
+  p->nsm = nsm;
   p->m = m; p->n = n; p->w = w; p->W = 2 * w - 1; p->levels = levels; p->dtype = dtype;
   p->bits = dtype == MOCO_U16 ? bits : 0; p->device = device;
   {
     const char *e = getenv("MOCO_REFINE");
     p->simple_refine = e && strcmp(e, "simple") == 0;
+    p->simple_level = (e && strncmp(e, "simple", 6) == 0 && e[6] >= '0' && e[6] <= '9') ? e[6] - '0' : -1;
   }
   for (int l = 0; l <= levels; ++l) {
     p->ml[l] = m >> l;
@@ -224,11 +234,25 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
   for (int l = 1; l <= levels; ++l)
     alloc(&p->scratch[l], (size_t)p->cap * p->ml[l] * p->pitch[l] * p->esz[l]);
   for (int l = 0; l <= levels; ++l) alloc((void **)&p->sh[l], (size_t)p->cap * 2 * sizeof(int32_t));
+  if (dtype == MOCO_U16 && levels > 0) {
+    alloc((void **)&p->racc, (size_t)p->cap * 18 * sizeof(u64));
+    if (rc == MOCO_OK && cudaMemset(p->racc, 0, (size_t)p->cap * 18 * sizeof(u64)) != cudaSuccess) rc = MOCO_ENOMEM;
+  }
   if (dtype == MOCO_U16)
     for (int l = 0; l < levels; ++l) {
-      alloc((void **)&p->cb[l], (size_t)(p->ml[l] + 1) * p->nl[l] * sizeof(u64));
-      // |T| at level l <= 2^(L-l) * w (doubled shift from the level above)
-      p->rpad[l] = ((w << (levels - l)) + 10 + 7) / 8 * 8;
+      alloc((void **)&p->pb2[l], (size_t)(p->ml[l] + 1) * (p->nl[l] + 1) * sizeof(u64));
+      // template-stationary refine (kernels_refine.cuh): row tiles x 256-column tiles
+      // sized to about one CTA per SM, rows per tile <= RS_MAXRT; ring as deep as fits
+      const int nct = (p->nl[l] + RS_CT - 1) / RS_CT;
+      int nrt = std::min(p->ml[l], std::max(1, nsm / nct));
+      int rt = (p->ml[l] + nrt - 1) / nrt;
+      if (rt > RS_MAXRT) {
+        rt = RS_MAXRT;
+        nrt = (p->ml[l] + rt - 1) / rt;
+      }
+      p->rrt[l] = rt;
+      p->rnrt[l] = nrt;
+      p->rstages[l] = std::min(32, (200 * 1024 - rs_smem_bytes(rt, 0)) / rs_stage_bytes(rt));
     }
   if (rc != MOCO_OK) { plan_free(p); return rc; }
   p->algo = MOCO_ALGO_DIRECT;
@@ -374,45 +398,64 @@ static int launch_refine(moco_plan *p, int l, const void *img, int64_t fstride, 
   return MOCO_OK;
 }
 
-// K6 (+K7 at level 0): fused u16 kernel when 32-bit partial sums are safe.
-static int launch_refine_apply(moco_plan *p, int l, const void *img, int64_t fstride, int64_t B,
-                               const int32_t *sin, int32_t *sout, double *fout, void *corr,
-                               cudaStream_t st) {
+// K6 (+K7 at level 0): template-stationary u16 refine (kernels_refine.cuh):
+// k_refine_sums (per-frame sums) then k_refine_pick (argmin + apply).
+static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride, int64_t B,
+                           const int32_t *sin, int32_t *sout, double *fout, void *corr, cudaStream_t st) {
   const int vb = p->bits + 2 * l;
-  RefineApplyArgs a;
-  a.frames = (const uint16_t *)img; a.fstride = fstride; a.pitch = p->pitch[l];
+  RefineSumArgs a;
   a.tpl = (const uint16_t *)p->tpl[l]; a.tpitch = p->pitch[l];
   a.ml = p->ml[l]; a.nl = p->nl[l];
-  a.scale = (double)(1u << (4 * l));
-  a.B = (int)B; a.shift_in = sin; a.shift_out = sout; a.f_out = fout;
-  a.corrected = (uint16_t *)corr;
-  a.pad = p->rpad[l];
-  a.cb = p->cb[l];
-  const double dmax = (double)((1u << vb) - 1);
-  a.flush = (int)std::min(1024.0, std::floor(4294967295.0 / (8.0 * dmax * dmax)));
+  a.B = (int)B; a.shift_in = sin; a.acc = p->racc;
+  a.rt = p->rrt[l]; a.nrt = p->rnrt[l]; a.stages = p->rstages[l];
+  // 32-bit lane partials hold (256-column halves) x rt rows x 8 products, each
+  // <= (2^vb - 1)^2, unless flushed to 64 bits after every row
+  {
+    const double halves = (double)((std::min(a.nl, RS_CT) + 255) / 256);
+    const double mx = (std::ldexp(1.0, vb) - 1.0) * (std::ldexp(1.0, vb) - 1.0);
+    a.wide = halves * a.rt * 8.0 * mx >= 4294967296.0 ? 1 : 0;
+  }
+  CUtensorMap tmF;
+  if (!tmap_u16_3d(&tmF, img, a.nl, a.ml, B, p->pitch[l], fstride, RS_BOX, a.rt + 2)) {
+    snprintf(g_err, sizeof(g_err), "cuTensorMapEncodeTiled failed (refine level %d)", l);
+    return MOCO_ECUDA;
+  }
+  RefinePickArgs b;
+  b.frames = (const uint16_t *)img; b.fstride = fstride; b.pitch = p->pitch[l];
+  b.pb2 = p->pb2[l]; b.ml = p->ml[l]; b.nl = p->nl[l];
+  b.scale = (double)(1u << (4 * l));
+  b.B = (int)B; b.shift_in = sin; b.acc = p->racc; b.shift_out = sout; b.f_out = fout;
+  b.corrected = (uint16_t *)corr;
   {
     ProfScope ps(p, MOCO_K_REFINE, st);
-    const int smem = 2 * (2 * REF_RB + 2) * (p->nl[l] + 2 * p->rpad[l] + 8) * 2;
+    const int smem = rs_smem_bytes(a.rt, a.stages);
     static int attr_smem = 0;
     if (smem > attr_smem) {
-      CK(cudaFuncSetAttribute(k_refine_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      CK(cudaFuncSetAttribute(k_refine_sums<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      CK(cudaFuncSetAttribute(k_refine_sums<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       attr_smem = smem;
     }
-    k_refine_apply<<<(unsigned)B, 256, smem, st>>>(a);
+    const int nct = (a.nl + RS_CT - 1) / RS_CT;
+    if (a.wide) k_refine_sums<true><<<(unsigned)(a.nrt * nct), RS_THREADS, smem, st>>>(tmF, a);
+    else k_refine_sums<false><<<(unsigned)(a.nrt * nct), RS_THREADS, smem, st>>>(tmF, a);
   }
   p->launches++;
-  CKL("k_refine_apply");
+  CKL("k_refine_sums");
+  {
+    ProfScope ps(p, MOCO_K_APPLY, st);
+    k_refine_pick<<<(unsigned)B, 256, 0, st>>>(b);
+  }
+  p->launches++;
+  CKL("k_refine_pick");
   return MOCO_OK;
 }
 
 static bool fused_ok(const moco_plan *p, int l) {
-  if (p->simple_refine || p->dtype != MOCO_U16 || p->bits + 2 * l > 14) return false;
-  // 32-bit partial sums must hold one band's items per thread (see refine_rows)
+  if (p->simple_refine || p->simple_level == l || p->dtype != MOCO_U16) return false;
+  // 32-bit partial sums: one template row adds 8 products (or one 8-square window sum)
   const double dmax = (double)((1u << (p->bits + 2 * l)) - 1);
-  const double flush = std::floor(4294967295.0 / (8.0 * dmax * dmax));
-  const int per_band = ((p->nl[l] + 7) / 8 + 31) / 32;
-  const size_t smem = 2 * (2 * REF_RB + 2) * (size_t)(p->nl[l] + 2 * p->rpad[l] + 8) * 2;
-  return flush >= per_band && p->nl[l] % 8 == 0 && smem <= 200 * 1024;
+  if (8.0 * dmax * dmax >= 2147483648.0) return false;   // one row's 8 products in 32 bits
+  return p->nl[l] % 8 == 0 && p->rstages[l] >= 2 && p->racc;
 }
 
 static int launch_apply(moco_plan *p, const void *in, void *out, const int32_t *sh, int64_t B,
@@ -455,9 +498,10 @@ int moco_set_template(moco_plan *p, const void *d_template, moco_stream_t stream
   CKL("k_template_energy");
   if (p->dtype == MOCO_U16)
     for (int l = 0; l < L; ++l) {
-      k_colprefix_u16<<<(p->nl[l] + 127) / 128, 128, 0, st>>>((const uint16_t *)p->tpl[l], p->pitch[l],
-                                                                p->ml[l], p->nl[l], p->cb[l]);
-      CKL("k_colprefix_u16");
+      k_prefix2d_rows<<<(p->ml[l] + 128) / 128, 128, 0, st>>>((const uint16_t *)p->tpl[l], p->pitch[l],
+                                                               p->ml[l], p->nl[l], p->pb2[l]);
+      k_prefix2d_cols<<<(p->nl[l] + 128) / 128, 128, 0, st>>>(p->ml[l], p->nl[l], p->pb2[l]);
+      CKL("k_prefix2d");
     }
   if (p->tc.ready) {
     if (tc_set_template(&p->tc, (const uint16_t *)p->tpl[L], p->pitch[L], st) != 0)
@@ -524,7 +568,7 @@ static int refine_levels(moco_plan *p, const void *const *img, const int64_t *fs
     double *fo = l == 0 ? fmin_b : nullptr;
     int rc;
     if (fused_ok(p, l))
-      rc = launch_refine_apply(p, l, img[l], fstride[l], B, p->sh[l + 1], so, fo, l == 0 ? corr_b : nullptr, st);
+      rc = launch_refine_h(p, l, img[l], fstride[l], B, p->sh[l + 1], so, fo, l == 0 ? corr_b : nullptr, st);
     else
       rc = launch_refine(p, l, img[l], fstride[l], B, p->sh[l + 1], so, fo, st);
     if (rc) return rc;

@@ -14,12 +14,13 @@ ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--frames", type=int, default=1184)
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--algo", default="auto")
+ap.add_argument("--no-corrected", action="store_true")
 args = ap.parse_args()
 spec = config_spec(args.config, T=args.frames)
 st = make_stack(spec, 0, args.frames, device="cuda")
 p = Plan(spec.m, spec.n, spec.w, spec.levels, spec.dtype, 12, device=0, algo=args.algo)
 p.set_template(st.template)
 for _ in range(args.iters):
-    sh, fm, co, _ = p.align(st.frames)
+    sh, fm, co, _ = p.align(st.frames, corrected=not args.no_corrected)
 torch.cuda.synchronize()
 print("ok", p.algo, sh[:2].tolist())
