@@ -228,8 +228,41 @@ __device__ __forceinline__ void coarse_pairs(const uint16_t *base, int n, uint32
   }
 }
 
+// 8 consecutive coarse values (2^L x 2^L block sums) of one coarse row as 4 pair-words.
 template <int L>
-__global__ void __launch_bounds__(256) k_tc_prep(TcPrepArgs a) {
+__device__ __forceinline__ void coarse8(const uint16_t *base, int n, uint32_t (&P)[4]) {
+  if constexpr (L == 0) {
+    const uint4 u = __ldcs(reinterpret_cast<const uint4 *>(base));
+    P[0] = u.x; P[1] = u.y; P[2] = u.z; P[3] = u.w;
+  } else {
+    constexpr int bs = 1 << L, nv = bs;           // raw 16-byte vectors per raw row (8 bs samples)
+    uint32_t s[4 * nv];                           // raw column pairs summed over the bs rows
+#pragma unroll
+    for (int k = 0; k < 4 * nv; ++k) s[k] = 0;
+#pragma unroll
+    for (int dy = 0; dy < bs; ++dy)
+#pragma unroll
+      for (int q = 0; q < nv; ++q) {
+        const uint4 u = __ldcs(reinterpret_cast<const uint4 *>(base + (int64_t)dy * n + q * 8));
+        s[4 * q + 0] += u.x; s[4 * q + 1] += u.y; s[4 * q + 2] += u.z; s[4 * q + 3] += u.w;   // halves < 2^14: no carry
+      }
+    // fold: coarse value k = both halves of its bs/2 raw pair words
+    uint32_t c[8];
+    constexpr int wpc = bs / 2;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      uint32_t acc = 0;
+#pragma unroll
+      for (int j = 0; j < wpc; ++j) acc += (s[k * wpc + j] & 0xffffu) + (s[k * wpc + j] >> 16);
+      c[k] = acc;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) P[k] = c[2 * k] | (c[2 * k + 1] << 16);
+  }
+}
+
+template <int L>
+__global__ void __launch_bounds__(256, 4) k_tc_prep(TcPrepArgs a) {
   const TcGeom &g = a.g;
   extern __shared__ __align__(16) unsigned char smem[];
   const int F = g.F, hw = g.hw, w = g.w, mc = g.mc, nc = g.nc, W = g.W;
@@ -242,83 +275,100 @@ __global__ void __launch_bounds__(256) k_tc_prep(TcPrepArgs a) {
   for (int k = tid; k < F * (4 * hw + 4 * CS + 1); k += nth) rowE[k] = 0;
   __syncthreads();
   const int grp = blockIdx.x;
-  constexpr int bs = 1 << L;
-  // thread -> fixed frame f of the group; rows r = tid/F, + nth/F, ...
-  const int f = tid % F, rstep = nth / F;
+  // warp = one (frame, plane row) item at a time, lanes = 8-column chunks of the coarse
+  // row: every load instruction reads 512 contiguous bytes of a raw row (L >= 1 folds
+  // 2^L raw rows); energies: row sums by warp reduction, edge columns by atomics on
+  // distinct addresses, corner tables by plain stores
+  const int warp = tid >> 5, lane = tid & 31, nwarp = nth >> 5;
+  const int nchunk = nc >> 3;
+  // F divides the warp count, so a warp always works on the same frame f = warp % F;
+  // edge-column energies accumulate in registers (a lane owns at most one left-edge
+  // and one right-edge chunk) and are added to shared memory once at the end
+  const int f = warp % F;
   const int fi = grp * F + f;
-  const bool fvalid = fi < a.B;
-  const uint16_t *frame = a.frames + (int64_t)(fvalid ? fi : 0) * a.fstride;
-  u64 mytot = 0;
-  for (int sk = 0; sk < 2 * g.nstrips; ++sk) {
-    const int st = sk >> 1, kc = sk & 1;
-    const int c0 = st * 32 + kc * 16;
-    uint8_t *dbase = a.G + (((int64_t)grp * g.nstrips + st) * 2 + kc) * g.R * (32 * F) + f * 32;
-    for (int r = tid / F; r < g.R; r += rstep) {
-      const int cr = r - hw;
-      const bool live = fvalid && cr >= 0 && cr < mc;   // c0 < nc always (nc % 32 == 0)
-      uint32_t P[8];
-      if (live) {
-        coarse_pairs<L>(frame + (int64_t)(cr * bs) * a.n + c0 * bs, a.n, P);
-      } else {
+  const uint16_t *frame = a.frames + (int64_t)(fi < a.B ? fi : 0) * a.fstride;
+  // this warp's edge-column sums (left hw, right hw), owned by the warp: no atomics
+  u64 *ce = tot + F + warp * 2 * hw;
+  for (int k = lane; k < 2 * hw; k += 32) ce[k] = 0;
+  __syncwarp();
+  u64 ftot = 0;
+  auto item = [&](int pr, const uint32_t (&P)[4], int cc, bool live, u64 &rs) {
+    const int cr = pr - hw;
+    const uint32_t h0 = (P[0] >> 7) & 0x007F007Fu, h1 = (P[1] >> 7) & 0x007F007Fu;
+    const uint32_t h2 = (P[2] >> 7) & 0x007F007Fu, h3 = (P[3] >> 7) & 0x007F007Fu;
+    const uint2 hi = make_uint2(__byte_perm(h0, h1, 0x6420), __byte_perm(h2, h3, 0x6420));
+    const uint2 lo = make_uint2(__byte_perm(P[0] & 0x007F007Fu, P[1] & 0x007F007Fu, 0x6420),
+                                __byte_perm(P[2] & 0x007F007Fu, P[3] & 0x007F007Fu, 0x6420));
+    uint8_t *dst = a.G + ((((int64_t)grp * g.nstrips + (cc >> 2)) * 2 + ((cc >> 1) & 1)) * g.R + pr) * (32 * F) +
+                   f * 32 + (cc & 1) * 8;
+    *reinterpret_cast<uint2 *>(dst) = hi;
+    *reinterpret_cast<uint2 *>(dst + 16) = lo;
+    if (!live) return;
+    uint32_t v[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) P[k] = 0;
-      }
-      // int8 parts: hi = v >> 7, lo = v & 127, two coarse values per word, four per byte-word
-      uint32_t hi[4], lo[4];
+    for (int k = 0; k < 4; ++k) { v[2 * k] = P[k] & 0xffffu; v[2 * k + 1] = P[k] >> 16; }
+    uint32_t cs = 0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t h0 = (P[2 * q] >> 7) & 0x007F007Fu, h1 = (P[2 * q + 1] >> 7) & 0x007F007Fu;
-        const uint32_t l0 = P[2 * q] & 0x007F007Fu, l1 = P[2 * q + 1] & 0x007F007Fu;
-        hi[q] = __byte_perm(h0, h1, 0x6420);
-        lo[q] = __byte_perm(l0, l1, 0x6420);
-      }
-      uint8_t *dst = dbase + r * (32 * F);
-      *reinterpret_cast<uint4 *>(dst) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-      *reinterpret_cast<uint4 *>(dst + 16) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-      if (!live) continue;
-      // energies (S2): totals, edge strips, corners
-      uint32_t rs = 0;
+    for (int x = 0; x < 8; ++x) cs += v[x] * v[x];   // 8 terms < 2^28: < 2^31
+    rs += cs;
+    const int c0 = cc * 8;
+    const bool eL = c0 < hw, eR = c0 + 8 > nc - hw;
+    if (!(eL || eR)) return;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint32_t v0 = P[k] & 0xffffu, v1 = P[k] >> 16;
-        rs += v0 * v0 + v1 * v1;   // 16 terms < 2^28 each: < 2^32
-      }
-      mytot += rs;
-      const bool top = cr < hw, bot = cr >= mc - hw;
-      if (top) atomicAdd(&rowE[f * 2 * hw + cr], (u64)rs);
-      if (bot) atomicAdd(&rowE[f * 2 * hw + hw + (mc - 1 - cr)], (u64)rs);
-      if (c0 >= hw && c0 + 16 <= nc - hw) continue;   // no edge column in this item
-      uint32_t v[16];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) { v[2 * k] = P[k] & 0xffffu; v[2 * k + 1] = P[k] >> 16; }
-#pragma unroll
-      for (int x = 0; x < 16; ++x) {
-        const int c = c0 + x;
-        const bool lf = c < hw, rt = c >= nc - hw;
-        if (!(lf || rt)) continue;
-        const u64 v2 = (u64)(v[x] * v[x]);
-        if (lf) atomicAdd(&colE[f * 2 * hw + c], v2);
-        if (rt) atomicAdd(&colE[f * 2 * hw + hw + (nc - 1 - c)], v2);
-        if (top || bot) {
-          for (int qb = 0; qb < 2; ++qb) {
-            if (!(qb ? bot : top)) continue;
-            const int p = qb ? mc - cr : cr + 1;
-            for (int qr = 0; qr < 2; ++qr) {
-              if (!(qr ? rt : lf)) continue;
-              const int qq = qr ? nc - c : c + 1;
-              cor[((f * 4) + (qb * 2 + qr)) * CS + p * w + qq] = v2;
-            }
-          }
+    for (int x = 0; x < 8; ++x) {
+      const int c = c0 + x;
+      const u64 v2 = (u64)(v[x] * v[x]);
+      if (c < hw) ce[c] += v2;                        // distinct columns per lane
+      if (c >= nc - hw) ce[hw + (nc - 1 - c)] += v2;
+    }
+    const bool top = cr < hw, bot = cr >= mc - hw;
+    if (!(top || bot)) return;
+    for (int x = 0; x < 8; ++x) {   // corner tables of the DP: plain stores
+      const int c = c0 + x;
+      const bool lf = c < hw, rt = c >= nc - hw;
+      const u64 v2 = (u64)(v[x] * v[x]);
+      for (int qb = 0; qb < 2; ++qb) {
+        if (!(qb ? bot : top)) continue;
+        const int pp = qb ? mc - cr : cr + 1;
+        for (int qr = 0; qr < 2; ++qr) {
+          if (!(qr ? rt : lf)) continue;
+          const int qq = qr ? nc - c : c + 1;
+          cor[((f * 4) + (qb * 2 + qr)) * CS + pp * w + qq] = v2;
         }
       }
     }
+  };
+  auto row_done = [&](int pr, bool live, u64 rs) {
+    if (!live) return;
+    const int cr = pr - hw;
+    rs = warp_sum(rs);
+    if (lane == 0) {
+      ftot += rs;
+      if (cr < hw) rowE[f * 2 * hw + cr] = rs;
+      if (cr >= mc - hw) rowE[f * 2 * hw + hw + (mc - 1 - cr)] = rs;
+    }
+  };
+  // plane rows pr = warp / F, + nwarp / F, ...; two rows per pass (loads first)
+  const int pstep = nwarp / F;
+  for (int pr = warp / F; pr < g.R; pr += 2 * pstep) {
+    const int pr2 = pr + pstep;
+    const bool live1 = fi < a.B && pr - hw >= 0 && pr - hw < mc;
+    const bool live2 = fi < a.B && pr2 < g.R && pr2 - hw >= 0 && pr2 - hw < mc;
+    u64 rs1 = 0, rs2 = 0;
+    for (int cc = lane; cc < nchunk; cc += 32) {
+      uint32_t P1[4] = {0, 0, 0, 0}, P2[4] = {0, 0, 0, 0};
+      if (live1) coarse8<L>(frame + (int64_t)((pr - hw) << L) * a.n + ((cc * 8) << L), a.n, P1);
+      if (live2) coarse8<L>(frame + (int64_t)((pr2 - hw) << L) * a.n + ((cc * 8) << L), a.n, P2);
+      item(pr, P1, cc, live1, rs1);
+      if (pr2 < g.R) item(pr2, P2, cc, live2, rs2);
+    }
+    row_done(pr, live1, rs1);
+    if (pr2 < g.R) row_done(pr2, live2, rs2);
   }
-  // totals: a warp's lanes cover all F frames (F | 32), so reduce within lanes of equal f
-  {
-    u64 sum = mytot;
-    for (int o = 16; o >= F; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if ((tid & 31) < F) atomicAdd(&tot[f], sum);
-  }
+  // flush this warp's edge-column and total energies
+  __syncwarp();
+  for (int k = lane; k < 2 * hw; k += 32) atomicAdd(&colE[f * 2 * hw + k], ce[k]);
+  if (lane == 0) atomicAdd(&tot[f], ftot);
   __syncthreads();
   // prefix sums: edge strips (1-D), corners (2-D, the DP of P:35 in each corner)
   for (int k = tid; k < F * 4; k += nth) {
@@ -340,7 +390,6 @@ __global__ void __launch_bounds__(256) k_tc_prep(TcPrepArgs a) {
     const int f = k / (W * W), lag = k % (W * W);
     const int fi = grp * F + f;
     if (fi >= a.B) continue;
-    (void)fvalid;
     const int s = lag / W - hw, t = lag % W - hw;
     const u64 *re = rowE + f * 2 * hw, *ce = colE + f * 2 * hw;
     // rows of the frame outside the frame-side rectangle of D_{s,t}:
@@ -682,7 +731,7 @@ inline bool tc_make_geom(TcGeom *gp, int w, int mc, int nc, int L) {
   while (cols < g.GG * g.NT * g.N) cols <<= 1;
   g.tmem_cols = cols;
   g.smem = smem_for(g.GG, g.ICH);
-  g.prep_smem = (g.F * (4 * g.hw + 4 * w * w + 1)) * 8;
+  g.prep_smem = (g.F * (4 * g.hw + 4 * w * w + 1) + 8 * 2 * g.hw) * 8;   // + per-warp edge-column sums
   *gp = g;
   return true;
 }
