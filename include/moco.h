@@ -63,10 +63,12 @@ enum moco_status {
 
 /* Coarse-search algorithm for S3 (the cross term).  AUTO picks by problem
  * size from measurement. */
-enum moco_algo { MOCO_ALGO_AUTO = 0, MOCO_ALGO_DIRECT = 1, MOCO_ALGO_TC = 2 };
+enum moco_algo { MOCO_ALGO_AUTO = 0, MOCO_ALGO_DIRECT = 1, MOCO_ALGO_TC = 2, MOCO_ALGO_FFT = 3 };
 
 /* Per-frame flag bits written to d_flags/h_flags when non-NULL. */
 #define MOCO_FLAG_EDGE 0x1u     /* coarse argmin on the window edge |s| or |t| = w-1 */
+#define MOCO_FLAG_FULL 0x2u     /* FFT path: certified candidate set exceeded its cap, every
+                                   coarse lag was re-scored exactly (result still exact) */
 
 /*
  * moco_plan_create -- validate the problem and allocate the workspace.
@@ -87,9 +89,10 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
                      int bits, int device);
 
 /* Force the coarse-search algorithm (tests/benchmarks); EINVAL if unsupported
- * for this plan (MOCO_ALGO_TC needs MOCO_U16 with bits + 2*levels <= 14). */
+ * for this plan (MOCO_ALGO_TC needs MOCO_U16 with bits + 2*levels <= 14;
+ * MOCO_ALGO_FFT needs MOCO_U16; MOCO_ALGO_DIRECT needs w <= 64). */
 int moco_plan_set_algo(moco_plan *p, int algo);
-/* Algorithm AUTO resolved to for this plan (MOCO_ALGO_DIRECT or MOCO_ALGO_TC). */
+/* Algorithm AUTO resolved to for this plan (MOCO_ALGO_DIRECT, _TC or _FFT). */
 int moco_plan_get_algo(const moco_plan *p);
 
 /*
@@ -136,6 +139,17 @@ int moco_align_host(moco_plan *p, const void *h_frames, int64_t T, int32_t *h_sh
  */
 int moco_score_grid(moco_plan *p, const void *d_frames, int64_t T, double *d_f,
                     moco_stream_t stream);
+
+/*
+ * moco_fft_cross -- diagnostics of the FFT path (S3 by FFT): for each of T
+ * device frames, d_h[k][s+w-1][t+w-1] = the fp32 FFT cross term h~(s,t) at the
+ * coarsest level (float [T][2w-1][2w-1]), d_shifts[k] = the certified exact coarse
+ * argmin (int32 [T][2], coarse pixels), d_qcount[k] = how many lags were re-scored
+ * exactly (int32 [T], may be NULL).  Works whatever algorithm the plan uses; EINVAL
+ * for non-U16 plans.  Same other errors as moco_align_batch.
+ */
+int moco_fft_cross(moco_plan *p, const void *d_frames, int64_t T, float *d_h, int32_t *d_shifts,
+                   int32_t *d_qcount, moco_stream_t stream);
 
 /* Number of kernel launches the last moco_align_batch/moco_score_grid issued. */
 int64_t moco_last_launch_count(const moco_plan *p);

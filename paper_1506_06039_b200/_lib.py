@@ -18,9 +18,10 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MOCO_LIB") or os.path.join(_HERE, "libmoco.so")
 
 MOCO_U16, MOCO_F32 = 1, 2
-MOCO_ALGO_AUTO, MOCO_ALGO_DIRECT, MOCO_ALGO_TC = 0, 1, 2
-ALGO_NAMES = {MOCO_ALGO_DIRECT: "direct", MOCO_ALGO_TC: "tc"}
+MOCO_ALGO_AUTO, MOCO_ALGO_DIRECT, MOCO_ALGO_TC, MOCO_ALGO_FFT = 0, 1, 2, 3
+ALGO_NAMES = {MOCO_ALGO_DIRECT: "direct", MOCO_ALGO_TC: "tc", MOCO_ALGO_FFT: "fft"}
 FLAG_EDGE = 0x1
+FLAG_FULL = 0x2
 
 # (name, restype, argtypes) for every symbol declared in include/moco.h
 _P = ctypes.c_void_p
@@ -34,6 +35,7 @@ SIGNATURES = [
     ("moco_align_batch", _I, [_P, _P, _I64, _P, _P, _P, _P, _P]),
     ("moco_align_host", _I, [_P, _P, _I64, _P, _P, _P, _P]),
     ("moco_score_grid", _I, [_P, _P, _I64, _P, _P]),
+    ("moco_fft_cross", _I, [_P, _P, _I64, _P, _P, _P, _P]),
     ("moco_last_launch_count", _I64, [_P]),
     ("moco_profile_enable", _I, [_P, _I]),
     ("moco_profile_read", _I, [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64), _I]),
@@ -110,7 +112,7 @@ class Plan:
 
     # -- algorithm selection (tests/bench)
     def set_algo(self, algo: str):
-        code = {"auto": MOCO_ALGO_AUTO, "direct": MOCO_ALGO_DIRECT, "tc": MOCO_ALGO_TC}[algo]
+        code = {"auto": MOCO_ALGO_AUTO, "direct": MOCO_ALGO_DIRECT, "tc": MOCO_ALGO_TC, "fft": MOCO_ALGO_FFT}[algo]
         _check(load().moco_plan_set_algo(self._h, code), "moco_plan_set_algo")
         return self
 
@@ -178,6 +180,18 @@ class Plan:
         _check(load().moco_score_grid(self._h, _ptr(frames), frames.shape[0], _ptr(out), self._stream()),
                "moco_score_grid")
         return out
+
+    def fft_cross(self, frames: torch.Tensor):
+        """FFT-path diagnostics: (h~ float32 (T, 2w-1, 2w-1), certified coarse shifts int32 (T, 2),
+        exactly re-scored candidate counts int32 (T,))."""
+        self._frames_ok(frames)
+        T, W = frames.shape[0], 2 * self.w - 1
+        h = torch.empty((T, W, W), dtype=torch.float32, device=self.device)
+        sh = torch.empty((T, 2), dtype=torch.int32, device=self.device)
+        q = torch.empty((T,), dtype=torch.int32, device=self.device)
+        _check(load().moco_fft_cross(self._h, _ptr(frames), T, _ptr(h), _ptr(sh), _ptr(q), self._stream()),
+               "moco_fft_cross")
+        return h, sh, q
 
     def align_host(self, frames: torch.Tensor, shifts=None, fmin=None, corrected=None, flags=None):
         """End-to-end moco_align_host on HOST tensors (pinned for full speed)."""

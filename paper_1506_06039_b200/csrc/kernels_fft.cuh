@@ -1,0 +1,480 @@
+// kernels_fft.cuh -- S3 by FFT cross-correlation (the paper's method), with a
+// certified candidate set and exact rescoring (S4), for MOCO_U16.
+//
+// The cross term of P:31 for every coarse lag,
+//     h(s,t) = sum_{(i,j) in D_{s,t}} a[i+s][j+t] b[i][j],
+// is a circular cross-correlation once a and b are zero-padded to Mr x Mc with
+// Mr >= m_c + w - 1 and Mc >= n_c + w - 1 (no wrap-around for |s|,|t| <= w-1):
+//     H = IFFT2( FFT2(a_pad) . conj(FFT2(b_pad)) ),   h(s,t) = H[s mod Mr][t mod Mc]
+// (the paper writes it with the rotated template b^ and pad m+w; the two are
+// the same numbers -- pinned in tests/test_oracle_pins.py).  The sizes are products of
+// 2, 3, 4, 5 (288 = 4*4*2*3*3 for 256 + 31 or + 63) and every 1-D transform is a
+// shared-memory Stockham autosort FFT (natural order in and out, no bit reversal).
+//
+//   k_fft_rows    two real rows packed as one complex row -> FFT_Mc -> Hermitian halves,
+//                 stored column-major per frame: S[f][k][row], k in [0, Mc/2]
+//   k_fft_cols    per column bin k: FFT_Mr over rows, times conj(B^)/(Mr Mc), IFFT_Mr,
+//                 keep only the 2w-1 lag rows: P[f][s+w-1][k]   (template: store conj(B^))
+//   k_fft_score   per frame: two lag rows packed -> IFFT_Mc -> h~(s,t); then the
+//                 certified search of S4 (below) and exact rescoring
+//
+// fp32 certification (S4): with |h~ - h| <= eps_h = C u log2(Mr Mc) ||a||_2 ||b||_2
+// (u = 2^-24; C = RS_FFT_C, validated against exact h in the GPU tests), the score
+// f~ = (g_a + g_b - 2 h~) / (16^L A) is within delta = 2 eps_h / (16^L A) of the exact
+// f.  Every lag whose interval [f~ - delta, f~ + delta] reaches below min(f~ + delta)
+// is re-scored EXACTLY (64-bit integer direct sum of P:31) and the argmin of the key
+// (f, s, t) is taken over those exact values -- the result is the exact method's,
+// bit for bit.  More than FFT_QCAP candidates: every lag is re-scored (flag bit 1).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kernels_direct.cuh"
+
+namespace moco {
+
+constexpr double RS_FFT_C = 8.0;   // error-bound constant (measured max ~0.5)
+constexpr int FFT_QCAP = 64;
+constexpr int FFT_MAXST = 10;
+
+struct FftLen {
+  int N, nst;
+  int rad[FFT_MAXST];
+};
+
+// smallest N >= lo with N = 2^a 3^b 5^c, factored into radices 4, 2, 3, 5
+inline bool fft_len_make(int lo, FftLen *L) {
+  for (int N = lo; N < 4 * lo + 64; ++N) {
+    int x = N, c4 = 0, c2 = 0, c3 = 0, c5 = 0;
+    while (x % 4 == 0) { x /= 4; ++c4; }
+    while (x % 2 == 0) { x /= 2; ++c2; }
+    while (x % 3 == 0) { x /= 3; ++c3; }
+    while (x % 5 == 0) { x /= 5; ++c5; }
+    if (x != 1 || c4 + c2 + c3 + c5 > FFT_MAXST) continue;
+    L->N = N;
+    L->nst = 0;
+    for (int k = 0; k < c4; ++k) L->rad[L->nst++] = 4;
+    for (int k = 0; k < c2; ++k) L->rad[L->nst++] = 2;
+    for (int k = 0; k < c3; ++k) L->rad[L->nst++] = 3;
+    for (int k = 0; k < c5; ++k) L->rad[L->nst++] = 5;
+    return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) { return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
+
+// In-place R-point DFT, sign -1 (forward) or +1 (inverse).
+template <int R>
+__device__ __forceinline__ void dft_small(float2 (&v)[5], float sign) {
+  if constexpr (R == 2) {
+    const float2 a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  } else if constexpr (R == 4) {
+    const float2 a = cadd(v[0], v[2]), b = csub(v[0], v[2]);
+    const float2 c = cadd(v[1], v[3]), d = csub(v[1], v[3]);
+    // -i*sign*d for the forward (sign=-1) gives -i d
+    const float2 jd = make_float2(-sign * d.y, sign * d.x);   // i*sign*d
+    v[0] = cadd(a, c);
+    v[2] = csub(a, c);
+    v[1] = cadd(b, jd);
+    v[3] = csub(b, jd);
+  } else if constexpr (R == 3) {
+    const float c1 = -0.5f, s1 = sign * 0.86602540378443865f;
+    const float2 a = v[0], b = v[1], c = v[2];
+    const float2 t = cadd(b, c), u = csub(b, c);
+    v[0] = cadd(a, t);
+    const float2 m = make_float2(a.x + c1 * t.x, a.y + c1 * t.y);
+    const float2 r = make_float2(-s1 * u.y, s1 * u.x);   // i*s1*u
+    v[1] = cadd(m, r);
+    v[2] = csub(m, r);
+  } else {   // R == 5
+    const float c1 = 0.30901699437494742f, c2 = -0.80901699437494742f;
+    const float s1 = sign * 0.95105651629515357f, s2 = sign * 0.58778525229247313f;
+    const float2 a = v[0];
+    const float2 t1 = cadd(v[1], v[4]), u1 = csub(v[1], v[4]);
+    const float2 t2 = cadd(v[2], v[3]), u2 = csub(v[2], v[3]);
+    v[0] = cadd(a, cadd(t1, t2));
+    const float2 m1 = make_float2(a.x + c1 * t1.x + c2 * t2.x, a.y + c1 * t1.y + c2 * t2.y);
+    const float2 m2 = make_float2(a.x + c2 * t1.x + c1 * t2.x, a.y + c2 * t1.y + c1 * t2.y);
+    const float2 r1 = make_float2(-(s1 * u1.y + s2 * u2.y), s1 * u1.x + s2 * u2.x);   // i(s1 u1 + s2 u2)
+    const float2 r2 = make_float2(-(s2 * u1.y - s1 * u2.y), s2 * u1.x - s1 * u2.x);   // i(s2 u1 - s1 u2)
+    v[1] = cadd(m1, r1);
+    v[4] = csub(m1, r1);
+    v[2] = cadd(m2, r2);
+    v[3] = csub(m2, r2);
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void fft_stage(const float2 *x, float2 *y, const float2 *tw, int N, int Ns, int nfft,
+                                          float sign) {
+  const int nb = N / R, tstep = N / (Ns * R);
+  for (int e = threadIdx.x; e < nfft * nb; e += blockDim.x) {
+    const int f = e / nb, j = e - f * nb;
+    const float2 *in = x + f * N;
+    float2 *out = y + f * N;
+    const int k = j % Ns;
+    float2 v[5];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = in[j + r * nb];
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      float2 t = tw[(k * r * tstep) % N];   // exp(-2 pi i k r / (Ns R))
+      if (sign > 0) t.y = -t.y;
+      v[r] = cmul(v[r], t);
+    }
+    dft_small<R>(v, sign);
+    const int o = (j / Ns) * Ns * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) out[o + r * Ns] = v[r];
+  }
+}
+
+// nfft transforms of length L.N stored contiguously in x; y is scratch of the same
+// size.  Returns the buffer holding the result.  All threads of the block take part.
+__device__ float2 *fft_batch(float2 *x, float2 *y, const float2 *tw, const FftLen &L, int nfft, float sign) {
+  int Ns = 1;
+  for (int st = 0; st < L.nst; ++st) {
+    const int R = L.rad[st];
+    switch (R) {
+      case 2: fft_stage<2>(x, y, tw, L.N, Ns, nfft, sign); break;
+      case 3: fft_stage<3>(x, y, tw, L.N, Ns, nfft, sign); break;
+      case 4: fft_stage<4>(x, y, tw, L.N, Ns, nfft, sign); break;
+      default: fft_stage<5>(x, y, tw, L.N, Ns, nfft, sign); break;
+    }
+    __syncthreads();
+    float2 *t = x; x = y; y = t;
+    Ns *= R;
+  }
+  return x;
+}
+
+// twiddles exp(-2 pi i k / N), k < N, computed in double
+__global__ void k_fft_twiddles(float2 *tw, int N) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+    double s, c;
+    sincospi(-2.0 * k / N, &s, &c);
+    tw[k] = make_float2((float)c, (float)s);
+  }
+}
+
+struct FftGeom {
+  int mc, nc, w, hw, W;
+  FftLen Lr, Lc;   // column length Mr (over rows), row length Mc (over columns)
+  int Kc;          // Mc/2 + 1 column bins kept
+  int mcp;         // rows stored per column of S (mc rounded up to even)
+};
+
+constexpr int FFT_ROWS_PAIRS = 8;   // row pairs per k_fft_rows block
+constexpr int FFT_COLS = 8;         // column bins per k_fft_cols block
+constexpr int FFT_THREADS = 256;
+
+// ---------------------------------------------------------------- forward rows
+// S[f][k][r] = sum_j a_f[r][j] exp(-2 pi i j k / Mc), k in [0, Kc), r in [0, mcp)
+__global__ void __launch_bounds__(FFT_THREADS) k_fft_rows(const uint16_t *__restrict__ img, int64_t fstride,
+                                                          int pitch, FftGeom g, const float2 *__restrict__ twc,
+                                                          float2 *__restrict__ S) {
+  extern __shared__ __align__(16) float2 fsm[];
+  const int Mc = g.Lc.N;
+  float2 *tw = fsm;
+  float2 *x = tw + Mc, *y = x + FFT_ROWS_PAIRS * Mc;
+  const int nrb = (g.mcp / 2 + FFT_ROWS_PAIRS - 1) / FFT_ROWS_PAIRS;
+  const int f = blockIdx.x / nrb, rb = blockIdx.x % nrb;
+  const int p0 = rb * FFT_ROWS_PAIRS, np = min(FFT_ROWS_PAIRS, g.mcp / 2 - p0);
+  for (int k = threadIdx.x; k < Mc; k += blockDim.x) tw[k] = twc[k];
+  const uint16_t *A = img + (int64_t)f * fstride;
+  for (int e = threadIdx.x; e < np * Mc; e += blockDim.x) {
+    const int q = e / Mc, j = e - q * Mc;
+    const int r0 = 2 * (p0 + q), r1 = r0 + 1;
+    float re = 0.f, im = 0.f;
+    if (j < g.nc) {
+      if (r0 < g.mc) re = (float)A[(int64_t)r0 * pitch + j];
+      if (r1 < g.mc) im = (float)A[(int64_t)r1 * pitch + j];
+    }
+    x[q * Mc + j] = make_float2(re, im);
+  }
+  __syncthreads();
+  const float2 *Z = fft_batch(x, y, tw, g.Lc, np, -1.f);
+  // unpack the two real rows' spectra; store column-major S[f][k][row]
+  float2 *Sf = S + (int64_t)f * g.Kc * g.mcp;
+  for (int e = threadIdx.x; e < g.Kc * np; e += blockDim.x) {
+    const int k = e / np, q = e - k * np;
+    const float2 zk = Z[q * Mc + k], zn = conjf2(Z[q * Mc + (Mc - k) % Mc]);
+    const float2 x0 = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y + zn.y));
+    const float2 d = make_float2(0.5f * (zk.x - zn.x), 0.5f * (zk.y - zn.y));
+    const float2 x1 = make_float2(d.y, -d.x);   // d / i
+    float2 *dst = Sf + (int64_t)k * g.mcp + 2 * (p0 + q);
+    dst[0] = x0;
+    dst[1] = x1;
+  }
+}
+
+// ---------------------------------------------------------------- columns
+// mode 0 (frames): P[f][s+hw][k] = (1/(Mr Mc)) sum_u X[u][k] Bc[k][u] e^{+2 pi i u s / Mr}
+//                  for s in [-hw, hw], X = FFT over rows of S[f][k][*]
+// mode 1 (template): Bc[k][u] = conj(X[u][k]) / (Mr Mc)
+__global__ void __launch_bounds__(FFT_THREADS) k_fft_cols(const float2 *__restrict__ S, FftGeom g,
+                                                          const float2 *__restrict__ twr, float2 *__restrict__ Bc,
+                                                          float2 *__restrict__ P, int mode) {
+  extern __shared__ __align__(16) float2 fsm[];
+  const int Mr = g.Lr.N;
+  float2 *tw = fsm;
+  float2 *x = tw + Mr, *y = x + FFT_COLS * Mr;
+  const int ncb = (g.Kc + FFT_COLS - 1) / FFT_COLS;
+  const int f = blockIdx.x / ncb, cb = blockIdx.x % ncb;
+  const int k0 = cb * FFT_COLS, nk = min(FFT_COLS, g.Kc - k0);
+  for (int k = threadIdx.x; k < Mr; k += blockDim.x) tw[k] = twr[k];
+  const float2 *Sf = S + (int64_t)f * g.Kc * g.mcp;
+  for (int e = threadIdx.x; e < nk * Mr; e += blockDim.x) {
+    const int q = e / Mr, u = e - q * Mr;
+    x[q * Mr + u] = u < g.mc ? Sf[(int64_t)(k0 + q) * g.mcp + u] : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+  float2 *X = fft_batch(x, y, tw, g.Lr, nk, -1.f);
+  const float scale = 1.0f / ((float)Mr * (float)g.Lc.N);
+  if (mode == 1) {
+    for (int e = threadIdx.x; e < nk * Mr; e += blockDim.x) {
+      const int q = e / Mr, u = e - q * Mr;
+      const float2 v = X[q * Mr + u];
+      Bc[(int64_t)(k0 + q) * Mr + u] = make_float2(v.x * scale, -v.y * scale);
+    }
+    return;
+  }
+  for (int e = threadIdx.x; e < nk * Mr; e += blockDim.x) {
+    const int q = e / Mr, u = e - q * Mr;
+    X[q * Mr + u] = cmul(X[q * Mr + u], Bc[(int64_t)(k0 + q) * Mr + u]);
+  }
+  __syncthreads();
+  float2 *other = X == x ? y : x;
+  const float2 *Hc = fft_batch(X, other, tw, g.Lr, nk, +1.f);
+  float2 *Pf = P + (int64_t)f * g.W * g.Kc;
+  for (int e = threadIdx.x; e < g.W * nk; e += blockDim.x) {
+    const int si = e / nk, q = e - si * nk;
+    const int u = (si - g.hw + Mr) % Mr;
+    Pf[(int64_t)si * g.Kc + k0 + q] = Hc[q * Mr + u];
+  }
+}
+
+// ---------------------------------------------------------------- score + certify
+struct FftScoreArgs {
+  const float2 *P;          // [B][W][Kc]
+  const float2 *twc;        // [Mc]
+  const uint16_t *img;      // coarse frames (exact rescoring)
+  int64_t fstride;
+  int pitch;
+  const uint16_t *tpl;      // coarse template
+  int tpitch;
+  const u64 *ga;            // [B][W*W]
+  const u64 *gb;            // [W*W]
+  FftGeom g;
+  double scale;             // 16^L
+  double eps_rel;           // C u log2(Mr Mc): eps_h = eps_rel ||a|| ||b||
+  int B;
+  int32_t *shift_out;       // [B][2]
+  double *f_out;            // [B] or null
+  uint8_t *flags;           // [B] or null
+  int *qcount;              // [B] or null: candidates re-scored (diagnostics)
+  float *h_out;             // [B][W*W] or null: the fp32 FFT cross term h~ (diagnostics)
+};
+
+// exact h(s,t) for one lag, 64-bit, all threads of the block; result to thread 0
+__device__ u64 exact_h(const FftScoreArgs &a, const uint16_t *A, int s, int t, u64 *red) {
+  const int mc = a.g.mc, nc = a.g.nc;
+  const int i0 = max(0, -s), i1 = mc - max(0, s), j0 = max(0, -t), j1 = nc - max(0, t);
+  u64 acc = 0;
+  for (int i = i0; i < i1; ++i) {
+    const uint16_t *ar = A + (int64_t)(i + s) * a.pitch + t;
+    const uint16_t *br = a.tpl + (int64_t)i * a.tpitch;
+    for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) acc += (u64)((uint32_t)ar[j] * (uint32_t)br[j]);
+  }
+  acc = warp_sum(acc);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  u64 tot = 0;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) tot += red[k];
+  return tot;
+}
+
+__global__ void __launch_bounds__(FFT_THREADS) k_fft_score(FftScoreArgs a) {
+  extern __shared__ __align__(16) float2 fsm[];
+  const FftGeom &g = a.g;
+  const int Mc = g.Lc.N, W = g.W, hw = g.hw;
+  float2 *tw = fsm;
+  float2 *x = tw + Mc, *y = x + FFT_ROWS_PAIRS * Mc;
+  float *hb = reinterpret_cast<float *>(y + FFT_ROWS_PAIRS * Mc);   // [W][W] h~
+  __shared__ u64 red[32];
+  __shared__ float fmin_hi_s;
+  __shared__ int qn;
+  __shared__ int qlist[FFT_QCAP];
+  const int64_t f = blockIdx.x;
+  for (int k = threadIdx.x; k < Mc; k += blockDim.x) tw[k] = a.twc[k];
+  const float2 *Pf = a.P + f * W * g.Kc;
+  const int npairs = (W + 1) / 2;
+  for (int p0 = 0; p0 < npairs; p0 += FFT_ROWS_PAIRS) {
+    const int np = min(FFT_ROWS_PAIRS, npairs - p0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < np * Mc; e += blockDim.x) {
+      const int q = e / Mc, k = e - q * Mc;
+      const int s1 = 2 * (p0 + q), s2 = s1 + 1;
+      // Hermitian extension of each lag row's half spectrum, packed as re + i*im
+      const bool lo = k < g.Kc;
+      const int kk = lo ? k : Mc - k;
+      float2 v1 = Pf[(int64_t)s1 * g.Kc + kk];
+      float2 v2 = s2 < W ? Pf[(int64_t)s2 * g.Kc + kk] : make_float2(0.f, 0.f);
+      if (!lo) { v1.y = -v1.y; v2.y = -v2.y; }
+      x[q * Mc + k] = make_float2(v1.x - v2.y, v1.y + v2.x);
+    }
+    __syncthreads();
+    const float2 *Hr = fft_batch(x, y, tw, g.Lc, np, +1.f);
+    for (int e = threadIdx.x; e < np * W; e += blockDim.x) {
+      const int q = e / W, ti = e - q * W;
+      const int s1 = 2 * (p0 + q), s2 = s1 + 1;
+      const float2 v = Hr[q * Mc + (ti - hw + Mc) % Mc];
+      hb[s1 * W + ti] = v.x;
+      if (s2 < W) hb[s2 * W + ti] = v.y;
+    }
+  }
+  __syncthreads();
+  if (a.h_out)
+    for (int lag = threadIdx.x; lag < W * W; lag += blockDim.x) a.h_out[f * W * W + lag] = hb[lag];
+  // scores with certified error intervals
+  const u64 *gaf = a.ga + f * W * W;
+  const double na = sqrt((double)gaf[hw * W + hw]), nb = sqrt((double)a.gb[hw * W + hw]);
+  const double eps_h = a.eps_rel * na * nb;
+  float best = 3.0e38f;
+  for (int lag = threadIdx.x; lag < W * W; lag += blockDim.x) {
+    const int s = lag / W - hw, t = lag % W - hw;
+    const double A = (double)((g.mc - abs(s)) * (g.nc - abs(t)));
+    const double fa = ((double)gaf[lag] + (double)a.gb[lag] - 2.0 * (double)hb[lag]) / (a.scale * A);
+    const double del = 2.0 * eps_h / (a.scale * A);
+    best = fminf(best, (float)(fa + del) * (1.0f + 1e-6f));
+  }
+  for (int o = 16; o > 0; o >>= 1) best = fminf(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) reinterpret_cast<float *>(red)[threadIdx.x >> 5] = best;
+  if (threadIdx.x == 0) qn = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float b = 3.0e38f;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) b = fminf(b, reinterpret_cast<float *>(red)[k]);
+    fmin_hi_s = b;
+  }
+  __syncthreads();
+  const float thr = fmin_hi_s;
+  for (int lag = threadIdx.x; lag < W * W; lag += blockDim.x) {
+    const int s = lag / W - hw, t = lag % W - hw;
+    const double A = (double)((g.mc - abs(s)) * (g.nc - abs(t)));
+    const double fa = ((double)gaf[lag] + (double)a.gb[lag] - 2.0 * (double)hb[lag]) / (a.scale * A);
+    const double del = 2.0 * eps_h / (a.scale * A);
+    if ((float)((fa - del) * (1.0 - 1e-6)) <= thr) {
+      const int q = atomicAdd(&qn, 1);
+      if (q < FFT_QCAP) qlist[q] = lag;
+    }
+  }
+  __syncthreads();
+  const int nq = qn;
+  const bool all = nq > FFT_QCAP;
+  const int ncand = all ? W * W : nq;
+  const uint16_t *A = a.img + f * a.fstride;
+  Key bk{~0ull, ~0u};
+  for (int c = 0; c < ncand; ++c) {
+    const int lag = all ? c : qlist[c];
+    const int s = lag / W - hw, t = lag % W - hw;
+    const u64 h = exact_h(a, A, s, t, red);
+    if (threadIdx.x == 0) {
+      const u64 N = gaf[lag] + a.gb[lag] - 2 * h;
+      const double area = (double)((g.mc - abs(s)) * (g.nc - abs(t)));
+      const double fv = (double)N / (a.scale * area);
+      const Key kk{(u64)__double_as_longlong(fv), (unsigned)lag};
+      if (key_less(kk, bk)) bk = kk;
+    }
+  }
+  if (threadIdx.x == 0) {
+    const int s = (int)(bk.idx / W) - hw, t = (int)(bk.idx % W) - hw;
+    a.shift_out[2 * f] = s;
+    a.shift_out[2 * f + 1] = t;
+    if (a.f_out) a.f_out[f] = __longlong_as_double((long long)bk.f);
+    if (a.flags) a.flags[f] = (uint8_t)(((abs(s) == hw || abs(t) == hw) ? 1 : 0) | (all ? 2 : 0));
+    if (a.qcount) a.qcount[f] = nq;
+  }
+}
+
+// ---------------------------------------------------------------- frame energies
+// g_a(s,t) = sum over the frame-side rectangle of D_{s,t} of a^2 for every coarse lag
+// (P:32-35): total minus the excluded edge strips plus the doubly excluded corner --
+// the paper's DP of P:35 run in each corner (a (w x w) prefix table per corner).
+// One block per frame; works for any w (tables in dynamic shared memory).
+__global__ void __launch_bounds__(256) k_energy_u16(const uint16_t *__restrict__ img, int64_t fstride, int pitch,
+                                                    int mc, int nc, int w, u64 *__restrict__ ga) {
+  extern __shared__ __align__(16) u64 esm[];
+  const int hw = w - 1, W = 2 * w - 1, CS = w * w;
+  u64 *rowE = esm;                 // [2 hw]: top rows, bottom rows (from the bottom)
+  u64 *colE = rowE + 2 * hw;       // [2 hw]
+  u64 *cor = colE + 2 * hw;        // [4][w][w]
+  u64 *tot = cor + 4 * CS;         // [1]
+  for (int k = threadIdx.x; k < 4 * hw + 4 * CS + 1; k += blockDim.x) esm[k] = 0;
+  __syncthreads();
+  const uint16_t *A = img + (int64_t)blockIdx.x * fstride;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+  u64 mytot = 0;
+  for (int r = warp; r < mc; r += nwarp) {
+    u64 rs = 0;
+    const bool top = r < hw, bot = r >= mc - hw;
+    for (int c = lane; c < nc; c += 32) {
+      const u64 v2 = (u64)A[(int64_t)r * pitch + c] * A[(int64_t)r * pitch + c];
+      rs += v2;
+      const bool lf = c < hw, rt = c >= nc - hw;
+      if (lf) atomicAdd(&colE[c], v2);
+      if (rt) atomicAdd(&colE[hw + (nc - 1 - c)], v2);
+      if ((lf || rt) && (top || bot)) {
+        if (top && lf) cor[0 * CS + (r + 1) * w + (c + 1)] = v2;
+        if (top && rt) cor[1 * CS + (r + 1) * w + (nc - c)] = v2;
+        if (bot && lf) cor[2 * CS + (mc - r) * w + (c + 1)] = v2;
+        if (bot && rt) cor[3 * CS + (mc - r) * w + (nc - c)] = v2;
+      }
+    }
+    rs = warp_sum(rs);
+    if (lane == 0) {
+      mytot += rs;
+      if (top) rowE[r] = rs;
+      if (bot) rowE[hw + (mc - 1 - r)] = rs;
+    }
+  }
+  if (lane == 0) atomicAdd(tot, mytot);
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    u64 *e = (threadIdx.x & 2) ? colE : rowE;
+    u64 *p = e + (threadIdx.x & 1) * hw;
+    for (int q = 1; q < hw; ++q) p[q] += p[q - 1];
+  }
+  for (int k = threadIdx.x; k < 4 * w; k += blockDim.x) {
+    u64 *c = cor + (k / w) * CS + (k % w) * w;
+    for (int q = 1; q < w; ++q) c[q] += c[q - 1];
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < 4 * w; k += blockDim.x) {
+    u64 *c = cor + (k / w) * CS + (k % w);
+    for (int p = 1; p < w; ++p) c[p * w] += c[(p - 1) * w];
+  }
+  __syncthreads();
+  u64 *gf = ga + (int64_t)blockIdx.x * W * W;
+  for (int lag = threadIdx.x; lag < W * W; lag += blockDim.x) {
+    const int s = lag / W - hw, t = lag % W - hw;
+    const u64 rex = s > 0 ? rowE[s - 1] : (s < 0 ? rowE[hw + (-s) - 1] : 0);
+    const u64 cex = t > 0 ? colE[t - 1] : (t < 0 ? colE[hw + (-t) - 1] : 0);
+    u64 corner = 0;
+    if (s != 0 && t != 0) {
+      const int quad = (s < 0 ? 2 : 0) | (t < 0 ? 1 : 0);
+      corner = cor[quad * CS + abs(s) * w + abs(t)];
+    }
+    gf[lag] = *tot - rex - cex + corner;
+  }
+}
+
+}  // namespace moco

@@ -742,8 +742,11 @@ inline bool tc_supported(int dtype, int bits, int levels, int w, int mc, int nc)
   TcGeom g;
   return tc_make_geom(&g, w, mc, nc, levels);
 }
-// AUTO policy: the tensor-core search wherever it is supported.
+// AUTO policy (from measurement): the tensor-core search wherever it is
+// supported; otherwise the FFT path for 16-bit data (exact after certification), with
+// the CUDA-core direct search for float32 data.
 inline bool tc_auto_prefers(int w) { (void)w; return true; }
+inline bool fft_auto_prefers(int w, bool tc_ok) { (void)w; return !tc_ok; }
 
 inline int tc_init(TcPlan *tc, int w, int mc, int nc, int L, int64_t cap) {
   if (!tc_make_geom(&tc->g, w, mc, nc, L)) return -1;

@@ -19,6 +19,7 @@
 #include "kernels_direct.cuh"
 #include "kernels_tc.cuh"
 #include "kernels_refine.cuh"
+#include "kernels_fft.cuh"
 
 using namespace moco;
 
@@ -63,6 +64,17 @@ struct moco_plan {
   size_t c_smem;
   // tensor-core path state
   TcPlan tc;
+  // FFT path state (kernels_fft.cuh)
+  struct {
+    bool ready = false, tpl_ready = false;
+    FftGeom g;
+    float2 *twr = nullptr, *twc = nullptr, *Bc = nullptr, *S = nullptr, *P = nullptr;
+    u64 *ga = nullptr;
+    int *qc = nullptr;
+    int64_t cap = 0;
+    double eps_rel = 0;
+    int smem_rows = 0, smem_cols = 0, smem_score = 0, smem_energy = 0;
+  } fft;
   // end-to-end staging
   bool host_ready;
   int64_t host_ch;
@@ -155,6 +167,9 @@ static void plan_free(moco_plan *p) {
   for (int l = 0; l < 3; ++l)
     if (p->pb2[l]) cudaFree(p->pb2[l]);
   tc_free(&p->tc);
+  for (void *q : {(void *)p->fft.twr, (void *)p->fft.twc, (void *)p->fft.Bc, (void *)p->fft.S, (void *)p->fft.P,
+                  (void *)p->fft.ga, (void *)p->fft.qc})
+    if (q) cudaFree(q);
   for (int k = 0; k < 2; ++k) {
     if (p->slot_in[k]) cudaFree(p->slot_in[k]);
     if (p->slot_out[k]) cudaFree(p->slot_out[k]);
@@ -172,6 +187,107 @@ static void plan_free(moco_plan *p) {
   delete p;
 }
 
+// ---------------------------------------------------------------- FFT path (S3 by FFT)
+static bool fft_supported(const moco_plan *p) {
+  if (p->dtype != MOCO_U16) return false;
+  const int L = p->levels;
+  FftLen a, b;
+  return fft_len_make(p->ml[L] + p->w - 1, &a) && fft_len_make(p->nl[L] + p->w - 1, &b);
+}
+
+static int fft_init(moco_plan *p) {
+  auto &F = p->fft;
+  if (F.ready) return MOCO_OK;
+  const int L = p->levels;
+  FftGeom &g = F.g;
+  g.mc = p->ml[L]; g.nc = p->nl[L]; g.w = p->w; g.hw = p->w - 1; g.W = p->W;
+  if (!fft_len_make(g.mc + g.hw, &g.Lr) || !fft_len_make(g.nc + g.hw, &g.Lc)) return MOCO_EINVAL;
+  g.Kc = g.Lc.N / 2 + 1;
+  g.mcp = (g.mc + 1) / 2 * 2;
+  // sub-batches sized so the spectra stay in L2 (about 80 MB)
+  const size_t per = (size_t)g.Kc * g.mcp * 8 + (size_t)g.W * g.Kc * 8 + (size_t)g.W * g.W * 8;
+  F.cap = std::max<int64_t>(1, std::min<int64_t>(p->cap, (int64_t)((80u << 20) / per)));
+  const int Mr = g.Lr.N, Mc = g.Lc.N;
+  auto al = [&](void **q, size_t bytes) {
+    if (cudaMalloc(q, bytes) != cudaSuccess) { cudaGetLastError(); return false; }
+    return true;
+  };
+  if (!al((void **)&F.twr, Mr * 8) || !al((void **)&F.twc, Mc * 8) || !al((void **)&F.Bc, (size_t)g.Kc * Mr * 8) ||
+      !al((void **)&F.S, (size_t)F.cap * g.Kc * g.mcp * 8) || !al((void **)&F.P, (size_t)F.cap * g.W * g.Kc * 8) ||
+      !al((void **)&F.ga, (size_t)F.cap * g.W * g.W * 8) || !al((void **)&F.qc, (size_t)p->cap * sizeof(int)))
+    return MOCO_ENOMEM;
+  F.eps_rel = RS_FFT_C * std::ldexp(1.0, -24) * std::log2((double)Mr * (double)Mc);
+  F.smem_rows = (Mc + 2 * FFT_ROWS_PAIRS * Mc) * 8;
+  F.smem_cols = (Mr + 2 * FFT_COLS * Mr) * 8;
+  F.smem_score = (Mc + 2 * FFT_ROWS_PAIRS * Mc) * 8 + g.W * g.W * 4;
+  F.smem_energy = (4 * g.hw + 4 * g.w * g.w + 1) * 8;
+  if (F.smem_score > 227 * 1024 || F.smem_energy > 227 * 1024) return MOCO_EINVAL;
+  CK(cudaFuncSetAttribute(k_fft_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, F.smem_rows));
+  CK(cudaFuncSetAttribute(k_fft_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, F.smem_cols));
+  CK(cudaFuncSetAttribute(k_fft_score, cudaFuncAttributeMaxDynamicSharedMemorySize, F.smem_score));
+  CK(cudaFuncSetAttribute(k_energy_u16, cudaFuncAttributeMaxDynamicSharedMemorySize, F.smem_energy));
+  k_fft_twiddles<<<(Mr + 255) / 256, 256>>>(F.twr, Mr);
+  k_fft_twiddles<<<(Mc + 255) / 256, 256>>>(F.twc, Mc);
+  CKL("k_fft_twiddles");
+  CK(cudaDeviceSynchronize());
+  F.ready = true;
+  return MOCO_OK;
+}
+
+// template spectrum conj(B^)/(Mr Mc), column-major [k][u] (once per template)
+static int fft_set_template(moco_plan *p, cudaStream_t st) {
+  auto &F = p->fft;
+  const int L = p->levels;
+  const FftGeom &g = F.g;
+  const int nrb = (g.mcp / 2 + FFT_ROWS_PAIRS - 1) / FFT_ROWS_PAIRS;
+  const int ncb = (g.Kc + FFT_COLS - 1) / FFT_COLS;
+  k_fft_rows<<<nrb, FFT_THREADS, F.smem_rows, st>>>((const uint16_t *)p->tpl[L], 0, p->pitch[L], g, F.twc, F.S);
+  k_fft_cols<<<ncb, FFT_THREADS, F.smem_cols, st>>>(F.S, g, F.twr, F.Bc, nullptr, 1);
+  CKL("fft_set_template");
+  F.tpl_ready = true;
+  return MOCO_OK;
+}
+
+// S3+S4 by FFT with certification, for B coarse frames (level-L images).
+static int launch_fft(moco_plan *p, const void *img, int64_t fstride, int pitch, int64_t B, int32_t *shift_out,
+                      double *f_out, uint8_t *flags, cudaStream_t st, float *h_out = nullptr,
+                      int *qcount = nullptr) {
+  auto &F = p->fft;
+  const FftGeom &g = F.g;
+  const int L = p->levels;
+  const int nrb = (g.mcp / 2 + FFT_ROWS_PAIRS - 1) / FFT_ROWS_PAIRS;
+  const int ncb = (g.Kc + FFT_COLS - 1) / FFT_COLS;
+  for (int64_t b0 = 0; b0 < B; b0 += F.cap) {
+    const int64_t nb = std::min<int64_t>(F.cap, B - b0);
+    const uint16_t *im = (const uint16_t *)img + b0 * fstride;
+    {
+      ProfScope ps(p, MOCO_K_PREP, st);
+      k_energy_u16<<<(unsigned)nb, 256, F.smem_energy, st>>>(im, fstride, pitch, g.mc, g.nc, g.w, F.ga);
+    }
+    {
+      ProfScope ps(p, MOCO_K_COARSE, st);
+      k_fft_rows<<<(unsigned)(nb * nrb), FFT_THREADS, F.smem_rows, st>>>(im, fstride, pitch, g, F.twc, F.S);
+      k_fft_cols<<<(unsigned)(nb * ncb), FFT_THREADS, F.smem_cols, st>>>(F.S, g, F.twr, F.Bc, F.P, 0);
+    }
+    FftScoreArgs a;
+    a.P = F.P; a.twc = F.twc; a.img = im; a.fstride = fstride; a.pitch = pitch;
+    a.tpl = (const uint16_t *)p->tpl[L]; a.tpitch = p->pitch[L];
+    a.ga = F.ga; a.gb = (const u64 *)p->gb; a.g = g;
+    a.scale = (double)(1u << (4 * L)); a.eps_rel = F.eps_rel; a.B = (int)nb;
+    a.shift_out = shift_out + 2 * b0; a.f_out = f_out ? f_out + b0 : nullptr;
+    a.flags = flags ? flags + b0 : nullptr;
+    a.qcount = qcount ? qcount + b0 : F.qc + b0;
+    a.h_out = h_out ? h_out + b0 * g.W * g.W : nullptr;
+    {
+      ProfScope ps(p, MOCO_K_SCORE, st);
+      k_fft_score<<<(unsigned)nb, FFT_THREADS, F.smem_score, st>>>(a);
+    }
+    p->launches += 4;
+    CKL("fft path");
+  }
+  return MOCO_OK;
+}
+
 int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype, int bits,
                      int device) {
   if (!out) return MOCO_EINVAL;
@@ -184,7 +300,7 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
   if ((n * e0) % 16 != 0) return MOCO_EINVAL;
   const int mL = m >> levels, nL = n >> levels;
   if (w < 1 || w >= std::min(mL, nL)) return MOCO_EINVAL;
-  if (w > 64) return MOCO_EINVAL;   // shared-memory lag tables sized for w <= 64
+  if (w > 64 && dtype != MOCO_U16) return MOCO_EINVAL;   // w > 64: FFT path only
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
     snprintf(g_err, sizeof(g_err), "no CUDA device %d (count %d)", device, ndev);
@@ -228,6 +344,8 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
   alloc(&p->gb, (size_t)W * W * 8);
   size_t per_frame = 0;
   for (int l = 1; l <= levels; ++l) per_frame += (size_t)p->ml[l] * p->pitch[l] * p->esz[l];
+  // tensor-core operand planes + lag energies (upper bound: rows <= m_L + 128, int8 hi/lo)
+  if (dtype == MOCO_U16) per_frame += (size_t)2 * (p->ml[levels] + 128) * p->nl[levels] + (size_t)W * W * 8;
   const size_t budget = (size_t)256 << 20;
   p->cap = per_frame ? std::max<int64_t>(1, (int64_t)(budget / per_frame)) : (int64_t)1 << 20;
   p->cap = std::min<int64_t>(p->cap, (int64_t)1 << 20);
@@ -256,22 +374,47 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
     }
   if (rc != MOCO_OK) { plan_free(p); return rc; }
   p->algo = MOCO_ALGO_DIRECT;
-  if (tc_supported(p->dtype, p->bits, p->levels, p->w, p->ml[levels], p->nl[levels]) &&
-      tc_auto_prefers(p->w)) {
+  const bool tc_ok = tc_supported(p->dtype, p->bits, p->levels, p->w, p->ml[levels], p->nl[levels]);
+  if (tc_ok && tc_auto_prefers(p->w)) {
     if (tc_init(&p->tc, p->w, p->ml[levels], p->nl[levels], levels, p->cap) == 0) p->algo = MOCO_ALGO_TC;
     else cudaGetLastError();
   }
+  if (p->algo == MOCO_ALGO_DIRECT && fft_supported(p) && (w > 64 || fft_auto_prefers(p->w, tc_ok))) {
+    if (fft_init(p) == MOCO_OK) p->algo = MOCO_ALGO_FFT;
+    else cudaGetLastError();
+  }
+  if (w > 64 && p->algo != MOCO_ALGO_FFT) { plan_free(p); return MOCO_EINVAL; }
   *out = p;
   return MOCO_OK;
 }
 
 int moco_plan_set_algo(moco_plan *p, int algo) {
   if (!p) return MOCO_EINVAL;
-  if (algo == MOCO_ALGO_DIRECT) { p->algo = algo; return MOCO_OK; }
+  if (algo == MOCO_ALGO_DIRECT) {
+    if (p->w > 64) return MOCO_EINVAL;
+    p->algo = algo;
+    return MOCO_OK;
+  }
+  if (algo == MOCO_ALGO_FFT) {
+    if (!fft_supported(p)) return MOCO_EINVAL;
+    CK(cudaSetDevice(p->device));
+    int rc = fft_init(p);
+    if (rc) return rc;
+    if (p->has_tpl && !p->fft.tpl_ready) {
+      rc = fft_set_template(p, 0);
+      if (rc) return rc;
+      CK(cudaDeviceSynchronize());
+    }
+    p->algo = MOCO_ALGO_FFT;
+    return MOCO_OK;
+  }
   const int L = p->levels;
   if (algo == MOCO_ALGO_TC || algo == MOCO_ALGO_AUTO) {
     const bool ok = tc_supported(p->dtype, p->bits, L, p->w, p->ml[L], p->nl[L]);
-    if (algo == MOCO_ALGO_AUTO && !(ok && tc_auto_prefers(p->w))) { p->algo = MOCO_ALGO_DIRECT; return MOCO_OK; }
+    if (algo == MOCO_ALGO_AUTO && !(ok && tc_auto_prefers(p->w))) {
+      if (fft_supported(p) && (p->w > 64 || fft_auto_prefers(p->w, ok))) return moco_plan_set_algo(p, MOCO_ALGO_FFT);
+      return moco_plan_set_algo(p, MOCO_ALGO_DIRECT);
+    }
     if (!ok) return MOCO_EINVAL;
     CK(cudaSetDevice(p->device));
     if (!p->tc.ready && tc_init(&p->tc, p->w, p->ml[L], p->nl[L], L, p->cap) != 0) return MOCO_ENOMEM;
@@ -507,6 +650,10 @@ int moco_set_template(moco_plan *p, const void *d_template, moco_stream_t stream
     if (tc_set_template(&p->tc, (const uint16_t *)p->tpl[L], p->pitch[L], st) != 0)
       return set_cuda_err(cudaGetLastError(), "tc_set_template");
   }
+  if (p->fft.ready) {
+    const int rc = fft_set_template(p, st);
+    if (rc) return rc;
+  }
   p->has_tpl = true;
   return MOCO_OK;
 }
@@ -604,8 +751,16 @@ static int run_batch(moco_plan *p, const void *frames_b, int64_t B, int32_t *shi
     if (rc || grid_b) return rc;
     return refine_levels(p, img, fstride, B, shifts_b, fmin_b, corr_b, st);
   }
-  if (grid_b) return launch_coarse(p, img[L], fstride[L], p->pitch[L], B, nullptr, nullptr, grid_b,
-                                   nullptr, st);
+  if (grid_b) {
+    if (p->w > 64) return MOCO_EINVAL;   // no exact all-lag path for w > 64
+    return launch_coarse(p, img[L], fstride[L], p->pitch[L], B, nullptr, nullptr, grid_b, nullptr, st);
+  }
+  if (p->algo == MOCO_ALGO_FFT) {
+    int rc = launch_fft(p, img[L], fstride[L], p->pitch[L], B, L == 0 ? shifts_b : p->sh[L],
+                        L == 0 ? fmin_b : nullptr, flags_b, st);
+    if (rc) return rc;
+    return refine_levels(p, img, fstride, B, shifts_b, fmin_b, corr_b, st);
+  }
   int32_t *sc_out = L == 0 ? shifts_b : p->sh[L];
   int rc = launch_coarse(p, img[L], fstride[L], p->pitch[L], B, sc_out, L == 0 ? fmin_b : nullptr,
                          nullptr, flags_b, st);
@@ -646,6 +801,41 @@ int moco_score_grid(moco_plan *p, const void *d_frames, int64_t T, double *d_f,
     const int64_t B = std::min<int64_t>(p->cap, T - f0);
     rc = run_batch(p, (const char *)d_frames + f0 * fbytes, B, nullptr, nullptr, nullptr, nullptr,
                    d_f + f0 * WW, (cudaStream_t)stream);
+    if (rc) return rc;
+  }
+  return MOCO_OK;
+}
+
+int moco_fft_cross(moco_plan *p, const void *d_frames, int64_t T, float *d_h, int32_t *d_shifts,
+                   int32_t *d_qcount, moco_stream_t stream) {
+  int rc = check_align_args(p, d_frames, T);
+  if (rc) return rc;
+  if (T > 0 && (!d_h || !d_shifts)) return MOCO_EINVAL;
+  if (!fft_supported(p)) return MOCO_EINVAL;
+  CK(cudaSetDevice(p->device));
+  rc = fft_init(p);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!p->fft.tpl_ready) {
+    rc = fft_set_template(p, st);
+    if (rc) return rc;
+  }
+  p->launches = 0;
+  const int L = p->levels;
+  const size_t fbytes = (size_t)p->m * p->n * p->esz[0];
+  const int64_t WW = (int64_t)p->W * p->W;
+  for (int64_t f0 = 0; f0 < T; f0 += p->cap) {
+    const int64_t B = std::min<int64_t>(p->cap, T - f0);
+    const void *img = (const char *)d_frames + f0 * fbytes;
+    int64_t fs = (int64_t)p->m * p->n;
+    for (int l = 0; l < L; ++l) {
+      rc = launch_downsample(p, l, img, fs, p->scratch[l + 1], B, st);
+      if (rc) return rc;
+      img = p->scratch[l + 1];
+      fs = (int64_t)p->ml[l + 1] * p->pitch[l + 1];
+    }
+    rc = launch_fft(p, img, fs, p->pitch[L], B, d_shifts + 2 * f0, nullptr, nullptr, st, d_h + f0 * WW,
+                    d_qcount ? d_qcount + f0 : nullptr);
     if (rc) return rc;
   }
   return MOCO_OK;

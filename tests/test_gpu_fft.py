@@ -1,0 +1,140 @@
+"""GPU: the FFT path of S3 with the certified candidate set of S4.
+
+The FFT path computes the cross term in fp32; its results must still be the exact
+method's bit for bit (certification + exact rescoring, kernels_fft.cuh), and its
+measured error must sit well inside the bound the certification assumes."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1506_06039_b200 import FLAG_FULL, Plan
+from synth import config_spec, make_stack
+from tests import paper_forms as pf
+from tests.parity import check_frame
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda", 0)
+RS_FFT_C = 8.0   # kernels_fft.cuh
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _exact_h(A, B, w):
+    """h(s,t) = sum_{D_{s,t}} A[i+s][j+t] B[i][j] in int64, all |s|,|t| < w."""
+    m, n = B.shape
+    A = A.astype(np.int64)
+    B = B.astype(np.int64)
+    W = 2 * w - 1
+    out = np.zeros((W, W), dtype=np.int64)
+    for s in range(-(w - 1), w):
+        i0, i1 = max(0, -s), m - max(0, s)
+        for t in range(-(w - 1), w):
+            j0, j1 = max(0, -t), n - max(0, t)
+            out[s + w - 1, t + w - 1] = (A[i0 + s:i1 + s, j0 + t:j1 + t] * B[i0:i1, j0:j1]).sum()
+    return out
+
+
+def _fft_len(lo):
+    N = lo
+    while True:
+        x = N
+        for r in (2, 3, 5):
+            while x % r == 0:
+                x //= r
+        if x == 1:
+            return N
+        N += 1
+
+
+@pytest.mark.parametrize("c", [1, 2, 3, 4])
+def test_fft_cross_term_error_within_bound(c):
+    """|h~ - h| / (u log2(Mr Mc) ||a|| ||b||) measured on the configs' own data (stripes
+    included for C3) stays at most RS_FFT_C / 4: the certification bound has 4x margin."""
+    T = 3
+    spec = config_spec(c, T=T)
+    st = make_stack(spec, 0, T, device=DEV)
+    p = Plan(spec.m, spec.n, spec.w, spec.levels, "u16", 12, device=0)
+    p.set_template(st.template)
+    h, sh, q = p.fft_cross(st.frames)
+    h = _np(h).astype(np.float64)
+    B = oracle.pyramid(_np(st.template).astype(np.int64), spec.levels)[spec.levels]
+    mc, nc = B.shape
+    M = _fft_len(mc + spec.w - 1) * _fft_len(nc + spec.w - 1)
+    worst = 0.0
+    for k in range(T):
+        A = _np(st.frames[k]).astype(np.int64)
+        for _ in range(spec.levels):
+            A = A[0::2, 0::2] + A[0::2, 1::2] + A[1::2, 0::2] + A[1::2, 1::2]
+        Bs = _np(st.template).astype(np.int64)
+        for _ in range(spec.levels):
+            Bs = Bs[0::2, 0::2] + Bs[0::2, 1::2] + Bs[1::2, 0::2] + Bs[1::2, 1::2]
+        ex = _exact_h(A, Bs, spec.w)
+        scale = 2.0 ** -24 * math.log2(M) * math.sqrt(float((A * A).sum())) * math.sqrt(float((Bs * Bs).sum()))
+        worst = max(worst, float(np.abs(h[k] - ex).max()) / scale)
+    assert worst <= RS_FFT_C / 4, worst
+
+
+@pytest.mark.parametrize("c,T", [(1, 400), (2, 600), (3, 200), (4, 24)])
+def test_fft_equals_exact_path_whole_stack(c, T):
+    """FFT (certified) and the exact tensor-core / CUDA-core searches agree bit for bit:
+    shifts, f_min, corrected frames, edge flag."""
+    spec = config_spec(c, T=T)
+    st = make_stack(spec, 0, T, device=DEV)
+    out = {}
+    exact = "tc" if c in (1, 2, 3) else "direct"   # C4: 16-bit coarse sums, no int8 split
+    for algo in ("fft", exact):
+        p = Plan(spec.m, spec.n, spec.w, spec.levels, "u16", 12, device=0, algo=algo)
+        assert p.algo == algo
+        p.set_template(st.template)
+        sh, fm, co, fl = p.align(st.frames, corrected=True, flags=True)
+        out["fft" if algo == "fft" else "exact"] = (sh, fm, co.view(torch.int16), fl & 1)
+    for a, b in zip(out["fft"], out["exact"]):
+        assert torch.equal(a, b)
+
+
+def test_fft_large_w_against_oracle():
+    """w beyond the exact direct/tensor-core paths (the paper's default w = min(m,n)/3,
+    P:49, at the coarse level): AUTO takes the FFT path; bit-exact vs the oracle."""
+    spec = config_spec(2, m=256, n=256, w=42, T=3, n_blobs=120, shift_bound=60)
+    st = make_stack(spec, 0, 3, device="cpu")
+    p = Plan(256, 256, 42, 1, "u16", 12, device=0)
+    assert p.algo == "fft"
+    p.set_template(st.template.to(DEV))
+    sh, fm, co, _ = p.align(st.frames.to(DEV))
+    sh, fm = _np(sh), _np(fm)
+    for k in range(3):
+        check_frame(st.frames[k].numpy(), st.template.numpy(), 42, 1, sh[k], fm[k], _np(co[k]))
+
+
+def test_fft_full_rescore_on_ties():
+    """All f equal (constant frames): the candidate set overflows its cap, every lag is
+    re-scored exactly (FLAG_FULL) and the tie-break (R4) still gives (-(w-1), -(w-1))."""
+    m = n = 64
+    c = torch.full((2, m, n), 9, dtype=torch.int32).to(torch.uint16).to(DEV)
+    p = Plan(m, n, 6, 1, "u16", 12, device=0, algo="fft")
+    p.set_template(c[0])
+    sh, fm, _, fl = p.align(c, corrected=False, flags=True)
+    r = oracle.align_frame(_np(c[0]), _np(c[0]), 6, 1)
+    assert _np(sh).tolist() == [[r.s, r.t]] * 2 and (_np(fm) == 0).all()
+    assert (_np(fl) & FLAG_FULL).all()
+
+
+@pytest.mark.parametrize("m,n,levels,w", [(80, 72, 1, 9), (64, 48, 0, 11), (96, 104, 2, 5), (120, 88, 0, 17)])
+def test_fft_ragged_shapes_exact(m, n, levels, w):
+    """Ragged/odd FFT sizes (2, 3, 5 radices), exact translates and random frames."""
+    rng = np.random.default_rng(m + n + w)
+    tp = rng.integers(0, 4096, size=(m, n)).astype(np.uint16)
+    fr = rng.integers(0, 4096, size=(4, m, n)).astype(np.uint16)
+    fr[1] = pf.translate_zero_fill(tp, 2 << levels, -(1 << levels))
+    p = Plan(m, n, w, levels, "u16", 12, device=0, algo="fft")
+    p.set_template(torch.from_numpy(tp).to(DEV))
+    sh, fm, co, _ = p.align(torch.from_numpy(fr).to(DEV))
+    sh, fm = _np(sh), _np(fm)
+    for k in range(4):
+        check_frame(fr[k], tp, w, levels, sh[k], fm[k], _np(co[k]))
+    assert sh[1].tolist() == [2 << levels, -(1 << levels)] and fm[1] == 0
