@@ -66,17 +66,29 @@ def fft_model(spec):
             "total": f_fft + f_energy + f_score + f_down + f_refine}
 
 
-def kernel_models(spec, esz):
-    """Per-frame algorithmic work of each kernel kind -> (bound, amount, unit)."""
+def kernel_models(spec, esz, algo):
+    """Per-frame algorithmic work of each kernel kind -> (bound, amount, unit) (DESIGN.md §6)."""
     L = spec.levels
     m, n = spec.m, spec.n
+    mc, nc = m >> L, n >> L
+    W = 2 * spec.w - 1
     fm = fft_model(spec)
     down_bytes = sum((m >> l) * (n >> l) * esz + (m >> (l + 1)) * (n >> (l + 1)) * 2 for l in range(L))
+    if algo == "tc":
+        # exact int8 direct correlation: 4 part products (hi/lo x hi/lo) per pixel per lag
+        coarse = ("tensor_i8", 2.0 * 4 * W * W * mc * nc, "op")
+        prep = ("hbm", m * n * esz + 2 * (mc + 64) * nc, "B")
+    elif algo == "fft":
+        coarse = ("alu", fm["coarse"], "flop")
+        prep = ("hbm", mc * nc * 2, "B")        # k_energy_u16 reads the coarse image
+    else:
+        coarse = ("alu", 2.0 * W * W * mc * nc, "op")
+        prep = ("hbm", mc * nc * 2, "B")
     return {
         "downsample": ("hbm", down_bytes, "B"),
-        "coarse": ("alu", fm["coarse"], "flop"),
-        "tc_prep": ("hbm", (m >> L) * (n >> L) * 2 * 2, "B"),
-        "tc_score": ("alu", 6 * (2 * spec.w - 1) ** 2, "flop"),
+        "coarse": coarse,
+        "tc_prep": prep,
+        "tc_score": ("alu", 6 * W * W, "flop"),
         "refine": ("alu", fm["refine"], "flop"),
         "apply": ("hbm", 2 * m * n * esz, "B"),
     }
@@ -198,7 +210,7 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--frames", type=int, default=None, help="override frames per rank")
     ap.add_argument("--impl", default="moco", choices=["moco", "reference"])
-    ap.add_argument("--algo", default="auto", choices=["auto", "direct", "tc"])
+    ap.add_argument("--algo", default="auto", choices=["auto", "direct", "tc", "fft"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -283,7 +295,7 @@ def main():
 
     # ---- roofline of the dominant kernel (largest share of the timed region)
     peaks = read_peaks()
-    models = kernel_models(spec, esz)
+    models = kernel_models(spec, esz, plan.algo)
     kind = max((k for k in prof if prof[k][1] > 0), key=lambda k: prof[k][0])
     kms, klaunch = prof[kind]
     frames_timed = Tl * args.steps
@@ -292,6 +304,12 @@ def main():
         achieved = per_frame * frames_timed / (kms / 1e3) / 1e9
         peak, unit = peaks["hbm_gbs"], "GB/s"
         peak_note = f"MEASURED_PEAKS.json hbm_gbs ({peaks['source']})"
+    elif bound == "tensor_i8":
+        bound = "tensor"
+        achieved = per_frame * frames_timed / (kms / 1e3) / 1e12
+        peak, unit = 2.0 * peaks["bf16_tflops"], "TOP/s"
+        peak_note = (f"int8 dense = 2 x MEASURED_PEAKS.json bf16_tflops burst ({peaks['source']}; "
+                     "B200 nominal int8:bf16 = 4.5:2.25 P)")
     else:
         achieved = per_frame * frames_timed / (kms / 1e3) / 1e12
         peak = 148 * 128 * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12

@@ -346,7 +346,7 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
   for (int l = 1; l <= levels; ++l) per_frame += (size_t)p->ml[l] * p->pitch[l] * p->esz[l];
   // tensor-core operand planes + lag energies (upper bound: rows <= m_L + 128, int8 hi/lo)
   if (dtype == MOCO_U16) per_frame += (size_t)2 * (p->ml[levels] + 128) * p->nl[levels] + (size_t)W * W * 8;
-  const size_t budget = (size_t)256 << 20;
+  const size_t budget = (size_t)1 << 30;   // internal batch scratch (B200: 180 GB HBM)
   p->cap = per_frame ? std::max<int64_t>(1, (int64_t)(budget / per_frame)) : (int64_t)1 << 20;
   p->cap = std::min<int64_t>(p->cap, (int64_t)1 << 20);
   for (int l = 1; l <= levels; ++l)
@@ -376,8 +376,14 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
   p->algo = MOCO_ALGO_DIRECT;
   const bool tc_ok = tc_supported(p->dtype, p->bits, p->levels, p->w, p->ml[levels], p->nl[levels]);
   if (tc_ok && tc_auto_prefers(p->w)) {
-    if (tc_init(&p->tc, p->w, p->ml[levels], p->nl[levels], levels, p->cap) == 0) p->algo = MOCO_ALGO_TC;
-    else cudaGetLastError();
+    if (tc_init(&p->tc, p->w, p->ml[levels], p->nl[levels], levels, p->cap) == 0) {
+      p->algo = MOCO_ALGO_TC;
+      // whole waves of the tensor-core search per internal batch (2 CTAs/SM x GG*F frames)
+      const int64_t wave = (int64_t)nsm * 2 * p->tc.g.GG * p->tc.g.F;
+      if (p->cap >= wave) p->cap = p->cap / wave * wave;
+    } else {
+      cudaGetLastError();
+    }
   }
   if (p->algo == MOCO_ALGO_DIRECT && fft_supported(p) && (w > 64 || fft_auto_prefers(p->w, tc_ok))) {
     if (fft_init(p) == MOCO_OK) p->algo = MOCO_ALGO_FFT;
