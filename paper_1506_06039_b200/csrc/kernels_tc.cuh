@@ -5,12 +5,16 @@
 //
 //     h(s,t) = sum_i sum_j' a[i+s][j'] * b[i][j'-t]        (a, b zero outside the image)
 //
-// For each template row i and each 32-column strip of j' this is one MMA
-//     D[(s,f,pa), (pb,t)] += A[(s,f,pa), j'] * B[j', (pb,t)]
-// with M rows = (lag s, frame f, part pa) -- A is a sliding window over the frame's
-// rows (row i+s), addressed purely through the UMMA shared-memory descriptor, so the
-// Hankel structure costs no data movement -- and N columns = (part pb, lag t): B is
-// the Toeplitz expansion of template row i, generated in shared memory per step.
+// For each PAIR of template rows (i, i+1) and each 32-column strip of j' this is one MMA
+//     D[(s',f,pa), (d,pb,t)] += A[(s',f,pa), j'] * B[j', (d,pb,t)]
+// with M rows = (A-row lag s', frame f, part pa) -- A is a sliding window over the
+// frame's rows (row i+s'), addressed purely through the UMMA shared-memory descriptor,
+// so the Hankel structure costs no data movement -- and N columns = (d, part pb, lag t):
+// B is the Toeplitz expansion of template rows i (d = 0) and i+1 (d = 1), generated in
+// shared memory per step.  Frame row i+s' meets template row i+1 at lag s'-1, so
+//     h(s,t) = D[(s,.,.), (0,.,t)] + D[(s+1,.,.), (1,.,t)]
+// (A-row lags s' in [-(w-1), w]).  Pairing halves the MMA instructions and the A-operand
+// shared-memory reads per multiply-accumulate.
 //
 // Exactness: coarse values are < 2^14 (bits + 2L <= 14); each is split
 // into two 7-bit parts v = 128*hi + lo, both in [0,127], so every int8 product is exact
@@ -38,13 +42,15 @@ struct TcGeom {
   int ST;       // lag rows s per 128-row M tile = 64 / F
   int NT;       // M tiles
   int Wt;       // t lags padded to a multiple of 16
-  int N;        // 2 * Wt
+  int N1;       // columns per template row = 2 * Wt (parts x lags)
+  int N;        // 2 * N1: a template-row pair
   int R;        // rows per operand plane = mc + NT*ST (plane row = frame row + hw)
   int nstrips;  // 32-column strips of j'
   int planeB;   // bytes per 16-column plane = R * 32 * F
   int stripB;   // 2 planes
   int TPAD, TP; // padded template parts: TP = nc + 2*TPAD bytes per row, zeros in the pads
-  int ICH;      // template rows per super-stage (one ring slot per producer warp)
+  int ICH;      // template-row pairs per super-stage (one ring slot per producer warp)
+  int npairs;   // ceil(mc / 2)
   int GG;       // operand groups per CTA
   int tmem_cols;
   int smem;     // dynamic shared memory bytes
@@ -454,7 +460,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) k_tc_coarse(TcArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int F = g.F, hw = g.hw, mc = g.mc, nc = g.nc, N = g.N, NT = g.NT, GG = g.GG;
+  const int F = g.F, hw = g.hw, mc = g.mc, nc = g.nc, N = g.N, N1 = g.N1, NT = g.NT, GG = g.GG;
   constexpr int NSS = TC_PRODUCERS;                            // one ring slot per producer warp
   const int ICH = g.ICH;
   unsigned char *As = smem;                                   // [GG] strips of 2 planes
@@ -462,11 +468,11 @@ __global__ void __launch_bounds__(TC_THREADS, 2) k_tc_coarse(TcArgs a) {
   uint64_t *bars = reinterpret_cast<uint64_t *>(Bring + NSS * ICH * N * 32);
   uint64_t *full = bars, *empty = bars + NSS, *aload = bars + 2 * NSS;
   uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * NSS + 1);
-  Key *keys = reinterpret_cast<Key *>(smem);                 // epilogue: aliases the strips
   const int grp0 = blockIdx.x * GG;
   const int ngroups = (a.B + F - 1) / F;
   const int gcount = min(GG, ngroups - grp0);
-  const int nsuper = g.nstrips * (mc / ICH);
+  const int per_strip = g.npairs / ICH;
+  const int nsuper = g.nstrips * per_strip;
 
   if (warp == 0) tmem_alloc(tmem_holder, g.tmem_cols);
   if (tid == 0) {
@@ -503,7 +509,6 @@ __global__ void __launch_bounds__(TC_THREADS, 2) k_tc_coarse(TcArgs a) {
       tcol[j] = taddr + (uint32_t)(j * N);
     }
     const int nst = g.nstrips;
-    const int per_strip = mc / ICH;
     int ss = 0, round = 0;              // slot (= producer) and slot use of the super-stage
     int pss = NSS - 1, pround = -1;     // of the previous super-stage
     for (int st = 0; st < nst; ++st) {
@@ -517,12 +522,12 @@ __global__ void __launch_bounds__(TC_THREADS, 2) k_tc_coarse(TcArgs a) {
       __syncwarp();
       mbar_wait(aload, st & 1);
       tc_fence_after();
-      uint32_t arow = alo0;             // A descriptor low word at template row i
+      uint32_t arow = alo0;             // A descriptor low word at the pair's first template row
       for (int u = 0; u < per_strip; ++u) {
         mbar_wait(&full[ss], round & 1);
         tc_fence_after();
         uint32_t blo = blo0 + (uint32_t)ss * sstep;
-        for (int q = 0; q < ICH; ++q, blo += tilestep, arow += rowstep) {
+        for (int q = 0; q < ICH; ++q, blo += tilestep, arow += 2 * rowstep) {
           const uint32_t acc = (st | u | q) != 0 ? 1u : 0u;
 #pragma unroll
           for (int j = 0; j < 4; ++j)
@@ -536,32 +541,30 @@ __global__ void __launch_bounds__(TC_THREADS, 2) k_tc_coarse(TcArgs a) {
       }
     }
   } else {
-    // ---------------- B producers
+    // ---------------- B producers: tile of pair (i, i+1), row n = (d, pb, t)
     const int p = warp - 1;
-    // per-lane chunk geometry is the same for every tile: chunk cc = lane + 32q ->
-    // B row n = cc/2 = (pb, t), 16-byte half h = cc%2
     int srcoff[CPL], dstoff[CPL];
     bool live[CPL];
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
       const int cc = lane + 32 * q;
       const int n = cc >> 1, h = cc & 1;
-      const int pb = n >= g.Wt ? 1 : 0, ti = n - pb * g.Wt;
+      const int d = n >= N1 ? 1 : 0, r = n - d * N1;
+      const int pb = r >= g.Wt ? 1 : 0, ti = r - pb * g.Wt;
       live[q] = ti < g.W;
-      // bytes b_pb[i][J0 + 16h - t + x], x = 0..15, from the 4-aligned word below
+      // bytes b_pb[i+d][J0 + 16h - t + x], x = 0..15, from the 4-aligned word below
       const int col = 16 * h - (ti - hw) + g.TPAD;          // + J0, in the padded row
-      srcoff[q] = pb * mc * g.TP + col;
+      srcoff[q] = pb * (mc + 2) * g.TP + d * g.TP + col;
       dstoff[q] = (n >> 3) * 256 + h * 128 + (n & 7) * 16;
     }
-    const int per_strip = mc / ICH;
-    int st = p / per_strip, i0 = (p % per_strip) * ICH;
+    int st = p / per_strip, i0 = (p % per_strip) * ICH;   // strip, first pair of the super-stage
     const int ss = p;
     int round = 0;
     for (int u = p; u < nsuper; u += TC_PRODUCERS, ++round) {
       if (round > 0) mbar_wait(&empty[ss], (round - 1) & 1);
       unsigned char *Bs = Bring + ss * ICH * N * 32;
       for (int q = 0; q < ICH; ++q) {
-        const uint8_t *rowbase = a.T8 + (int64_t)(i0 + q) * g.TP + st * 32;
+        const uint8_t *rowbase = a.T8 + (int64_t)(2 * (i0 + q)) * g.TP + st * 32;
         uint32_t wv[CPL][5];
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
@@ -588,7 +591,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) k_tc_coarse(TcArgs a) {
       if (lane == 0) mbar_arrive(&full[ss]);
       // next super-stage of this warp: TC_PRODUCERS super-stages later
       i0 += TC_PRODUCERS * ICH;
-      while (i0 >= mc) { i0 -= mc; ++st; }
+      while (i0 >= g.npairs) { i0 -= g.npairs; ++st; }
     }
   }
   // all MMAs done -> accumulators final.  Every warp must be converged before the
@@ -603,30 +606,58 @@ __global__ void __launch_bounds__(TC_THREADS, 2) k_tc_coarse(TcArgs a) {
   tc_fence_after();
 
   // ---- epilogue: h -> N -> f -> argmin (S4), per frame.  Warp w reads TMEM lanes
-  // 32*(w%4).. of the tiles of groups gg = w/4, w/4 + 2, ...
+  // 32*(w%4).. of the tiles of groups gg = w/4, w/4 + 2, ...  Per 16-column chunk the
+  // d = 1 halves are first staged in shared memory (the strips are free now), so each
+  // row can add its partner row s'+1 (next lane block, or the next M tile).
   const int W = g.W;
   const int m = (warp & 3) * 32 + lane;     // accumulator row = TMEM lane
   const int sl = m / (2 * F), rho = m % (2 * F);
   const int f = rho >> 1, pa = rho & 1;
+  uint32_t *D1s = reinterpret_cast<uint32_t *>(smem);   // [GG*NT][128][32]: (pb hi 16 | pb lo 16)
+  Key *keys = reinterpret_cast<Key *>(smem + GG * NT * 128 * 32 * 4);
   Key best[4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    best[q] = Key{~0ull, ~0u};
-    const int gg = (warp >> 2) + 2 * q;
-    if (gg >= GG) continue;
-    const int fi = (grp0 + gg) * F + f;
-    Key bk{~0ull, ~0u};
-    for (int k = 0; k < NT; ++k) {
-      const int s = -hw + k * g.ST + sl;
-      const bool valid = gg < gcount && pa == 0 && s <= hw && fi < a.B;
-      for (int c = 0; c < g.Wt; c += 16) {
+  for (int q = 0; q < 4; ++q) best[q] = Key{~0ull, ~0u};
+  for (int c = 0; c < g.Wt; c += 16) {
+    // stage the d = 1 columns of this chunk
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int gg = (warp >> 2) + 2 * q;
+      if (gg >= GG) continue;
+      for (int k = 0; k < NT; ++k) {
+        uint32_t yh[16], yl[16];
+        const uint32_t tbase = taddr + ((uint32_t)((warp & 3) * 32) << 16) + (gg * NT + k) * N + N1;
+        tmem_ld16(tbase + c, yh);
+        tmem_ld16(tbase + g.Wt + c, yl);
+        tmem_wait_ld();
+        uint32_t *dst = D1s + ((gg * NT + k) * 128 + m) * 32;
+#pragma unroll
+        for (int qq = 0; qq < 16; ++qq) { dst[qq] = yh[qq]; dst[16 + qq] = yl[qq]; }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int gg = (warp >> 2) + 2 * q;
+      if (gg >= GG) continue;
+      const int fi = (grp0 + gg) * F + f;
+      Key bk = best[q];
+      for (int k = 0; k < NT; ++k) {
+        const int s = -hw + k * g.ST + sl;
+        const bool valid = gg < gcount && pa == 0 && s <= hw && fi < a.B;
+        // partner row s' = s + 1: same tile, 2F lanes further, or the next tile's first block
+        const int mp = sl + 1 < g.ST ? m + 2 * F : m + 2 * F - 128;
+        const int kp = sl + 1 < g.ST ? k : k + 1;
+        const bool haveP = kp < NT;   // s + 1 <= hw + 1 always lies inside the NT*ST lag rows
         uint32_t xh[16], xl[16];
         const uint32_t tbase = taddr + ((uint32_t)((warp & 3) * 32) << 16) + (gg * NT + k) * N;
-        tmem_ld16(tbase + c, xh);             // pb = hi
-        tmem_ld16(tbase + g.Wt + c, xl);      // pb = lo
+        tmem_ld16(tbase + c, xh);             // d = 0, pb = hi
+        tmem_ld16(tbase + g.Wt + c, xl);      // d = 0, pb = lo
         tmem_wait_ld();
+        const uint32_t *src = D1s + ((gg * NT + (haveP ? kp : 0)) * 128 + (haveP ? mp : 0)) * 32;
 #pragma unroll
         for (int qq = 0; qq < 16; ++qq) {
+          if (haveP) { xh[qq] += src[qq]; xl[qq] += src[16 + qq]; }   // each < 2^31: no wrap
           const uint32_t ph = __shfl_xor_sync(0xffffffffu, xh[qq], 1);   // partner row: pa = lo
           const uint32_t pl = __shfl_xor_sync(0xffffffffu, xl[qq], 1);
           const int ti = c + qq;
@@ -642,12 +673,11 @@ __global__ void __launch_bounds__(TC_THREADS, 2) k_tc_coarse(TcArgs a) {
           if (key_less(kk, bk)) bk = kk;
         }
       }
+      best[q] = bk;
     }
-    best[q] = bk;
+    __syncthreads();   // D1s is restaged by the next chunk
   }
   tc_fence_before();
-  fence_proxy_async();
-  __syncthreads();   // strip buffers are now free for the key table
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int gg = (warp >> 2) + 2 * q;
@@ -676,11 +706,12 @@ __global__ void __launch_bounds__(TC_THREADS, 2) k_tc_coarse(TcArgs a) {
 // (b >> 7, b & 127)[pb] for j in [0, nc), 0 in the pads
 __global__ void k_tc_template(const uint16_t *__restrict__ b, int pitch, int mc, int nc, int TPAD, int TP,
                               uint8_t *T8) {
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 2 * mc * TP; e += gridDim.x * blockDim.x) {
-    const int pb = e / (mc * TP), r = e % (mc * TP);
+  const int rows = mc + 2;   // zero rows past the template (second row of an odd-mc pair)
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 2 * rows * TP; e += gridDim.x * blockDim.x) {
+    const int pb = e / (rows * TP), r = e % (rows * TP);
     const int i = r / TP, j = r % TP - TPAD;
     uint8_t v = 0;
-    if (j >= 0 && j < nc) {
+    if (j >= 0 && j < nc && i < mc) {
       const uint32_t x = b[(int64_t)i * pitch + j];
       v = (uint8_t)(pb == 0 ? (x >> 7) : (x & 127u));
     }
@@ -693,38 +724,44 @@ inline bool tc_make_geom(TcGeom *gp, int w, int mc, int nc, int L) {
   TcGeom g{};
   g.mc = mc; g.nc = nc; g.w = w; g.hw = w - 1; g.W = 2 * w - 1; g.L = L;
   g.Wt = (g.W + 15) / 16 * 16;
-  g.N = 2 * g.Wt;
+  g.N1 = 2 * g.Wt;
+  g.N = 2 * g.N1;
   if (g.N > 256) return false;
+  const int lagrows = g.W + 1;   // A-row lags s' in [-(w-1), w]
   // frames per group: the largest F with the fewest padded lag rows and NT*N <= 256
   int bestF = 0, bestRows = 1 << 30;
   for (int F : {4, 2, 1}) {
-    const int ST = 64 / F, NT = (g.W + ST - 1) / ST;
+    const int ST = 64 / F, NT = (lagrows + ST - 1) / ST;
     if (NT * g.N > 256) continue;
     if (NT * ST < bestRows) { bestRows = NT * ST; bestF = F; }
   }
   if (!bestF) return false;
-  g.F = bestF; g.ST = 64 / g.F; g.NT = (g.W + g.ST - 1) / g.ST;
+  g.F = bestF; g.ST = 64 / g.F; g.NT = (lagrows + g.ST - 1) / g.ST;
   g.R = mc + g.NT * g.ST;
   g.nstrips = (nc + 31) / 32;
   g.planeB = g.R * 32 * g.F;
   g.stripB = 2 * g.planeB;
   g.TPAD = (g.hw + 8 + 15) / 16 * 16;
   g.TP = nc + 2 * g.TPAD;
+  g.npairs = (mc + 1) / 2;
   auto smem_for = [&](int GG, int ICH) {
     return 1024 + GG * g.stripB + TC_PRODUCERS * ICH * g.N * 32 + (2 * TC_PRODUCERS + 1) * 8 + 16;
   };
   // two CTAs per SM (one loads its next strip while the other computes): as many
-  // groups per CTA as half of shared memory and half of TMEM allow, then the
-  // largest super-stage (ICH | mc) that still fits
+  // groups per CTA as half of shared memory and half of TMEM allow, then the largest
+  // super-stage (ICH | npairs) that still fits; the epilogue's staging of the d = 1
+  // accumulator halves (GG*NT*128*32 words + keys) must fit in the same memory
   g.GG = 0;
   for (int GG = 4; GG >= 1 && !g.GG; --GG) {
     if (GG * g.NT * g.N > 256 || GG * g.NT > 4) continue;
-    for (int ICH = 4; ICH >= 1; ICH /= 2)
-      if (mc % ICH == 0 && smem_for(GG, ICH) <= 113 * 1024 && GG * 128 * 16 <= GG * g.stripB) {
+    for (int ICH = 4; ICH >= 1; ICH /= 2) {
+      const int sm = smem_for(GG, ICH);
+      if (g.npairs % ICH == 0 && sm <= 113 * 1024 && GG * g.NT * 128 * 128 + GG * 128 * 16 <= sm - 1024 - 256) {
         g.GG = GG;
         g.ICH = ICH;
         break;
       }
+    }
   }
   if (!g.GG) return false;
   int cols = 32;
@@ -755,7 +792,7 @@ inline int tc_init(TcPlan *tc, int w, int mc, int nc, int L, int64_t cap) {
   const int64_t groups = (cap + g.F - 1) / g.F;
   if (cudaMalloc(&tc->G, (size_t)groups * g.nstrips * g.stripB) != cudaSuccess) return -1;
   if (cudaMalloc(&tc->ga, (size_t)cap * g.W * g.W * sizeof(u64)) != cudaSuccess) return -1;
-  if (cudaMalloc(&tc->T8, (size_t)2 * mc * g.TP) != cudaSuccess) return -1;
+  if (cudaMalloc(&tc->T8, (size_t)2 * (mc + 2) * g.TP) != cudaSuccess) return -1;
   if (cudaFuncSetAttribute(k_tc_coarse<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_tc_coarse<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_tc_coarse<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||

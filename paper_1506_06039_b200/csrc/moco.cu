@@ -695,7 +695,7 @@ static int launch_tc(moco_plan *p, const void *frames_b, int64_t B, int32_t *shi
   {
     ProfScope ps(p, MOCO_K_COARSE, st);
     const unsigned grid = (unsigned)((groups + g.GG - 1) / g.GG);
-    switch (g.N / 16) {   // chunks per producer lane = 2N/32
+    switch (g.N / 16) {   // chunks per producer lane = 2N/32 (N = 128 / 192 / 256 for C2 / C1 / C3)
       case 2: k_tc_coarse<2><<<grid, TC_THREADS, g.smem, st>>>(ta); break;
       case 4: k_tc_coarse<4><<<grid, TC_THREADS, g.smem, st>>>(ta); break;
       case 10: k_tc_coarse<10><<<grid, TC_THREADS, g.smem, st>>>(ta); break;
