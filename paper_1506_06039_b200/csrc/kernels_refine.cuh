@@ -277,12 +277,16 @@ __global__ void __launch_bounds__(RS_THREADS, 1)
     for (int k = 0; k < NS; ++k) {
       mbar_init(&full[k], 1);
       mbar_init(&empty[k], 1);
+      reinterpret_cast<int *>(empty + 32)[32 + k] = -1;
     }
     fence_mbar_init();
   }
   __syncthreads();
   if (nr <= 0) return;
   int *stg_offa = reinterpret_cast<int *>(empty + 32);   // [32] misalignment of the frame in each stage
+  int *stg_tag = stg_offa + 32;                           // [32] frame a stage was last issued for
+  // (a parity wait alone can alias: a consumer may start waiting on a stage while its
+  // previous use is still in flight, two phases behind; the tag orders it first)
   if (warp == 0) {
     // ---------------- producer: frame f's rows [r0+S-1, r0+nr+S+1) into stage f % NS.
     // Lanes 0..7 each own every 8th frame (independent stages), so eight frames are
@@ -302,6 +306,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1)
           const int x0 = c0 + (T - 1) - ((T - 1) & 7);
           uint16_t *Fs = reinterpret_cast<uint16_t *>(ring + stg * SB);
           stg_offa[stg] = (T - 1) & 7;
+          *reinterpret_cast<volatile int *>(&stg_tag[stg]) = f;
           mbar_arrive_expect_tx(&full[stg], bytes);
 #pragma unroll
           for (int bx = 0; bx < RS_NBOX; ++bx)
@@ -317,6 +322,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1)
   uint32_t *rw = red + cw * 32 * 19;
   for (int f = cw; f < a.B; f += RS_CW) {
     const int stg = f % NS;
+    while (*reinterpret_cast<volatile int *>(&stg_tag[stg]) != f) __nanosleep(32);
     mbar_wait(&full[stg], (f / NS) & 1);
     const int offa = stg_offa[stg];
     const uint16_t *Fs = reinterpret_cast<const uint16_t *>(ring + stg * SB);

@@ -64,6 +64,8 @@ struct TcPlan {
   int64_t cap = 0;          // frames per batch
   uint8_t *G = nullptr;     // operand planes for cap frames
   u64 *ga = nullptr;        // [cap][W*W] frame energies
+  uint8_t *G2 = nullptr;    // second buffers: the prep of batch k+1 overlaps batch k
+  u64 *ga2 = nullptr;
   uint8_t *T8 = nullptr;    // template parts [2][mc][nc]
 };
 
@@ -792,6 +794,13 @@ inline int tc_init(TcPlan *tc, int w, int mc, int nc, int L, int64_t cap) {
   const int64_t groups = (cap + g.F - 1) / g.F;
   if (cudaMalloc(&tc->G, (size_t)groups * g.nstrips * g.stripB) != cudaSuccess) return -1;
   if (cudaMalloc(&tc->ga, (size_t)cap * g.W * g.W * sizeof(u64)) != cudaSuccess) return -1;
+  if (cudaMalloc(&tc->G2, (size_t)groups * g.nstrips * g.stripB) != cudaSuccess ||
+      cudaMalloc(&tc->ga2, (size_t)cap * g.W * g.W * sizeof(u64)) != cudaSuccess) {
+    cudaGetLastError();   // optional: without them batches run back to back
+    if (tc->G2) cudaFree(tc->G2);
+    tc->G2 = nullptr;
+    tc->ga2 = nullptr;
+  }
   if (cudaMalloc(&tc->T8, (size_t)2 * (mc + 2) * g.TP) != cudaSuccess) return -1;
   if (cudaFuncSetAttribute(k_tc_coarse<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_tc_coarse<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
@@ -821,6 +830,9 @@ inline int tc_set_template(TcPlan *tc, const uint16_t *tpl_coarse, int pitch, cu
 inline void tc_free(TcPlan *tc) {
   if (tc->G) cudaFree(tc->G);
   if (tc->ga) cudaFree(tc->ga);
+  if (tc->G2) cudaFree(tc->G2);
+  if (tc->ga2) cudaFree(tc->ga2);
+  tc->G2 = nullptr; tc->ga2 = nullptr;
   if (tc->T8) cudaFree(tc->T8);
   tc->G = nullptr; tc->ga = nullptr; tc->T8 = nullptr;
   tc->ready = tc->tpl_ready = false;

@@ -75,6 +75,10 @@ struct moco_plan {
     double eps_rel = 0;
     int smem_rows = 0, smem_cols = 0, smem_score = 0, smem_energy = 0;
   } fft;
+  // two-stream batch pipeline (align_tc_pipelined)
+  bool pipe_ready;
+  cudaStream_t ps[2];
+  cudaEvent_t pe_prep[2], pe_free[2], pe_start, pe_end;
   // end-to-end staging
   bool host_ready;
   int64_t host_ch;
@@ -182,6 +186,13 @@ static void plan_free(moco_plan *p) {
   }
   for (int k = 0; k < 3; ++k)
     if (p->hs[k]) cudaStreamDestroy(p->hs[k]);
+  for (int k = 0; k < 2; ++k) {
+    if (p->ps[k]) cudaStreamDestroy(p->ps[k]);
+    if (p->pe_prep[k]) cudaEventDestroy(p->pe_prep[k]);
+    if (p->pe_free[k]) cudaEventDestroy(p->pe_free[k]);
+  }
+  if (p->pe_start) cudaEventDestroy(p->pe_start);
+  if (p->pe_end) cudaEventDestroy(p->pe_end);
   for (auto &r : p->prof_live) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : p->prof_pool) cudaEventDestroy(e);
   delete p;
@@ -370,7 +381,8 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
       }
       p->rrt[l] = rt;
       p->rnrt[l] = nrt;
-      p->rstages[l] = std::min(32, (200 * 1024 - rs_smem_bytes(rt, 0)) / rs_stage_bytes(rt));
+      // (ring within ~150 KB: a 37 KB operand-prep CTA of the next batch fits beside it)
+      p->rstages[l] = std::min(32, (150 * 1024 - rs_smem_bytes(rt, 0)) / rs_stage_bytes(rt));
     }
   if (rc != MOCO_OK) { plan_free(p); return rc; }
   p->algo = MOCO_ALGO_DIRECT;
@@ -672,14 +684,14 @@ static int check_align_args(moco_plan *p, const void *frames, int64_t T) {
   return MOCO_OK;
 }
 
-// Tensor-core coarse search (kernels_tc.cuh) straight from the level-0 frames.
-static int launch_tc(moco_plan *p, const void *frames_b, int64_t B, int32_t *shift_out, double *f_out,
-                     uint8_t *flags, double *grid_out, cudaStream_t st) {
+// Tensor-core coarse search (kernels_tc.cuh) straight from the level-0 frames:
+// K_prep (operand planes G + lag energies ga) then K_tc.
+static int launch_tc_prep(moco_plan *p, const void *frames_b, int64_t B, uint8_t *G, u64 *ga, cudaStream_t st) {
   const TcGeom &g = p->tc.g;
   const int64_t groups = (B + g.F - 1) / g.F;
   TcPrepArgs pa;
   pa.frames = (const uint16_t *)frames_b; pa.fstride = (int64_t)p->m * p->n; pa.n = p->n;
-  pa.B = (int)B; pa.g = g; pa.G = p->tc.G; pa.ga = p->tc.ga;
+  pa.B = (int)B; pa.g = g; pa.G = G; pa.ga = ga;
   {
     ProfScope ps(p, MOCO_K_PREP, st);
     if (p->levels == 0) k_tc_prep<0><<<(unsigned)groups, 256, g.prep_smem, st>>>(pa);
@@ -688,8 +700,15 @@ static int launch_tc(moco_plan *p, const void *frames_b, int64_t B, int32_t *shi
   }
   p->launches++;
   CKL("k_tc_prep");
+  return MOCO_OK;
+}
+
+static int launch_tc_coarse(moco_plan *p, int64_t B, const uint8_t *G, const u64 *ga, int32_t *shift_out,
+                            double *f_out, uint8_t *flags, double *grid_out, cudaStream_t st) {
+  const TcGeom &g = p->tc.g;
+  const int64_t groups = (B + g.F - 1) / g.F;
   TcArgs ta;
-  ta.G = p->tc.G; ta.T8 = p->tc.T8; ta.ga = p->tc.ga; ta.gb = (const u64 *)p->gb; ta.g = g;
+  ta.G = G; ta.T8 = p->tc.T8; ta.ga = ga; ta.gb = (const u64 *)p->gb; ta.g = g;
   ta.scale = (double)(1u << (4 * p->levels)); ta.B = (int)B;
   ta.shift_out = shift_out; ta.f_out = f_out; ta.flags = flags; ta.grid_out = grid_out;
   {
@@ -709,6 +728,13 @@ static int launch_tc(moco_plan *p, const void *frames_b, int64_t B, int32_t *shi
   p->launches++;
   CKL("k_tc_coarse");
   return MOCO_OK;
+}
+
+static int launch_tc(moco_plan *p, const void *frames_b, int64_t B, int32_t *shift_out, double *f_out,
+                     uint8_t *flags, double *grid_out, cudaStream_t st) {
+  int rc = launch_tc_prep(p, frames_b, B, p->tc.G, p->tc.ga, st);
+  if (rc) return rc;
+  return launch_tc_coarse(p, B, p->tc.G, p->tc.ga, shift_out, f_out, flags, grid_out, st);
 }
 
 // S5 refine at levels L-1..0, then S6 apply (fused into the level-0 refine when possible).
@@ -774,6 +800,58 @@ static int run_batch(moco_plan *p, const void *frames_b, int64_t B, int32_t *shi
   return refine_levels(p, img, fstride, B, shifts_b, fmin_b, corr_b, st);
 }
 
+// Several internal batches on the tensor-core path (levels = 1): the HBM-bound operand
+// preparation of batch k+1 runs on a second stream into the other G/ga buffer while the
+// tensor-core search, refine and apply of batch k run on the main stream, so the
+// memory-bound and the compute-bound kernels share the SMs.  Stream-ordered with respect
+// to the caller's stream on entry and exit.
+static int align_tc_pipelined(moco_plan *p, const void *d_frames, int64_t T, int32_t *d_shifts, double *d_fmin,
+                              void *d_corrected, uint8_t *d_flags, cudaStream_t user) {
+  if (!p->pipe_ready) {
+    CK(cudaStreamCreateWithFlags(&p->ps[0], cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&p->ps[1], cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+      CK(cudaEventCreateWithFlags(&p->pe_prep[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&p->pe_free[k], cudaEventDisableTiming));
+    }
+    CK(cudaEventCreateWithFlags(&p->pe_start, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&p->pe_end, cudaEventDisableTiming));
+    p->pipe_ready = true;
+  }
+  cudaStream_t sp = p->ps[0], sm = p->ps[1];
+  CK(cudaEventRecord(p->pe_start, user));
+  CK(cudaStreamWaitEvent(sp, p->pe_start, 0));
+  CK(cudaStreamWaitEvent(sm, p->pe_start, 0));
+  const size_t fbytes = (size_t)p->m * p->n * p->esz[0];
+  uint8_t *G[2] = {p->tc.G, p->tc.G2};
+  u64 *ga[2] = {p->tc.ga, p->tc.ga2};
+  // equal batches of whole tensor-core waves where possible
+  const int64_t nb = (T + p->cap - 1) / p->cap;
+  int64_t k = 0;
+  for (int64_t f0 = 0; f0 < T; f0 += p->cap, ++k) {
+    const int64_t B = std::min<int64_t>(p->cap, T - f0);
+    const int buf = (int)(k & 1);
+    const char *fr = (const char *)d_frames + f0 * fbytes;
+    if (k >= 2) CK(cudaStreamWaitEvent(sp, p->pe_free[buf], 0));
+    int rc = launch_tc_prep(p, fr, B, G[buf], ga[buf], sp);
+    if (rc) return rc;
+    CK(cudaEventRecord(p->pe_prep[buf], sp));
+    CK(cudaStreamWaitEvent(sm, p->pe_prep[buf], 0));
+    rc = launch_tc_coarse(p, B, G[buf], ga[buf], p->sh[1], nullptr, d_flags ? d_flags + f0 : nullptr, nullptr, sm);
+    if (rc) return rc;
+    CK(cudaEventRecord(p->pe_free[buf], sm));
+    const void *img[3] = {fr, nullptr, nullptr};
+    const int64_t fstride[3] = {(int64_t)p->m * p->n, 0, 0};
+    rc = refine_levels(p, img, fstride, B, d_shifts + 2 * f0, d_fmin + f0,
+                       d_corrected ? (char *)d_corrected + f0 * fbytes : nullptr, sm);
+    if (rc) return rc;
+  }
+  (void)nb;
+  CK(cudaEventRecord(p->pe_end, sm));
+  CK(cudaStreamWaitEvent(user, p->pe_end, 0));
+  return MOCO_OK;
+}
+
 int moco_align_batch(moco_plan *p, const void *d_frames, int64_t T, int32_t *d_shifts,
                      double *d_fmin, void *d_corrected, uint8_t *d_flags, moco_stream_t stream) {
   int rc = check_align_args(p, d_frames, T);
@@ -784,6 +862,8 @@ int moco_align_batch(moco_plan *p, const void *d_frames, int64_t T, int32_t *d_s
   CK(cudaSetDevice(p->device));
   p->launches = 0;
   const size_t fbytes = (size_t)p->m * p->n * p->esz[0];
+  if (p->algo == MOCO_ALGO_TC && p->levels == 1 && T > p->cap && p->tc.G2 && !getenv("MOCO_NOPIPE"))
+    return align_tc_pipelined(p, d_frames, T, d_shifts, d_fmin, d_corrected, d_flags, (cudaStream_t)stream);
   for (int64_t f0 = 0; f0 < T; f0 += p->cap) {
     const int64_t B = std::min<int64_t>(p->cap, T - f0);
     rc = run_batch(p, (const char *)d_frames + f0 * fbytes, B, d_shifts + 2 * f0, d_fmin + f0,
