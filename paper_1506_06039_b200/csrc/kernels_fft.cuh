@@ -286,11 +286,13 @@ struct FftScoreArgs {
 __device__ u64 exact_h(const FftScoreArgs &a, const uint16_t *A, int s, int t, u64 *red) {
   const int mc = a.g.mc, nc = a.g.nc;
   const int i0 = max(0, -s), i1 = mc - max(0, s), j0 = max(0, -t), j1 = nc - max(0, t);
+  // flattened over the overlap so every thread has many independent loads in flight
+  const int wdt = j1 - j0, total = (i1 - i0) * wdt;
   u64 acc = 0;
-  for (int i = i0; i < i1; ++i) {
-    const uint16_t *ar = A + (int64_t)(i + s) * a.pitch + t;
-    const uint16_t *br = a.tpl + (int64_t)i * a.tpitch;
-    for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) acc += (u64)((uint32_t)ar[j] * (uint32_t)br[j]);
+#pragma unroll 4
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int i = i0 + e / wdt, j = j0 + e % wdt;
+    acc += (u64)((uint32_t)A[(int64_t)(i + s) * a.pitch + j + t] * (uint32_t)a.tpl[(int64_t)i * a.tpitch + j]);
   }
   acc = warp_sum(acc);
   __syncthreads();
@@ -302,7 +304,7 @@ __device__ u64 exact_h(const FftScoreArgs &a, const uint16_t *A, int s, int t, u
   return tot;
 }
 
-__global__ void __launch_bounds__(FFT_THREADS) k_fft_score(FftScoreArgs a) {
+__global__ void __launch_bounds__(1024) k_fft_score(FftScoreArgs a) {
   extern __shared__ __align__(16) float2 fsm[];
   const FftGeom &g = a.g;
   const int Mc = g.Lc.N, W = g.W, hw = g.hw;
@@ -410,7 +412,7 @@ __global__ void __launch_bounds__(FFT_THREADS) k_fft_score(FftScoreArgs a) {
 // (P:32-35): total minus the excluded edge strips plus the doubly excluded corner --
 // the paper's DP of P:35 run in each corner (a (w x w) prefix table per corner).
 // One block per frame; works for any w (tables in dynamic shared memory).
-__global__ void __launch_bounds__(256) k_energy_u16(const uint16_t *__restrict__ img, int64_t fstride, int pitch,
+__global__ void __launch_bounds__(1024) k_energy_u16(const uint16_t *__restrict__ img, int64_t fstride, int pitch,
                                                     int mc, int nc, int w, u64 *__restrict__ ga) {
   extern __shared__ __align__(16) u64 esm[];
   const int hw = w - 1, W = 2 * w - 1, CS = w * w;

@@ -378,14 +378,15 @@ struct RefinePickArgs {
   int32_t *shift_out;       // [B][2] at level l
   double *f_out;            // [B] or null
   uint16_t *corrected;      // [B][ml][nl] or null (level 0)
+  int parts;                // CTAs per frame (apply rows split among them)
 };
 
 template <int SH>
 __device__ __forceinline__ void pick_apply_rows(const uint16_t *A, uint16_t *O, int pitch, int s, int t, int ml,
-                                                int nl) {
+                                                int nl, int r0, int r1) {
   // output chunk (i, 8-column group j0): source samples a[i+s][j0+t .. j0+t+7]; the two
   // aligned vectors at ab = j0 + t - SH cover them; out-of-frame samples are 0
-  const int groups = nl >> 3, total = ml * groups;
+  const int groups = nl >> 3, total = (r1 - r0) * groups;
   constexpr int U = 4;
   for (int e0 = threadIdx.x; e0 < total; e0 += U * blockDim.x) {
     uint4 lo[U], hi[U];
@@ -394,7 +395,7 @@ __device__ __forceinline__ void pick_apply_rows(const uint16_t *A, uint16_t *O, 
     for (int k = 0; k < U; ++k) {
       const int e = e0 + k * blockDim.x;
       const int ec = e < total ? e : 0;
-      ii[k] = ec / groups;
+      ii[k] = r0 + ec / groups;
       jj[k] = (ec % groups) * 8;
       const int r = ii[k] + s, ab = jj[k] + t - SH;
       const bool rok = e < total && r >= 0 && r < ml;
@@ -419,10 +420,14 @@ __device__ __forceinline__ void pick_apply_rows(const uint16_t *A, uint16_t *O, 
   }
 }
 
-// One CTA per frame: argmin of the nine candidates, then (level 0) the corrected frame.
+// CTA (frame f, part) with gridDim.x = B * parts: argmin of the nine candidates (every
+// part computes it; part 0 stores it), then (level 0) rows [part ml/parts, ...) of the
+// corrected frame -- small batches (the closed-loop case) spread one frame over many SMs.
 __global__ void __launch_bounds__(256) k_refine_pick(RefinePickArgs a) {
   __shared__ int res[2];
-  const int64_t f = blockIdx.x;
+  const int parts = a.parts;
+  const int64_t f = blockIdx.x / parts;
+  const int part = blockIdx.x % parts;
   const int S = 2 * a.shift_in[2 * f], T = 2 * a.shift_in[2 * f + 1];
   const int ml = a.ml, nl = a.nl;
   if (threadIdx.x < 32) {
@@ -442,30 +447,33 @@ __global__ void __launch_bounds__(256) k_refine_pick(RefinePickArgs a) {
       k = Key{(u64)__double_as_longlong(fv), (unsigned)c};   // rank == (s,t) lexicographic order
     }
     k = warp_min_key(k);
-    if (lane < 18) acc[lane] = 0;   // ready for the next call
     if (lane == 0) {
       const int s = S + (int)(k.idx / 3) - 1, t = T + (int)(k.idx % 3) - 1;
-      a.shift_out[2 * f] = s;
-      a.shift_out[2 * f + 1] = t;
-      if (a.f_out) a.f_out[f] = __longlong_as_double((long long)k.f);
+      if (part == 0) {
+        a.shift_out[2 * f] = s;
+        a.shift_out[2 * f + 1] = t;
+        if (a.f_out) a.f_out[f] = __longlong_as_double((long long)k.f);
+      }
       res[0] = s;
       res[1] = t;
     }
   }
+  if (parts == 1 && threadIdx.x < 18) a.acc[f * 18 + threadIdx.x] = 0;   // ready for the next call
   if (!a.corrected) return;
   __syncthreads();
   const int s = res[0], t = res[1];
   const uint16_t *A = a.frames + f * a.fstride;
   uint16_t *O = a.corrected + f * (int64_t)ml * nl;
+  const int r0 = (int)((int64_t)part * ml / parts), r1 = (int)((int64_t)(part + 1) * ml / parts);
   switch (t & 7) {
-    case 0: pick_apply_rows<0>(A, O, a.pitch, s, t, ml, nl); break;
-    case 1: pick_apply_rows<1>(A, O, a.pitch, s, t, ml, nl); break;
-    case 2: pick_apply_rows<2>(A, O, a.pitch, s, t, ml, nl); break;
-    case 3: pick_apply_rows<3>(A, O, a.pitch, s, t, ml, nl); break;
-    case 4: pick_apply_rows<4>(A, O, a.pitch, s, t, ml, nl); break;
-    case 5: pick_apply_rows<5>(A, O, a.pitch, s, t, ml, nl); break;
-    case 6: pick_apply_rows<6>(A, O, a.pitch, s, t, ml, nl); break;
-    default: pick_apply_rows<7>(A, O, a.pitch, s, t, ml, nl); break;
+    case 0: pick_apply_rows<0>(A, O, a.pitch, s, t, ml, nl, r0, r1); break;
+    case 1: pick_apply_rows<1>(A, O, a.pitch, s, t, ml, nl, r0, r1); break;
+    case 2: pick_apply_rows<2>(A, O, a.pitch, s, t, ml, nl, r0, r1); break;
+    case 3: pick_apply_rows<3>(A, O, a.pitch, s, t, ml, nl, r0, r1); break;
+    case 4: pick_apply_rows<4>(A, O, a.pitch, s, t, ml, nl, r0, r1); break;
+    case 5: pick_apply_rows<5>(A, O, a.pitch, s, t, ml, nl, r0, r1); break;
+    case 6: pick_apply_rows<6>(A, O, a.pitch, s, t, ml, nl, r0, r1); break;
+    default: pick_apply_rows<7>(A, O, a.pitch, s, t, ml, nl, r0, r1); break;
   }
 }
 

@@ -43,6 +43,7 @@ static int set_cuda_err(cudaError_t e, const char *what) {
 struct moco_plan {
   int m, n, w, W, levels, dtype, bits, device;
   int algo;                   // resolved MOCO_ALGO_*
+  bool algo_forced;           // set by moco_plan_set_algo (no per-call routing)
   int ml[3], nl[3], pitch[3]; // per level dims and row pitch (elements)
   size_t esz[3];              // element size per level
   void *tpl[3];               // template pyramid
@@ -273,7 +274,9 @@ static int launch_fft(moco_plan *p, const void *img, int64_t fstride, int pitch,
     const uint16_t *im = (const uint16_t *)img + b0 * fstride;
     {
       ProfScope ps(p, MOCO_K_PREP, st);
-      k_energy_u16<<<(unsigned)nb, 256, F.smem_energy, st>>>(im, fstride, pitch, g.mc, g.nc, g.w, F.ga);
+      // small batches (closed loop): a whole SM per frame for the per-frame kernels
+      const int eth = nb < p->nsm ? 1024 : 256;
+      k_energy_u16<<<(unsigned)nb, eth, F.smem_energy, st>>>(im, fstride, pitch, g.mc, g.nc, g.w, F.ga);
     }
     {
       ProfScope ps(p, MOCO_K_COARSE, st);
@@ -291,7 +294,7 @@ static int launch_fft(moco_plan *p, const void *img, int64_t fstride, int pitch,
     a.h_out = h_out ? h_out + b0 * g.W * g.W : nullptr;
     {
       ProfScope ps(p, MOCO_K_SCORE, st);
-      k_fft_score<<<(unsigned)nb, FFT_THREADS, F.smem_score, st>>>(a);
+      k_fft_score<<<(unsigned)nb, nb < p->nsm ? 1024 : FFT_THREADS, F.smem_score, st>>>(a);
     }
     p->launches += 4;
     CKL("fft path");
@@ -400,6 +403,8 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
   if (p->algo == MOCO_ALGO_DIRECT && fft_supported(p) && (w > 64 || fft_auto_prefers(p->w, tc_ok))) {
     if (fft_init(p) == MOCO_OK) p->algo = MOCO_ALGO_FFT;
     else cudaGetLastError();
+  } else if (p->algo == MOCO_ALGO_TC && fft_supported(p)) {
+    if (fft_init(p) != MOCO_OK) cudaGetLastError();   // latency route for small calls (optional)
   }
   if (w > 64 && p->algo != MOCO_ALGO_FFT) { plan_free(p); return MOCO_EINVAL; }
   *out = p;
@@ -442,6 +447,7 @@ int moco_plan_set_algo(moco_plan *p, int algo) {
       CK(cudaDeviceSynchronize());
     }
     p->algo = MOCO_ALGO_TC;
+    p->algo_forced = algo == MOCO_ALGO_TC;
     return MOCO_OK;
   }
   return MOCO_EINVAL;
@@ -587,6 +593,10 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
   b.scale = (double)(1u << (4 * l));
   b.B = (int)B; b.shift_in = sin; b.acc = p->racc; b.shift_out = sout; b.f_out = fout;
   b.corrected = (uint16_t *)corr;
+  // small batches: several CTAs per frame for the apply (the accumulators are then
+  // cleared by a memset after the pick instead of by the single CTA)
+  b.parts = (int)std::max<int64_t>(1, std::min<int64_t>(16, p->nsm / std::max<int64_t>(1, B)));
+  if (!corr) b.parts = 1;
   {
     ProfScope ps(p, MOCO_K_REFINE, st);
     const int smem = rs_smem_bytes(a.rt, a.stages);
@@ -604,10 +614,11 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
   CKL("k_refine_sums");
   {
     ProfScope ps(p, MOCO_K_APPLY, st);
-    k_refine_pick<<<(unsigned)B, 256, 0, st>>>(b);
+    k_refine_pick<<<(unsigned)(B * b.parts), 256, 0, st>>>(b);
   }
   p->launches++;
   CKL("k_refine_pick");
+  if (b.parts > 1) CK(cudaMemsetAsync(p->racc, 0, (size_t)B * 18 * sizeof(u64), st));
   return MOCO_OK;
 }
 
@@ -805,6 +816,8 @@ static int run_batch(moco_plan *p, const void *frames_b, int64_t B, int32_t *shi
 // tensor-core search, refine and apply of batch k run on the main stream, so the
 // memory-bound and the compute-bound kernels share the SMs.  Stream-ordered with respect
 // to the caller's stream on entry and exit.
+constexpr int64_t LAT_T = 16;   // calls with at most this many frames take the latency route
+
 static int align_tc_pipelined(moco_plan *p, const void *d_frames, int64_t T, int32_t *d_shifts, double *d_fmin,
                               void *d_corrected, uint8_t *d_flags, cudaStream_t user) {
   if (!p->pipe_ready) {
@@ -862,6 +875,18 @@ int moco_align_batch(moco_plan *p, const void *d_frames, int64_t T, int32_t *d_s
   CK(cudaSetDevice(p->device));
   p->launches = 0;
   const size_t fbytes = (size_t)p->m * p->n * p->esz[0];
+  // closed-loop sizes: the FFT path spreads one frame over many SMs (DESIGN.md §8 latency)
+  if (p->algo == MOCO_ALGO_TC && T <= LAT_T && p->fft.ready && p->fft.tpl_ready && !p->algo_forced) {
+    p->algo = MOCO_ALGO_FFT;
+    for (int64_t f0 = 0; f0 < T && rc == MOCO_OK; f0 += p->cap) {
+      const int64_t B = std::min<int64_t>(p->cap, T - f0);
+      rc = run_batch(p, (const char *)d_frames + f0 * fbytes, B, d_shifts + 2 * f0, d_fmin + f0,
+                     d_corrected ? (char *)d_corrected + f0 * fbytes : nullptr,
+                     d_flags ? d_flags + f0 : nullptr, nullptr, (cudaStream_t)stream);
+    }
+    p->algo = MOCO_ALGO_TC;
+    return rc;
+  }
   if (p->algo == MOCO_ALGO_TC && p->levels == 1 && T > p->cap && p->tc.G2 && !getenv("MOCO_NOPIPE"))
     return align_tc_pipelined(p, d_frames, T, d_shifts, d_fmin, d_corrected, d_flags, (cudaStream_t)stream);
   for (int64_t f0 = 0; f0 < T; f0 += p->cap) {
