@@ -83,12 +83,12 @@ struct moco_plan {
   // end-to-end staging
   bool host_ready;
   int64_t host_ch;
-  void *slot_in[2], *slot_out[2];
-  int32_t *slot_sh[2];
-  double *slot_f[2];
-  uint8_t *slot_flags[2];
+  void *slot_in[3], *slot_out[3];
+  int32_t *slot_sh[3];
+  double *slot_f[3];
+  uint8_t *slot_flags[3];
   cudaStream_t hs[3];
-  cudaEvent_t ev_in[2], ev_done[2], ev_free[2];
+  cudaEvent_t ev_in[3], ev_done[3], ev_free[3];
   // live per-kernel timing (moco_profile_*)
   bool prof_on;
   struct ProfRec { int kind; cudaEvent_t a, b; };
@@ -175,7 +175,7 @@ static void plan_free(moco_plan *p) {
   for (void *q : {(void *)p->fft.twr, (void *)p->fft.twc, (void *)p->fft.Bc, (void *)p->fft.S, (void *)p->fft.P,
                   (void *)p->fft.ga, (void *)p->fft.qc})
     if (q) cudaFree(q);
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < 3; ++k) {
     if (p->slot_in[k]) cudaFree(p->slot_in[k]);
     if (p->slot_out[k]) cudaFree(p->slot_out[k]);
     if (p->slot_sh[k]) cudaFree(p->slot_sh[k]);
@@ -961,11 +961,12 @@ int moco_align_host(moco_plan *p, const void *h_frames, int64_t T, int32_t *h_sh
   CK(cudaSetDevice(p->device));
   const size_t fbytes = (size_t)p->m * p->n * p->esz[0];
   if (!p->host_ready) {
-    // chunks of ~32 MiB of frames, capped by the plan's batch capacity; two
-    // slots so the copy of chunk k+1 in and chunk k-1 out overlap chunk k's
-    // kernels.  Compute stays on ONE stream (the plan's scratch is shared).
-    p->host_ch = std::max<int64_t>(1, std::min<int64_t>(p->cap, ((int64_t)32 << 20) / (int64_t)fbytes));
-    for (int k = 0; k < 2; ++k) {
+    // chunks of ~128 MiB of frames, capped by the plan's batch capacity; three slots so
+    // the copy of chunk k+1 in, the kernels of chunk k and the copy of chunk k-1 out
+    // all overlap (PCIe is full duplex).  Compute stays on ONE stream (the plan's
+    // scratch is shared).
+    p->host_ch = std::max<int64_t>(1, std::min<int64_t>(p->cap, ((int64_t)128 << 20) / (int64_t)fbytes));
+    for (int k = 0; k < 3; ++k) {
       if (cudaMalloc(&p->slot_in[k], p->host_ch * fbytes) != cudaSuccess ||
           cudaMalloc(&p->slot_out[k], p->host_ch * fbytes) != cudaSuccess ||
           cudaMalloc((void **)&p->slot_sh[k], p->host_ch * 2 * sizeof(int32_t)) != cudaSuccess ||
@@ -976,7 +977,7 @@ int moco_align_host(moco_plan *p, const void *h_frames, int64_t T, int32_t *h_sh
       }
     }
     for (int k = 0; k < 3; ++k) CK(cudaStreamCreateWithFlags(&p->hs[k], cudaStreamNonBlocking));
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < 3; ++k) {
       CK(cudaEventCreateWithFlags(&p->ev_in[k], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&p->ev_done[k], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&p->ev_free[k], cudaEventDisableTiming));
@@ -987,14 +988,14 @@ int moco_align_host(moco_plan *p, const void *h_frames, int64_t T, int32_t *h_sh
   int64_t total_launches = 0;
   int64_t chunk = 0;
   for (int64_t f0 = 0; f0 < T; f0 += p->host_ch, ++chunk) {
-    const int k = (int)(chunk & 1);
+    const int k = (int)(chunk % 3);
     const int64_t B = std::min<int64_t>(p->host_ch, T - f0);
-    if (chunk >= 2) CK(cudaStreamWaitEvent(s_in, p->ev_free[k], 0));
+    if (chunk >= 3) CK(cudaStreamWaitEvent(s_in, p->ev_free[k], 0));
     CK(cudaMemcpyAsync(p->slot_in[k], (const char *)h_frames + f0 * fbytes, B * fbytes,
                        cudaMemcpyHostToDevice, s_in));
     CK(cudaEventRecord(p->ev_in[k], s_in));
     CK(cudaStreamWaitEvent(s_comp, p->ev_in[k], 0));
-    if (chunk >= 2) CK(cudaStreamWaitEvent(s_comp, p->ev_free[k], 0));
+    if (chunk >= 3) CK(cudaStreamWaitEvent(s_comp, p->ev_free[k], 0));
     int rc = moco_align_batch(p, p->slot_in[k], B, p->slot_sh[k], p->slot_f[k],
                               h_corrected ? p->slot_out[k] : nullptr,
                               h_flags ? p->slot_flags[k] : nullptr, s_comp);
