@@ -457,7 +457,7 @@ __device__ __forceinline__ bool elect_one() {
 }
 
 template <int CPL>   // B chunks (16 bytes) per producer lane per tile = 2N/32
-__global__ void __launch_bounds__(TC_THREADS, 2) k_tc_coarse(TcArgs a) {
+__global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {
   const TcGeom &g = a.g;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);

@@ -78,8 +78,10 @@ struct moco_plan {
   } fft;
   // two-stream batch pipeline (align_tc_pipelined)
   bool pipe_ready;
-  cudaStream_t ps[2];
-  cudaEvent_t pe_prep[2], pe_free[2], pe_start, pe_end;
+  cudaStream_t ps[3];
+  cudaEvent_t pe_prep[2], pe_free[2], pe_sums[2], pe_pick[2], pe_start, pe_end, pe_end2;
+  int32_t *sh1b;              // second level-1 shift buffer (pipeline)
+  u64 *racc2;                 // second refine accumulator buffer (pipeline)
   // end-to-end staging
   bool host_ready;
   int64_t host_ch;
@@ -187,13 +189,15 @@ static void plan_free(moco_plan *p) {
   }
   for (int k = 0; k < 3; ++k)
     if (p->hs[k]) cudaStreamDestroy(p->hs[k]);
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < 3; ++k)
     if (p->ps[k]) cudaStreamDestroy(p->ps[k]);
-    if (p->pe_prep[k]) cudaEventDestroy(p->pe_prep[k]);
-    if (p->pe_free[k]) cudaEventDestroy(p->pe_free[k]);
-  }
-  if (p->pe_start) cudaEventDestroy(p->pe_start);
-  if (p->pe_end) cudaEventDestroy(p->pe_end);
+  for (int k = 0; k < 2; ++k)
+    for (cudaEvent_t e : {p->pe_prep[k], p->pe_free[k], p->pe_sums[k], p->pe_pick[k]})
+      if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : {p->pe_start, p->pe_end, p->pe_end2})
+    if (e) cudaEventDestroy(e);
+  if (p->sh1b) cudaFree(p->sh1b);
+  if (p->racc2) cudaFree(p->racc2);
   for (auto &r : p->prof_live) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : p->prof_pool) cudaEventDestroy(e);
   delete p;
@@ -368,7 +372,11 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
   for (int l = 0; l <= levels; ++l) alloc((void **)&p->sh[l], (size_t)p->cap * 2 * sizeof(int32_t));
   if (dtype == MOCO_U16 && levels > 0) {
     alloc((void **)&p->racc, (size_t)p->cap * 18 * sizeof(u64));
-    if (rc == MOCO_OK && cudaMemset(p->racc, 0, (size_t)p->cap * 18 * sizeof(u64)) != cudaSuccess) rc = MOCO_ENOMEM;
+    alloc((void **)&p->racc2, (size_t)p->cap * 18 * sizeof(u64));
+    alloc((void **)&p->sh1b, (size_t)p->cap * 2 * sizeof(int32_t));
+    if (rc == MOCO_OK && (cudaMemset(p->racc, 0, (size_t)p->cap * 18 * sizeof(u64)) != cudaSuccess ||
+                          cudaMemset(p->racc2, 0, (size_t)p->cap * 18 * sizeof(u64)) != cudaSuccess))
+      rc = MOCO_ENOMEM;
   }
   if (dtype == MOCO_U16)
     for (int l = 0; l < levels; ++l) {
@@ -568,12 +576,14 @@ static int launch_refine(moco_plan *p, int l, const void *img, int64_t fstride, 
 // K6 (+K7 at level 0): template-stationary u16 refine (kernels_refine.cuh):
 // k_refine_sums (per-frame sums) then k_refine_pick (argmin + apply).
 static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride, int64_t B,
-                           const int32_t *sin, int32_t *sout, double *fout, void *corr, cudaStream_t st) {
+                           const int32_t *sin, int32_t *sout, double *fout, void *corr, cudaStream_t st,
+                           u64 *racc = nullptr, cudaStream_t st_pick = nullptr, cudaEvent_t ev_sums = nullptr) {
   const int vb = p->bits + 2 * l;
+  if (!racc) racc = p->racc;
   RefineSumArgs a;
   a.tpl = (const uint16_t *)p->tpl[l]; a.tpitch = p->pitch[l];
   a.ml = p->ml[l]; a.nl = p->nl[l];
-  a.B = (int)B; a.shift_in = sin; a.acc = p->racc;
+  a.B = (int)B; a.shift_in = sin; a.acc = racc;
   a.rt = p->rrt[l]; a.nrt = p->rnrt[l]; a.stages = p->rstages[l];
   // 32-bit lane partials hold (256-column halves) x rt rows x 8 products, each
   // <= (2^vb - 1)^2, unless flushed to 64 bits after every row
@@ -591,7 +601,7 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
   b.frames = (const uint16_t *)img; b.fstride = fstride; b.pitch = p->pitch[l];
   b.pb2 = p->pb2[l]; b.ml = p->ml[l]; b.nl = p->nl[l];
   b.scale = (double)(1u << (4 * l));
-  b.B = (int)B; b.shift_in = sin; b.acc = p->racc; b.shift_out = sout; b.f_out = fout;
+  b.B = (int)B; b.shift_in = sin; b.acc = racc; b.shift_out = sout; b.f_out = fout;
   b.corrected = (uint16_t *)corr;
   // small batches: several CTAs per frame for the apply (the accumulators are then
   // cleared by a memset after the pick instead of by the single CTA)
@@ -612,13 +622,18 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
   }
   p->launches++;
   CKL("k_refine_sums");
+  if (st_pick) {   // pick/apply on another stream (align_tc_pipelined)
+    CK(cudaEventRecord(ev_sums, st));
+    CK(cudaStreamWaitEvent(st_pick, ev_sums, 0));
+    st = st_pick;
+  }
   {
     ProfScope ps(p, MOCO_K_APPLY, st);
     k_refine_pick<<<(unsigned)(B * b.parts), 256, 0, st>>>(b);
   }
   p->launches++;
   CKL("k_refine_pick");
-  if (b.parts > 1) CK(cudaMemsetAsync(p->racc, 0, (size_t)B * 18 * sizeof(u64), st));
+  if (b.parts > 1) CK(cudaMemsetAsync(racc, 0, (size_t)B * 18 * sizeof(u64), st));
   return MOCO_OK;
 }
 
@@ -821,25 +836,29 @@ constexpr int64_t LAT_T = 16;   // calls with at most this many frames take the 
 static int align_tc_pipelined(moco_plan *p, const void *d_frames, int64_t T, int32_t *d_shifts, double *d_fmin,
                               void *d_corrected, uint8_t *d_flags, cudaStream_t user) {
   if (!p->pipe_ready) {
-    CK(cudaStreamCreateWithFlags(&p->ps[0], cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&p->ps[1], cudaStreamNonBlocking));
+    for (int k = 0; k < 3; ++k) CK(cudaStreamCreateWithFlags(&p->ps[k], cudaStreamNonBlocking));
     for (int k = 0; k < 2; ++k) {
       CK(cudaEventCreateWithFlags(&p->pe_prep[k], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&p->pe_free[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&p->pe_sums[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&p->pe_pick[k], cudaEventDisableTiming));
     }
     CK(cudaEventCreateWithFlags(&p->pe_start, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&p->pe_end, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&p->pe_end2, cudaEventDisableTiming));
     p->pipe_ready = true;
   }
-  cudaStream_t sp = p->ps[0], sm = p->ps[1];
+  // prep stream | main stream (TC search, refine sums) | pick/apply stream.  Per batch
+  // parity: operand planes G/ga, coarse shifts and refine accumulators are double-
+  // buffered; a buffer is reused two batches later, after the events below.
+  cudaStream_t sp = p->ps[0], sm = p->ps[1], sa = p->ps[2];
   CK(cudaEventRecord(p->pe_start, user));
-  CK(cudaStreamWaitEvent(sp, p->pe_start, 0));
-  CK(cudaStreamWaitEvent(sm, p->pe_start, 0));
+  for (int k = 0; k < 3; ++k) CK(cudaStreamWaitEvent(p->ps[k], p->pe_start, 0));
   const size_t fbytes = (size_t)p->m * p->n * p->esz[0];
   uint8_t *G[2] = {p->tc.G, p->tc.G2};
   u64 *ga[2] = {p->tc.ga, p->tc.ga2};
-  // equal batches of whole tensor-core waves where possible
-  const int64_t nb = (T + p->cap - 1) / p->cap;
+  int32_t *sh1[2] = {p->sh[1], p->sh1b};
+  u64 *racc[2] = {p->racc, p->racc2};
   int64_t k = 0;
   for (int64_t f0 = 0; f0 < T; f0 += p->cap, ++k) {
     const int64_t B = std::min<int64_t>(p->cap, T - f0);
@@ -850,18 +869,20 @@ static int align_tc_pipelined(moco_plan *p, const void *d_frames, int64_t T, int
     if (rc) return rc;
     CK(cudaEventRecord(p->pe_prep[buf], sp));
     CK(cudaStreamWaitEvent(sm, p->pe_prep[buf], 0));
-    rc = launch_tc_coarse(p, B, G[buf], ga[buf], p->sh[1], nullptr, d_flags ? d_flags + f0 : nullptr, nullptr, sm);
+    if (k >= 2) CK(cudaStreamWaitEvent(sm, p->pe_pick[buf], 0));   // sh1/racc of batch k-2 consumed
+    rc = launch_tc_coarse(p, B, G[buf], ga[buf], sh1[buf], nullptr, d_flags ? d_flags + f0 : nullptr, nullptr, sm);
     if (rc) return rc;
     CK(cudaEventRecord(p->pe_free[buf], sm));
-    const void *img[3] = {fr, nullptr, nullptr};
-    const int64_t fstride[3] = {(int64_t)p->m * p->n, 0, 0};
-    rc = refine_levels(p, img, fstride, B, d_shifts + 2 * f0, d_fmin + f0,
-                       d_corrected ? (char *)d_corrected + f0 * fbytes : nullptr, sm);
+    rc = launch_refine_h(p, 0, fr, (int64_t)p->m * p->n, B, sh1[buf], d_shifts + 2 * f0, d_fmin + f0,
+                         d_corrected ? (char *)d_corrected + f0 * fbytes : nullptr, sm, racc[buf], sa,
+                         p->pe_sums[buf]);
     if (rc) return rc;
+    CK(cudaEventRecord(p->pe_pick[buf], sa));
   }
-  (void)nb;
   CK(cudaEventRecord(p->pe_end, sm));
+  CK(cudaEventRecord(p->pe_end2, sa));
   CK(cudaStreamWaitEvent(user, p->pe_end, 0));
+  CK(cudaStreamWaitEvent(user, p->pe_end2, 0));
   return MOCO_OK;
 }
 
@@ -887,7 +908,8 @@ int moco_align_batch(moco_plan *p, const void *d_frames, int64_t T, int32_t *d_s
     p->algo = MOCO_ALGO_TC;
     return rc;
   }
-  if (p->algo == MOCO_ALGO_TC && p->levels == 1 && T > p->cap && p->tc.G2 && !getenv("MOCO_NOPIPE"))
+  if (p->algo == MOCO_ALGO_TC && p->levels == 1 && T > p->cap && p->tc.G2 && p->racc2 && p->sh1b &&
+      fused_ok(p, 0) && !getenv("MOCO_NOPIPE"))
     return align_tc_pipelined(p, d_frames, T, d_shifts, d_fmin, d_corrected, d_flags, (cudaStream_t)stream);
   for (int64_t f0 = 0; f0 < T; f0 += p->cap) {
     const int64_t B = std::min<int64_t>(p->cap, T - f0);
