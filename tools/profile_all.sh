@@ -1,0 +1,19 @@
+#!/bin/bash
+# Round profiling pass (run on a GPU box from the repo root): bench line, ncu launch list
+# of the bench command, and one --set full capture per hot kernel.  Outputs gpurun_out/.
+set -x
+O=gpurun_out
+timeout 600 python bench.py --steps 10 --warmup 3 > $O/bench_full.log 2>&1
+tail -1 $O/bench_full.log > $O/bench_full.json
+timeout 300 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > $O/bench_small.log 2>&1 && \
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_ -c 400 --csv \
+    --log-file $O/ncu_launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > $O/ncu_launches.log 2>&1
+timeout 120 python tools/profile_run.py --frames 2368 --iters 1 > $O/plain_c2.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on \
+    -k regex:"k_tc_prep|k_tc_coarse|k_refine_sums|k_refine_pick" -c 4 -o $O/prof_c2 \
+    python tools/profile_run.py --frames 2368 --iters 1 > $O/ncu_c2.log 2>&1
+timeout 120 python tools/profile_run.py --config 4 --frames 256 --iters 1 > $O/plain_c4.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on \
+    -k regex:"k_energy_u16|k_fft_rows|k_fft_cols|k_fft_score" -c 4 -o $O/prof_c4 \
+    python tools/profile_run.py --config 4 --frames 256 --iters 1 > $O/ncu_c4.log 2>&1
+ls -la $O
