@@ -110,26 +110,31 @@ __device__ __forceinline__ void dft_small(float2 (&v)[5], float sign) {
   }
 }
 
+// q = x / d for x, d < 2^16 via multiply-high by the magic m = floor((2^32 - 1) / d) + 1
+__device__ __forceinline__ uint32_t fdiv16(uint32_t x, uint32_t m) { return __umulhi(x, m); }
+
 template <int R>
 __device__ __forceinline__ void fft_stage(const float2 *x, float2 *y, const float2 *tw, int N, int Ns, int nfft,
                                           float sign) {
   const int nb = N / R, tstep = N / (Ns * R);
+  const uint32_t mnb = 0xffffffffu / (uint32_t)nb + 1u, mns = 0xffffffffu / (uint32_t)Ns + 1u;
   for (int e = threadIdx.x; e < nfft * nb; e += blockDim.x) {
-    const int f = e / nb, j = e - f * nb;
+    const int f = (int)fdiv16((uint32_t)e, mnb), j = e - f * nb;
     const float2 *in = x + f * N;
     float2 *out = y + f * N;
-    const int k = j % Ns;
+    const int jq = Ns == 1 ? j : (int)fdiv16((uint32_t)j, mns);
+    const int k = j - jq * Ns;
     float2 v[5];
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = in[j + r * nb];
 #pragma unroll
     for (int r = 1; r < R; ++r) {
-      float2 t = tw[(k * r * tstep) % N];   // exp(-2 pi i k r / (Ns R))
+      float2 t = tw[k * r * tstep];   // exp(-2 pi i k r / (Ns R)); k r tstep < N
       if (sign > 0) t.y = -t.y;
       v[r] = cmul(v[r], t);
     }
     dft_small<R>(v, sign);
-    const int o = (j / Ns) * Ns * R + k;
+    const int o = jq * Ns * R + k;
 #pragma unroll
     for (int r = 0; r < R; ++r) out[o + r * Ns] = v[r];
   }
@@ -286,13 +291,18 @@ struct FftScoreArgs {
 __device__ u64 exact_h(const FftScoreArgs &a, const uint16_t *A, int s, int t, u64 *red) {
   const int mc = a.g.mc, nc = a.g.nc;
   const int i0 = max(0, -s), i1 = mc - max(0, s), j0 = max(0, -t), j1 = nc - max(0, t);
-  // flattened over the overlap so every thread has many independent loads in flight
-  const int wdt = j1 - j0, total = (i1 - i0) * wdt;
+  // threads over columns, rows unrolled so every thread keeps several loads in flight
   u64 acc = 0;
-#pragma unroll 4
-  for (int e = threadIdx.x; e < total; e += blockDim.x) {
-    const int i = i0 + e / wdt, j = j0 + e % wdt;
-    acc += (u64)((uint32_t)A[(int64_t)(i + s) * a.pitch + j + t] * (uint32_t)a.tpl[(int64_t)i * a.tpitch + j]);
+  for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+    const uint16_t *ar = A + (int64_t)(i0 + s) * a.pitch + j + t;
+    const uint16_t *br = a.tpl + (int64_t)i0 * a.tpitch + j;
+    int i = i0;
+    for (; i + 4 <= i1; i += 4, ar += 4 * a.pitch, br += 4 * a.tpitch) {
+      const uint32_t p0 = (uint32_t)ar[0] * br[0], p1 = (uint32_t)ar[a.pitch] * br[a.tpitch];
+      const uint32_t p2 = (uint32_t)ar[2 * a.pitch] * br[2 * a.tpitch], p3 = (uint32_t)ar[3 * a.pitch] * br[3 * a.tpitch];
+      acc += (u64)p0 + p1 + (u64)p2 + p3;
+    }
+    for (; i < i1; ++i, ar += a.pitch, br += a.tpitch) acc += (u64)((uint32_t)ar[0] * br[0]);
   }
   acc = warp_sum(acc);
   __syncthreads();
@@ -346,17 +356,26 @@ __global__ void __launch_bounds__(1024) k_fft_score(FftScoreArgs a) {
   __syncthreads();
   if (a.h_out)
     for (int lag = threadIdx.x; lag < W * W; lag += blockDim.x) a.h_out[f * W * W + lag] = hb[lag];
-  // scores with certified error intervals
+  // scores with certified error intervals.  1/(16^L A) = rinv[s] * cinv[t]; pass 1 takes
+  // min(f~ + delta) and leaves the lower bound f~ - delta of every lag in hb for pass 2
+  double *rinv = reinterpret_cast<double *>(hb + ((W * W + 1) & ~1));   // [W]
+  double *cinv = rinv + W;                                              // [W]
+  for (int k = threadIdx.x; k < W; k += blockDim.x) {
+    rinv[k] = 1.0 / (a.scale * (double)(g.mc - abs(k - hw)));
+    cinv[k] = 1.0 / (double)(g.nc - abs(k - hw));
+  }
+  __syncthreads();
   const u64 *gaf = a.ga + f * W * W;
   const double na = sqrt((double)gaf[hw * W + hw]), nb = sqrt((double)a.gb[hw * W + hw]);
-  const double eps_h = a.eps_rel * na * nb;
+  const double eps2 = 2.0 * a.eps_rel * na * nb;
   float best = 3.0e38f;
   for (int lag = threadIdx.x; lag < W * W; lag += blockDim.x) {
-    const int s = lag / W - hw, t = lag % W - hw;
-    const double A = (double)((g.mc - abs(s)) * (g.nc - abs(t)));
-    const double fa = ((double)gaf[lag] + (double)a.gb[lag] - 2.0 * (double)hb[lag]) / (a.scale * A);
-    const double del = 2.0 * eps_h / (a.scale * A);
+    const int si = lag / W, ti = lag - si * W;
+    const double inv = rinv[si] * cinv[ti];
+    const double fa = ((double)gaf[lag] + (double)a.gb[lag] - 2.0 * (double)hb[lag]) * inv;
+    const double del = eps2 * inv;
     best = fminf(best, (float)(fa + del) * (1.0f + 1e-6f));
+    hb[lag] = (float)(fa - del) * (1.0f - 1e-6f);
   }
   for (int o = 16; o > 0; o >>= 1) best = fminf(best, __shfl_xor_sync(0xffffffffu, best, o));
   if ((threadIdx.x & 31) == 0) reinterpret_cast<float *>(red)[threadIdx.x >> 5] = best;
@@ -370,11 +389,7 @@ __global__ void __launch_bounds__(1024) k_fft_score(FftScoreArgs a) {
   __syncthreads();
   const float thr = fmin_hi_s;
   for (int lag = threadIdx.x; lag < W * W; lag += blockDim.x) {
-    const int s = lag / W - hw, t = lag % W - hw;
-    const double A = (double)((g.mc - abs(s)) * (g.nc - abs(t)));
-    const double fa = ((double)gaf[lag] + (double)a.gb[lag] - 2.0 * (double)hb[lag]) / (a.scale * A);
-    const double del = 2.0 * eps_h / (a.scale * A);
-    if ((float)((fa - del) * (1.0 - 1e-6)) <= thr) {
+    if (hb[lag] <= thr) {
       const int q = atomicAdd(&qn, 1);
       if (q < FFT_QCAP) qlist[q] = lag;
     }
@@ -428,8 +443,10 @@ __global__ void __launch_bounds__(1024) k_energy_u16(const uint16_t *__restrict_
   for (int r = warp; r < mc; r += nwarp) {
     u64 rs = 0;
     const bool top = r < hw, bot = r >= mc - hw;
+    const uint16_t *row = A + (int64_t)r * pitch;
+#pragma unroll 4
     for (int c = lane; c < nc; c += 32) {
-      const u64 v2 = (u64)A[(int64_t)r * pitch + c] * A[(int64_t)r * pitch + c];
+      const u64 v2 = (u64)row[c] * row[c];
       rs += v2;
       const bool lf = c < hw, rt = c >= nc - hw;
       if (lf) atomicAdd(&colE[c], v2);

@@ -235,7 +235,7 @@ static int fft_init(moco_plan *p) {
   F.eps_rel = RS_FFT_C * std::ldexp(1.0, -24) * std::log2((double)Mr * (double)Mc);
   F.smem_rows = (Mc + 2 * FFT_ROWS_PAIRS * Mc) * 8;
   F.smem_cols = (Mr + 2 * FFT_COLS * Mr) * 8;
-  F.smem_score = (Mc + 2 * FFT_ROWS_PAIRS * Mc) * 8 + g.W * g.W * 4;
+  F.smem_score = (Mc + 2 * FFT_ROWS_PAIRS * Mc) * 8 + ((g.W * g.W + 1) & ~1) * 4 + 2 * g.W * 8;
   F.smem_energy = (4 * g.hw + 4 * g.w * g.w + 1) * 8;
   if (F.smem_score > 227 * 1024 || F.smem_energy > 227 * 1024) return MOCO_EINVAL;
   CK(cudaFuncSetAttribute(k_fft_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, F.smem_rows));
