@@ -30,6 +30,9 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
+
+#include <algorithm>
 
 #include "kernels_direct.cuh"
 
@@ -50,6 +53,7 @@ struct TcGeom {
   int stripB;   // 2 planes
   int TPAD, TP; // padded template parts: TP = nc + 2*TPAD bytes per row, zeros in the pads
   int ICH;      // template-row pairs per super-stage (one ring slot per producer warp)
+  int ctas;     // CTAs per SM the geometry is sized for
   int npairs;   // ceil(mc / 2)
   int GG;       // operand groups per CTA
   int tmem_cols;
@@ -457,7 +461,7 @@ __device__ __forceinline__ bool elect_one() {
 }
 
 template <int CPL>   // B chunks (16 bytes) per producer lane per tile = 2N/32
-__global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {
+__global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <= 85 registers: 3 CTAs/SM fit
   const TcGeom &g = a.g;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -730,11 +734,19 @@ inline bool tc_make_geom(TcGeom *gp, int w, int mc, int nc, int L) {
   g.N = 2 * g.N1;
   if (g.N > 256) return false;
   const int lagrows = g.W + 1;   // A-row lags s' in [-(w-1), w]
-  // frames per group: the largest F with the fewest padded lag rows and NT*N <= 256
+  // One CTA per SM by default (measured on B200: more operand groups per
+  // CTA -- each B tile feeds more MMAs -- beat two CTAs overlapping their strip loads).
+  const char *ce = getenv("MOCO_TC_CTAS");   // tuning experiments: CTAs per SM target
+  const int ctas = ce ? std::max(1, atoi(ce)) : 1;
+  const int smem_cap = (228 * 1024) / ctas - 1024, tmem_cap = 512 / ctas;
+  // frames per group: the fewest padded lag rows with NT*N within TMEM; ties -> F = 2
+  // (one M tile per group: every MMA of a pair step shares the B tile)
   int bestF = 0, bestRows = 1 << 30;
-  for (int F : {4, 2, 1}) {
+  const char *fe = getenv("MOCO_TC_F");   // tuning experiments
+  for (int F : {2, 4, 1}) {
+    if (fe && atoi(fe) != F) continue;
     const int ST = 64 / F, NT = (lagrows + ST - 1) / ST;
-    if (NT * g.N > 256) continue;
+    if (NT * g.N > tmem_cap) continue;
     if (NT * ST < bestRows) { bestRows = NT * ST; bestF = F; }
   }
   if (!bestF) return false;
@@ -754,11 +766,12 @@ inline bool tc_make_geom(TcGeom *gp, int w, int mc, int nc, int L) {
   // super-stage (ICH | npairs) that still fits; the epilogue's staging of the d = 1
   // accumulator halves (GG*NT*128*32 words + keys) must fit in the same memory
   g.GG = 0;
+  g.ctas = ctas;
   for (int GG = 4; GG >= 1 && !g.GG; --GG) {
-    if (GG * g.NT * g.N > 256 || GG * g.NT > 4) continue;
+    if (GG * g.NT * g.N > tmem_cap || GG * g.NT > 4) continue;
     for (int ICH = 4; ICH >= 1; ICH /= 2) {
       const int sm = smem_for(GG, ICH);
-      if (g.npairs % ICH == 0 && sm <= 113 * 1024 && GG * g.NT * 128 * 128 + GG * 128 * 16 <= sm - 1024 - 256) {
+      if (g.npairs % ICH == 0 && sm <= smem_cap && GG * g.NT * 128 * 128 + GG * 128 * 16 <= sm - 1024 - 256) {
         g.GG = GG;
         g.ICH = ICH;
         break;

@@ -401,8 +401,8 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
   if (tc_ok && tc_auto_prefers(p->w)) {
     if (tc_init(&p->tc, p->w, p->ml[levels], p->nl[levels], levels, p->cap) == 0) {
       p->algo = MOCO_ALGO_TC;
-      // whole waves of the tensor-core search per internal batch (2 CTAs/SM x GG*F frames)
-      const int64_t wave = (int64_t)nsm * 2 * p->tc.g.GG * p->tc.g.F;
+      // whole waves of the tensor-core search per internal batch (CTAs/SM x GG*F frames)
+      const int64_t wave = (int64_t)nsm * p->tc.g.ctas * p->tc.g.GG * p->tc.g.F;
       if (p->cap >= wave) p->cap = p->cap / wave * wave;
     } else {
       cudaGetLastError();
