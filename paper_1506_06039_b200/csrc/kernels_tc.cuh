@@ -103,6 +103,9 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -524,6 +527,10 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
         for (int gg = 0; gg < gcount; ++gg)
           bulk_g2s(As + gg * g.stripB, a.G + ((int64_t)(grp0 + gg) * nst + st) * g.stripB,
                    (uint32_t)g.stripB, aload);
+        // the next strip streams from HBM into L2 while this one is multiplied
+        if (st + 1 < nst)
+          for (int gg = 0; gg < gcount; ++gg)
+            bulk_prefetch_l2(a.G + ((int64_t)(grp0 + gg) * nst + st + 1) * g.stripB, (uint32_t)g.stripB);
       }
       __syncwarp();
       mbar_wait(aload, st & 1);
