@@ -425,17 +425,17 @@ __global__ void __launch_bounds__(1024) k_fft_score(FftScoreArgs a) {
 // ---------------------------------------------------------------- frame energies
 // g_a(s,t) = sum over the frame-side rectangle of D_{s,t} of a^2 for every coarse lag
 // (P:32-35): total minus the excluded edge strips plus the doubly excluded corner --
-// the paper's DP of P:35 run in each corner (a (w x w) prefix table per corner).
-// One block per frame; works for any w (tables in dynamic shared memory).
+// the paper's DP of P:35 run in each corner (a (w x w) prefix table per corner, built
+// one quadrant at a time so any w fits in shared memory).  One block per frame.
 __global__ void __launch_bounds__(1024) k_energy_u16(const uint16_t *__restrict__ img, int64_t fstride, int pitch,
                                                     int mc, int nc, int w, u64 *__restrict__ ga) {
   extern __shared__ __align__(16) u64 esm[];
   const int hw = w - 1, W = 2 * w - 1, CS = w * w;
   u64 *rowE = esm;                 // [2 hw]: top rows, bottom rows (from the bottom)
   u64 *colE = rowE + 2 * hw;       // [2 hw]
-  u64 *cor = colE + 2 * hw;        // [4][w][w]
-  u64 *tot = cor + 4 * CS;         // [1]
-  for (int k = threadIdx.x; k < 4 * hw + 4 * CS + 1; k += blockDim.x) esm[k] = 0;
+  u64 *cor = colE + 2 * hw;        // [w][w]: one quadrant at a time
+  u64 *tot = cor + CS;             // [1]
+  for (int k = threadIdx.x; k < 4 * hw + CS + 1; k += blockDim.x) esm[k] = 0;
   __syncthreads();
   const uint16_t *A = img + (int64_t)blockIdx.x * fstride;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
@@ -448,15 +448,8 @@ __global__ void __launch_bounds__(1024) k_energy_u16(const uint16_t *__restrict_
     for (int c = lane; c < nc; c += 32) {
       const u64 v2 = (u64)row[c] * row[c];
       rs += v2;
-      const bool lf = c < hw, rt = c >= nc - hw;
-      if (lf) atomicAdd(&colE[c], v2);
-      if (rt) atomicAdd(&colE[hw + (nc - 1 - c)], v2);
-      if ((lf || rt) && (top || bot)) {
-        if (top && lf) cor[0 * CS + (r + 1) * w + (c + 1)] = v2;
-        if (top && rt) cor[1 * CS + (r + 1) * w + (nc - c)] = v2;
-        if (bot && lf) cor[2 * CS + (mc - r) * w + (c + 1)] = v2;
-        if (bot && rt) cor[3 * CS + (mc - r) * w + (nc - c)] = v2;
-      }
+      if (c < hw) atomicAdd(&colE[c], v2);
+      if (c >= nc - hw) atomicAdd(&colE[hw + (nc - 1 - c)], v2);
     }
     rs = warp_sum(rs);
     if (lane == 0) {
@@ -472,27 +465,41 @@ __global__ void __launch_bounds__(1024) k_energy_u16(const uint16_t *__restrict_
     u64 *p = e + (threadIdx.x & 1) * hw;
     for (int q = 1; q < hw; ++q) p[q] += p[q - 1];
   }
-  for (int k = threadIdx.x; k < 4 * w; k += blockDim.x) {
-    u64 *c = cor + (k / w) * CS + (k % w) * w;
-    for (int q = 1; q < w; ++q) c[q] += c[q - 1];
-  }
-  __syncthreads();
-  for (int k = threadIdx.x; k < 4 * w; k += blockDim.x) {
-    u64 *c = cor + (k / w) * CS + (k % w);
-    for (int p = 1; p < w; ++p) c[p * w] += c[(p - 1) * w];
-  }
   __syncthreads();
   u64 *gf = ga + (int64_t)blockIdx.x * W * W;
   for (int lag = threadIdx.x; lag < W * W; lag += blockDim.x) {
     const int s = lag / W - hw, t = lag % W - hw;
     const u64 rex = s > 0 ? rowE[s - 1] : (s < 0 ? rowE[hw + (-s) - 1] : 0);
     const u64 cex = t > 0 ? colE[t - 1] : (t < 0 ? colE[hw + (-t) - 1] : 0);
-    u64 corner = 0;
-    if (s != 0 && t != 0) {
-      const int quad = (s < 0 ? 2 : 0) | (t < 0 ? 1 : 0);
-      corner = cor[quad * CS + abs(s) * w + abs(t)];
+    gf[lag] = *tot - rex - cex;
+  }
+  // corners: quadrant (s<0 ? 2 : 0) | (t<0 ? 1 : 0) -- s > 0 excludes the TOP rows, t > 0
+  // the LEFT columns; table[p][q] = sum of a^2 over the p x q corner block
+  for (int quad = 0; quad < 4; ++quad) {
+    const bool bot = quad & 2, rt = quad & 1;
+    __syncthreads();
+    for (int e = threadIdx.x; e < CS; e += blockDim.x) {
+      const int pp = e / w, qq = e % w;
+      u64 v2 = 0;
+      if (pp > 0 && qq > 0) {
+        const int r = bot ? mc - pp : pp - 1, c = rt ? nc - qq : qq - 1;
+        const u64 v = A[(int64_t)r * pitch + c];
+        v2 = v * v;
+      }
+      cor[e] = v2;
     }
-    gf[lag] = *tot - rex - cex + corner;
+    __syncthreads();
+    for (int k = threadIdx.x; k < w; k += blockDim.x)
+      for (int q = 1; q < w; ++q) cor[k * w + q] += cor[k * w + q - 1];
+    __syncthreads();
+    for (int k = threadIdx.x; k < w; k += blockDim.x)
+      for (int p = 1; p < w; ++p) cor[p * w + k] += cor[(p - 1) * w + k];
+    __syncthreads();
+    for (int e = threadIdx.x; e < hw * hw; e += blockDim.x) {
+      const int as = e / hw + 1, at = e % hw + 1;
+      const int s = bot ? -as : as, t = rt ? -at : at;
+      gf[(s + hw) * W + (t + hw)] += cor[as * w + at];
+    }
   }
 }
 

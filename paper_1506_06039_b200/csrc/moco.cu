@@ -236,7 +236,7 @@ static int fft_init(moco_plan *p) {
   F.smem_rows = (Mc + 2 * FFT_ROWS_PAIRS * Mc) * 8;
   F.smem_cols = (Mr + 2 * FFT_COLS * Mr) * 8;
   F.smem_score = (Mc + 2 * FFT_ROWS_PAIRS * Mc) * 8 + ((g.W * g.W + 1) & ~1) * 4 + 2 * g.W * 8;
-  F.smem_energy = (4 * g.hw + 4 * g.w * g.w + 1) * 8;
+  F.smem_energy = (4 * g.hw + g.w * g.w + 1) * 8;
   if (F.smem_score > 227 * 1024 || F.smem_energy > 227 * 1024) return MOCO_EINVAL;
   CK(cudaFuncSetAttribute(k_fft_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, F.smem_rows));
   CK(cudaFuncSetAttribute(k_fft_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, F.smem_cols));
@@ -351,7 +351,7 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
   const int tasks = p->c_sc * G;
   p->c_threads = std::min(512, std::max(64, round_up(tasks, 32)));
   p->c_smem = coarse_smem(p, p->c_sc, p->c_br, p->c_fpitch);
-  if (p->c_smem > 227 * 1024) { plan_free(p); return MOCO_EINVAL; }
+  if (p->c_smem > 227 * 1024 && w <= 64) { plan_free(p); return MOCO_EINVAL; }   // (w > 64: FFT only)
   // workspace: template pyramid, tables, one batch of frame pyramid levels
   int rc = MOCO_OK;
   auto alloc = [&](void **ptr, size_t bytes) {

@@ -138,3 +138,18 @@ def test_fft_ragged_shapes_exact(m, n, levels, w):
     for k in range(4):
         check_frame(fr[k], tp, w, levels, sh[k], fm[k], _np(co[k]))
     assert sh[1].tolist() == [2 << levels, -(1 << levels)] and fm[1] == 0
+
+
+def test_fft_paper_default_window_w_over_64():
+    """w = 85 > 64 (PAPER.md:49's default w = min(m,n)/3 at a 256x256 coarse level, here
+    on 256x256 frames with one level -> 128x128 coarse): only the FFT path exists; the
+    plan accepts it, AUTO picks it, results bit-exact vs the oracle on two frames."""
+    spec = config_spec(2, m=256, n=256, w=85, T=2, n_blobs=120, shift_bound=100)
+    st = make_stack(spec, 0, 2, device="cpu")
+    p = Plan(256, 256, 85, 1, "u16", 12, device=0)
+    assert p.algo == "fft"
+    p.set_template(st.template.to(DEV))
+    sh, fm, co, _ = p.align(st.frames.to(DEV))
+    sh, fm = _np(sh), _np(fm)
+    for k in range(2):
+        check_frame(st.frames[k].numpy(), st.template.numpy(), 85, 1, sh[k], fm[k], _np(co[k]))
