@@ -83,7 +83,7 @@ struct RefineSumArgs {
 constexpr int RS_CT = RS_CTW;         // template columns per tile (a warp walks it in 256-column halves)
 constexpr int RS_BOX = RS_CT == 512 ? 176 : 136;   // frame box columns: the boxes cover CT + 9
 constexpr int RS_NBOX = RS_CT == 512 ? 3 : 2;
-constexpr int RS_MAXRT = 8;
+constexpr int RS_MAXRT = 16;
 constexpr int RS_CW = 12;             // consumer warps (frames in flight per CTA)
 constexpr int RS_THREADS = 32 * (1 + RS_CW);
 
