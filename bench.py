@@ -317,15 +317,22 @@ def main():
         unit = "TFLOP/s"
         peak_note = "148 SM x 128 FP32/INT32 lanes x 2 x sm_max_mhz (DESIGN.md §8)"
     traffic = None
+    isolated = None
     try:
         ncu = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
         entry = ncu.get(f"C{spec.index}", {}).get(plan.algo, {}).get(kind)
         if entry:   # per-frame DRAM bytes from the committed ncu capture x frames per launch
             traffic = entry["bytes_per_frame"] * frames_timed / klaunch
+            # the same kernel alone (ncu, serialised launches): the live duration above
+            # includes the time it shares the GPU with the other two pipeline streams
+            us = entry["duration_us"] / entry["frames_in_capture"]
+            ach = per_frame / (us * 1e-6) / (1e9 if bound == "hbm" else 1e12)
+            isolated = {"us_per_frame": us, "achieved": ach, "frac": ach / peak,
+                        "source": "profiles/ncu_traffic.json (ncu --set full, one launch alone)"}
     except Exception:
         pass
     roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
-                "frac": achieved / peak, "traffic": traffic, "kernel": kind,
+                "frac": achieved / peak, "traffic": traffic, "kernel": kind, "isolated": isolated,
                 "kernel_share": kms / ms if ms > 0 else None,
                 "per_frame_work": per_frame, "peak_source": peak_note,
                 "kernels_ms": {k: round(v[0], 4) for k, v in prof.items() if v[1]},
