@@ -152,6 +152,28 @@ __device__ __forceinline__ void mma_i8_elect(uint32_t tmem_d, uint32_t alo, uint
       "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "r"(0), "r"(accumulate)
       : "memory");
 }
+// Four MMAs sharing one B tile (the four operand groups of a template-row pair): one
+// elect, one predicate, four issues -- a quarter of the per-MMA issue overhead.
+__device__ __forceinline__ void mma_i8_x4_elect(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3, uint32_t a0,
+                                                uint32_t a1, uint32_t a2, uint32_t a3, uint32_t ahi, uint32_t blo,
+                                                uint32_t bhi, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 da0, da1, da2, da3, db;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %13, 0;\n\t"
+      "mov.b64 da0, {%4, %8};\n\t"
+      "mov.b64 da1, {%5, %8};\n\t"
+      "mov.b64 da2, {%6, %8};\n\t"
+      "mov.b64 da3, {%7, %8};\n\t"
+      "mov.b64 db, {%9, %10};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], da0, db, %11, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%1], da1, db, %11, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%2], da2, db, %11, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%3], da3, db, %11, p;\n\t}" ::"r"(t0),
+      "r"(t1), "r"(t2), "r"(t3), "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc),
+      "r"(0), "r"(accumulate)
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit_elect(uint64_t *bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
@@ -542,9 +564,14 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
         uint32_t blo = blo0 + (uint32_t)ss * sstep;
         for (int q = 0; q < ICH; ++q, blo += tilestep, arow += 2 * rowstep) {
           const uint32_t acc = (st | u | q) != 0 ? 1u : 0u;
+          if (ntg == 4) {
+            mma_i8_x4_elect(tcol[0], tcol[1], tcol[2], tcol[3], arow + aoff[0], arow + aoff[1], arow + aoff[2],
+                            arow + aoff[3], ahi, blo, bhi, idesc, acc);
+          } else {
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (j < ntg) mma_i8_elect(tcol[j], arow + aoff[j], ahi, blo, bhi, idesc, acc);
+            for (int j = 0; j < 4; ++j)
+              if (j < ntg) mma_i8_elect(tcol[j], arow + aoff[j], ahi, blo, bhi, idesc, acc);
+          }
         }
         mma_commit_elect(&empty[ss]);
         __syncwarp();
