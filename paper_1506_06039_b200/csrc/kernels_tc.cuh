@@ -329,6 +329,25 @@ __global__ void __launch_bounds__(256, 4) k_tc_prep(TcPrepArgs a) {
   for (int k = lane; k < 2 * hw; k += 32) ce[k] = 0;
   __syncwarp();
   u64 ftot = 0;
+  // coarse rows of <= 256 values: each lane owns one 8-column chunk, so its edge-column
+  // squares (< 2^28 each: coarse values < 2^14) accumulate in 32-bit registers and are
+  // flushed to the warp's shared sums every 16 rows
+  const bool one_chunk = nchunk <= 32;
+  uint32_t eacc[8];
+#pragma unroll
+  for (int x = 0; x < 8; ++x) eacc[x] = 0;
+  auto flush_edges = [&]() {
+    const int c0 = lane * 8;
+    if (lane < nchunk && (c0 < hw || c0 + 8 > nc - hw)) {
+#pragma unroll
+      for (int x = 0; x < 8; ++x) {
+        const int c = c0 + x;
+        if (c < hw) ce[c] += eacc[x];
+        if (c >= nc - hw) ce[hw + (nc - 1 - c)] += eacc[x];
+        eacc[x] = 0;
+      }
+    }
+  };
   auto item = [&](int pr, const uint32_t (&P)[4], int cc, bool live, u64 &rs) {
     const int cr = pr - hw;
     const uint32_t h0 = (P[0] >> 7) & 0x007F007Fu, h1 = (P[1] >> 7) & 0x007F007Fu;
@@ -351,12 +370,17 @@ __global__ void __launch_bounds__(256, 4) k_tc_prep(TcPrepArgs a) {
     const int c0 = cc * 8;
     const bool eL = c0 < hw, eR = c0 + 8 > nc - hw;
     if (!(eL || eR)) return;
+    if (one_chunk) {
 #pragma unroll
-    for (int x = 0; x < 8; ++x) {
-      const int c = c0 + x;
-      const u64 v2 = (u64)(v[x] * v[x]);
-      if (c < hw) ce[c] += v2;                        // distinct columns per lane
-      if (c >= nc - hw) ce[hw + (nc - 1 - c)] += v2;
+      for (int x = 0; x < 8; ++x) eacc[x] += v[x] * v[x];
+    } else {
+#pragma unroll
+      for (int x = 0; x < 8; ++x) {
+        const int c = c0 + x;
+        const u64 v2 = (u64)(v[x] * v[x]);
+        if (c < hw) ce[c] += v2;                        // distinct columns per lane
+        if (c >= nc - hw) ce[hw + (nc - 1 - c)] += v2;
+      }
     }
     const bool top = cr < hw, bot = cr >= mc - hw;
     if (!(top || bot)) return;
@@ -387,7 +411,12 @@ __global__ void __launch_bounds__(256, 4) k_tc_prep(TcPrepArgs a) {
   };
   // plane rows pr = warp / F, + nwarp / F, ...; two rows per pass (loads first)
   const int pstep = nwarp / F;
+  int npass = 0;
   for (int pr = warp / F; pr < g.R; pr += 2 * pstep) {
+    if (one_chunk && ++npass == 8) {   // 16 rows since the last flush
+      flush_edges();
+      npass = 0;
+    }
     const int pr2 = pr + pstep;
     const bool live1 = fi < a.B && pr - hw >= 0 && pr - hw < mc;
     const bool live2 = fi < a.B && pr2 < g.R && pr2 - hw >= 0 && pr2 - hw < mc;
@@ -403,6 +432,7 @@ __global__ void __launch_bounds__(256, 4) k_tc_prep(TcPrepArgs a) {
     if (pr2 < g.R) row_done(pr2, live2, rs2);
   }
   // flush this warp's edge-column and total energies
+  if (one_chunk) flush_edges();
   __syncwarp();
   for (int k = lane; k < 2 * hw; k += 32) atomicAdd(&colE[f * 2 * hw + k], ce[k]);
   if (lane == 0) atomicAdd(&tot[f], ftot);
