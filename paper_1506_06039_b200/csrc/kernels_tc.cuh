@@ -52,6 +52,7 @@ struct TcGeom {
   int planeB;   // bytes per 16-column plane = R * 32 * F
   int stripB;   // 2 planes
   int TPAD, TP; // padded template parts: TP = nc + 2*TPAD bytes per row, zeros in the pads
+  int SEGB;     // bytes of one template part row a strip's B tiles read: 32 + 2*TPAD
   int ICH;      // template-row pairs per super-stage (one ring slot per producer warp)
   int ctas;     // CTAs per SM the geometry is sized for
   int npairs;   // ceil(mc / 2)
@@ -106,6 +107,13 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 __device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
+// 16-byte LDGSTS (L1-bypassing) into shared memory, per-thread commit groups
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -502,6 +510,16 @@ struct TcArgs {
 // Producers depend only on the template, so they run up to NSS super-stages ahead,
 // across strip boundaries; the strip reload stall is covered by the second CTA on
 // the SM.
+#ifdef MOCO_TC_TIMING   // debug builds only: per-CTA phase times, printed for a few CTAs
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TC_T(...) __VA_ARGS__
+#else
+#define TC_T(...)
+#endif
 constexpr int TC_THREADS = 256;
 constexpr int TC_PRODUCERS = 7;
 
@@ -526,7 +544,9 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
   const int ICH = g.ICH;
   unsigned char *As = smem;                                   // [GG] strips of 2 planes
   unsigned char *Bring = As + GG * g.stripB;                  // [NSS][ICH][N*32]
-  uint64_t *bars = reinterpret_cast<uint64_t *>(Bring + NSS * ICH * N * 32);
+  const int SEGB = g.SEGB, PAIRB = 4 * SEGB;
+  unsigned char *Stg = Bring + NSS * ICH * N * 32;            // [NSS][2][ICH][pb][d][SEGB]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(Stg + NSS * 2 * ICH * PAIRB);
   uint64_t *full = bars, *empty = bars + NSS, *aload = bars + 2 * NSS;
   uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * NSS + 1);
   const int grp0 = blockIdx.x * GG;
@@ -535,6 +555,7 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
   const int per_strip = g.npairs / ICH;
   const int nsuper = g.nstrips * per_strip;
 
+  TC_T(const uint64_t t_start = gtimer(); uint64_t w_strip = 0, w_full = 0, w_empty = 0, t_issue = 0;)
   if (warp == 0) tmem_alloc(tmem_holder, g.tmem_cols);
   if (tid == 0) {
     for (int s = 0; s < NSS; ++s) {
@@ -569,11 +590,19 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
       aoff[j] = (uint32_t)(gg * g.stripB >> 4) + (uint32_t)(k * g.ST) * rowstep;
       tcol[j] = taddr + (uint32_t)(j * N);
     }
+    if (elect_one()) {   // the epilogue's frame energies: HBM -> L2 while the MMAs run
+      const uintptr_t b0 = (uintptr_t)(a.ga + (int64_t)grp0 * F * g.W * g.W) & ~(uintptr_t)15;
+      const uintptr_t b1 = (uintptr_t)(a.ga + (int64_t)min((grp0 + gcount) * F, a.B) * g.W * g.W) & ~(uintptr_t)15;
+      if (b1 > b0) bulk_prefetch_l2(reinterpret_cast<const void *>(b0), (uint32_t)(b1 - b0));
+    }
+    __syncwarp();
     const int nst = g.nstrips;
     int ss = 0, round = 0;              // slot (= producer) and slot use of the super-stage
     int pss = NSS - 1, pround = -1;     // of the previous super-stage
     for (int st = 0; st < nst; ++st) {
+      TC_T(uint64_t t0 = gtimer();)
       if (st > 0) mbar_wait(&empty[pss], pround & 1);   // strip buffers free
+      TC_T(w_empty += gtimer() - t0;)
       if (elect_one()) {
         mbar_arrive_expect_tx(aload, (uint32_t)(gcount * g.stripB));
         for (int gg = 0; gg < gcount; ++gg)
@@ -585,11 +614,15 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
             bulk_prefetch_l2(a.G + ((int64_t)(grp0 + gg) * nst + st + 1) * g.stripB, (uint32_t)g.stripB);
       }
       __syncwarp();
+      TC_T(t0 = gtimer();)
       mbar_wait(aload, st & 1);
+      TC_T(w_strip += gtimer() - t0;)
       tc_fence_after();
       uint32_t arow = alo0;             // A descriptor low word at the pair's first template row
       for (int u = 0; u < per_strip; ++u) {
+        TC_T(t0 = gtimer();)
         mbar_wait(&full[ss], round & 1);
+        TC_T(w_full += gtimer() - t0;)
         tc_fence_after();
         uint32_t blo = blo0 + (uint32_t)ss * sstep;
         for (int q = 0; q < ICH; ++q, blo += tilestep, arow += 2 * rowstep) {
@@ -610,59 +643,82 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
         if (++ss == NSS) { ss = 0; ++round; }
       }
     }
+    TC_T(t_issue = gtimer();)
   } else {
     // ---------------- B producers: tile of pair (i, i+1), row n = (d, pb, t)
     const int p = warp - 1;
-    int srcoff[CPL], dstoff[CPL];
-    bool live[CPL];
+    int srcoff[CPL];
+    uint32_t live = 0;
+    // chunk c of this lane: row n = (lane&7) + 8*(lane>>4) + 16c, half h = (lane>>3)&1,
+    // 512 bytes apart; each 8-lane phase of a 16-byte store covers all 32 banks
+    const int dst0 = (lane >> 4) * 256 + ((lane >> 3) & 1) * 128 + (lane & 7) * 16;
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
-      const int cc = lane + 32 * q;
-      const int n = cc >> 1, h = cc & 1;
+      const int n = (lane & 7) + 8 * (lane >> 4) + 16 * q, h = (lane >> 3) & 1;
       const int d = n >= N1 ? 1 : 0, r = n - d * N1;
       const int pb = r >= g.Wt ? 1 : 0, ti = r - pb * g.Wt;
-      live[q] = ti < g.W;
+      if (ti < g.W) live |= 1u << q;
       // bytes b_pb[i+d][J0 + 16h - t + x], x = 0..15, from the 4-aligned word below
-      const int col = 16 * h - (ti - hw) + g.TPAD;          // + J0, in the padded row
-      srcoff[q] = pb * (mc + 2) * g.TP + d * g.TP + col;
-      dstoff[q] = (n >> 3) * 256 + h * 128 + (n & 7) * 16;
+      const int col = 16 * h - (ti - hw) + g.TPAD;          // in the staged band [J0, J0 + SEGB)
+      srcoff[q] = (pb * 2 + d) * SEGB + col;
     }
     int st = p / per_strip, i0 = (p % per_strip) * ICH;   // strip, first pair of the super-stage
     const int ss = p;
+    // The band of template-part rows a super-stage reads (ICH pairs x 2 parts x 2 rows x
+    // SEGB bytes) is staged in shared memory with LDGSTS one super-stage ahead: the tile
+    // build then waits on shared-memory latency only (the T8 band of a strip does not
+    // stay L1-resident next to the strips and the ring, so direct loads went to L2).
+    unsigned char *stg = Stg + p * 2 * ICH * PAIRB;
+    const int nchunk = ICH * PAIRB / 16, segc = SEGB / 16;
+    auto stage_band = [&](int st_, int i0_, unsigned char *dst) {
+      for (int k = lane; k < nchunk; k += 32) {
+        const int q = k / (4 * segc), r = k % (4 * segc);
+        const int seg = r / segc, c16 = r % segc;   // seg = pb*2 + d
+        const uint8_t *src = a.T8 + (int64_t)(seg >> 1) * (mc + 2) * g.TP +
+                             (int64_t)(2 * (i0_ + q) + (seg & 1)) * g.TP + st_ * 32 + c16 * 16;
+        cp_async16(dst + q * PAIRB + seg * SEGB + c16 * 16, src);
+      }
+      cp_async_commit();
+    };
+    stage_band(st, i0, stg);
     int round = 0;
     for (int u = p; u < nsuper; u += TC_PRODUCERS, ++round) {
+      // next super-stage of this warp: TC_PRODUCERS super-stages later
+      int nst = st, ni0 = i0 + TC_PRODUCERS * ICH;
+      while (ni0 >= g.npairs) { ni0 -= g.npairs; ++nst; }
+      unsigned char *cur = stg + (round & 1) * ICH * PAIRB;
+      __syncwarp();   // every lane is done reading the other buffer (previous round)
+      if (u + TC_PRODUCERS < nsuper) stage_band(nst, ni0, stg + ((round + 1) & 1) * ICH * PAIRB);
+      else cp_async_commit();
       if (round > 0) mbar_wait(&empty[ss], (round - 1) & 1);
+      cp_async_wait<1>();
+      __syncwarp();
       unsigned char *Bs = Bring + ss * ICH * N * 32;
       for (int q = 0; q < ICH; ++q) {
-        const uint8_t *rowbase = a.T8 + (int64_t)(2 * (i0 + q)) * g.TP + st * 32;
-        uint32_t wv[CPL][5];
+        const unsigned char *rowbase = cur + q * PAIRB;
+        unsigned char *Bt = Bs + q * N * 32 + dst0;
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
           const uint32_t *wp = reinterpret_cast<const uint32_t *>(rowbase + (srcoff[c] & ~3));
-#pragma unroll
-          for (int e = 0; e < 5; ++e) wv[c][e] = __ldg(wp + e);
-        }
-        unsigned char *Bt = Bs + q * N * 32;
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) {
           const uint32_t sh = (srcoff[c] & 3) * 8;
           uint4 outv = make_uint4(0, 0, 0, 0);
-          if (live[c]) {
-            outv.x = __funnelshift_r(wv[c][0], wv[c][1], sh);
-            outv.y = __funnelshift_r(wv[c][1], wv[c][2], sh);
-            outv.z = __funnelshift_r(wv[c][2], wv[c][3], sh);
-            outv.w = __funnelshift_r(wv[c][3], wv[c][4], sh);
+          if ((live >> c) & 1u) {
+            const uint32_t w0 = wp[0], w1 = wp[1], w2 = wp[2], w3 = wp[3], w4 = wp[4];
+            outv.x = __funnelshift_r(w0, w1, sh);
+            outv.y = __funnelshift_r(w1, w2, sh);
+            outv.z = __funnelshift_r(w2, w3, sh);
+            outv.w = __funnelshift_r(w3, w4, sh);
           }
-          *reinterpret_cast<uint4 *>(Bt + dstoff[c]) = outv;
+          *reinterpret_cast<uint4 *>(Bt + c * 512) = outv;
         }
       }
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[ss]);
-      // next super-stage of this warp: TC_PRODUCERS super-stages later
-      i0 += TC_PRODUCERS * ICH;
-      while (i0 >= g.npairs) { i0 -= g.npairs; ++st; }
+      st = nst;
+      i0 = ni0;
     }
+    cp_async_wait<0>();
   }
   // all MMAs done -> accumulators final.  Every warp must be converged before the
   // .sync.aligned TMEM loads (threads can leave the mbarrier spin at different times).
@@ -671,6 +727,7 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
     mbar_wait(&empty[last % NSS], (last / NSS) & 1);
   }
   __syncwarp();
+  TC_T(const uint64_t t_mma = gtimer();)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -683,8 +740,20 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
   const int m = (warp & 3) * 32 + lane;     // accumulator row = TMEM lane
   const int sl = m / (2 * F), rho = m % (2 * F);
   const int f = rho >> 1, pa = rho & 1;
-  uint32_t *D1s = reinterpret_cast<uint32_t *>(smem);   // [GG*NT][128][32]: (pb hi 16 | pb lo 16)
-  Key *keys = reinterpret_cast<Key *>(smem + GG * NT * 128 * 32 * 4);
+  // [GG*NT][128][33 words]: (pb hi 16 | pb lo 16), rows padded to 33 words so the 32
+  // lanes (consecutive rows) of a warp hit 32 different banks
+  uint32_t *D1s = reinterpret_cast<uint32_t *>(smem);
+  Key *keys = reinterpret_cast<Key *>(smem + GG * NT * 128 * 33 * 4);
+  // the frame energies of this CTA's frames, staged once with coalesced loads (per-lag
+  // loads straight from global memory, one row s per lane, were the epilogue's cost)
+  u64 *gas = reinterpret_cast<u64 *>(keys + GG * 128);
+  const int64_t fi0 = (int64_t)grp0 * F;
+  {
+    const int64_t nga = (int64_t)min(gcount * F, a.B - (int)fi0) * W * W;
+    const u64 *src = a.ga + fi0 * W * W;
+    for (int64_t k = tid; k < nga; k += TC_THREADS) gas[k] = src[k];
+  }
+  __syncthreads();
   Key best[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) best[q] = Key{~0ull, ~0u};
@@ -700,7 +769,7 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
         tmem_ld16(tbase + c, yh);
         tmem_ld16(tbase + g.Wt + c, yl);
         tmem_wait_ld();
-        uint32_t *dst = D1s + ((gg * NT + k) * 128 + m) * 32;
+        uint32_t *dst = D1s + ((gg * NT + k) * 128 + m) * 33;
 #pragma unroll
         for (int qq = 0; qq < 16; ++qq) { dst[qq] = yh[qq]; dst[16 + qq] = yl[qq]; }
       }
@@ -724,7 +793,7 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
         tmem_ld16(tbase + c, xh);             // d = 0, pb = hi
         tmem_ld16(tbase + g.Wt + c, xl);      // d = 0, pb = lo
         tmem_wait_ld();
-        const uint32_t *src = D1s + ((gg * NT + (haveP ? kp : 0)) * 128 + (haveP ? mp : 0)) * 32;
+        const uint32_t *src = D1s + ((gg * NT + (haveP ? kp : 0)) * 128 + (haveP ? mp : 0)) * 33;
 #pragma unroll
         for (int qq = 0; qq < 16; ++qq) {
           if (haveP) { xh[qq] += src[qq]; xl[qq] += src[16 + qq]; }   // each < 2^31: no wrap
@@ -734,7 +803,7 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
           if (!valid || ti >= W) continue;
           const u64 h = ((u64)xh[qq] << 14) + (((u64)xl[qq] + (u64)ph) << 7) + (u64)pl;
           const int lag = (s + hw) * W + ti;
-          const u64 Nn = a.ga[(int64_t)fi * W * W + lag] + a.gb[lag] - 2 * h;
+          const u64 Nn = gas[(fi - fi0) * W * W + lag] + a.gb[lag] - 2 * h;
           const int t = ti - hw;
           const double area = (double)((mc - abs(s)) * (nc - abs(t)));
           const double fv = (double)Nn / (a.scale * area);
@@ -770,6 +839,7 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
   }
   __syncthreads();
   if (warp == 0) tmem_dealloc(taddr, g.tmem_cols);
+  TC_T(if (tid == 0 && (blockIdx.x % 149 == 0)) printf("TCT cta %d total %llu mma_done %llu issue_end %llu wait_strip %llu wait_full %llu wait_empty %llu\n", blockIdx.x, (unsigned long long)(gtimer() - t_start), (unsigned long long)(t_mma - t_start), (unsigned long long)(t_issue - t_start), (unsigned long long)w_strip, (unsigned long long)w_full, (unsigned long long)w_empty);)
 }
 
 // template parts for the B operand, zero-padded rows: T8[pb][i][TPAD + j] =
@@ -822,8 +892,10 @@ inline bool tc_make_geom(TcGeom *gp, int w, int mc, int nc, int L) {
   g.TPAD = (g.hw + 8 + 15) / 16 * 16;
   g.TP = nc + 2 * g.TPAD;
   g.npairs = (mc + 1) / 2;
+  g.SEGB = 32 + 2 * g.TPAD;
   auto smem_for = [&](int GG, int ICH) {
-    return 1024 + GG * g.stripB + TC_PRODUCERS * ICH * g.N * 32 + (2 * TC_PRODUCERS + 1) * 8 + 16;
+    return 1024 + GG * g.stripB + TC_PRODUCERS * ICH * g.N * 32 + TC_PRODUCERS * 2 * ICH * 4 * g.SEGB +
+           (2 * TC_PRODUCERS + 1) * 8 + 16;
   };
   // two CTAs per SM (one loads its next strip while the other computes): as many
   // groups per CTA as half of shared memory and half of TMEM allow, then the largest
@@ -835,7 +907,7 @@ inline bool tc_make_geom(TcGeom *gp, int w, int mc, int nc, int L) {
     if (GG * g.NT * g.N > tmem_cap || GG * g.NT > 4) continue;
     for (int ICH = 4; ICH >= 1; ICH /= 2) {
       const int sm = smem_for(GG, ICH);
-      if (g.npairs % ICH == 0 && sm <= smem_cap && GG * g.NT * 128 * 128 + GG * 128 * 16 <= sm - 1024 - 256) {
+      if (g.npairs % ICH == 0 && sm <= smem_cap && GG * g.NT * 128 * 132 + GG * 128 * 16 + GG * g.F * g.W * g.W * 8 <= sm - 1024 - 256) {
         g.GG = GG;
         g.ICH = ICH;
         break;
