@@ -53,6 +53,7 @@ struct TcGeom {
   int stripB;   // 2 planes
   int TPAD, TP; // padded template parts: TP = nc + 2*TPAD bytes per row, zeros in the pads
   int SEGB;     // bytes of one template part row a strip's B tiles read: 32 + 2*TPAD
+  int TS;       // TMEM columns between accumulator tiles (N, or 256 when there is room)
   int ICH;      // template-row pairs per super-stage (one ring slot per producer warp)
   int ctas;     // CTAs per SM the geometry is sized for
   int npairs;   // ceil(mc / 2)
@@ -110,6 +111,11 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes
 // 16-byte LDGSTS (L1-bypassing) into shared memory, per-thread commit groups
 __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+// the same with zero fill: src_bytes (0 or 16) bytes are read, the rest of the 16 written as 0
+__device__ __forceinline__ void cp_async16_zfill(void *dst, const void *src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -180,6 +186,21 @@ __device__ __forceinline__ void mma_i8_x4_elect(uint32_t t0, uint32_t t1, uint32
       "@e tcgen05.mma.cta_group::1.kind::i8 [%3], da3, db, %11, p;\n\t}" ::"r"(t0),
       "r"(t1), "r"(t2), "r"(t3), "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc),
       "r"(0), "r"(accumulate)
+      : "memory");
+}
+// Two MMAs sharing one B tile (two M tiles of one operand group, C1-C3's geometry).
+__device__ __forceinline__ void mma_i8_x2_elect(uint32_t t0, uint32_t t1, uint32_t a0, uint32_t a1, uint32_t ahi,
+                                                uint32_t blo, uint32_t bhi, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 da0, da1, db;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %9, 0;\n\t"
+      "mov.b64 da0, {%2, %4};\n\t"
+      "mov.b64 da1, {%3, %4};\n\t"
+      "mov.b64 db, {%5, %6};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], da0, db, %7, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%1], da1, db, %7, p;\n\t}" ::"r"(t0),
+      "r"(t1), "r"(a0), "r"(a1), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "r"(0), "r"(accumulate)
       : "memory");
 }
 __device__ __forceinline__ void mma_commit_elect(uint64_t *bar) {
@@ -555,7 +576,7 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
   const int per_strip = g.npairs / ICH;
   const int nsuper = g.nstrips * per_strip;
 
-  TC_T(const uint64_t t_start = gtimer(); uint64_t w_strip = 0, w_full = 0, w_empty = 0, t_issue = 0;)
+  TC_T(const uint64_t t_start = gtimer(); const long long c_start = clock64(); uint64_t w_strip = 0, w_full = 0, w_empty = 0, t_issue = 0;)
   if (warp == 0) tmem_alloc(tmem_holder, g.tmem_cols);
   if (tid == 0) {
     for (int s = 0; s < NSS; ++s) {
@@ -588,7 +609,7 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
     for (int j = 0; j < 4; ++j) {
       const int gg = j / NT, k = j % NT;
       aoff[j] = (uint32_t)(gg * g.stripB >> 4) + (uint32_t)(k * g.ST) * rowstep;
-      tcol[j] = taddr + (uint32_t)(j * N);
+      tcol[j] = taddr + (uint32_t)(j * g.TS);
     }
     if (elect_one()) {   // the epilogue's frame energies: HBM -> L2 while the MMAs run
       const uintptr_t b0 = (uintptr_t)(a.ga + (int64_t)grp0 * F * g.W * g.W) & ~(uintptr_t)15;
@@ -630,6 +651,8 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
           if (ntg == 4) {
             mma_i8_x4_elect(tcol[0], tcol[1], tcol[2], tcol[3], arow + aoff[0], arow + aoff[1], arow + aoff[2],
                             arow + aoff[3], ahi, blo, bhi, idesc, acc);
+          } else if (ntg == 2) {
+            mma_i8_x2_elect(tcol[0], tcol[1], arow + aoff[0], arow + aoff[1], ahi, blo, bhi, idesc, acc);
           } else {
 #pragma unroll
             for (int j = 0; j < 4; ++j)
@@ -694,7 +717,11 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
       cp_async_wait<1>();
       __syncwarp();
       unsigned char *Bs = Bring + ss * ICH * N * 32;
+#ifdef MOCO_TC_NOPROD   // timing experiments: MMAs on stale B tiles
+      for (int q = 0; q < 0; ++q) {
+#else
       for (int q = 0; q < ICH; ++q) {
+#endif
         const unsigned char *rowbase = cur + q * PAIRB;
         unsigned char *Bt = Bs + q * N * 32 + dst0;
 #pragma unroll
@@ -727,7 +754,7 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
     mbar_wait(&empty[last % NSS], (last / NSS) & 1);
   }
   __syncwarp();
-  TC_T(const uint64_t t_mma = gtimer();)
+  TC_T(const uint64_t t_mma = gtimer(); const long long c_mma = clock64();)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -765,7 +792,7 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
       if (gg >= GG) continue;
       for (int k = 0; k < NT; ++k) {
         uint32_t yh[16], yl[16];
-        const uint32_t tbase = taddr + ((uint32_t)((warp & 3) * 32) << 16) + (gg * NT + k) * N + N1;
+        const uint32_t tbase = taddr + ((uint32_t)((warp & 3) * 32) << 16) + (gg * NT + k) * g.TS + N1;
         tmem_ld16(tbase + c, yh);
         tmem_ld16(tbase + g.Wt + c, yl);
         tmem_wait_ld();
@@ -789,7 +816,7 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
         const int kp = sl + 1 < g.ST ? k : k + 1;
         const bool haveP = kp < NT;   // s + 1 <= hw + 1 always lies inside the NT*ST lag rows
         uint32_t xh[16], xl[16];
-        const uint32_t tbase = taddr + ((uint32_t)((warp & 3) * 32) << 16) + (gg * NT + k) * N;
+        const uint32_t tbase = taddr + ((uint32_t)((warp & 3) * 32) << 16) + (gg * NT + k) * g.TS;
         tmem_ld16(tbase + c, xh);             // d = 0, pb = hi
         tmem_ld16(tbase + g.Wt + c, xl);      // d = 0, pb = lo
         tmem_wait_ld();
@@ -839,7 +866,7 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
   }
   __syncthreads();
   if (warp == 0) tmem_dealloc(taddr, g.tmem_cols);
-  TC_T(if (tid == 0 && (blockIdx.x % 149 == 0)) printf("TCT cta %d total %llu mma_done %llu issue_end %llu wait_strip %llu wait_full %llu wait_empty %llu\n", blockIdx.x, (unsigned long long)(gtimer() - t_start), (unsigned long long)(t_mma - t_start), (unsigned long long)(t_issue - t_start), (unsigned long long)w_strip, (unsigned long long)w_full, (unsigned long long)w_empty);)
+  TC_T(if (tid == 0 && (blockIdx.x % 149 == 0)) printf("TCT cta %d mma_cycles %lld total %llu mma_done %llu issue_end %llu wait_strip %llu wait_full %llu wait_empty %llu\n", blockIdx.x, c_mma - c_start, (unsigned long long)(gtimer() - t_start), (unsigned long long)(t_mma - t_start), (unsigned long long)(t_issue - t_start), (unsigned long long)w_strip, (unsigned long long)w_full, (unsigned long long)w_empty);)
 }
 
 // template parts for the B operand, zero-padded rows: T8[pb][i][TPAD + j] =
@@ -915,8 +942,9 @@ inline bool tc_make_geom(TcGeom *gp, int w, int mc, int nc, int L) {
     }
   }
   if (!g.GG) return false;
+  g.TS = g.N;   // (256-column-aligned tiles measured no faster)
   int cols = 32;
-  while (cols < g.GG * g.NT * g.N) cols <<= 1;
+  while (cols < g.GG * g.NT * g.TS) cols <<= 1;
   g.tmem_cols = cols;
   g.smem = smem_for(g.GG, g.ICH);
   g.prep_smem = (g.F * (4 * g.hw + 4 * w * w + 1) + 8 * 2 * g.hw) * 8;   // + per-warp edge-column sums

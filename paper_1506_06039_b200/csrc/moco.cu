@@ -19,6 +19,7 @@
 #include "kernels_direct.cuh"
 #include "kernels_tc.cuh"
 #include "kernels_refine.cuh"
+#include "kernels_rtc.cuh"
 #include "kernels_fft.cuh"
 
 using namespace moco;
@@ -52,6 +53,8 @@ struct moco_plan {
   int rstages[3];             // refine levels: bulk-copy ring depth
   int rrt[3], rnrt[3];        // refine levels: template rows per tile, row tiles
   u64 *racc;                  // refine accumulators [cap][18] (kept zero between calls)
+  RtcGeom rtc[3];             // tensor-core refine geometry per level (kernels_rtc.cuh)
+  uint8_t *rtab[3];           // its template candidate tiles, or null: CUDA-core refine
   int nsm;                    // multiprocessors of the plan's device
   int64_t cap;                // frames per internal batch
   void *scratch[3];           // frame pyramid levels 1..L for one batch
@@ -171,8 +174,10 @@ static void plan_free(moco_plan *p) {
   }
   if (p->gb) cudaFree(p->gb);
   if (p->racc) cudaFree(p->racc);
-  for (int l = 0; l < 3; ++l)
+  for (int l = 0; l < 3; ++l) {
     if (p->pb2[l]) cudaFree(p->pb2[l]);
+    if (p->rtab[l]) cudaFree(p->rtab[l]);
+  }
   tc_free(&p->tc);
   for (void *q : {(void *)p->fft.twr, (void *)p->fft.twc, (void *)p->fft.Bc, (void *)p->fft.S, (void *)p->fft.P,
                   (void *)p->fft.ga, (void *)p->fft.qc})
@@ -394,6 +399,16 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
       p->rnrt[l] = nrt;
       // (ring within ~150 KB: a 37 KB operand-prep CTA of the next batch fits beside it)
       p->rstages[l] = std::min(32, (150 * 1024 - rs_smem_bytes(rt, 0)) / rs_stage_bytes(rt));
+      // tensor-core refine sums (kernels_rtc.cuh), opt-in with MOCO_RTC=1: exact, but
+      // slower than the CUDA-core kernel on B200 as measured
+      const char *re = getenv("MOCO_RTC");
+      if (re && atoi(re) == 1 && rtc_make(&p->rtc[l], p->ml[l], p->nl[l], bits + 2 * l)) {
+        const size_t tb = (size_t)(p->ml[l] + 2) * p->rtc[l].nsteps * 1024;
+        if (cudaMalloc((void **)&p->rtab[l], tb) != cudaSuccess) {
+          cudaGetLastError();
+          p->rtab[l] = nullptr;
+        }
+      }
     }
   if (rc != MOCO_OK) { plan_free(p); return rc; }
   p->algo = MOCO_ALGO_DIRECT;
@@ -593,7 +608,8 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
     a.wide = halves * a.rt * 8.0 * mx >= 4294967296.0 ? 1 : 0;
   }
   CUtensorMap tmF;
-  if (!tmap_u16_3d(&tmF, img, a.nl, a.ml, B, p->pitch[l], fstride, RS_BOX, a.rt + 2)) {
+  const bool rtc = p->rtab[l] != nullptr;
+  if (!rtc && !tmap_u16_3d(&tmF, img, a.nl, a.ml, B, p->pitch[l], fstride, RS_BOX, a.rt + 2)) {
     snprintf(g_err, sizeof(g_err), "cuTensorMapEncodeTiled failed (refine level %d)", l);
     return MOCO_ECUDA;
   }
@@ -607,7 +623,30 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
   // cleared by a memset after the pick instead of by the single CTA)
   b.parts = (int)std::max<int64_t>(1, std::min<int64_t>(16, p->nsm / std::max<int64_t>(1, B)));
   if (!corr) b.parts = 1;
-  {
+  if (rtc) {
+    ProfScope ps(p, MOCO_K_REFINE, st);
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(k_refine_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, RTC_SMEM));
+      attr = true;
+    }
+    RtcArgs r;
+    r.img = (const uint16_t *)img; r.fstride = fstride; r.pitch = p->pitch[l];
+    r.tab = p->rtab[l]; r.acc = racc; r.shift_in = sin; r.B = (int)B; r.g = p->rtc[l];
+    // row parts per 64-frame group: the fewest that bring the last wave near full
+    const int64_t groups = (B + RTC_F - 1) / RTC_F;
+    const int R = p->ml[l] + 2;
+    int best = 1;
+    double bestc = 1e30;
+    for (int parts = 1; parts <= 16 && R / parts >= 16; ++parts) {
+      const double waves = std::ceil((double)(groups * parts) / p->nsm);
+      const double cost = waves / parts + 0.01 * parts;   // per-CTA fixed costs
+      if (cost < bestc) { bestc = cost; best = parts; }
+    }
+    r.parts = best;
+    r.rows_per_part = (R + best - 1) / best;
+    k_refine_tc<<<(unsigned)(groups * best), RTC_THREADS, RTC_SMEM, st>>>(r);
+  } else {
     ProfScope ps(p, MOCO_K_REFINE, st);
     const int smem = rs_smem_bytes(a.rt, a.stages);
     static int attr_smem = 0;
@@ -621,7 +660,7 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
     else k_refine_sums<false><<<(unsigned)(a.nrt * nct), RS_THREADS, smem, st>>>(tmF, a);
   }
   p->launches++;
-  CKL("k_refine_sums");
+  CKL(rtc ? "k_refine_tc" : "k_refine_sums");
   if (st_pick) {   // pick/apply on another stream (align_tc_pipelined)
     CK(cudaEventRecord(ev_sums, st));
     CK(cudaStreamWaitEvent(st_pick, ev_sums, 0));
@@ -689,6 +728,11 @@ int moco_set_template(moco_plan *p, const void *d_template, moco_stream_t stream
                                                                p->ml[l], p->nl[l], p->pb2[l]);
       k_prefix2d_cols<<<(p->nl[l] + 128) / 128, 128, 0, st>>>(p->ml[l], p->nl[l], p->pb2[l]);
       CKL("k_prefix2d");
+      if (p->rtab[l]) {
+        k_rtc_table<<<1024, 256, 0, st>>>((const uint16_t *)p->tpl[l], p->pitch[l], p->ml[l], p->nl[l],
+                                          p->rtc[l].nsteps, p->rtab[l]);
+        CKL("k_rtc_table");
+      }
     }
   if (p->tc.ready) {
     if (tc_set_template(&p->tc, (const uint16_t *)p->tpl[L], p->pitch[L], st) != 0)

@@ -126,6 +126,25 @@ def test_fused_refine_equals_simple_refine(c, T, monkeypatch):
         assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("c,T", [(2, 300), (4, 24), (3, 130)])
+def test_tensor_core_refine_equals_cuda_core_refine(c, T, monkeypatch):
+    """The opt-in tensor-core refine sums (MOCO_RTC=1, kernels_rtc.cuh: 64 frames x hi/lo
+    parts as M, the nine shifted template parts as N, pixels as K, GA from the converter
+    warps) give bit-identical shifts, f_min and corrected frames to the CUDA-core kernel;
+    ragged frame groups (T % 64 != 0) and both pyramid levels of C4 included."""
+    spec = config_spec(c, T=T)
+    st = make_stack(spec, 0, T, device=DEV)
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("MOCO_RTC", mode)
+        p = _plan_for(spec)
+        p.set_template(st.template)
+        sh, fm, co, _ = p.align(st.frames, corrected=True)
+        out[mode] = (sh, fm, co.view(torch.int16))
+    for a, b in zip(out["1"], out["0"]):
+        assert torch.equal(a, b)
+
+
 def test_refine_all_alignments():
     """Refine+apply at every column misalignment of the doubled shift (the fused
     kernel specialises on (T-1) mod 8): exact translates with dx = -9..9."""

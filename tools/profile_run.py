@@ -15,8 +15,9 @@ ap.add_argument("--frames", type=int, default=1184)
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--algo", default="auto")
 ap.add_argument("--no-corrected", action="store_true")
+ap.add_argument("--w", type=int, default=0)
 args = ap.parse_args()
-spec = config_spec(args.config, T=args.frames)
+spec = config_spec(args.config, T=args.frames, **({"w": args.w} if args.w else {}))
 st = make_stack(spec, 0, args.frames, device="cuda")
 p = Plan(spec.m, spec.n, spec.w, spec.levels, spec.dtype, 12, device=0, algo=args.algo)
 p.set_template(st.template)
