@@ -359,6 +359,55 @@ def main():
             b.synchronize()
             ts.append(a.elapsed_time(b))
         lat = {"p50_ms": float(np.percentile(ts, 50)), "p99_ms": float(np.percentile(ts, 99))}
+        # host wall time, call -> results on the device and the stream drained
+        hs = []
+        for _ in range(200):
+            t0 = time.perf_counter()
+            plan.align_into(one, s1, f1, c1)
+            torch.cuda.current_stream().synchronize()
+            hs.append((time.perf_counter() - t0) * 1e3)
+        lat.update(host_p50_ms=float(np.percentile(hs, 50)), host_p99_ms=float(np.percentile(hs, 99)))
+        # the same call captured once in a CUDA graph and replayed (launch overhead removed)
+        try:
+            g = torch.cuda.CUDAGraph()
+            cs = torch.cuda.Stream()
+            cs.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(cs):
+                plan.align_into(one, s1, f1, c1)   # warm on the capture stream
+                torch.cuda.synchronize()
+                with torch.cuda.graph(g, stream=cs):
+                    plan.align_into(one, s1, f1, c1)
+            torch.cuda.synchronize()
+            ref = s1.clone()
+            ge, gh = [], []
+            for _ in range(200):
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                t0 = time.perf_counter()
+                a.record()
+                g.replay()
+                b.record()
+                b.synchronize()
+                gh.append((time.perf_counter() - t0) * 1e3)
+                ge.append(a.elapsed_time(b))
+            lat["graph"] = {"p50_ms": float(np.percentile(ge, 50)), "p99_ms": float(np.percentile(ge, 99)),
+                            "host_p50_ms": float(np.percentile(gh, 50)), "host_p99_ms": float(np.percentile(gh, 99)),
+                            "same_result": bool(torch.equal(ref, s1))}
+        except Exception as e:   # report, do not fail the bench line
+            lat["graph"] = {"error": str(e)[:200]}
+        # closed loop from pinned host memory: frame in -> (shift, f_min) back on the host
+        hf1 = frames[:1].cpu().pin_memory()
+        hsh = torch.empty((1, 2), dtype=torch.int32).pin_memory()
+        hfm = torch.empty((1,), dtype=torch.float64).pin_memory()
+        for _ in range(20):
+            plan.align_host(hf1, hsh, hfm)
+        ws = []
+        for _ in range(200):
+            t0 = time.perf_counter()
+            plan.align_host(hf1, hsh, hfm)
+            ws.append((time.perf_counter() - t0) * 1e3)
+        lat["frame_to_shift_host"] = {"p50_ms": float(np.percentile(ws, 50)), "p99_ms": float(np.percentile(ws, 99)),
+                                      "api": "moco_align_host, 1 pinned frame in, shift + f_min out"}
 
     # ---- context: the paper's own setting (downsample once, w = min(m,n)/3 of the
     # 256x256 coarse frame = 85), FFT path; the paper quotes ~23 frames/s for its Java
