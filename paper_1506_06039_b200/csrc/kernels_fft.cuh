@@ -35,6 +35,7 @@ namespace moco {
 
 constexpr double RS_FFT_C = 8.0;   // error-bound constant (measured max ~0.5)
 constexpr int FFT_QCAP = 64;
+constexpr int FFT_UB_INIT = 0x7f7f7f7f;   // ~3.4e38f: a.ub between calls
 constexpr int FFT_MAXST = 10;
 
 struct FftLen {
@@ -183,14 +184,14 @@ constexpr int FFT_THREADS = 256;
 // S[f][k][r] = sum_j a_f[r][j] exp(-2 pi i j k / Mc), k in [0, Kc), r in [0, mcp)
 __global__ void __launch_bounds__(FFT_THREADS) k_fft_rows(const uint16_t *__restrict__ img, int64_t fstride,
                                                           int pitch, FftGeom g, const float2 *__restrict__ twc,
-                                                          float2 *__restrict__ S) {
+                                                          float2 *__restrict__ S, int per) {
   extern __shared__ __align__(16) float2 fsm[];
   const int Mc = g.Lc.N;
   float2 *tw = fsm;
   float2 *x = tw + Mc, *y = x + FFT_ROWS_PAIRS * Mc;
-  const int nrb = (g.mcp / 2 + FFT_ROWS_PAIRS - 1) / FFT_ROWS_PAIRS;
+  const int nrb = (g.mcp / 2 + per - 1) / per;   // per <= FFT_ROWS_PAIRS row pairs per block
   const int f = blockIdx.x / nrb, rb = blockIdx.x % nrb;
-  const int p0 = rb * FFT_ROWS_PAIRS, np = min(FFT_ROWS_PAIRS, g.mcp / 2 - p0);
+  const int p0 = rb * per, np = min(per, g.mcp / 2 - p0);
   for (int k = threadIdx.x; k < Mc; k += blockDim.x) tw[k] = twc[k];
   const uint16_t *A = img + (int64_t)f * fstride;
   for (int e = threadIdx.x; e < np * Mc; e += blockDim.x) {
@@ -225,14 +226,14 @@ __global__ void __launch_bounds__(FFT_THREADS) k_fft_rows(const uint16_t *__rest
 // mode 1 (template): Bc[k][u] = conj(X[u][k]) / (Mr Mc)
 __global__ void __launch_bounds__(FFT_THREADS) k_fft_cols(const float2 *__restrict__ S, FftGeom g,
                                                           const float2 *__restrict__ twr, float2 *__restrict__ Bc,
-                                                          float2 *__restrict__ P, int mode) {
+                                                          float2 *__restrict__ P, int mode, int per) {
   extern __shared__ __align__(16) float2 fsm[];
   const int Mr = g.Lr.N;
   float2 *tw = fsm;
   float2 *x = tw + Mr, *y = x + FFT_COLS * Mr;
-  const int ncb = (g.Kc + FFT_COLS - 1) / FFT_COLS;
+  const int ncb = (g.Kc + per - 1) / per;   // per <= FFT_COLS column bins per block
   const int f = blockIdx.x / ncb, cb = blockIdx.x % ncb;
-  const int k0 = cb * FFT_COLS, nk = min(FFT_COLS, g.Kc - k0);
+  const int k0 = cb * per, nk = min(per, g.Kc - k0);
   for (int k = threadIdx.x; k < Mr; k += blockDim.x) tw[k] = twr[k];
   const float2 *Sf = S + (int64_t)f * g.Kc * g.mcp;
   for (int e = threadIdx.x; e < nk * Mr; e += blockDim.x) {
@@ -285,24 +286,32 @@ struct FftScoreArgs {
   uint8_t *flags;           // [B] or null
   int *qcount;              // [B] or null: candidates re-scored (diagnostics)
   float *h_out;             // [B][W*W] or null: the fp32 FFT cross term h~ (diagnostics)
+  float *lb;                // [B][W*W] lower bounds f~ - delta (split, small-batch path)
+  int *ub;                  // [B] min(f~ + delta) as float bits, kept at +inf between calls
 };
 
 // exact h(s,t) for one lag, 64-bit, all threads of the block; result to thread 0
 __device__ u64 exact_h(const FftScoreArgs &a, const uint16_t *A, int s, int t, u64 *red) {
   const int mc = a.g.mc, nc = a.g.nc;
   const int i0 = max(0, -s), i1 = mc - max(0, s), j0 = max(0, -t), j1 = nc - max(0, t);
-  // threads over columns, rows unrolled so every thread keeps several loads in flight
+  // warps over rows, lanes over columns (coalesced), four independent rows in flight
+  const int nw = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   u64 acc = 0;
-  for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
-    const uint16_t *ar = A + (int64_t)(i0 + s) * a.pitch + j + t;
-    const uint16_t *br = a.tpl + (int64_t)i0 * a.tpitch + j;
-    int i = i0;
-    for (; i + 4 <= i1; i += 4, ar += 4 * a.pitch, br += 4 * a.tpitch) {
-      const uint32_t p0 = (uint32_t)ar[0] * br[0], p1 = (uint32_t)ar[a.pitch] * br[a.tpitch];
-      const uint32_t p2 = (uint32_t)ar[2 * a.pitch] * br[2 * a.tpitch], p3 = (uint32_t)ar[3 * a.pitch] * br[3 * a.tpitch];
-      acc += (u64)p0 + p1 + (u64)p2 + p3;
+  for (int i = i0 + wid; i < i1; i += 4 * nw) {
+    const uint16_t *ar[4], *br[4];
+    bool ok[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int ii = i + q * nw;
+      ok[q] = ii < i1;
+      ar[q] = A + (int64_t)((ok[q] ? ii : i) + s) * a.pitch + t;
+      br[q] = a.tpl + (int64_t)(ok[q] ? ii : i) * a.tpitch;
     }
-    for (; i < i1; ++i, ar += a.pitch, br += a.tpitch) acc += (u64)((uint32_t)ar[0] * br[0]);
+    for (int j = j0 + lane; j < j1; j += 32) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)   // products < 2^32 (coarse values < 2^16), sums in 64 bits
+        if (ok[q]) acc += (u64)((uint32_t)ar[q][j] * br[q][j]);
+    }
   }
   acc = warp_sum(acc);
   __syncthreads();
@@ -312,6 +321,48 @@ __device__ u64 exact_h(const FftScoreArgs &a, const uint16_t *A, int s, int t, u
   if (threadIdx.x == 0)
     for (int k = 0; k < (int)(blockDim.x >> 5); ++k) tot += red[k];
   return tot;
+}
+
+// Candidate set Q = {lag : lower bound <= thr} (lower bounds in lbs, shared or global),
+// exact 64-bit rescoring of Q (all lags past FFT_QCAP), argmin key (f, s, t) (S4).
+// qn_s must be zero on entry (set before the block barrier that precedes the call).
+__device__ __forceinline__ void fft_pick_tail(const FftScoreArgs &a, int64_t f, const float *lbs, float thr, u64 *red,
+                                              int *qn_s, int *qlist) {
+  const FftGeom &g = a.g;
+  const int W = g.W, hw = g.hw;
+  const u64 *gaf = a.ga + f * W * W;
+  for (int lag = threadIdx.x; lag < W * W; lag += blockDim.x) {
+    if (lbs[lag] <= thr) {
+      const int q = atomicAdd(qn_s, 1);
+      if (q < FFT_QCAP) qlist[q] = lag;
+    }
+  }
+  __syncthreads();
+  const int nq = *qn_s;
+  const bool all = nq > FFT_QCAP;
+  const int ncand = all ? W * W : nq;
+  const uint16_t *A = a.img + f * a.fstride;
+  Key bk{~0ull, ~0u};
+  for (int c = 0; c < ncand; ++c) {
+    const int lag = all ? c : qlist[c];
+    const int s = lag / W - hw, t = lag % W - hw;
+    const u64 h = exact_h(a, A, s, t, red);
+    if (threadIdx.x == 0) {
+      const u64 N = gaf[lag] + a.gb[lag] - 2 * h;
+      const double area = (double)((g.mc - abs(s)) * (g.nc - abs(t)));
+      const double fv = (double)N / (a.scale * area);
+      const Key kk{(u64)__double_as_longlong(fv), (unsigned)lag};
+      if (key_less(kk, bk)) bk = kk;
+    }
+  }
+  if (threadIdx.x == 0) {
+    const int s = (int)(bk.idx / W) - hw, t = (int)(bk.idx % W) - hw;
+    a.shift_out[2 * f] = s;
+    a.shift_out[2 * f + 1] = t;
+    if (a.f_out) a.f_out[f] = __longlong_as_double((long long)bk.f);
+    if (a.flags) a.flags[f] = (uint8_t)(((abs(s) == hw || abs(t) == hw) ? 1 : 0) | (all ? 2 : 0));
+    if (a.qcount) a.qcount[f] = nq;
+  }
 }
 
 __global__ void __launch_bounds__(1024) k_fft_score(FftScoreArgs a) {
@@ -387,39 +438,78 @@ __global__ void __launch_bounds__(1024) k_fft_score(FftScoreArgs a) {
     fmin_hi_s = b;
   }
   __syncthreads();
-  const float thr = fmin_hi_s;
-  for (int lag = threadIdx.x; lag < W * W; lag += blockDim.x) {
-    if (hb[lag] <= thr) {
-      const int q = atomicAdd(&qn, 1);
-      if (q < FFT_QCAP) qlist[q] = lag;
-    }
+  fft_pick_tail(a, f, hb, fmin_hi_s, red, &qn, qlist);
+}
+
+// Small batches (the closed-loop case): the score step spread over many blocks.
+// k_fft_score_rows: block (frame f, group of FFT_ROWS_PAIRS lag-row pairs) -> inverse FFT
+// of its lag rows and the certified interval of each of its lags (same arithmetic as
+// k_fft_score): lower bound to a.lb, min of the upper bounds by atomicMin into a.ub[f]
+// (non-negative floats order like their bit patterns).
+__global__ void __launch_bounds__(FFT_THREADS) k_fft_score_rows(FftScoreArgs a, int per) {
+  extern __shared__ __align__(16) float2 fsm[];
+  const FftGeom &g = a.g;
+  const int Mc = g.Lc.N, W = g.W, hw = g.hw;
+  float2 *tw = fsm;
+  float2 *x = tw + Mc, *y = x + FFT_ROWS_PAIRS * Mc;
+  __shared__ float redf[FFT_THREADS / 32];
+  const int npairs = (W + 1) / 2, npb = (npairs + per - 1) / per;
+  const int64_t f = blockIdx.x / npb;
+  const int p0 = (blockIdx.x % npb) * per, np = min(per, npairs - p0);
+  for (int k = threadIdx.x; k < Mc; k += blockDim.x) tw[k] = a.twc[k];
+  const float2 *Pf = a.P + f * W * g.Kc;
+  for (int e = threadIdx.x; e < np * Mc; e += blockDim.x) {
+    const int q = e / Mc, k = e - q * Mc;
+    const int s1 = 2 * (p0 + q), s2 = s1 + 1;
+    const bool lo = k < g.Kc;
+    const int kk = lo ? k : Mc - k;
+    float2 v1 = Pf[(int64_t)s1 * g.Kc + kk];
+    float2 v2 = s2 < W ? Pf[(int64_t)s2 * g.Kc + kk] : make_float2(0.f, 0.f);
+    if (!lo) { v1.y = -v1.y; v2.y = -v2.y; }
+    x[q * Mc + k] = make_float2(v1.x - v2.y, v1.y + v2.x);
   }
   __syncthreads();
-  const int nq = qn;
-  const bool all = nq > FFT_QCAP;
-  const int ncand = all ? W * W : nq;
-  const uint16_t *A = a.img + f * a.fstride;
-  Key bk{~0ull, ~0u};
-  for (int c = 0; c < ncand; ++c) {
-    const int lag = all ? c : qlist[c];
-    const int s = lag / W - hw, t = lag % W - hw;
-    const u64 h = exact_h(a, A, s, t, red);
-    if (threadIdx.x == 0) {
-      const u64 N = gaf[lag] + a.gb[lag] - 2 * h;
-      const double area = (double)((g.mc - abs(s)) * (g.nc - abs(t)));
-      const double fv = (double)N / (a.scale * area);
-      const Key kk{(u64)__double_as_longlong(fv), (unsigned)lag};
-      if (key_less(kk, bk)) bk = kk;
-    }
+  const float2 *Hr = fft_batch(x, y, tw, g.Lc, np, +1.f);
+  const u64 *gaf = a.ga + f * W * W;
+  const double na = sqrt((double)gaf[hw * W + hw]), nb = sqrt((double)a.gb[hw * W + hw]);
+  const double eps2 = 2.0 * a.eps_rel * na * nb;
+  float best = 3.0e38f;
+  for (int e = threadIdx.x; e < np * 2 * W; e += blockDim.x) {
+    const int q = e / (2 * W), r = e - q * 2 * W, half = r / W, ti = r - half * W;
+    const int si = 2 * (p0 + q) + half;
+    if (si >= W) continue;
+    const float2 v = Hr[q * Mc + (ti - hw + Mc) % Mc];
+    const float h = half ? v.y : v.x;
+    const int lag = si * W + ti;
+    if (a.h_out) a.h_out[f * W * W + lag] = h;
+    const double inv = (1.0 / (a.scale * (double)(g.mc - abs(si - hw)))) * (1.0 / (double)(g.nc - abs(ti - hw)));
+    const double fa = ((double)gaf[lag] + (double)a.gb[lag] - 2.0 * (double)h) * inv;
+    const double del = eps2 * inv;
+    best = fminf(best, (float)(fa + del) * (1.0f + 1e-6f));
+    a.lb[f * W * W + lag] = (float)(fa - del) * (1.0f - 1e-6f);
   }
+  for (int o = 16; o > 0; o >>= 1) best = fminf(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) redf[threadIdx.x >> 5] = best;
+  __syncthreads();
   if (threadIdx.x == 0) {
-    const int s = (int)(bk.idx / W) - hw, t = (int)(bk.idx % W) - hw;
-    a.shift_out[2 * f] = s;
-    a.shift_out[2 * f + 1] = t;
-    if (a.f_out) a.f_out[f] = __longlong_as_double((long long)bk.f);
-    if (a.flags) a.flags[f] = (uint8_t)(((abs(s) == hw || abs(t) == hw) ? 1 : 0) | (all ? 2 : 0));
-    if (a.qcount) a.qcount[f] = nq;
+    float b = 3.0e38f;
+    for (int k = 0; k < FFT_THREADS / 32; ++k) b = fminf(b, redf[k]);
+    atomicMin(a.ub + f, __float_as_int(fmaxf(b, 0.f)));
   }
+}
+
+// k_fft_score_pick: one block per frame: Q from the lower bounds, exact rescoring, argmin;
+// a.ub[f] is put back to "+inf" for the next call.
+__global__ void __launch_bounds__(1024) k_fft_score_pick(FftScoreArgs a) {
+  __shared__ u64 red[32];
+  __shared__ int qn;
+  __shared__ int qlist[FFT_QCAP];
+  const int64_t f = blockIdx.x;
+  const float thr = __int_as_float(a.ub[f]);
+  if (threadIdx.x == 0) qn = 0;
+  __syncthreads();
+  fft_pick_tail(a, f, a.lb + f * a.g.W * a.g.W, thr, red, &qn, qlist);
+  if (threadIdx.x == 0) a.ub[f] = FFT_UB_INIT;
 }
 
 // ---------------------------------------------------------------- frame energies
@@ -427,8 +517,43 @@ __global__ void __launch_bounds__(1024) k_fft_score(FftScoreArgs a) {
 // (P:32-35): total minus the excluded edge strips plus the doubly excluded corner --
 // the paper's DP of P:35 run in each corner (a (w x w) prefix table per corner, built
 // one quadrant at a time so any w fits in shared memory).  One block per frame.
+// Small batches: the row pass of k_energy_u16 split over blocks (frame f, row band),
+// partial sums into a per-frame scratch [4 hw + 1] (row edges stored, column edges and
+// the total added atomically); k_energy_fin then does the rest per frame and clears it.
+__global__ void __launch_bounds__(256) k_energy_rows(const uint16_t *__restrict__ img, int64_t fstride, int pitch,
+                                                     int mc, int nc, int w, int rpb, u64 *__restrict__ scr) {
+  const int hw = w - 1;
+  const int nb = (mc + rpb - 1) / rpb;
+  const int64_t f = blockIdx.x / nb;
+  const int r0 = (blockIdx.x % nb) * rpb, r1 = min(mc, r0 + rpb);
+  u64 *rowE = scr + f * (4 * hw + 1), *colE = rowE + 2 * hw, *tot = colE + 2 * hw;
+  const uint16_t *A = img + f * fstride;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+  u64 mytot = 0;
+  for (int r = r0 + warp; r < r1; r += nwarp) {
+    u64 rs = 0;
+    const uint16_t *row = A + (int64_t)r * pitch;
+#pragma unroll 4
+    for (int c = lane; c < nc; c += 32) {
+      const u64 v2 = (u64)row[c] * row[c];
+      rs += v2;
+      if (c < hw) atomicAdd(reinterpret_cast<unsigned long long *>(&colE[c]), (unsigned long long)v2);
+      if (c >= nc - hw)
+        atomicAdd(reinterpret_cast<unsigned long long *>(&colE[hw + (nc - 1 - c)]), (unsigned long long)v2);
+    }
+    rs = warp_sum(rs);
+    if (lane == 0) {
+      mytot += rs;
+      if (r < hw) rowE[r] = rs;
+      if (r >= mc - hw) rowE[hw + (mc - 1 - r)] = rs;
+    }
+  }
+  if (lane == 0 && mytot) atomicAdd(reinterpret_cast<unsigned long long *>(tot), (unsigned long long)mytot);
+}
+
 __global__ void __launch_bounds__(1024) k_energy_u16(const uint16_t *__restrict__ img, int64_t fstride, int pitch,
-                                                    int mc, int nc, int w, u64 *__restrict__ ga) {
+                                                    int mc, int nc, int w, u64 *__restrict__ ga,
+                                                    u64 *__restrict__ part) {
   extern __shared__ __align__(16) u64 esm[];
   const int hw = w - 1, W = 2 * w - 1, CS = w * w;
   u64 *rowE = esm;                 // [2 hw]: top rows, bottom rows (from the bottom)
@@ -440,7 +565,15 @@ __global__ void __launch_bounds__(1024) k_energy_u16(const uint16_t *__restrict_
   const uint16_t *A = img + (int64_t)blockIdx.x * fstride;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
   u64 mytot = 0;
-  for (int r = warp; r < mc; r += nwarp) {
+  if (part) {   // the row pass was done by k_energy_rows: take its sums and clear them
+    u64 *pf = part + (int64_t)blockIdx.x * (4 * hw + 1);
+    __syncthreads();
+    for (int k = threadIdx.x; k < 4 * hw + 1; k += blockDim.x) {
+      esm[k < 4 * hw ? k : 4 * hw + CS] = pf[k];
+      pf[k] = 0;
+    }
+  }
+  for (int r = warp; r < (part ? 0 : mc); r += nwarp) {
     u64 rs = 0;
     const bool top = r < hw, bot = r >= mc - hw;
     const uint16_t *row = A + (int64_t)r * pitch;
@@ -458,7 +591,7 @@ __global__ void __launch_bounds__(1024) k_energy_u16(const uint16_t *__restrict_
       if (bot) rowE[hw + (mc - 1 - r)] = rs;
     }
   }
-  if (lane == 0) atomicAdd(tot, mytot);
+  if (lane == 0 && !part) atomicAdd(tot, mytot);
   __syncthreads();
   if (threadIdx.x < 4) {
     u64 *e = (threadIdx.x & 2) ? colE : rowE;

@@ -328,7 +328,13 @@ __device__ __forceinline__ void coarse8(const uint16_t *base, int n, uint32_t (&
 }
 
 template <int L>
-__global__ void __launch_bounds__(256, 4) k_tc_prep(TcPrepArgs a) {
+#ifndef TC_PREP_RPP
+#define TC_PREP_RPP 2
+#endif
+#ifndef TC_PREP_MINB
+#define TC_PREP_MINB 4
+#endif
+__global__ void __launch_bounds__(256, TC_PREP_MINB) k_tc_prep(TcPrepArgs a) {
   const TcGeom &g = a.g;
   extern __shared__ __align__(16) unsigned char smem[];
   const int F = g.F, hw = g.hw, w = g.w, mc = g.mc, nc = g.nc, W = g.W;
@@ -438,27 +444,42 @@ __global__ void __launch_bounds__(256, 4) k_tc_prep(TcPrepArgs a) {
       if (cr >= mc - hw) rowE[f * 2 * hw + hw + (mc - 1 - cr)] = rs;
     }
   };
-  // plane rows pr = warp / F, + nwarp / F, ...; two rows per pass (loads first)
+  // plane rows pr = warp / F, + nwarp / F, ...; TC_PREP_RPP rows per pass (loads first)
   const int pstep = nwarp / F;
-  int npass = 0;
-  for (int pr = warp / F; pr < g.R; pr += 2 * pstep) {
-    if (one_chunk && ++npass == 8) {   // 16 rows since the last flush
+  int nrows = 0;
+  for (int pr0 = warp / F; pr0 < g.R; pr0 += TC_PREP_RPP * pstep) {
+    if (one_chunk && nrows + TC_PREP_RPP > 16) {   // <= 16 rows of squares per flush
       flush_edges();
-      npass = 0;
+      nrows = 0;
     }
-    const int pr2 = pr + pstep;
-    const bool live1 = fi < a.B && pr - hw >= 0 && pr - hw < mc;
-    const bool live2 = fi < a.B && pr2 < g.R && pr2 - hw >= 0 && pr2 - hw < mc;
-    u64 rs1 = 0, rs2 = 0;
+    nrows += TC_PREP_RPP;
+    bool live[TC_PREP_RPP];
+    u64 rs[TC_PREP_RPP];
+#pragma unroll
+    for (int q = 0; q < TC_PREP_RPP; ++q) {
+      const int pr = pr0 + q * pstep;
+      live[q] = fi < a.B && pr < g.R && pr - hw >= 0 && pr - hw < mc;
+      rs[q] = 0;
+    }
     for (int cc = lane; cc < nchunk; cc += 32) {
-      uint32_t P1[4] = {0, 0, 0, 0}, P2[4] = {0, 0, 0, 0};
-      if (live1) coarse8<L>(frame + (int64_t)((pr - hw) << L) * a.n + ((cc * 8) << L), a.n, P1);
-      if (live2) coarse8<L>(frame + (int64_t)((pr2 - hw) << L) * a.n + ((cc * 8) << L), a.n, P2);
-      item(pr, P1, cc, live1, rs1);
-      if (pr2 < g.R) item(pr2, P2, cc, live2, rs2);
+      uint32_t P[TC_PREP_RPP][4];
+#pragma unroll
+      for (int q = 0; q < TC_PREP_RPP; ++q) {
+        const int pr = pr0 + q * pstep;
+        P[q][0] = P[q][1] = P[q][2] = P[q][3] = 0;
+        if (live[q]) coarse8<L>(frame + (int64_t)((pr - hw) << L) * a.n + ((cc * 8) << L), a.n, P[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < TC_PREP_RPP; ++q) {
+        const int pr = pr0 + q * pstep;
+        if (pr < g.R) item(pr, P[q], cc, live[q], rs[q]);
+      }
     }
-    row_done(pr, live1, rs1);
-    if (pr2 < g.R) row_done(pr2, live2, rs2);
+#pragma unroll
+    for (int q = 0; q < TC_PREP_RPP; ++q) {
+      const int pr = pr0 + q * pstep;
+      if (pr < g.R) row_done(pr, live[q], rs[q]);
+    }
   }
   // flush this warp's edge-column and total energies
   if (one_chunk) flush_edges();

@@ -75,6 +75,11 @@ struct moco_plan {
     float2 *twr = nullptr, *twc = nullptr, *Bc = nullptr, *S = nullptr, *P = nullptr;
     u64 *ga = nullptr;
     int *qc = nullptr;
+    u64 *epart = nullptr;       // small batches: row-pass energy partials [cap][4 hw + 1], kept zero
+    float *lb = nullptr;        // small-batch split score: lower bounds [cap][W*W]
+    int *ub = nullptr;          // and min upper bound per frame [cap]
+    cudaStream_t side = nullptr;   // small batches: frame energies beside the FFT
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int64_t cap = 0;
     double eps_rel = 0;
     int smem_rows = 0, smem_cols = 0, smem_score = 0, smem_energy = 0;
@@ -180,8 +185,11 @@ static void plan_free(moco_plan *p) {
   }
   tc_free(&p->tc);
   for (void *q : {(void *)p->fft.twr, (void *)p->fft.twc, (void *)p->fft.Bc, (void *)p->fft.S, (void *)p->fft.P,
-                  (void *)p->fft.ga, (void *)p->fft.qc})
+                  (void *)p->fft.ga, (void *)p->fft.qc, (void *)p->fft.lb, (void *)p->fft.ub, (void *)p->fft.epart})
     if (q) cudaFree(q);
+  if (p->fft.side) cudaStreamDestroy(p->fft.side);
+  if (p->fft.ev_fork) cudaEventDestroy(p->fft.ev_fork);
+  if (p->fft.ev_join) cudaEventDestroy(p->fft.ev_join);
   for (int k = 0; k < 3; ++k) {
     if (p->slot_in[k]) cudaFree(p->slot_in[k]);
     if (p->slot_out[k]) cudaFree(p->slot_out[k]);
@@ -235,8 +243,15 @@ static int fft_init(moco_plan *p) {
   };
   if (!al((void **)&F.twr, Mr * 8) || !al((void **)&F.twc, Mc * 8) || !al((void **)&F.Bc, (size_t)g.Kc * Mr * 8) ||
       !al((void **)&F.S, (size_t)F.cap * g.Kc * g.mcp * 8) || !al((void **)&F.P, (size_t)F.cap * g.W * g.Kc * 8) ||
-      !al((void **)&F.ga, (size_t)F.cap * g.W * g.W * 8) || !al((void **)&F.qc, (size_t)p->cap * sizeof(int)))
+      !al((void **)&F.ga, (size_t)F.cap * g.W * g.W * 8) || !al((void **)&F.qc, (size_t)p->cap * sizeof(int)) ||
+      !al((void **)&F.lb, (size_t)F.cap * g.W * g.W * 4) || !al((void **)&F.ub, (size_t)F.cap * sizeof(int)) ||
+      !al((void **)&F.epart, (size_t)F.cap * (4 * g.hw + 1) * 8))
     return MOCO_ENOMEM;
+  CK(cudaMemset(F.epart, 0, (size_t)F.cap * (4 * g.hw + 1) * 8));
+  CK(cudaMemset(F.ub, 0x7f, (size_t)F.cap * sizeof(int)));   // FFT_UB_INIT
+  CK(cudaStreamCreateWithFlags(&F.side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&F.ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&F.ev_join, cudaEventDisableTiming));
   F.eps_rel = RS_FFT_C * std::ldexp(1.0, -24) * std::log2((double)Mr * (double)Mc);
   F.smem_rows = (Mc + 2 * FFT_ROWS_PAIRS * Mc) * 8;
   F.smem_cols = (Mr + 2 * FFT_COLS * Mr) * 8;
@@ -244,6 +259,7 @@ static int fft_init(moco_plan *p) {
   F.smem_energy = (4 * g.hw + g.w * g.w + 1) * 8;
   if (F.smem_score > 227 * 1024 || F.smem_energy > 227 * 1024) return MOCO_EINVAL;
   CK(cudaFuncSetAttribute(k_fft_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, F.smem_rows));
+  CK(cudaFuncSetAttribute(k_fft_score_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, F.smem_rows));
   CK(cudaFuncSetAttribute(k_fft_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, F.smem_cols));
   CK(cudaFuncSetAttribute(k_fft_score, cudaFuncAttributeMaxDynamicSharedMemorySize, F.smem_score));
   CK(cudaFuncSetAttribute(k_energy_u16, cudaFuncAttributeMaxDynamicSharedMemorySize, F.smem_energy));
@@ -262,8 +278,9 @@ static int fft_set_template(moco_plan *p, cudaStream_t st) {
   const FftGeom &g = F.g;
   const int nrb = (g.mcp / 2 + FFT_ROWS_PAIRS - 1) / FFT_ROWS_PAIRS;
   const int ncb = (g.Kc + FFT_COLS - 1) / FFT_COLS;
-  k_fft_rows<<<nrb, FFT_THREADS, F.smem_rows, st>>>((const uint16_t *)p->tpl[L], 0, p->pitch[L], g, F.twc, F.S);
-  k_fft_cols<<<ncb, FFT_THREADS, F.smem_cols, st>>>(F.S, g, F.twr, F.Bc, nullptr, 1);
+  k_fft_rows<<<nrb, FFT_THREADS, F.smem_rows, st>>>((const uint16_t *)p->tpl[L], 0, p->pitch[L], g, F.twc, F.S,
+                                                    FFT_ROWS_PAIRS);
+  k_fft_cols<<<ncb, FFT_THREADS, F.smem_cols, st>>>(F.S, g, F.twr, F.Bc, nullptr, 1, FFT_COLS);
   CKL("fft_set_template");
   F.tpl_ready = true;
   return MOCO_OK;
@@ -276,22 +293,43 @@ static int launch_fft(moco_plan *p, const void *img, int64_t fstride, int pitch,
   auto &F = p->fft;
   const FftGeom &g = F.g;
   const int L = p->levels;
-  const int nrb = (g.mcp / 2 + FFT_ROWS_PAIRS - 1) / FFT_ROWS_PAIRS;
-  const int ncb = (g.Kc + FFT_COLS - 1) / FFT_COLS;
   for (int64_t b0 = 0; b0 < B; b0 += F.cap) {
     const int64_t nb = std::min<int64_t>(F.cap, B - b0);
     const uint16_t *im = (const uint16_t *)img + b0 * fstride;
-    {
-      ProfScope ps(p, MOCO_K_PREP, st);
-      // small batches (closed loop): a whole SM per frame for the per-frame kernels
-      const int eth = nb < p->nsm ? 1024 : 256;
-      k_energy_u16<<<(unsigned)nb, eth, F.smem_energy, st>>>(im, fstride, pitch, g.mc, g.nc, g.w, F.ga);
+    // small batches (closed loop): a whole SM per frame for the per-frame kernels, the
+    // frame energies on a side stream beside the FFT, the score step split over blocks
+    const bool small = nb * (((g.W + 1) / 2 + FFT_ROWS_PAIRS - 1) / FFT_ROWS_PAIRS) <= p->nsm;
+    // transforms per block: fewer when the batch alone cannot fill the SMs
+    const int rper = small ? std::max(1, std::min(FFT_ROWS_PAIRS, (int)(nb * (g.mcp / 2) / p->nsm))) : FFT_ROWS_PAIRS;
+    const int cper = small ? std::max(1, std::min(FFT_COLS, (int)(nb * g.Kc / p->nsm))) : FFT_COLS;
+    const int sper = small ? std::max(1, std::min(FFT_ROWS_PAIRS, (int)(nb * ((g.W + 1) / 2) / p->nsm))) : FFT_ROWS_PAIRS;
+    const int nrb = (g.mcp / 2 + rper - 1) / rper, ncb = (g.Kc + cper - 1) / cper;
+    const int npb = ((g.W + 1) / 2 + sper - 1) / sper;
+    cudaStream_t se = st;
+    if (small) {
+      CK(cudaEventRecord(F.ev_fork, st));
+      CK(cudaStreamWaitEvent(F.side, F.ev_fork, 0));
+      se = F.side;
     }
+    {
+      ProfScope ps(p, MOCO_K_PREP, se);
+      const int eth = nb < p->nsm ? 1024 : 256;
+      if (small) {   // row pass over ~all SMs, then the per-frame remainder
+        const int rpb = std::max<int>(8, (int)((nb * g.mc + p->nsm - 1) / p->nsm));
+        k_energy_rows<<<(unsigned)(nb * ((g.mc + rpb - 1) / rpb)), 256, 0, se>>>(im, fstride, pitch, g.mc, g.nc,
+                                                                                  g.w, rpb, F.epart);
+        k_energy_u16<<<(unsigned)nb, eth, F.smem_energy, se>>>(im, fstride, pitch, g.mc, g.nc, g.w, F.ga, F.epart);
+      } else {
+        k_energy_u16<<<(unsigned)nb, eth, F.smem_energy, se>>>(im, fstride, pitch, g.mc, g.nc, g.w, F.ga, nullptr);
+      }
+    }
+    if (small) CK(cudaEventRecord(F.ev_join, se));
     {
       ProfScope ps(p, MOCO_K_COARSE, st);
-      k_fft_rows<<<(unsigned)(nb * nrb), FFT_THREADS, F.smem_rows, st>>>(im, fstride, pitch, g, F.twc, F.S);
-      k_fft_cols<<<(unsigned)(nb * ncb), FFT_THREADS, F.smem_cols, st>>>(F.S, g, F.twr, F.Bc, F.P, 0);
+      k_fft_rows<<<(unsigned)(nb * nrb), FFT_THREADS, F.smem_rows, st>>>(im, fstride, pitch, g, F.twc, F.S, rper);
+      k_fft_cols<<<(unsigned)(nb * ncb), FFT_THREADS, F.smem_cols, st>>>(F.S, g, F.twr, F.Bc, F.P, 0, cper);
     }
+    if (small) CK(cudaStreamWaitEvent(st, F.ev_join, 0));
     FftScoreArgs a;
     a.P = F.P; a.twc = F.twc; a.img = im; a.fstride = fstride; a.pitch = pitch;
     a.tpl = (const uint16_t *)p->tpl[L]; a.tpitch = p->pitch[L];
@@ -301,11 +339,17 @@ static int launch_fft(moco_plan *p, const void *img, int64_t fstride, int pitch,
     a.flags = flags ? flags + b0 : nullptr;
     a.qcount = qcount ? qcount + b0 : F.qc + b0;
     a.h_out = h_out ? h_out + b0 * g.W * g.W : nullptr;
+    a.lb = F.lb; a.ub = F.ub;
     {
       ProfScope ps(p, MOCO_K_SCORE, st);
-      k_fft_score<<<(unsigned)nb, nb < p->nsm ? 1024 : FFT_THREADS, F.smem_score, st>>>(a);
+      if (small) {
+        k_fft_score_rows<<<(unsigned)(nb * npb), FFT_THREADS, F.smem_rows, st>>>(a, sper);
+        k_fft_score_pick<<<(unsigned)nb, 1024, 0, st>>>(a);
+      } else {
+        k_fft_score<<<(unsigned)nb, nb < p->nsm ? 1024 : FFT_THREADS, F.smem_score, st>>>(a);
+      }
     }
-    p->launches += 4;
+    p->launches += small ? 6 : 4;
     CKL("fft path");
   }
   return MOCO_OK;
