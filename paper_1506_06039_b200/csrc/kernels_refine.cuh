@@ -388,9 +388,46 @@ template <int SH>
 __device__ __forceinline__ void pick_apply_rows(const uint16_t *A, uint16_t *O, int pitch, int s, int t, int ml,
                                                 int nl, int r0, int r1) {
   // output chunk (i, 8-column group j0): source samples a[i+s][j0+t .. j0+t+7]; the two
-  // aligned vectors at ab = j0 + t - SH cover them; out-of-frame samples are 0
-  const int groups = nl >> 3, total = (r1 - r0) * groups;
+  // aligned vectors at ab = j0 + t - SH cover them (ab is a multiple of 8, so each vector
+  // lies wholly inside or wholly outside the row); out-of-frame samples are 0
+  const int groups = nl >> 3;
   constexpr int U = 4;
+  if (groups <= (int)blockDim.x) {
+    // a thread keeps one column group and walks rows: no per-element division, the
+    // column tests once per thread
+    const int rstep = blockDim.x / groups;
+    if ((int)threadIdx.x >= rstep * groups) return;
+    const int jj = (threadIdx.x % groups) * 8, ab = jj + t - SH;
+    const bool lok = ab >= 0 && ab + 8 <= nl, hok = SH && ab + 8 >= 0 && ab + 16 <= nl;
+    const uint16_t *src = A + ab;
+    uint16_t *dst = O + jj;
+    for (int i0 = r0 + (int)threadIdx.x / groups; i0 < r1; i0 += U * rstep) {
+      uint4 lo[U], hi[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int i = i0 + k * rstep, r = i + s;
+        const bool rok = i < r1 && r >= 0 && r < ml;
+        const uint16_t *row = src + (int64_t)(rok ? r : 0) * pitch;
+        lo[k] = (rok && lok) ? __ldcs(reinterpret_cast<const uint4 *>(row)) : make_uint4(0, 0, 0, 0);
+        hi[k] = (rok && hok) ? __ldcs(reinterpret_cast<const uint4 *>(row + 8)) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int i = i0 + k * rstep;
+        if (i >= r1) continue;
+        const uint32_t w[8] = {lo[k].x, lo[k].y, lo[k].z, lo[k].w, hi[k].x, hi[k].y, hi[k].z, hi[k].w};
+        uint32_t o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int e2 = SH + 2 * q;
+          o[q] = (e2 & 1) ? __funnelshift_r(w[e2 >> 1], w[(e2 >> 1) + 1], 16) : w[e2 >> 1];
+        }
+        __stcs(reinterpret_cast<uint4 *>(dst + (int64_t)i * nl), make_uint4(o[0], o[1], o[2], o[3]));
+      }
+    }
+    return;
+  }
+  const int total = (r1 - r0) * groups;
   for (int e0 = threadIdx.x; e0 < total; e0 += U * blockDim.x) {
     uint4 lo[U], hi[U];
     int ii[U], jj[U];
