@@ -312,6 +312,15 @@ __device__ __forceinline__ void coarse8(const uint16_t *base, int n, uint32_t (&
         const uint4 u = __ldcs(reinterpret_cast<const uint4 *>(base + (int64_t)dy * n + q * 8));
         s[4 * q + 0] += u.x; s[4 * q + 1] += u.y; s[4 * q + 2] += u.z; s[4 * q + 3] += u.w;   // halves < 2^14: no carry
       }
+    if constexpr (L == 1) {
+      // coarse values k, k+1 are the half sums of words s[k], s[k+1]: gather the low
+      // halves and the high halves of the two words with one byte-permute each and add
+      // (each half < 2^14: no carry into the other half)
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        P[k] = __byte_perm(s[2 * k], s[2 * k + 1], 0x5410) + __byte_perm(s[2 * k], s[2 * k + 1], 0x7632);
+      return;
+    }
     // fold: coarse value k = both halves of its bs/2 raw pair words
     uint32_t c[8];
     constexpr int wpc = bs / 2;
