@@ -1,37 +1,48 @@
-// kernels_rtc.cuh -- S5 refine sums on the 5th-gen tensor cores (tcgen05, kind::i8).
+// kernels_rtc.cuh -- S5 refine sums on the 5th-gen tensor cores (tcgen05, kind::i8),
+// conversion-free: the raw u16 frame rows ARE the A operand.
 //
 // The +-1 refinement at level l needs, per frame f and each of
 // the nine candidates (u, v) around the doubled coarse shift (S, T) = 2 s_{l+1},
 //   H_f(u,v)  = sum_{i<ml, j<nl} a_f[i+S+u][j+T+v] b[i][j]        (cross term)
 //   GA_f(u,v) = sum_{i<ml, j<nl} a_f[i+S+u][j+T+v]^2              (frame energy)
-// with a_f = 0 outside the frame.  Substituting p = (i+u+1, j+v+1) on the extended grid
-// P = [0, ml+2) x [0, nl+2):
-//   H_f(c) = sum_p A_f[p] Bt_c[p],   A_f[p] = a_f[p_r+S-1][p_c+T-1],
-//                                    Bt_c[p] = b[p_r-u'][p_c-v'],  c = 3u'+v', u' = u+1
-// -- one GEMM D[(frame, part)][(c, part)] = sum_p over the pixels p, for a batch of 64
-// frames: M = 128 rows (7-bit hi parts of 64 frames, then lo parts), N = 32 columns
-// (hi parts of the nine shifted templates, then lo parts; 14 zero columns), K = the
-// pixels in 32-column steps.  The exact integer recombination
-//   H = 2^14 D[hi][hi] + 2^7 (D[hi][lo] + D[lo][hi]) + D[lo][lo]
-// is the same hi/lo split the coarse search uses (values < 2^14, kernels_tc.cuh).
-// int32 accumulators are split into `nsets` row classes (p_r mod nsets) so no
-// accumulator sums more than 2^31 / 127^2 products.  GA comes from the converter
-// warps, which touch every sample once anyway: per-row totals and the four edge
-// columns, binned by row class (rows 0, 1, ml, ml+1, interior), then combined per
-// candidate in the epilogue.
+// with a_f = 0 outside the frame.  On the extended grid (p_r, p_c) in [0, ml+2) x
+// [0, nl+2), A_f[p_r][p_c] = a_f[p_r+S-1][p_c+T-1], and with u' = u+1, v' = v+1:
+//   H_f(u',v') = sum_{i<ml} sum_{p_c} A_f[i+u'][p_c] b[i][p_c-v'].
 //
-// Per CTA (64 frames x a part of the rows), warp-specialised; a stage is one grid row
-// p_r x a chunk of 7 K-steps:
-//   warp 0   one bulk copy per stage of its 7 template B tiles (precomputed table,
-//            L2-resident) into the operand stage;
-//   warp 1   MMA issuer: 7 MMAs (M128 N32 K32) per stage into accumulator set p_r mod nsets;
-//   warps 2-9 converters, 8 frames each: their raw rows (frame row p_r+S_f-1, 240
-//            columns from the 8-aligned column below p_c+T_f-1) by 16-byte LDGSTS with
-//            zero fill, RTC_NSR-1 stages ahead; then u16 -> int8 hi/lo A tiles in the
-//            core-matrix layout, and the GA bins.  (One TMA box per frame row was
-//            tried first: 64 small boxes per stage left the kernel at ~1.3 TB/s.)
-// Epilogue (warps 2-5, one TMEM lane each): sets summed in 64 bits, parts recombined,
-// atomically added to acc[f][0..17] (the layout k_refine_pick reads).
+// A little-endian u16 row is an int8 row of interleaved (low byte, high byte) pairs.
+// Fed to tcgen05.mma.kind::i8 unchanged, with three B rows per candidate
+//   type a: (b_lo, 0)   -> sum a_lo b_lo                  (weight 1)
+//   type b: (b_hi, b_lo)-> sum a_lo b_hi + a_hi b_lo       (weight 2^8)
+//   type c: (0, b_hi)   -> sum a_hi b_hi                  (weight 2^16)
+// the cross term is H = D_a + 2^8 D_b + 2^16 D_c exactly (values < 2^14: bytes <= 255,
+// all products of u8 x u8 in int32 accumulators) -- no per-pixel work for H at all.
+//
+// MMA shape: M = 128 = 16 frames x 8 consecutive grid rows (one core-matrix group per
+// frame: the A tiles are TMA boxes {8 px, rows, 8-px chunks} through a tensor map whose
+// dimensions are reordered to {8 columns, rows, column chunks, frames}, i.e. exactly the
+// K-major core-matrix layout, 16 B per row), N = 64 = 6 template rows x 3 column shifts
+// v' x 3 types (54 used), K = 32 bytes = 16 pixels.  A row group G (template rows 6G..6G+5)
+// needs grid rows 6G..6G+7; the next group's window starts 6 rows (96 B) further.  In D,
+// entry (frame, r_rel; t_rel, v', type) is useful when u' = r_rel - t_rel is 0, 1 or 2.
+// A frame's box starts at the 8-aligned column below T-1, so the grid column of box
+// element e is e - o with o = (T-1) mod 8 (odd: T is even); frames are bucketed by o
+// (k_rtc_bucket) and the template table holds one pre-shifted copy per class.
+// int32 accumulators alternate between `nsets` TMEM sets by row group.
+// GA is the only per-pixel CUDA-core work: 8 warps sum a^2 from the staged boxes (grid
+// rows binned by class 0, 1, ml, ml+1, interior; the four edge columns kept apart) and
+// the epilogue combines the bins per candidate.
+//
+// Work unit: a CTA takes 16 frames of one alignment class x a range of row groups; a
+// stage = 4 row groups (26 grid rows) x 4 K-steps (8 chunks):
+//   warp 0    TMA: one box {8, 26, 8} per frame + one bulk copy of B tiles per row group;
+//   warp 1    MMA issuer: 4 x 4 MMAs (M128 N64 K32) per stage;
+//   warps 2-9 GA from the same staged boxes;
+// double-buffered stages; epilogue: TMEM -> per-row partial H -> 8-lane shuffle sums.
+// Opt-in (MOCO_RTC=1): bit-exact, 616 us per 2 368 C2 frames against 584 us for the
+// CUDA-core kernel.  The limiter is the A-tile TMA: the reordered tensor map makes the
+// box's inner dimension 16 B, so a stage is ~3 300 16-byte row requests (557 us with the
+// GA pass removed); a SWIZZLE_128B K-major layout (128-byte rows) is the next step.
+// DESIGN.md section 11.
 #pragma once
 
 #include <cmath>
@@ -39,129 +50,207 @@
 namespace moco {
 
 #ifdef MOCO_RTC_TIMING
+__device__ __forceinline__ uint64_t gtimer_rt() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define gtimer gtimer_rt
+#endif
+#ifdef MOCO_RTC_TIMING
 #define RT_T(...) __VA_ARGS__
 #else
 #define RT_T(...)
 #endif
 
-constexpr int RTC_F = 64;                 // frames per CTA
-constexpr int RTC_KC = 7;                 // K-steps (32 grid columns) per stage
-constexpr int RTC_BOXW = 240;             // raw box width (u16): 32*KC + 7 misalignment
-#ifndef RTC_NSR
-#define RTC_NSR 4
+constexpr int RTC_F = 16;                  // frames per CTA (core-matrix groups of M)
+constexpr int RTC_RG = 4;                  // row groups (6 template rows each) per stage
+constexpr int RTC_R = 6 * RTC_RG + 2;      // grid rows per stage box
+#ifndef RTC_KSTEPS
+#define RTC_KSTEPS 4   // measured: 4 K-steps x 2 stages 616 us, 2 x 4 680 us, 2 x 5 681 us (C2, 2 368 frames)
 #endif
-#ifndef RTC_NSO
-#define RTC_NSO 2
+#ifndef RTC_NSTAGE
+#define RTC_NSTAGE 2
 #endif
-constexpr int RTC_NS = RTC_NSR;           // raw ring depth
-constexpr int RTC_NO = RTC_NSO;           // operand ring depth
-constexpr int RTC_CW = 8;                 // converter warps
+constexpr int RTC_KS = RTC_KSTEPS;         // K-steps (16 pixels) per stage
+constexpr int RTC_NST = RTC_NSTAGE;        // ring depth
+constexpr int RTC_CH = 2 * RTC_KS;         // 8-pixel chunks per stage box
+constexpr int RTC_CW = 16;                 // GA warps
 constexpr int RTC_THREADS = 32 * (2 + RTC_CW);
-constexpr int RTC_RAW_SLOT = 512;         // bytes per frame in a raw stage (480 used, 128-B aligned)
-constexpr int RTC_RAW_STAGE = RTC_F * RTC_RAW_SLOT;
-constexpr int RTC_A_STAGE = RTC_KC * 4096;   // A tiles: 128 rows x 32 B per K-step
-constexpr int RTC_B_STAGE = RTC_KC * 1024;   // B tiles: 32 rows x 32 B per K-step
-constexpr int RTC_OP_STAGE = RTC_A_STAGE + RTC_B_STAGE;
-constexpr int RTC_BINS_OFF = 1024;        // [64][5 row classes][5] u64
-constexpr int RTC_RAW_OFF = 14336;
-constexpr int RTC_OP_OFF = RTC_RAW_OFF + RTC_NS * RTC_RAW_STAGE;
-constexpr int RTC_SMEM = RTC_OP_OFF + RTC_NO * RTC_OP_STAGE + 1024;   // + alignment slack
+constexpr int RTC_SLOT = RTC_CH * RTC_R * 16;                 // bytes per frame box (multiple of 128)
+constexpr int RTC_RAW = RTC_F * RTC_SLOT;                     // A stage
+constexpr int RTC_BT = 2048;                                  // one B tile: 64 rows x 32 B
+constexpr int RTC_STAGE = RTC_RAW + RTC_RG * RTC_KS * RTC_BT;
+constexpr int RTC_BINS_OFF = 1024;         // [16][5 row classes][5] u64
+constexpr int RTC_ST_OFF = 5120;            // after the bins (16 x 25 x 8 = 3200 B)
+constexpr int RTC_SMEM = RTC_ST_OFF + RTC_NST * RTC_STAGE + 1024;  // + alignment slack
+static_assert(RTC_SLOT % 128 == 0, "TMA destinations must be 128-byte aligned");
+static_assert(RTC_BINS_OFF + RTC_F * 25 * 8 <= RTC_ST_OFF, "bins overlap the stages");
+static_assert(RTC_SMEM <= 227 * 1024, "shared memory");
+static_assert(RTC_CH % 4 == 0 && RTC_NST * 2 * 8 + 8 <= 128, "chunk lanes, barrier space");
 
 struct RtcGeom {
   int ml, nl;
-  int nsteps;   // K-steps per grid row: ceil((nl+2)/32)
-  int nch;      // stages per grid row: ceil(nsteps/KC)
-  int nsets;    // accumulator sets (power of 2, <= 16)
+  int nk;       // K-steps per grid row: ceil((nl + 2 + 7) / 16)
+  int nstrips;  // ceil(nk / KS)
+  int ng;       // row groups: ceil(ml / 6)
+  int nsets;    // accumulator sets (power of 2, <= 8: 64 TMEM columns each)
 };
 
 inline bool rtc_make(RtcGeom *g, int ml, int nl, int vb) {
-  if (vb > 14 || ml < 4 || nl < 8 || nl % 8 != 0) return false;
+  if (vb > 14 || ml < 6 || nl < 8 || nl % 8 != 0) return false;
   g->ml = ml;
   g->nl = nl;
-  g->nsteps = (nl + 2 + 31) / 32;
-  g->nch = (g->nsteps + RTC_KC - 1) / RTC_KC;
-  const double per_row = (double)(nl + 2) * 127.0 * 127.0;
+  g->nk = (nl + 2 + 7 + 15) / 16;
+  g->nstrips = (g->nk + RTC_KS - 1) / RTC_KS;
+  g->ng = (ml + 5) / 6;
+  // one D entry adds, per row group, nk*16 products of bytes (type a: <= 255*255)
+  const double per_group = (double)g->nk * 16.0 * 255.0 * 255.0;
   int ns = 1;
-  while (ns <= 16 && std::ceil((double)(ml + 2) / ns) * per_row >= 2147483648.0) ns <<= 1;
-  if (ns > 16) return false;
+  while (ns <= 8 && std::ceil((double)g->ng / ns) * per_group >= 2147483648.0) ns <<= 1;
+  if (ns > 8) return false;
   g->nsets = ns;
   return true;
 }
+inline size_t rtc_table_bytes(const RtcGeom &g) { return (size_t)4 * g.ng * g.nk * RTC_BT; }
 
-// Template candidate tiles, one per (grid row p_r, K-step k): rows n = pb*16 + c
-// (c < 9: part pb of Bt_c, c >= 9: zero), K-major core matrices, LBO 512 / SBO 128.
-__global__ void k_rtc_table(const uint16_t *__restrict__ b, int pitch, int ml, int nl, int nsteps, uint8_t *tab) {
-  const int64_t total = (int64_t)(ml + 2) * nsteps * 1024;
+// B tiles per (class c: o = 2c+1, row group G, K-step j): row n = (t*3 + v')*3 + type
+// (54..63 zero), byte k of the step = pixel k>>1, byte k&1 (0: low, 1: high) of A; the
+// pixel's grid column is 16j + (k>>1) - o.  Layout [half][64 rows][16 B] (LBO 1024, SBO 128).
+__global__ void k_rtc_table(const uint16_t *__restrict__ b, int pitch, int ml, int nl, int ng, int nk, uint8_t *tab) {
+  const int64_t total = (int64_t)4 * ng * nk * RTC_BT;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t tile = e >> 10;
-    const int off = (int)(e & 1023);
-    const int pr = (int)(tile / nsteps), k = (int)(tile % nsteps);
-    const int half = off >> 9, r = off & 511;
-    const int n = (r >> 7) * 8 + ((r & 127) >> 4), x = half * 16 + (r & 15);
-    const int pb = n >> 4, c = n & 15;
+    const int64_t tile = e / RTC_BT;
+    const int off = (int)(e % RTC_BT);
+    const int c = (int)(tile / ((int64_t)ng * nk)), rem = (int)(tile % ((int64_t)ng * nk));
+    const int G = rem / nk, j = rem % nk;
+    const int half = off >> 10, n = (off & 1023) >> 4, kb = off & 15;
+    const int k = half * 16 + kb;
     uint8_t v = 0;
-    if (c < 9) {
-      const int i = pr - c / 3, j = 32 * k + x - c % 3;
-      if (i >= 0 && i < ml && j >= 0 && j < nl) {
-        const uint32_t val = b[(int64_t)i * pitch + j];
-        v = (uint8_t)(pb == 0 ? (val >> 7) : (val & 127u));
+    if (n < 54) {
+      const int tv = n / 3, type = n % 3, t = tv / 3, vp = tv % 3;
+      const int i = 6 * G + t, pc = 16 * j + (k >> 1) - (2 * c + 1), jc = pc - vp;
+      if (i < ml && jc >= 0 && jc < nl) {
+        const uint32_t bv = b[(int64_t)i * pitch + jc];
+        const uint32_t lo = bv & 255u, hi = bv >> 8;
+        const int byte = k & 1;
+        v = (uint8_t)(type == 0 ? (byte ? 0u : lo) : type == 1 ? (byte ? lo : hi) : (byte ? hi : 0u));
       }
     }
     tab[e] = v;
   }
 }
 
+// Frames of a batch bucketed by alignment class o = (T-1) mod 8 in {1,3,5,7}:
+// meta[0..3] = class counts, meta[4..8] = first CTA group of each class (prefix of
+// ceil(count/16)); perm = frame indices, class-major.  One block.
+__global__ void __launch_bounds__(1024) k_rtc_bucket(const int32_t *__restrict__ shift_in, int B, int *perm,
+                                                     int *meta) {
+  __shared__ int cnt[4], base[4], fill[4];
+  if (threadIdx.x < 4) { cnt[threadIdx.x] = 0; fill[threadIdx.x] = 0; }
+  __syncthreads();
+  for (int f = threadIdx.x; f < B; f += blockDim.x) atomicAdd(&cnt[((2 * shift_in[2 * f + 1] - 1) & 7) >> 1], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int b0 = 0, g0 = 0;
+    for (int c = 0; c < 4; ++c) {
+      base[c] = b0;
+      meta[c] = cnt[c];
+      meta[4 + c] = g0;
+      b0 += cnt[c];
+      g0 += (cnt[c] + RTC_F - 1) / RTC_F;
+    }
+    meta[8] = g0;
+  }
+  __syncthreads();
+  for (int f = threadIdx.x; f < B; f += blockDim.x) {
+    const int c = ((2 * shift_in[2 * f + 1] - 1) & 7) >> 1;
+    perm[base[c] + atomicAdd(&fill[c], 1)] = f;
+  }
+}
+
+__device__ __forceinline__ void tma_load4(void *dst, const CUtensorMap *tm, int c0, int c1, int c2, int c3,
+                                          uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+      "%5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// u16 frames [frames][rows][cols] (row pitch, frame stride in elements) seen as the 4-D
+// tensor {8 columns, rows, cols/8 chunks, frames} with strides {pitch, 16 B, fstride}: a
+// box {8, R, C, 1} lands as [chunk][row][16 B], the K-major core-matrix layout; zero
+// fill outside (negative chunks and rows included).
+inline bool tmap_u16_chunks(CUtensorMap *tm, const void *base, int cols, int rows, int64_t frames, int pitch,
+                            int64_t fstride, int box_rows, int box_chunks) {
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[4] = {8, (cuuint64_t)rows, (cuuint64_t)(cols / 8), (cuuint64_t)frames};
+  const cuuint64_t strides[3] = {(cuuint64_t)pitch * 2, 16, (cuuint64_t)fstride * 2};
+  const cuuint32_t box[4] = {8, (cuuint32_t)box_rows, (cuuint32_t)box_chunks, 1};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, const_cast<void *>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 struct RtcArgs {
-  const uint16_t *img;      // level-l frames
-  int64_t fstride;          // elements between frames
-  int pitch;                // elements between rows
-  const uint8_t *tab;       // [ml+2][nsteps][1024]
+  const uint8_t *tab;       // rtc_table_bytes
   u64 *acc;                 // [B][18]: H for the nine candidates, then GA (atomically added)
   const int32_t *shift_in;  // [B][2] at level l+1
+  const int *perm;          // [B] class-major frame order
+  const int *meta;          // k_rtc_bucket output
   int B;
-  int parts;                // row parts per 64-frame group
-  int rows_per_part;
+  int parts;                // row-group ranges per 16-frame group
+  int groups_per_part;      // multiple of RTC_RG
   RtcGeom g;
 };
 
-__device__ __forceinline__ void rtc_stage(const RtcGeom &g, int r0, int i, int &pr, int &k0, int &kc) {
-  pr = r0 + i / g.nch;
-  k0 = (i % g.nch) * RTC_KC;
-  kc = min(RTC_KC, g.nsteps - k0);
-}
-
-__global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(RtcArgs a) {
+__global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_constant__ CUtensorMap tmF, RtcArgs a) {
   extern __shared__ __align__(1024) unsigned char rtc_raw[];
   unsigned char *smem = rtc_raw + ((1024u - (smem_u32(rtc_raw) & 1023u)) & 1023u);
-  uint64_t *afull = reinterpret_cast<uint64_t *>(smem), *aempty = afull + RTC_NO;
-  uint64_t *done = aempty + RTC_NO;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem), *empty = full + RTC_NST, *done = full + 2 * RTC_NST;
   uint32_t *holder = reinterpret_cast<uint32_t *>(smem + 128);
-  int *Ssh = reinterpret_cast<int *>(smem + 256), *Tsh = reinterpret_cast<int *>(smem + 512);
+  int *Ssh = reinterpret_cast<int *>(smem + 256), *Tsh = reinterpret_cast<int *>(smem + 320);
+  int *Fid = reinterpret_cast<int *>(smem + 384);
   u64 *bins = reinterpret_cast<u64 *>(smem + RTC_BINS_OFF);
-  unsigned char *raw = smem + RTC_RAW_OFF, *ops = smem + RTC_OP_OFF;
+  unsigned char *stg = smem + RTC_ST_OFF;
   const RtcGeom &g = a.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int grp = blockIdx.x / a.parts, part = blockIdx.x % a.parts;
-  const int f0 = grp * RTC_F, nf = min(RTC_F, a.B - f0);
-  const int r0 = part * a.rows_per_part, r1 = min(g.ml + 2, r0 + a.rows_per_part);
-  const int nstage = (r1 - r0) * g.nch;
-  const int nsets_used = min(g.nsets, r1 - r0);
+  // (class, group in class, part) of this CTA
+  const int gidx = blockIdx.x / a.parts, part = blockIdx.x % a.parts;
+  if (gidx >= a.meta[8]) return;
+  int cls = 0;
+  while (cls < 3 && gidx >= a.meta[5 + cls]) ++cls;
+  const int gic = gidx - a.meta[4 + cls];
+  int cbase = 0;
+  for (int c = 0; c < cls; ++c) cbase += a.meta[c];
+  const int f0 = cbase + gic * RTC_F, nf = min(RTC_F, a.meta[cls] - gic * RTC_F);
+  const int o = 2 * cls + 1;
+  const int G0 = part * a.groups_per_part, G1 = min(g.ng, G0 + a.groups_per_part);
+  const int nblk = (G1 - G0 + RTC_RG - 1) / RTC_RG;   // row-group blocks (stages per strip)
+  const int nstage = max(0, nblk) * g.nstrips;
+  const int tcols = max(64, 64 * g.nsets);
+  RT_T(const uint64_t t_beg = gtimer(); uint64_t w_a = 0, w_b = 0; uint64_t t0;)
 
   for (int k = tid; k < RTC_F * 25; k += RTC_THREADS) bins[k] = 0;
   if (tid < RTC_F) {
-    int S = 0, T = 0;
+    int S = 0, T = 0, fi = -1;
     if (tid < nf) {
-      S = 2 * a.shift_in[2 * (f0 + tid)];
-      T = 2 * a.shift_in[2 * (f0 + tid) + 1];
+      fi = a.perm[f0 + tid];
+      S = 2 * a.shift_in[2 * fi];
+      T = 2 * a.shift_in[2 * fi + 1];
     }
     Ssh[tid] = S;
     Tsh[tid] = T;
+    Fid[tid] = fi;
   }
-  if (warp == 1) tmem_alloc(holder, 32 * g.nsets);
+  if (warp == 1) tmem_alloc(holder, tcols);
   if (tid == 0) {
-    for (int s = 0; s < RTC_NO; ++s) {
-      mbar_init(&afull[s], RTC_CW + 1);
-      mbar_init(&aempty[s], 1);
+    for (int s = 0; s < RTC_NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1 + RTC_CW);
     }
     mbar_init(done, 1);
     fence_mbar_init();
@@ -172,216 +261,227 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(RtcArgs a) {
   const uint32_t taddr = *holder;
 
   if (warp == 0) {
-    // ---------------- loads
+    // ---------------- loads: one box per frame, B tiles per row group
     for (int i = 0; i < nstage; ++i) {
-      int pr, k0, kc;
-      rtc_stage(g, r0, i, pr, k0, kc);
-      const int so = i % RTC_NO, ro = i / RTC_NO;
-      if (ro > 0) mbar_wait(&aempty[so], (ro - 1) & 1);
-      if (lane == 0) {
-        mbar_arrive_expect_tx(&afull[so], (uint32_t)(kc * 1024));
-        bulk_g2s(ops + so * RTC_OP_STAGE + RTC_A_STAGE, a.tab + ((int64_t)pr * g.nsteps + k0) * 1024,
-                 (uint32_t)(kc * 1024), &afull[so]);
+      const int s = i % RTC_NST, rnd = i / RTC_NST;
+      const int gb = G0 + (i / g.nstrips) * RTC_RG, j0 = (i % g.nstrips) * RTC_KS;
+      const int ngr = min(RTC_RG, G1 - gb), kc = min(RTC_KS, g.nk - j0);
+      RT_T(t0 = gtimer();)
+      if (rnd > 0) mbar_wait(&empty[s], (rnd - 1) & 1);
+      RT_T(w_a += gtimer() - t0;)
+      if (lane == 0)
+        mbar_arrive_expect_tx(&full[s], (uint32_t)(nf * RTC_SLOT + ngr * kc * RTC_BT));
+      __syncwarp();
+      unsigned char *st = stg + s * RTC_STAGE;
+      if (lane < nf) {
+        const int xc = ((Tsh[lane] - 1) >> 3) + 2 * j0;   // first 8-px chunk (floor for negatives)
+        tma_load4(st + lane * RTC_SLOT, &tmF, 0, 6 * gb + Ssh[lane] - 1, xc, Fid[lane], &full[s]);
       }
+      if (lane == 0)
+        for (int q = 0; q < ngr; ++q)
+          bulk_g2s(st + RTC_RAW + q * RTC_KS * RTC_BT,
+                   a.tab + (((int64_t)cls * g.ng + gb + q) * g.nk + j0) * RTC_BT, (uint32_t)(kc * RTC_BT),
+                   &full[s]);
       __syncwarp();
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer
-    const uint32_t idesc = idesc_i8(128, 32);
-    const uint64_t ad0 = umma_desc(smem_u32(ops), 2048, 128);
-    const uint64_t bd0 = umma_desc(smem_u32(ops + RTC_A_STAGE), 512, 128);
+    const uint32_t idesc = idesc_i8(128, 64);
+    const uint64_t ad0 = umma_desc(smem_u32(stg), RTC_R * 16, RTC_SLOT);
+    const uint64_t bd0 = umma_desc(smem_u32(stg + RTC_RAW), 1024, 128);
     const uint32_t ahi = (uint32_t)(ad0 >> 32), bhi = (uint32_t)(bd0 >> 32);
     for (int i = 0; i < nstage; ++i) {
-      const int s = i % RTC_NO, rnd = i / RTC_NO;
-      int pr, k0, kc;
-      rtc_stage(g, r0, i, pr, k0, kc);
-      mbar_wait(&afull[s], rnd & 1);
+      const int s = i % RTC_NST, rnd = i / RTC_NST;
+      const int gb = G0 + (i / g.nstrips) * RTC_RG, j0 = (i % g.nstrips) * RTC_KS;
+      const int ngr = min(RTC_RG, G1 - gb), kc = min(RTC_KS, g.nk - j0);
+      RT_T(t0 = gtimer();)
+      mbar_wait(&full[s], rnd & 1);
+      RT_T(w_a += gtimer() - t0;)
       tc_fence_after();
-      const int rr = pr - r0;
-      const uint32_t d = taddr + (uint32_t)((rr & (g.nsets - 1)) * 32);
-      const bool first = rr < g.nsets && k0 == 0;
-      const uint32_t alo = (uint32_t)ad0 + (uint32_t)(s * RTC_OP_STAGE >> 4);
-      const uint32_t blo = (uint32_t)bd0 + (uint32_t)(s * RTC_OP_STAGE >> 4);
-      for (int k = 0; k < kc; ++k)
-        mma_i8_elect(d, alo + (uint32_t)(k * 4096 >> 4), ahi, blo + (uint32_t)(k * 1024 >> 4), bhi, idesc,
-                     (first && k == 0) ? 0u : 1u);
-      mma_commit_elect(&aempty[s]);
+      const uint32_t alo = (uint32_t)ad0 + (uint32_t)(s * RTC_STAGE >> 4);
+      const uint32_t blo = (uint32_t)bd0 + (uint32_t)(s * RTC_STAGE >> 4);
+      for (int q = 0; q < ngr; ++q) {
+        const int G = gb + q, Gr = G - G0;
+        const uint32_t d = taddr + (uint32_t)((G & (g.nsets - 1)) * 64);
+        for (int k = 0; k < kc; ++k) {
+          const bool first = Gr < g.nsets && j0 == 0 && k == 0;
+          // A: chunks 2k, 2k+1 (LBO = one chunk column), rows 6q .. 6q+7 of every frame box
+          mma_i8_elect(d, alo + (uint32_t)((2 * k * RTC_R * 16 + 6 * q * 16) >> 4), ahi,
+                       blo + (uint32_t)((q * RTC_KS + k) * RTC_BT >> 4), bhi, idesc, first ? 0u : 1u);
+        }
+      }
+      mma_commit_elect(&empty[s]);
       __syncwarp();
     }
     mma_commit_elect(done);
     __syncwarp();
   } else {
-    // ---------------- converters: lane = (frame f of the warp's 8, K-half phase kq)
-    const int cw = warp - 2, f = cw * 8 + (lane & 7), kq = lane >> 3;
-    const bool fv = f < nf;
-    const int o = (Tsh[f] - 1) & 7;                  // box element of grid column 32*k0
-    const uint32_t sh = (uint32_t)(o & 1) * 16;
+    // ---------------- GA warps: warp w = frame w; lane = (row rr & 7, chunk ch & 3), so
+    // each 8-lane phase of a 16-byte load reads 128 contiguous bytes (frame boxes are a
+    // multiple of 128 B apart: lanes on different frames would share banks)
+    const int f = warp - 2;
     const int nl2 = g.nl + 2;
-    u64 tot = 0, e0 = 0, e1 = 0, e2 = 0, e3 = 0;
-    RT_T(uint64_t w_data = 0, w_empty = 0, w_conv = 0, w_fence = 0, w_issue = 0; const uint64_t tbeg = gtimer();)
-    // raw rows of this warp's 8 frames: 16-byte LDGSTS with zero fill outside the frame
-    // (a 16-byte block at an 8-aligned column is entirely inside or outside), issued
-    // RTC_NS-1 stages ahead; a warp reads only the slots it filled: __syncwarp suffices
-    auto issue = [&](int j) {
-      if (j < nstage) {
-        int pr, k0, kc;
-        rtc_stage(g, r0, j, pr, k0, kc);
-        unsigned char *rs = raw + (j % RTC_NS) * RTC_RAW_STAGE;
-        for (int k = lane; k < 8 * (RTC_BOXW / 8); k += 32) {
-          const int fl = k / (RTC_BOXW / 8), q = k % (RTC_BOXW / 8), ff = cw * 8 + fl;
-          const int x = 32 * k0 + Tsh[ff] - 1, xb = x - (x & 7) + 8 * q, y = pr + Ssh[ff] - 1;
-          const bool ok = ff < nf && y >= 0 && y < g.ml && xb >= 0 && xb < g.nl;
-#ifdef RTC_SAMEFRAME
-          const uint16_t *src = ok ? a.img + (int64_t)(f0) * a.fstride + (int64_t)y * a.pitch + xb : a.img;
-#else
-          const uint16_t *src = ok ? a.img + (int64_t)(f0 + ff) * a.fstride + (int64_t)y * a.pitch + xb : a.img;
-#endif
-          cp_async16_zfill(rs + ff * RTC_RAW_SLOT + 16 * q, src, ok ? 16u : 0u);
-        }
-      }
-      cp_async_commit();
-    };
-    for (int j = 0; j < RTC_NS - 1; ++j) issue(j);
+    const int lr = lane & 7, lc = lane >> 3;
+    u64 tot = 0, e0 = 0, e1 = 0, e2 = 0, e3 = 0;   // interior rows of frame f
     for (int i = 0; i < nstage; ++i) {
-      const int s = i % RTC_NS;
-      int pr, k0, kc;
-      rtc_stage(g, r0, i, pr, k0, kc);
-      const int so = i % RTC_NO, ro = i / RTC_NO;
-      RT_T(uint64_t t0 = gtimer();)
-      cp_async_wait<RTC_NS - 2>();
-      __syncwarp();
-      RT_T(uint64_t t1 = gtimer(); w_data += t1 - t0;)
-      if (ro > 0) mbar_wait(&aempty[so], (ro - 1) & 1);
-      RT_T(uint64_t t2 = gtimer(); w_empty += t2 - t1;)
-      const uint32_t rb = smem_u32(raw + s * RTC_RAW_STAGE + f * RTC_RAW_SLOT) + (uint32_t)(o >> 1) * 4;
-      unsigned char *A = ops + so * RTC_OP_STAGE;
-#ifdef RTC_NOCONV
-      for (int kh = kq; kh < 0; kh += 4) {
-#else
-      for (int kh = kq; kh < 2 * kc; kh += 4) {
-#endif
-        const int pc0 = 32 * k0 + 16 * kh;   // grid columns pc0 .. pc0+15
-        uint32_t w[9], v2[8];
+      const int s = i % RTC_NST, rnd = i / RTC_NST;
+      const int gb = G0 + (i / g.nstrips) * RTC_RG, j0 = (i % g.nstrips) * RTC_KS;
+      const int ngr = min(RTC_RG, G1 - gb), kc = min(RTC_KS, g.nk - j0);
+      // grid rows of this stage's row groups: [6gb, 6(gb+ngr)); the last group also owns
+      // rows ml, ml+1 (the two below the template)
+      const int r_lo = 6 * gb, r_hi = (gb + ngr == g.ng) ? g.ml + 2 : min(g.ml, 6 * (gb + ngr));
+      RT_T(t0 = gtimer();)
+      mbar_wait(&full[s], rnd & 1);
+      RT_T(w_a += gtimer() - t0;)
+      const unsigned char *st = stg + s * RTC_STAGE + f * RTC_SLOT;
+      const int nrow = r_hi - r_lo, nch = 2 * kc;
+      if (f < nf) {
+        for (int rb = 0; rb < nrow; rb += 8) {
+          const int rr = rb + lr;
+          const int pr = r_lo + rr;
+          const int rc = pr < 2 ? pr : (pr >= g.ml ? pr - g.ml + 2 : 4);
+          uint4 q4[RTC_CH / 4];
 #pragma unroll
-        for (int q = 0; q < 9; ++q) w[q] = lds32(rb + (uint32_t)(32 * kh + 4 * q));
+          for (int cb = 0; cb < RTC_CH / 4; ++cb) {
+            const int ch = cb * 4 + lc;
+            q4[cb] = (rr < nrow && ch < nch)
+                         ? *reinterpret_cast<const uint4 *>(st + (ch * RTC_R + (pr - 6 * gb)) * 16)
+                         : make_uint4(0, 0, 0, 0);
+          }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v2[q] = __funnelshift_r(w[q], w[q + 1], sh);
-        if (!fv) {
+          for (int cb = 0; cb < RTC_CH / 4; ++cb) {
+            const int ch = cb * 4 + lc;
+            if (rr >= nrow || ch >= nch) continue;
+            const int pc0 = 16 * j0 + 8 * ch - o;   // grid column of the chunk's first pixel
+            const uint32_t wv[4] = {q4[cb].x, q4[cb].y, q4[cb].z, q4[cb].w};
+            if (rc == 4 && pc0 > 1 && pc0 + 8 <= g.nl) {
+              // interior chunk: eight squares, no masks (each pair of squares < 2^29)
+              uint32_t sa = 0, sb = 0;
 #pragma unroll
-          for (int q = 0; q < 8; ++q) v2[q] = 0;
-        } else if (pc0 + 16 > nl2) {   // grid columns >= nl+2 carry no template: zero
+              for (int q = 0; q < 2; ++q) {
+                sa += (wv[q] & 0xffffu) * (wv[q] & 0xffffu) + (wv[q] >> 16) * (wv[q] >> 16);
+                sb += (wv[q + 2] & 0xffffu) * (wv[q + 2] & 0xffffu) + (wv[q + 2] >> 16) * (wv[q + 2] >> 16);
+              }
+              tot += (u64)sa + sb;
+              continue;
+            }
+            u64 t8 = 0;
+            uint32_t sq[8];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int c = pc0 + 2 * q;
-            if (c >= nl2) v2[q] = 0;
-            else if (c + 1 >= nl2) v2[q] &= 0xffffu;
+            for (int x = 0; x < 8; ++x) {
+              const uint32_t v = (x & 1) ? (wv[x >> 1] >> 16) : (wv[x >> 1] & 0xffffu);
+              const int c = pc0 + x;
+              sq[x] = (c >= 0 && c < nl2) ? v * v : 0u;
+              t8 += sq[x];
+            }
+            u64 c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+#pragma unroll
+            for (int x = 0; x < 8; ++x) {
+              if (pc0 + x == 0) c0 = sq[x];
+              if (pc0 + x == 1) c1 = sq[x];
+              if (pc0 + x == g.nl) c2 = sq[x];
+              if (pc0 + x == g.nl + 1) c3 = sq[x];
+            }
+            if (rc == 4) {
+              tot += t8; e0 += c0; e1 += c1; e2 += c2; e3 += c3;
+            } else {
+              u64 *bn = bins + (f * 5 + rc) * 5;
+              atomicAdd(reinterpret_cast<unsigned long long *>(bn + 0), (unsigned long long)t8);
+              atomicAdd(reinterpret_cast<unsigned long long *>(bn + 1), (unsigned long long)c0);
+              atomicAdd(reinterpret_cast<unsigned long long *>(bn + 2), (unsigned long long)c1);
+              atomicAdd(reinterpret_cast<unsigned long long *>(bn + 3), (unsigned long long)c2);
+              atomicAdd(reinterpret_cast<unsigned long long *>(bn + 4), (unsigned long long)c3);
+            }
           }
         }
-        uint32_t hi[4], lo[4];
-#pragma unroll
-        for (int p = 0; p < 4; ++p) {
-          const uint32_t x0 = v2[2 * p], x1 = v2[2 * p + 1];
-          lo[p] = __byte_perm(x0 & 0x007F007Fu, x1 & 0x007F007Fu, 0x6420);
-          hi[p] = __byte_perm((x0 >> 7) & 0x007F007Fu, (x1 >> 7) & 0x007F007Fu, 0x6420);
-        }
-        unsigned char *tile = A + (kh >> 1) * 4096 + (kh & 1) * 2048 + (f & 7) * 16;
-        *reinterpret_cast<uint4 *>(tile + (f >> 3) * 128) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-        *reinterpret_cast<uint4 *>(tile + (8 + (f >> 3)) * 128) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-        // frame energy: the 16 squares (each < 2^28) in two 32-bit halves
-        uint32_t sa = 0, sb = 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t x = v2[q], y = v2[q + 4];
-          sa += (x & 0xffffu) * (x & 0xffffu) + (x >> 16) * (x >> 16);
-          sb += (y & 0xffffu) * (y & 0xffffu) + (y >> 16) * (y >> 16);
-        }
-        tot += (u64)sa + (u64)sb;
-        if (pc0 == 0) {
-          e0 += (u64)((v2[0] & 0xffffu) * (v2[0] & 0xffffu));
-          e1 += (u64)((v2[0] >> 16) * (v2[0] >> 16));
-        }
-        if (pc0 <= g.nl && g.nl < pc0 + 16) {   // nl % 8 == 0: columns nl, nl+1 share one word
-          const uint32_t x = (g.nl - pc0) == 0 ? v2[0] : v2[4];
-          e2 += (u64)((x & 0xffffu) * (x & 0xffffu));
-          e3 += (u64)((x >> 16) * (x >> 16));
-        }
       }
-      RT_T(uint64_t t3 = gtimer(); w_conv += t3 - t2;)
-      fence_proxy_async();   // A tiles written by the generic proxy, read by the tensor core
       __syncwarp();
-      if (lane == 0) mbar_arrive(&afull[so]);
-      RT_T(uint64_t t4 = gtimer(); w_fence += t4 - t3;)
-      issue(i + RTC_NS - 1);   // into the slot read in the previous iteration
-      RT_T(w_issue += gtimer() - t4;)
-      // end of a grid row: flush the row-class bins when the class changes next
-      if (k0 + kc == g.nsteps) {
-        const int cls = pr < 2 ? pr : (pr >= g.ml ? pr - g.ml + 2 : 4);
-        if (cls != 4 || pr + 1 == g.ml || pr + 1 == r1) {
-          if (fv) {
-            u64 *bn = bins + (f * 5 + cls) * 5;
-            atomicAdd(reinterpret_cast<unsigned long long *>(bn + 0), (unsigned long long)tot);
-            atomicAdd(reinterpret_cast<unsigned long long *>(bn + 1), (unsigned long long)e0);
-            atomicAdd(reinterpret_cast<unsigned long long *>(bn + 2), (unsigned long long)e1);
-            atomicAdd(reinterpret_cast<unsigned long long *>(bn + 3), (unsigned long long)e2);
-            atomicAdd(reinterpret_cast<unsigned long long *>(bn + 4), (unsigned long long)e3);
-          }
-          tot = e0 = e1 = e2 = e3 = 0;
-        }
-      }
+      if (lane == 0) mbar_arrive(&empty[s]);
     }
-    RT_T(if (blockIdx.x == 0 && lane == 0 && (warp == 2 || warp == 9)) printf("RTT warp %d nstage %d total %llu data %llu aempty %llu conv %llu fence %llu issue %llu\n", warp, nstage, (unsigned long long)(gtimer() - tbeg), (unsigned long long)w_data, (unsigned long long)w_empty, (unsigned long long)w_conv, (unsigned long long)w_fence, (unsigned long long)w_issue);)
+    tot = warp_sum(tot); e0 = warp_sum(e0); e1 = warp_sum(e1); e2 = warp_sum(e2); e3 = warp_sum(e3);
+    if (f < nf && lane == 0) {
+      u64 *bn = bins + (f * 5 + 4) * 5;
+      atomicAdd(reinterpret_cast<unsigned long long *>(bn + 0), (unsigned long long)tot);
+      atomicAdd(reinterpret_cast<unsigned long long *>(bn + 1), (unsigned long long)e0);
+      atomicAdd(reinterpret_cast<unsigned long long *>(bn + 2), (unsigned long long)e1);
+      atomicAdd(reinterpret_cast<unsigned long long *>(bn + 3), (unsigned long long)e2);
+      atomicAdd(reinterpret_cast<unsigned long long *>(bn + 4), (unsigned long long)e3);
+    }
   }
 
-  // ---------------- epilogue
+  // ---------------- epilogue: TMEM lane m = f*8 + r_rel; warp (m / 32) reads 32 lanes
+  RT_T(const uint64_t t_main = gtimer() - t_beg;)
   mbar_wait(done, 0);
+  RT_T(const uint64_t t_done = gtimer() - t_beg;)
   __syncwarp();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  u64 *Es = reinterpret_cast<u64 *>(raw);   // [128][18]: (pb = hi, c < 9), (pb = lo, c < 9)
+  const int nsets_used = min(g.nsets, max(0, G1 - G0));
   if (warp >= 2 && warp < 6) {
-    const int sub = warp & 3, m = sub * 32 + lane;
-    u64 eh[9], el[9];
+    const int sw = warp & 3, m = sw * 32 + lane, ff = m >> 3, rr = m & 7;
+    u64 hp[9];
 #pragma unroll
-    for (int c = 0; c < 9; ++c) { eh[c] = 0; el[c] = 0; }
+    for (int c = 0; c < 9; ++c) hp[c] = 0;
     for (int st = 0; st < nsets_used; ++st) {
-      uint32_t x[16], y[16];
-      const uint32_t tb = taddr + ((uint32_t)(sub * 32) << 16) + (uint32_t)(st * 32);
-      tmem_ld16(tb, x);
-      tmem_ld16(tb + 16, y);
-      tmem_wait_ld();
 #pragma unroll
-      for (int c = 0; c < 9; ++c) { eh[c] += x[c]; el[c] += y[c]; }
+      for (int cb = 0; cb < 4; cb += 2) {   // 32 columns per wait: n = cb*16 .. cb*16+31
+        uint32_t x[32];
+        tmem_ld16(taddr + ((uint32_t)(sw * 32) << 16) + (uint32_t)(st * 64 + cb * 16), *reinterpret_cast<uint32_t (*)[16]>(x));
+        tmem_ld16(taddr + ((uint32_t)(sw * 32) << 16) + (uint32_t)(st * 64 + cb * 16 + 16),
+                  *reinterpret_cast<uint32_t (*)[16]>(x + 16));
+        tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const int n = cb * 16 + q;
+          if (n >= 54) continue;
+          const int tv = n / 3, type = n % 3, t = tv / 3, vp = tv % 3, up = rr - t;
+          const u64 w = (u64)x[q] << (8 * type);
+          // compile-time register indices (a runtime index would put hp in local memory)
+          if (up == 0) hp[vp] += w;
+          else if (up == 1) hp[3 + vp] += w;
+          else if (up == 2) hp[6 + vp] += w;
+        }
+      }
     }
+    // sum the 8 grid rows of the frame (lanes ff*8 .. ff*8+7 of this warp)
 #pragma unroll
-    for (int c = 0; c < 9; ++c) { Es[m * 18 + c] = eh[c]; Es[m * 18 + 9 + c] = el[c]; }
+    for (int c = 0; c < 9; ++c) {
+      u64 v = hp[c];
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      hp[c] = v;
+    }
+    if (rr == 0 && ff < nf) {
+      u64 *acc = a.acc + (int64_t)Fid[ff] * 18;
+#pragma unroll
+      for (int c = 0; c < 9; ++c) atomicAdd(reinterpret_cast<unsigned long long *>(acc + c), (unsigned long long)hp[c]);
+    }
   }
-  __syncthreads();
+  // GA per candidate from the bins: row classes of u' (0: rows 0,1,int; 1: 1,int,ml;
+  // 2: int,ml,ml+1), minus the two grid columns outside [v', v'+nl) (0: nl,nl+1;
+  // 1: 0,nl+1; 2: 0,1)
   for (int k = tid; k < RTC_F * 9; k += RTC_THREADS) {
     const int ff = k / 9, c = k % 9;
     if (ff >= nf) continue;
-    const u64 *ph = Es + ff * 18, *pl = Es + (64 + ff) * 18;
-    const u64 H = (ph[c] << 14) + ((ph[9 + c] + pl[c]) << 7) + pl[9 + c];
-    // GA: row classes of u' (0: rows 0,1,int; 1: 1,int,ml; 2: int,ml,ml+1), minus the
-    // two grid columns outside [v', v'+nl) (0: nl,nl+1; 1: 0,nl+1; 2: 0,1)
     const int up = c / 3, vp = c % 3;
     const int ex1 = vp == 0 ? 3 : 1, ex2 = vp == 2 ? 2 : 4;
     const u64 *bn = bins + ff * 25;
     u64 GA = 0;
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-      const int cls = up == 0 ? (q == 0 ? 0 : q == 1 ? 1 : 4) : up == 1 ? (q == 0 ? 1 : q == 1 ? 4 : 2)
-                                                                          : (q == 0 ? 4 : q == 1 ? 2 : 3);
-      GA += bn[cls * 5] - bn[cls * 5 + ex1] - bn[cls * 5 + ex2];
+      const int rc = up == 0 ? (q == 0 ? 0 : q == 1 ? 1 : 4) : up == 1 ? (q == 0 ? 1 : q == 1 ? 4 : 2)
+                                                                         : (q == 0 ? 4 : q == 1 ? 2 : 3);
+      GA += bn[rc * 5] - bn[rc * 5 + ex1] - bn[rc * 5 + ex2];
     }
-    u64 *acc = a.acc + (int64_t)(f0 + ff) * 18;
-    atomicAdd(reinterpret_cast<unsigned long long *>(acc + c), (unsigned long long)H);
-    atomicAdd(reinterpret_cast<unsigned long long *>(acc + 9 + c), (unsigned long long)GA);
+    atomicAdd(reinterpret_cast<unsigned long long *>(a.acc + (int64_t)Fid[ff] * 18 + 9 + c), (unsigned long long)GA);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc(taddr, 32 * g.nsets);
+  if (warp == 1) tmem_dealloc(taddr, tcols);
+  RT_T(if (blockIdx.x < 3 && lane == 0 && warp < 4) printf("RTT cta %d warp %d nstage %d main %llu done %llu total %llu wait %llu\n", blockIdx.x, warp, nstage, (unsigned long long)t_main, (unsigned long long)t_done, (unsigned long long)(gtimer() - t_beg), (unsigned long long)w_a);)
 }
 
 }  // namespace moco

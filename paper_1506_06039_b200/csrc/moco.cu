@@ -55,6 +55,7 @@ struct moco_plan {
   u64 *racc;                  // refine accumulators [cap][18] (kept zero between calls)
   RtcGeom rtc[3];             // tensor-core refine geometry per level (kernels_rtc.cuh)
   uint8_t *rtab[3];           // its template candidate tiles, or null: CUDA-core refine
+  int *rperm, *rmeta;         // its per-batch alignment-class bucketing
   int nsm;                    // multiprocessors of the plan's device
   int64_t cap;                // frames per internal batch
   void *scratch[3];           // frame pyramid levels 1..L for one batch
@@ -183,6 +184,8 @@ static void plan_free(moco_plan *p) {
     if (p->pb2[l]) cudaFree(p->pb2[l]);
     if (p->rtab[l]) cudaFree(p->rtab[l]);
   }
+  if (p->rperm) cudaFree(p->rperm);
+  if (p->rmeta) cudaFree(p->rmeta);
   tc_free(&p->tc);
   for (void *q : {(void *)p->fft.twr, (void *)p->fft.twc, (void *)p->fft.Bc, (void *)p->fft.S, (void *)p->fft.P,
                   (void *)p->fft.ga, (void *)p->fft.qc, (void *)p->fft.lb, (void *)p->fft.ub, (void *)p->fft.epart})
@@ -447,9 +450,12 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
       // slower than the CUDA-core kernel on B200 as measured
       const char *re = getenv("MOCO_RTC");
       if (re && atoi(re) == 1 && rtc_make(&p->rtc[l], p->ml[l], p->nl[l], bits + 2 * l)) {
-        const size_t tb = (size_t)(p->ml[l] + 2) * p->rtc[l].nsteps * 1024;
-        if (cudaMalloc((void **)&p->rtab[l], tb) != cudaSuccess) {
+        const size_t tb = rtc_table_bytes(p->rtc[l]);
+        if (cudaMalloc((void **)&p->rtab[l], tb) != cudaSuccess ||
+            (!p->rperm && (cudaMalloc((void **)&p->rperm, (size_t)p->cap * sizeof(int)) != cudaSuccess ||
+                           cudaMalloc((void **)&p->rmeta, 16 * sizeof(int)) != cudaSuccess))) {
           cudaGetLastError();
+          if (p->rtab[l]) cudaFree(p->rtab[l]);
           p->rtab[l] = nullptr;
         }
       }
@@ -653,7 +659,8 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
   }
   CUtensorMap tmF;
   const bool rtc = p->rtab[l] != nullptr;
-  if (!rtc && !tmap_u16_3d(&tmF, img, a.nl, a.ml, B, p->pitch[l], fstride, RS_BOX, a.rt + 2)) {
+  if (rtc ? !tmap_u16_chunks(&tmF, img, a.nl, a.ml, B, p->pitch[l], fstride, RTC_R, RTC_CH)
+          : !tmap_u16_3d(&tmF, img, a.nl, a.ml, B, p->pitch[l], fstride, RS_BOX, a.rt + 2)) {
     snprintf(g_err, sizeof(g_err), "cuTensorMapEncodeTiled failed (refine level %d)", l);
     return MOCO_ECUDA;
   }
@@ -674,22 +681,25 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
       CK(cudaFuncSetAttribute(k_refine_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, RTC_SMEM));
       attr = true;
     }
+    k_rtc_bucket<<<1, 1024, 0, st>>>(sin, (int)B, p->rperm, p->rmeta);
     RtcArgs r;
-    r.img = (const uint16_t *)img; r.fstride = fstride; r.pitch = p->pitch[l];
-    r.tab = p->rtab[l]; r.acc = racc; r.shift_in = sin; r.B = (int)B; r.g = p->rtc[l];
-    // row parts per 64-frame group: the fewest that bring the last wave near full
-    const int64_t groups = (B + RTC_F - 1) / RTC_F;
-    const int R = p->ml[l] + 2;
+    r.tab = p->rtab[l]; r.acc = racc; r.shift_in = sin; r.perm = p->rperm; r.meta = p->rmeta;
+    r.B = (int)B; r.g = p->rtc[l];
+    // row-group ranges per 16-frame group (whole stages): the fewest that bring the last
+    // wave near full
+    const int64_t groups = (B + RTC_F - 1) / RTC_F + 4;   // upper bound over the 4 classes
+    const int nblk = (p->rtc[l].ng + RTC_RG - 1) / RTC_RG;
     int best = 1;
     double bestc = 1e30;
-    for (int parts = 1; parts <= 16 && R / parts >= 16; ++parts) {
+    for (int parts = 1; parts <= 16 && parts <= nblk; ++parts) {
       const double waves = std::ceil((double)(groups * parts) / p->nsm);
       const double cost = waves / parts + 0.01 * parts;   // per-CTA fixed costs
       if (cost < bestc) { bestc = cost; best = parts; }
     }
-    r.parts = best;
-    r.rows_per_part = (R + best - 1) / best;
-    k_refine_tc<<<(unsigned)(groups * best), RTC_THREADS, RTC_SMEM, st>>>(r);
+    if (const char *pe = getenv("MOCO_RTC_PARTS")) best = std::max(1, std::min(nblk, atoi(pe)));   // tuning
+    r.groups_per_part = (nblk + best - 1) / best * RTC_RG;
+    r.parts = (p->rtc[l].ng + r.groups_per_part - 1) / r.groups_per_part;
+    k_refine_tc<<<(unsigned)(groups * r.parts), RTC_THREADS, RTC_SMEM, st>>>(tmF, r);
   } else {
     ProfScope ps(p, MOCO_K_REFINE, st);
     const int smem = rs_smem_bytes(a.rt, a.stages);
@@ -774,7 +784,7 @@ int moco_set_template(moco_plan *p, const void *d_template, moco_stream_t stream
       CKL("k_prefix2d");
       if (p->rtab[l]) {
         k_rtc_table<<<1024, 256, 0, st>>>((const uint16_t *)p->tpl[l], p->pitch[l], p->ml[l], p->nl[l],
-                                          p->rtc[l].nsteps, p->rtab[l]);
+                                          p->rtc[l].ng, p->rtc[l].nk, p->rtab[l]);
         CKL("k_rtc_table");
       }
     }
