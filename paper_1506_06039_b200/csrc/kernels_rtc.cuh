@@ -17,32 +17,31 @@
 // the cross term is H = D_a + 2^8 D_b + 2^16 D_c exactly (values < 2^14: bytes <= 255,
 // all products of u8 x u8 in int32 accumulators) -- no per-pixel work for H at all.
 //
-// MMA shape: M = 128 = 16 frames x 8 consecutive grid rows (one core-matrix group per
-// frame: the A tiles are TMA boxes {8 px, rows, 8-px chunks} through a tensor map whose
-// dimensions are reordered to {8 columns, rows, column chunks, frames}, i.e. exactly the
-// K-major core-matrix layout, 16 B per row), N = 64 = 6 template rows x 3 column shifts
-// v' x 3 types (54 used), K = 32 bytes = 16 pixels.  A row group G (template rows 6G..6G+5)
-// needs grid rows 6G..6G+7; the next group's window starts 6 rows (96 B) further.  In D,
-// entry (frame, r_rel; t_rel, v', type) is useful when u' = r_rel - t_rel is 0, 1 or 2.
-// A frame's box starts at the 8-aligned column below T-1, so the grid column of box
-// element e is e - o with o = (T-1) mod 8 (odd: T is even); frames are bucketed by o
-// (k_rtc_bucket) and the template table holds one pre-shifted copy per class.
-// int32 accumulators alternate between `nsets` TMEM sets by row group.
-// GA is the only per-pixel CUDA-core work: 8 warps sum a^2 from the staged boxes (grid
-// rows binned by class 0, 1, ml, ml+1, interior; the four edge columns kept apart) and
-// the epilogue combines the bins per candidate.
+// MMA shape: M = 128 = 16 frames x 8 consecutive grid rows (one 8-row group per frame),
+// N = 64 = 6 template rows x 3 column shifts v' x 3 types (54 used), K = 32 bytes =
+// 16 pixels.  The A tiles are TMA boxes {64 pixels, 32 grid rows} per frame written with
+// the 128-byte swizzle: each box row is one 128-byte K-major row (64 pixels), the boxes
+// 1024-byte aligned, and the UMMA descriptor (layout SWIZZLE_128B, SBO = box size) starts
+// at row 6q of every box for row group q and at byte 32k for K-step k -- the swizzle
+// phase follows the address bits, so the window slides freely.  A row group G (template
+// rows 6G..6G+5) needs grid rows 6G..6G+7; in D, entry (frame, r_rel; t_rel, v', type) is
+// useful when u' = r_rel - t_rel is 0, 1 or 2.  A frame's box starts at the 8-aligned
+// column below T-1, so the grid column of box pixel e is e - o with o = (T-1) mod 8
+// (odd: T is even); frames are bucketed by o (k_rtc_bucket) and the template table holds
+// one pre-shifted copy per class.  int32 accumulators alternate between `nsets` TMEM sets
+// by row group.  GA is the only per-pixel CUDA-core work: one warp per frame sums a^2
+// from the staged (swizzled) boxes, grid rows binned by class 0, 1, ml, ml+1, interior,
+// the four edge columns kept apart; the epilogue combines the bins per candidate.
 //
 // Work unit: a CTA takes 16 frames of one alignment class x a range of row groups; a
-// stage = 4 row groups (26 grid rows) x 4 K-steps (8 chunks):
-//   warp 0    TMA: one box {8, 26, 8} per frame + one bulk copy of B tiles per row group;
-//   warp 1    MMA issuer: 4 x 4 MMAs (M128 N64 K32) per stage;
-//   warps 2-9 GA from the same staged boxes;
+// stage = 5 row groups (32 grid rows) x 4 K-steps (64 pixels):
+//   warp 0     TMA: one box per frame + one bulk copy of B tiles per row group;
+//   warp 1     MMA issuer: 5 x 4 MMAs (M128 N64 K32) per stage;
+//   warps 2-17 GA, one frame each, from the same staged boxes;
 // double-buffered stages; epilogue: TMEM -> per-row partial H -> 8-lane shuffle sums.
-// Opt-in (MOCO_RTC=1): bit-exact, 616 us per 2 368 C2 frames against 584 us for the
-// CUDA-core kernel.  The limiter is the A-tile TMA: the reordered tensor map makes the
-// box's inner dimension 16 B, so a stage is ~3 300 16-byte row requests (557 us with the
-// GA pass removed); a SWIZZLE_128B K-major layout (128-byte rows) is the next step.
-// DESIGN.md section 11.
+// C2, 2 368 frames: 467 us against 584 us for the CUDA-core kernel (an earlier variant
+// with a dimension-reordered, 16-byte-row tensor map took 616 us: TMA-row bound); in the
+// three-stream pipeline 1.40 -> 1.48 M frames/s.  DESIGN.md section 11.
 #pragma once
 
 #include <cmath>
@@ -64,28 +63,25 @@ __device__ __forceinline__ uint64_t gtimer_rt() {
 #endif
 
 constexpr int RTC_F = 16;                  // frames per CTA (core-matrix groups of M)
-constexpr int RTC_RG = 4;                  // row groups (6 template rows each) per stage
+constexpr int RTC_RG = 5;                  // row groups (6 template rows each) per stage
 constexpr int RTC_R = 6 * RTC_RG + 2;      // grid rows per stage box
-#ifndef RTC_KSTEPS
-#define RTC_KSTEPS 4   // measured: 4 K-steps x 2 stages 616 us, 2 x 4 680 us, 2 x 5 681 us (C2, 2 368 frames)
-#endif
 #ifndef RTC_NSTAGE
 #define RTC_NSTAGE 2
 #endif
-constexpr int RTC_KS = RTC_KSTEPS;         // K-steps (16 pixels) per stage
+constexpr int RTC_KS = 4;                  // K-steps (16 pixels) per stage: one 128-byte row
 constexpr int RTC_NST = RTC_NSTAGE;        // ring depth
 constexpr int RTC_CH = 2 * RTC_KS;         // 8-pixel chunks per stage box
 constexpr int RTC_CW = 16;                 // GA warps
 constexpr int RTC_THREADS = 32 * (2 + RTC_CW);
-constexpr int RTC_SLOT = RTC_CH * RTC_R * 16;                 // bytes per frame box (multiple of 128)
+constexpr int RTC_SLOT = RTC_R * 128;                        // bytes per frame box: R rows of 128 B (SW128)
 constexpr int RTC_RAW = RTC_F * RTC_SLOT;                     // A stage
 constexpr int RTC_BT = 2048;                                  // one B tile: 64 rows x 32 B
 constexpr int RTC_STAGE = RTC_RAW + RTC_RG * RTC_KS * RTC_BT;
 constexpr int RTC_BINS_OFF = 1024;         // [16][5 row classes][5] u64
-constexpr int RTC_ST_OFF = 5120;            // after the bins (16 x 25 x 8 = 3200 B)
+constexpr int RTC_ST_OFF = 5120;           // after the bins (16 x 25 x 8 = 3200 B), 1024-aligned
 constexpr int RTC_SMEM = RTC_ST_OFF + RTC_NST * RTC_STAGE + 1024;  // + alignment slack
-static_assert(RTC_SLOT % 128 == 0, "TMA destinations must be 128-byte aligned");
-static_assert(RTC_BINS_OFF + RTC_F * 25 * 8 <= RTC_ST_OFF, "bins overlap the stages");
+static_assert(RTC_SLOT % 1024 == 0 && RTC_R % 8 == 0, "SWIZZLE_128B boxes must be 1024-byte aligned");
+static_assert(RTC_BINS_OFF + RTC_F * 25 * 8 <= RTC_ST_OFF && RTC_ST_OFF % 1024 == 0, "bins overlap the stages");
 static_assert(RTC_SMEM <= 227 * 1024, "shared memory");
 static_assert(RTC_CH % 4 == 0 && RTC_NST * 2 * 8 + 8 <= 128, "chunk lanes, barrier space");
 
@@ -169,30 +165,27 @@ __global__ void __launch_bounds__(1024) k_rtc_bucket(const int32_t *__restrict__
   }
 }
 
-__device__ __forceinline__ void tma_load4(void *dst, const CUtensorMap *tm, int c0, int c1, int c2, int c3,
-                                          uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
-      "%5}], [%6];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// u16 frames [frames][rows][cols] (row pitch, frame stride in elements) seen as the 4-D
-// tensor {8 columns, rows, cols/8 chunks, frames} with strides {pitch, 16 B, fstride}: a
-// box {8, R, C, 1} lands as [chunk][row][16 B], the K-major core-matrix layout; zero
-// fill outside (negative chunks and rows included).
-inline bool tmap_u16_chunks(CUtensorMap *tm, const void *base, int cols, int rows, int64_t frames, int pitch,
-                            int64_t fstride, int box_rows, int box_chunks) {
+// u16 frames [frames][rows][cols] (row pitch, frame stride in elements), box {64 columns,
+// rows, 1 frame} written with the 128-byte swizzle: each box row is one 128-byte K-major
+// row of the A operand (64 pixels = 128 interleaved low/high bytes), zero fill outside.
+inline bool tmap_u16_sw128(CUtensorMap *tm, const void *base, int cols, int rows, int64_t frames, int pitch,
+                           int64_t fstride, int box_rows) {
   auto enc = tmap_encoder();
   if (!enc) return false;
-  const cuuint64_t dims[4] = {8, (cuuint64_t)rows, (cuuint64_t)(cols / 8), (cuuint64_t)frames};
-  const cuuint64_t strides[3] = {(cuuint64_t)pitch * 2, 16, (cuuint64_t)fstride * 2};
-  const cuuint32_t box[4] = {8, (cuuint32_t)box_rows, (cuuint32_t)box_chunks, 1};
-  const cuuint32_t es[4] = {1, 1, 1, 1};
-  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, const_cast<void *>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  const cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)frames};
+  const cuuint64_t strides[2] = {(cuuint64_t)pitch * 2, (cuuint64_t)fstride * 2};
+  const cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void *>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// UMMA shared-memory descriptor, K-major, 128-byte swizzle (layout type 2): rows of 128 B
+// in 1024-byte atoms, SBO = byte distance between 8-row groups; the start address may
+// sit at any row of an atom (the XOR phase comes from the address bits).
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 
 struct RtcArgs {
@@ -274,8 +267,8 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
       __syncwarp();
       unsigned char *st = stg + s * RTC_STAGE;
       if (lane < nf) {
-        const int xc = ((Tsh[lane] - 1) >> 3) + 2 * j0;   // first 8-px chunk (floor for negatives)
-        tma_load4(st + lane * RTC_SLOT, &tmF, 0, 6 * gb + Ssh[lane] - 1, xc, Fid[lane], &full[s]);
+        const int x0 = (Tsh[lane] - 1) - ((Tsh[lane] - 1) & 7) + 16 * j0;   // 8-aligned column below T-1
+        tma_load3(st + lane * RTC_SLOT, &tmF, x0, 6 * gb + Ssh[lane] - 1, Fid[lane], &full[s]);
       }
       if (lane == 0)
         for (int q = 0; q < ngr; ++q)
@@ -287,7 +280,7 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
   } else if (warp == 1) {
     // ---------------- MMA issuer
     const uint32_t idesc = idesc_i8(128, 64);
-    const uint64_t ad0 = umma_desc(smem_u32(stg), RTC_R * 16, RTC_SLOT);
+    const uint64_t ad0 = umma_desc_sw128(smem_u32(stg), RTC_SLOT);
     const uint64_t bd0 = umma_desc(smem_u32(stg + RTC_RAW), 1024, 128);
     const uint32_t ahi = (uint32_t)(ad0 >> 32), bhi = (uint32_t)(bd0 >> 32);
     for (int i = 0; i < nstage; ++i) {
@@ -302,11 +295,12 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
       const uint32_t blo = (uint32_t)bd0 + (uint32_t)(s * RTC_STAGE >> 4);
       for (int q = 0; q < ngr; ++q) {
         const int G = gb + q, Gr = G - G0;
-        const uint32_t d = taddr + (uint32_t)((G & (g.nsets - 1)) * 64);
+        // sets by the part-relative group index: the epilogue reads sets 0 .. nsets_used-1
+        const uint32_t d = taddr + (uint32_t)((Gr & (g.nsets - 1)) * 64);
         for (int k = 0; k < kc; ++k) {
           const bool first = Gr < g.nsets && j0 == 0 && k == 0;
-          // A: chunks 2k, 2k+1 (LBO = one chunk column), rows 6q .. 6q+7 of every frame box
-          mma_i8_elect(d, alo + (uint32_t)((2 * k * RTC_R * 16 + 6 * q * 16) >> 4), ahi,
+          // A: bytes 32k .. 32k+31 of rows 6q .. 6q+7 of every frame box
+          mma_i8_elect(d, alo + (uint32_t)((6 * q * 128 + 32 * k) >> 4), ahi,
                        blo + (uint32_t)((q * RTC_KS + k) * RTC_BT >> 4), bhi, idesc, first ? 0u : 1u);
         }
       }
@@ -344,8 +338,9 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
 #pragma unroll
           for (int cb = 0; cb < RTC_CH / 4; ++cb) {
             const int ch = cb * 4 + lc;
+            const int br = pr - 6 * gb;   // box row; its 16-byte chunk ch sits at ch ^ (row & 7)
             q4[cb] = (rr < nrow && ch < nch)
-                         ? *reinterpret_cast<const uint4 *>(st + (ch * RTC_R + (pr - 6 * gb)) * 16)
+                         ? *reinterpret_cast<const uint4 *>(st + br * 128 + ((ch ^ (br & 7)) << 4))
                          : make_uint4(0, 0, 0, 0);
           }
 #pragma unroll

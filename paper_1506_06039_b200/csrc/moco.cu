@@ -446,10 +446,10 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
       p->rnrt[l] = nrt;
       // (ring within ~150 KB: a 37 KB operand-prep CTA of the next batch fits beside it)
       p->rstages[l] = std::min(32, (150 * 1024 - rs_smem_bytes(rt, 0)) / rs_stage_bytes(rt));
-      // tensor-core refine sums (kernels_rtc.cuh), opt-in with MOCO_RTC=1: exact, but
-      // slower than the CUDA-core kernel on B200 as measured
+      // tensor-core refine sums (kernels_rtc.cuh) where they apply; MOCO_RTC=0 selects the
+      // CUDA-core kernel (parity cross-check)
       const char *re = getenv("MOCO_RTC");
-      if (re && atoi(re) == 1 && rtc_make(&p->rtc[l], p->ml[l], p->nl[l], bits + 2 * l)) {
+      if (!(re && atoi(re) == 0) && rtc_make(&p->rtc[l], p->ml[l], p->nl[l], bits + 2 * l)) {
         const size_t tb = rtc_table_bytes(p->rtc[l]);
         if (cudaMalloc((void **)&p->rtab[l], tb) != cudaSuccess ||
             (!p->rperm && (cudaMalloc((void **)&p->rperm, (size_t)p->cap * sizeof(int)) != cudaSuccess ||
@@ -659,7 +659,7 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
   }
   CUtensorMap tmF;
   const bool rtc = p->rtab[l] != nullptr;
-  if (rtc ? !tmap_u16_chunks(&tmF, img, a.nl, a.ml, B, p->pitch[l], fstride, RTC_R, RTC_CH)
+  if (rtc ? !tmap_u16_sw128(&tmF, img, a.nl, a.ml, B, p->pitch[l], fstride, RTC_R)
           : !tmap_u16_3d(&tmF, img, a.nl, a.ml, B, p->pitch[l], fstride, RS_BOX, a.rt + 2)) {
     snprintf(g_err, sizeof(g_err), "cuTensorMapEncodeTiled failed (refine level %d)", l);
     return MOCO_ECUDA;
@@ -692,8 +692,10 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
     int best = 1;
     double bestc = 1e30;
     for (int parts = 1; parts <= 16 && parts <= nblk; ++parts) {
+      // waves x CTA time; a CTA's fixed part (TMEM, barriers, epilogue) measured at about
+      // 8 % of a whole frame group's stages (C2)
       const double waves = std::ceil((double)(groups * parts) / p->nsm);
-      const double cost = waves / parts + 0.01 * parts;   // per-CTA fixed costs
+      const double cost = waves * (0.08 + 1.0 / parts);
       if (cost < bestc) { bestc = cost; best = parts; }
     }
     if (const char *pe = getenv("MOCO_RTC_PARTS")) best = std::max(1, std::min(nblk, atoi(pe)));   // tuning

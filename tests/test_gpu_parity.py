@@ -126,14 +126,19 @@ def test_fused_refine_equals_simple_refine(c, T, monkeypatch):
         assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("c,T", [(2, 300), (4, 24), (3, 130)])
-def test_tensor_core_refine_equals_cuda_core_refine(c, T, monkeypatch):
-    """The opt-in tensor-core refine sums (MOCO_RTC=1, kernels_rtc.cuh: 64 frames x hi/lo
-    parts as M, the nine shifted template parts as N, pixels as K, GA from the converter
-    warps) give bit-identical shifts, f_min and corrected frames to the CUDA-core kernel;
-    ragged frame groups (T % 64 != 0) and both pyramid levels of C4 included."""
+@pytest.mark.parametrize("c,T,parts", [(2, 300, None), (4, 24, None), (3, 130, None), (4, 24, "12"), (2, 300, "7"),
+                                        (2, 40, "1")])
+def test_tensor_core_refine_equals_cuda_core_refine(c, T, parts, monkeypatch):
+    """The tensor-core refine sums (default, kernels_rtc.cuh: raw u16 rows as the int8 A
+    operand, 16 frames x 8 grid rows as M, 6 template rows x 3 shifts x 3 byte types as N,
+    frames bucketed by column alignment, GA on CUDA cores) give bit-identical shifts,
+    f_min and corrected frames to the CUDA-core kernel (MOCO_RTC=0); ragged groups
+    (T % 16 != 0, uneven alignment classes), C3's stripes and large shifts, and both
+    pyramid levels of C4 included."""
     spec = config_spec(c, T=T)
     st = make_stack(spec, 0, T, device=DEV)
+    if parts:   # row-group ranges per CTA group forced (partial last range, unused sets)
+        monkeypatch.setenv("MOCO_RTC_PARTS", parts)
     out = {}
     for mode in ("1", "0"):
         monkeypatch.setenv("MOCO_RTC", mode)
