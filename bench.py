@@ -89,7 +89,10 @@ def kernel_models(spec, esz, algo):
         "coarse": coarse,
         "tc_prep": prep,
         "tc_score": ("alu", 6 * W * W, "flop"),
-        "refine": ("alu", fm["refine"], "flop"),
+        # tensor-core refine sums (kernels_rtc.cuh): one read of each refine level's frame;
+        # the MMAs need < 10 % of the tensor pipe, so the bound is the read
+        "refine": ("hbm", sum((m >> l) * (n >> l) * 2 for l in range(L)), "B") if esz == 2
+        else ("alu", fm["refine"], "flop"),
         "apply": ("hbm", 2 * m * n * esz, "B"),
     }
 
