@@ -658,7 +658,11 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
     a.wide = halves * a.rt * 8.0 * mx >= 4294967296.0 ? 1 : 0;
   }
   CUtensorMap tmF;
-  const bool rtc = p->rtab[l] != nullptr;
+  // the tensor-core kernel parallelises over 16-frame groups: small batches (the closed
+  // loop) keep the CUDA-core kernel, whose 148 template tiles spread even one frame
+  // (MOCO_RTC=1 forces the tensor-core kernel at any size: parity tests)
+  const char *rf = getenv("MOCO_RTC");
+  const bool rtc = p->rtab[l] != nullptr && (B >= 256 || (rf && atoi(rf) == 1));
   if (rtc ? !tmap_u16_sw128(&tmF, img, a.nl, a.ml, B, p->pitch[l], fstride, RTC_R)
           : !tmap_u16_3d(&tmF, img, a.nl, a.ml, B, p->pitch[l], fstride, RS_BOX, a.rt + 2)) {
     snprintf(g_err, sizeof(g_err), "cuTensorMapEncodeTiled failed (refine level %d)", l);

@@ -10,7 +10,7 @@ timeout 300 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > $O/bench_sm
     --log-file $O/ncu_launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > $O/ncu_launches.log 2>&1
 timeout 120 python tools/profile_run.py --frames 2368 --iters 1 > $O/plain_c2.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_tc_prep|k_tc_coarse|k_refine_sums|k_refine_pick" -c 4 -o $O/prof_c2 \
+    -k regex:"k_tc_prep|k_tc_coarse|k_refine_tc|k_refine_pick" -c 4 -o $O/prof_c2 \
     python tools/profile_run.py --frames 2368 --iters 1 > $O/ncu_c2.log 2>&1
 timeout 120 python tools/profile_run.py --config 4 --frames 256 --iters 1 > $O/plain_c4.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on \
