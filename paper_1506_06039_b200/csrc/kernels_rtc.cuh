@@ -411,13 +411,15 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
   __syncwarp();
   tc_fence_before();
   __syncthreads();
+  RT_T(const uint64_t t_sync = gtimer() - t_beg; uint64_t t_tm = 0;)
   tc_fence_after();
   const int nsets_used = min(g.nsets, max(0, G1 - G0));
   if (warp >= 2 && warp < 6) {
     const int sw = warp & 3, m = sw * 32 + lane, ff = m >> 3, rr = m & 7;
-    u64 hp[9];
+    // w[t*3 + v'] = D_a + 2^8 D_b + 2^16 D_c of this row (all sets), compile-time indices
+    u64 w[18];
 #pragma unroll
-    for (int c = 0; c < 9; ++c) hp[c] = 0;
+    for (int c = 0; c < 18; ++c) w[c] = 0;
     for (int st = 0; st < nsets_used; ++st) {
 #pragma unroll
       for (int cb = 0; cb < 4; cb += 2) {   // 32 columns per wait: n = cb*16 .. cb*16+31
@@ -429,16 +431,24 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
 #pragma unroll
         for (int q = 0; q < 32; ++q) {
           const int n = cb * 16 + q;
-          if (n >= 54) continue;
-          const int tv = n / 3, type = n % 3, t = tv / 3, vp = tv % 3, up = rr - t;
-          const u64 w = (u64)x[q] << (8 * type);
-          // compile-time register indices (a runtime index would put hp in local memory)
-          if (up == 0) hp[vp] += w;
-          else if (up == 1) hp[3 + vp] += w;
-          else if (up == 2) hp[6 + vp] += w;
+          if (n < 54) w[n / 3] += (u64)x[q] << (8 * (n % 3));
         }
       }
     }
+    // candidate (u', v') takes template row t = rr - u' of this grid row: branch-free selects
+    u64 hp[9];
+#pragma unroll
+    for (int up = 0; up < 3; ++up) {
+      const int t = rr - up;
+#pragma unroll
+      for (int vp = 0; vp < 3; ++vp) {
+        u64 v = 0;
+#pragma unroll
+        for (int tt = 0; tt < 6; ++tt) v = (t == tt) ? w[tt * 3 + vp] : v;
+        hp[up * 3 + vp] = v;
+      }
+    }
+    RT_T(t_tm = gtimer() - t_beg;)
     // sum the 8 grid rows of the frame (lanes ff*8 .. ff*8+7 of this warp)
 #pragma unroll
     for (int c = 0; c < 9; ++c) {
@@ -454,6 +464,7 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
       for (int c = 0; c < 9; ++c) atomicAdd(reinterpret_cast<unsigned long long *>(acc + c), (unsigned long long)hp[c]);
     }
   }
+  RT_T(const uint64_t t_h = gtimer() - t_beg;)
   // GA per candidate from the bins: row classes of u' (0: rows 0,1,int; 1: 1,int,ml;
   // 2: int,ml,ml+1), minus the two grid columns outside [v', v'+nl) (0: nl,nl+1;
   // 1: 0,nl+1; 2: 0,1)
@@ -476,7 +487,7 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
   __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc(taddr, tcols);
-  RT_T(if (blockIdx.x < 3 && lane == 0 && warp < 4) printf("RTT cta %d warp %d nstage %d main %llu done %llu total %llu wait %llu\n", blockIdx.x, warp, nstage, (unsigned long long)t_main, (unsigned long long)t_done, (unsigned long long)(gtimer() - t_beg), (unsigned long long)w_a);)
+  RT_T(if (blockIdx.x < 3 && lane == 0 && warp < 4) printf("RTT cta %d warp %d nstage %d main %llu done %llu sync %llu tmem %llu h %llu total %llu wait %llu\n", blockIdx.x, warp, nstage, (unsigned long long)t_main, (unsigned long long)t_done, (unsigned long long)t_sync, (unsigned long long)t_tm, (unsigned long long)t_h, (unsigned long long)(gtimer() - t_beg), (unsigned long long)w_a);)
 }
 
 }  // namespace moco
