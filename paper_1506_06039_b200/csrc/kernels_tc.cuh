@@ -840,7 +840,9 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
       Key bk = best[q];
       for (int k = 0; k < NT; ++k) {
         const int s = -hw + k * g.ST + sl;
-        const bool valid = gg < gcount && pa == 0 && s <= hw && fi < a.B;
+        // both rows of the (hi, lo) lane pair evaluate lags: hi lane the first 8 columns of
+        // the chunk, lo lane the last 8 (each has the pair's four part sums after the swap)
+        const bool valid = gg < gcount && s <= hw && fi < a.B;
         // partner row s' = s + 1: same tile, 2F lanes further, or the next tile's first block
         const int mp = sl + 1 < g.ST ? m + 2 * F : m + 2 * F - 128;
         const int kp = sl + 1 < g.ST ? k : k + 1;
@@ -851,14 +853,21 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
         tmem_ld16(tbase + g.Wt + c, xl);      // d = 0, pb = lo
         tmem_wait_ld();
         const uint32_t *src = D1s + ((gg * NT + (haveP ? kp : 0)) * 128 + (haveP ? mp : 0)) * 33;
+        if (haveP) {
 #pragma unroll
-        for (int qq = 0; qq < 16; ++qq) {
-          if (haveP) { xh[qq] += src[qq]; xl[qq] += src[16 + qq]; }   // each < 2^31: no wrap
-          const uint32_t ph = __shfl_xor_sync(0xffffffffu, xh[qq], 1);   // partner row: pa = lo
-          const uint32_t pl = __shfl_xor_sync(0xffffffffu, xl[qq], 1);
-          const int ti = c + qq;
+          for (int qq = 0; qq < 16; ++qq) { xh[qq] += src[qq]; xl[qq] += src[16 + qq]; }   // each < 2^31: no wrap
+        }
+        // the (hi, lo) lane pair splits the chunk: iteration j, hi lane column j, lo lane
+        // column j+8; each sends its partner the part sums of the partner's column
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t mh = pa ? xh[j + 8] : xh[j], ml = pa ? xl[j + 8] : xl[j];
+          const uint32_t ph = __shfl_xor_sync(0xffffffffu, pa ? xh[j] : xh[j + 8], 1);
+          const uint32_t pl = __shfl_xor_sync(0xffffffffu, pa ? xl[j] : xl[j + 8], 1);
+          const int ti = c + j + (pa ? 8 : 0);
           if (!valid || ti >= W) continue;
-          const u64 h = ((u64)xh[qq] << 14) + (((u64)xl[qq] + (u64)ph) << 7) + (u64)pl;
+          const u64 h = pa == 0 ? ((u64)mh << 14) + (((u64)ml + (u64)ph) << 7) + (u64)pl
+                                : ((u64)ph << 14) + (((u64)pl + (u64)mh) << 7) + (u64)ml;
           const int lag = (s + hw) * W + ti;
           const u64 Nn = gas[(fi - fi0) * W * W + lag] + a.gb[lag] - 2 * h;
           const int t = ti - hw;
@@ -885,8 +894,10 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
     const int fo = (grp0 + gg) * F + ff;
     if (gg < gcount && fo < a.B && a.shift_out) {
       Key b{~0ull, ~0u};
-      for (int q = 2 * ff; q < 128; q += 2 * F)
+      for (int q = 2 * ff; q < 128; q += 2 * F) {   // both lanes of each row pair
         if (key_less(keys[gg * 128 + q], b)) b = keys[gg * 128 + q];
+        if (key_less(keys[gg * 128 + q + 1], b)) b = keys[gg * 128 + q + 1];
+      }
       const int s = (int)(b.idx / W) - hw, t = (int)(b.idx % W) - hw;
       a.shift_out[2 * fo] = s;
       a.shift_out[2 * fo + 1] = t;
