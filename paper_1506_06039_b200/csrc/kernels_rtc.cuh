@@ -71,7 +71,10 @@ constexpr int RTC_R = 6 * RTC_RG + 2;      // grid rows per stage box
 constexpr int RTC_KS = 4;                  // K-steps (16 pixels) per stage: one 128-byte row
 constexpr int RTC_NST = RTC_NSTAGE;        // ring depth
 constexpr int RTC_CH = 2 * RTC_KS;         // 8-pixel chunks per stage box
-constexpr int RTC_CW = 16;                 // GA warps
+#ifndef RTC_GA_WARPS
+#define RTC_GA_WARPS 16
+#endif
+constexpr int RTC_CW = RTC_GA_WARPS;       // GA warps (16 / RTC_CW frames each)
 constexpr int RTC_THREADS = 32 * (2 + RTC_CW);
 constexpr int RTC_SLOT = RTC_R * 128;                        // bytes per frame box: R rows of 128 B (SW128)
 constexpr int RTC_RAW = RTC_F * RTC_SLOT;                     // A stage
@@ -313,10 +316,13 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
     // ---------------- GA warps: warp w = frame w; lane = (row rr & 7, chunk ch & 3), so
     // each 8-lane phase of a 16-byte load reads 128 contiguous bytes (frame boxes are a
     // multiple of 128 B apart: lanes on different frames would share banks)
-    const int f = warp - 2;
+    const int cw = warp - 2;
+    constexpr int FPW = RTC_F / RTC_CW;             // frames per GA warp
     const int nl2 = g.nl + 2;
     const int lr = lane & 7, lc = lane >> 3;
-    u64 tot = 0, e0 = 0, e1 = 0, e2 = 0, e3 = 0;   // interior rows of frame f
+    u64 tot[FPW], e0[FPW], e1[FPW], e2[FPW], e3[FPW];   // interior rows, per frame of this warp
+#pragma unroll
+    for (int k = 0; k < FPW; ++k) tot[k] = e0[k] = e1[k] = e2[k] = e3[k] = 0;
     for (int i = 0; i < nstage; ++i) {
       const int s = i % RTC_NST, rnd = i / RTC_NST;
       const int gb = G0 + (i / g.nstrips) * RTC_RG, j0 = (i % g.nstrips) * RTC_KS;
@@ -327,9 +333,12 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
       RT_T(t0 = gtimer();)
       mbar_wait(&full[s], rnd & 1);
       RT_T(w_a += gtimer() - t0;)
-      const unsigned char *st = stg + s * RTC_STAGE + f * RTC_SLOT;
       const int nrow = r_hi - r_lo, nch = 2 * kc;
-      if (f < nf) {
+#pragma unroll
+      for (int fk = 0; fk < FPW; ++fk) {
+        const int f = cw + fk * RTC_CW;
+        if (f >= nf) continue;
+        const unsigned char *st = stg + s * RTC_STAGE + f * RTC_SLOT;
         for (int rb = 0; rb < nrow; rb += 8) {
           const int rr = rb + lr;
           const int pr = r_lo + rr;
@@ -357,7 +366,7 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
                 sa += (wv[q] & 0xffffu) * (wv[q] & 0xffffu) + (wv[q] >> 16) * (wv[q] >> 16);
                 sb += (wv[q + 2] & 0xffffu) * (wv[q + 2] & 0xffffu) + (wv[q + 2] >> 16) * (wv[q + 2] >> 16);
               }
-              tot += (u64)sa + sb;
+              tot[fk] += (u64)sa + sb;
               continue;
             }
             u64 t8 = 0;
@@ -378,7 +387,7 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
               if (pc0 + x == g.nl + 1) c3 = sq[x];
             }
             if (rc == 4) {
-              tot += t8; e0 += c0; e1 += c1; e2 += c2; e3 += c3;
+              tot[fk] += t8; e0[fk] += c0; e1[fk] += c1; e2[fk] += c2; e3[fk] += c3;
             } else {
               u64 *bn = bins + (f * 5 + rc) * 5;
               atomicAdd(reinterpret_cast<unsigned long long *>(bn + 0), (unsigned long long)t8);
@@ -393,14 +402,19 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
-    tot = warp_sum(tot); e0 = warp_sum(e0); e1 = warp_sum(e1); e2 = warp_sum(e2); e3 = warp_sum(e3);
-    if (f < nf && lane == 0) {
-      u64 *bn = bins + (f * 5 + 4) * 5;
-      atomicAdd(reinterpret_cast<unsigned long long *>(bn + 0), (unsigned long long)tot);
-      atomicAdd(reinterpret_cast<unsigned long long *>(bn + 1), (unsigned long long)e0);
-      atomicAdd(reinterpret_cast<unsigned long long *>(bn + 2), (unsigned long long)e1);
-      atomicAdd(reinterpret_cast<unsigned long long *>(bn + 3), (unsigned long long)e2);
-      atomicAdd(reinterpret_cast<unsigned long long *>(bn + 4), (unsigned long long)e3);
+#pragma unroll
+    for (int fk = 0; fk < FPW; ++fk) {
+      const int f = cw + fk * RTC_CW;
+      const u64 t = warp_sum(tot[fk]), a0 = warp_sum(e0[fk]), a1 = warp_sum(e1[fk]), a2 = warp_sum(e2[fk]),
+                a3 = warp_sum(e3[fk]);
+      if (f < nf && lane == 0) {
+        u64 *bn = bins + (f * 5 + 4) * 5;
+        atomicAdd(reinterpret_cast<unsigned long long *>(bn + 0), (unsigned long long)t);
+        atomicAdd(reinterpret_cast<unsigned long long *>(bn + 1), (unsigned long long)a0);
+        atomicAdd(reinterpret_cast<unsigned long long *>(bn + 2), (unsigned long long)a1);
+        atomicAdd(reinterpret_cast<unsigned long long *>(bn + 3), (unsigned long long)a2);
+        atomicAdd(reinterpret_cast<unsigned long long *>(bn + 4), (unsigned long long)a3);
+      }
     }
   }
 
