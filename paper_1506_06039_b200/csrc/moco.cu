@@ -416,7 +416,8 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
   for (int l = 1; l <= levels; ++l) per_frame += (size_t)p->ml[l] * p->pitch[l] * p->esz[l];
   // tensor-core operand planes + lag energies (upper bound: rows <= m_L + 128, int8 hi/lo)
   if (dtype == MOCO_U16) per_frame += (size_t)2 * (p->ml[levels] + 128) * p->nl[levels] + (size_t)W * W * 8;
-  const size_t budget = (size_t)1 << 30;   // internal batch scratch (B200: 180 GB HBM)
+  size_t budget = (size_t)1 << 30;   // internal batch scratch (B200: 180 GB HBM)
+  if (const char *bm = getenv("MOCO_BATCH_MB")) budget = (size_t)std::max(64, atoi(bm)) << 20;   // tuning
   p->cap = per_frame ? std::max<int64_t>(1, (int64_t)(budget / per_frame)) : (int64_t)1 << 20;
   p->cap = std::min<int64_t>(p->cap, (int64_t)1 << 20);
   for (int l = 1; l <= levels; ++l)
@@ -469,6 +470,8 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
       // whole waves of the tensor-core search per internal batch (CTAs/SM x GG*F frames)
       const int64_t wave = (int64_t)nsm * p->tc.g.ctas * p->tc.g.GG * p->tc.g.F;
       if (p->cap >= wave) p->cap = p->cap / wave * wave;
+      if (const char *bw = getenv("MOCO_BATCH_WAVES"))   // tuning: waves per internal batch
+        p->cap = std::min<int64_t>(p->cap, std::max(1, atoi(bw)) * wave);
     } else {
       cudaGetLastError();
     }
