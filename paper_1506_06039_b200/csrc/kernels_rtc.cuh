@@ -191,6 +191,32 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr, uint32_t sbo
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 
+// Four MMAs into one accumulator (the four K-steps of a row group): one elect, one
+// predicate for the first (accumulate = acc0), the other three accumulate.
+__device__ __forceinline__ void mma_i8_k4_elect(uint32_t d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                                uint32_t ahi, uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3,
+                                                uint32_t bhi, uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 da0, da1, da2, da3, db0, db1, db2, db3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %12, 0;\n\t"
+      "mov.b64 da0, {%1, %5};\n\t"
+      "mov.b64 da1, {%2, %5};\n\t"
+      "mov.b64 da2, {%3, %5};\n\t"
+      "mov.b64 da3, {%4, %5};\n\t"
+      "mov.b64 db0, {%6, %10};\n\t"
+      "mov.b64 db1, {%7, %10};\n\t"
+      "mov.b64 db2, {%8, %10};\n\t"
+      "mov.b64 db3, {%9, %10};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], da0, db0, %11, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], da1, db1, %11, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], da2, db2, %11, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], da3, db3, %11, 1;\n\t}" ::"r"(d),
+      "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(ahi), "r"(b0), "r"(b1), "r"(b2), "r"(b3), "r"(bhi), "r"(idesc),
+      "r"(acc0)
+      : "memory");
+}
+
 struct RtcArgs {
   const uint8_t *tab;       // rtc_table_bytes
   u64 *acc;                 // [B][18]: H for the nine candidates, then GA (atomically added)
@@ -300,11 +326,16 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
         const int G = gb + q, Gr = G - G0;
         // sets by the part-relative group index: the epilogue reads sets 0 .. nsets_used-1
         const uint32_t d = taddr + (uint32_t)((Gr & (g.nsets - 1)) * 64);
-        for (int k = 0; k < kc; ++k) {
-          const bool first = Gr < g.nsets && j0 == 0 && k == 0;
-          // A: bytes 32k .. 32k+31 of rows 6q .. 6q+7 of every frame box
-          mma_i8_elect(d, alo + (uint32_t)((6 * q * 128 + 32 * k) >> 4), ahi,
-                       blo + (uint32_t)((q * RTC_KS + k) * RTC_BT >> 4), bhi, idesc, first ? 0u : 1u);
+        // A: bytes 32k .. 32k+31 of rows 6q .. 6q+7 of every frame box
+        const uint32_t aq = alo + (uint32_t)((6 * q * 128) >> 4), bq = blo + (uint32_t)((q * RTC_KS * RTC_BT) >> 4);
+        const uint32_t acc0 = (Gr < g.nsets && j0 == 0) ? 0u : 1u;
+        if (kc == 4) {
+          mma_i8_k4_elect(d, aq, aq + 2, aq + 4, aq + 6, ahi, bq, bq + (RTC_BT >> 4), bq + 2 * (RTC_BT >> 4),
+                          bq + 3 * (RTC_BT >> 4), bhi, idesc, acc0);
+        } else {
+          for (int k = 0; k < kc; ++k)
+            mma_i8_elect(d, aq + (uint32_t)(2 * k), ahi, bq + (uint32_t)(k * (RTC_BT >> 4)), bhi, idesc,
+                         k == 0 ? acc0 : 1u);
         }
       }
       mma_commit_elect(&empty[s]);
