@@ -150,6 +150,30 @@ def test_tensor_core_refine_equals_cuda_core_refine(c, T, parts, monkeypatch):
         assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("m,n,levels,w,T", [(200, 136, 1, 9, 37), (98, 72, 1, 5, 21), (260, 200, 2, 6, 18),
+                                           (64, 64, 1, 4, 5)])
+def test_tensor_core_refine_ragged_shapes(m, n, levels, w, T, monkeypatch):
+    """Tensor-core refine vs CUDA-core refine on ragged shapes: row counts that are not
+    multiples of the 6-row groups or the 5-group stages, widths that are not multiples of
+    the 64-pixel strips, partial frame groups, both refine levels; random frames plus
+    exact translates with odd and even shifts (every alignment class)."""
+    rng = np.random.default_rng(m * 7 + n + w)
+    tp = rng.integers(0, 4096, size=(m, n)).astype(np.uint16)
+    fr = rng.integers(0, 4096, size=(T, m, n)).astype(np.uint16)
+    for k in range(min(T, 8)):
+        fr[k] = pf.translate_zero_fill(tp, (k % 5) - 2, (3 * k % 7) - 3)
+    frames = torch.from_numpy(fr).to(DEV)
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("MOCO_RTC", mode)
+        p = Plan(m, n, w, levels, "u16", 12, device=0)
+        p.set_template(torch.from_numpy(tp).to(DEV))
+        sh, fm, co, _ = p.align(frames, corrected=True)
+        out[mode] = (sh, fm, co.view(torch.int16))
+    for a, b in zip(out["1"], out["0"]):
+        assert torch.equal(a, b)
+
+
 def test_refine_all_alignments():
     """Refine+apply at every column misalignment of the doubled shift (the fused
     kernel specialises on (T-1) mod 8): exact translates with dx = -9..9."""
