@@ -48,10 +48,15 @@ __global__ void probe(int N, int mode, int reps, unsigned long long *out) {
       mma_i8_x2_elect(t0c, t1c, alo, alo + 128, ahi, blo, bhi, idesc, acc);
       mma_i8_x2_elect(t0c, t1c, alo + 8, alo + 136, ahi, blo + 256, bhi, idesc, acc);
       alo = alo0 + ((alo - alo0 + 16) & 1023);
-      if (mode >= 1) {
-        mma_commit_elect(&cb[g & 7]);
+      if (mode >= 1 && (mode != 4 || (g & 1))) {   // mode 4: commit every 8 MMAs (2 groups)
+        const int c = mode == 4 ? g >> 1 : g;
+        mma_commit_elect(&cb[c & 7]);
         __syncwarp();
-        if (mode == 2 && g >= 7) mbar_wait(&cb[(g - 7) & 7], ((g - 7) >> 3) & 1);
+        if ((mode == 2 || mode == 4) && c >= 7) mbar_wait(&cb[(c - 7) & 7], ((c - 7) >> 3) & 1);
+        if (mode == 4) {
+          mbar_wait(done, 0);
+          tc_fence_after();
+        }
       }
     }
     mma_commit_elect(bar);
@@ -70,8 +75,8 @@ int main() {
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 201 * 1024);
   const int reps = 4096;
   const int Ns[4] = {64, 128, 192, 256};
-  for (int mode = 0; mode < 4; ++mode)
-    for (int ni = 2; ni < 4; ++ni) {
+  for (int mode = 0; mode < 5; ++mode)
+    for (int ni = 1; ni < 4; ++ni) {
       const int N = Ns[ni], grid = 148;
       probe<<<grid, 128, 201 * 1024>>>(N, mode, reps, d);
       cudaError_t e = cudaDeviceSynchronize();
