@@ -462,6 +462,23 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
       }
     }
   if (rc != MOCO_OK) { plan_free(p); return rc; }
+  // refine kernels' shared-memory limits, on this plan's device (function attributes are
+  // per device: a process may hold plans on several GPUs)
+  if (dtype == MOCO_U16 && levels > 0) {
+    int smem = 0;
+    bool any_rtc = false;
+    for (int l = 0; l < levels; ++l) {
+      smem = std::max(smem, rs_smem_bytes(p->rrt[l], p->rstages[l]));
+      any_rtc = any_rtc || p->rtab[l] != nullptr;
+    }
+    if (cudaFuncSetAttribute(k_refine_sums<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+        cudaFuncSetAttribute(k_refine_sums<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+        (any_rtc &&
+         cudaFuncSetAttribute(k_refine_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, RTC_SMEM) != cudaSuccess)) {
+      plan_free(p);
+      return set_cuda_err(cudaGetLastError(), "refine kernel attributes");
+    }
+  }
   p->algo = MOCO_ALGO_DIRECT;
   const bool tc_ok = tc_supported(p->dtype, p->bits, p->levels, p->w, p->ml[levels], p->nl[levels]);
   if (tc_ok && tc_auto_prefers(p->w)) {
@@ -683,11 +700,6 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
   if (!corr) b.parts = 1;
   if (rtc) {
     ProfScope ps(p, MOCO_K_REFINE, st);
-    static bool attr = false;
-    if (!attr) {
-      CK(cudaFuncSetAttribute(k_refine_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, RTC_SMEM));
-      attr = true;
-    }
     k_rtc_bucket<<<1, 1024, 0, st>>>(sin, (int)B, p->rperm, p->rmeta);
     RtcArgs r;
     r.tab = p->rtab[l]; r.acc = racc; r.shift_in = sin; r.perm = p->rperm; r.meta = p->rmeta;
@@ -712,12 +724,6 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
   } else {
     ProfScope ps(p, MOCO_K_REFINE, st);
     const int smem = rs_smem_bytes(a.rt, a.stages);
-    static int attr_smem = 0;
-    if (smem > attr_smem) {
-      CK(cudaFuncSetAttribute(k_refine_sums<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      CK(cudaFuncSetAttribute(k_refine_sums<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attr_smem = smem;
-    }
     const int nct = (a.nl + RS_CT - 1) / RS_CT;
     if (a.wide) k_refine_sums<true><<<(unsigned)(a.nrt * nct), RS_THREADS, smem, st>>>(tmF, a);
     else k_refine_sums<false><<<(unsigned)(a.nrt * nct), RS_THREADS, smem, st>>>(tmF, a);
