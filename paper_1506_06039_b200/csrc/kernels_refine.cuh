@@ -145,16 +145,6 @@ template <int N>
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-// 10 consecutive samples starting OFF elements into the 16 held by (lo, hi).
-template <int OFF>
-__device__ __forceinline__ void extract10(const uint4 &lo, const uint4 &hi, uint32_t (&v)[10]) {
-  const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-#pragma unroll
-  for (int x = 0; x < 10; ++x) {
-    const int e = OFF + x;   // e == 16 only for OFF == 7: set by the caller
-    if (e < 16) v[x] = (e & 1) ? (w[e >> 1] >> 16) : (w[e >> 1] & 0xffffu);
-  }
-}
 
 // Frame row window for template columns j0..j0+7: the 10 samples at frame columns
 // j0+T-1 .. j0+T+8 (staged columns j0+OFFA .. j0+OFFA+9), plus the three 8-wide sums

@@ -112,11 +112,6 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes
 __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
-// the same with zero fill: src_bytes (0 or 16) bytes are read, the rest of the 16 written as 0
-__device__ __forceinline__ void cp_async16_zfill(void *dst, const void *src, uint32_t src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
-               : "memory");
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -250,50 +245,6 @@ struct TcPrepArgs {
   u64 *ga;                  // [B][W*W]
 };
 
-// One CTA per operand group of F frames.  Shared: per frame, edge-row and edge-column
-// sums of a^2, the four (hw+1)^2 corner tables and the total.
-// Coarse values of 16 consecutive coarse columns as 8 pair-words P[k] = v[2k] | v[2k+1]<<16.
-// L=0: the raw words are the pairs.  L=1: rows 2r and 2r+1 are added word-wise (each
-// 16-bit half < 2^13, no carry), then the two halves of each word (raw columns 2c,
-// 2c+1 of coarse column c) are folded with two byte-permutes and one add.
-template <int L>
-__device__ __forceinline__ void coarse_pairs(const uint16_t *base, int n, uint32_t (&P)[8]) {
-  if constexpr (L == 0) {
-    const uint4 u0 = *reinterpret_cast<const uint4 *>(base);
-    const uint4 u1 = *reinterpret_cast<const uint4 *>(base + 8);
-    P[0] = u0.x; P[1] = u0.y; P[2] = u0.z; P[3] = u0.w;
-    P[4] = u1.x; P[5] = u1.y; P[6] = u1.z; P[7] = u1.w;
-  } else if constexpr (L == 1) {
-    uint32_t s[16];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint4 x = *reinterpret_cast<const uint4 *>(base + q * 8);
-      const uint4 y = *reinterpret_cast<const uint4 *>(base + n + q * 8);
-      s[4 * q + 0] = x.x + y.x; s[4 * q + 1] = x.y + y.y;
-      s[4 * q + 2] = x.z + y.z; s[4 * q + 3] = x.w + y.w;
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      P[k] = __byte_perm(s[2 * k], s[2 * k + 1], 0x5410) + __byte_perm(s[2 * k], s[2 * k + 1], 0x7632);
-  } else {
-    uint32_t v[16];
-#pragma unroll
-    for (int x = 0; x < 16; ++x) v[x] = 0;
-    constexpr int bs = 1 << L;
-#pragma unroll
-    for (int dy = 0; dy < bs; ++dy)
-#pragma unroll
-      for (int q = 0; q < 2 * bs; ++q) {
-        const uint4 u = *reinterpret_cast<const uint4 *>(base + (int64_t)dy * n + q * 8);
-        const uint32_t ws[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-        for (int e = 0; e < 8; ++e) v[(q * 8 + e) / bs] += (ws[e >> 1] >> (16 * (e & 1))) & 0xffffu;
-      }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) P[k] = v[2 * k] | (v[2 * k + 1] << 16);
-  }
-}
-
 // 8 consecutive coarse values (2^L x 2^L block sums) of one coarse row as 4 pair-words.
 template <int L>
 __device__ __forceinline__ void coarse8(const uint16_t *base, int n, uint32_t (&P)[4]) {
@@ -337,6 +288,8 @@ __device__ __forceinline__ void coarse8(const uint16_t *base, int n, uint32_t (&
 }
 
 template <int L>
+// One CTA per operand group of F frames.  Shared: per frame, edge-row and edge-column
+// sums of a^2, the four (hw+1)^2 corner tables and the total.
 #ifndef TC_PREP_RPP
 #define TC_PREP_RPP 2
 #endif
