@@ -73,6 +73,7 @@ struct TcPlan {
   uint8_t *G2 = nullptr;    // second buffers: the prep of batch k+1 overlaps batch k
   u64 *ga2 = nullptr;
   uint8_t *T8 = nullptr;    // template parts [2][mc][nc]
+  uint8_t *Btab = nullptr;  // the B tiles of every (strip, pair), built once per template (or null)
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -488,6 +489,7 @@ __global__ void __launch_bounds__(256, TC_PREP_MINB) k_tc_prep(TcPrepArgs a) {
 struct TcArgs {
   const uint8_t *G;
   const uint8_t *T8;     // template parts [2][mc][nc]
+  const uint8_t *Btab;   // [nstrips][npairs][N*32] precomputed B tiles, or null: built by the producers
   const u64 *ga;         // [B][W*W]
   const u64 *gb;         // [W*W]
   TcGeom g;
@@ -670,6 +672,21 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
     }
     int st = p / per_strip, i0 = (p % per_strip) * ICH;   // strip, first pair of the super-stage
     const int ss = p;
+    if (a.Btab) {
+      // B tiles precomputed per template: one bulk copy of the super-stage's ICH tiles
+      const uint32_t bytes = (uint32_t)(ICH * N * 32);
+      int round = 0;
+      for (int u = p; u < nsuper; u += TC_PRODUCERS, ++round) {
+        if (round > 0) mbar_wait(&empty[ss], (round - 1) & 1);
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&full[ss], bytes);
+          bulk_g2s(Bring + ss * ICH * N * 32, a.Btab + ((int64_t)st * g.npairs + i0) * (N * 32), bytes, &full[ss]);
+        }
+        __syncwarp();
+        i0 += TC_PRODUCERS * ICH;
+        while (i0 >= g.npairs) { i0 -= g.npairs; ++st; }
+      }
+    } else {
     // The band of template-part rows a super-stage reads (ICH pairs x 2 parts x 2 rows x
     // SEGB bytes) is staged in shared memory with LDGSTS one super-stage ahead: the tile
     // build then waits on shared-memory latency only (the T8 band of a strip does not
@@ -729,6 +746,7 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
       i0 = ni0;
     }
     cp_async_wait<0>();
+    }
   }
   // all MMAs done -> accumulators final.  Every warp must be converged before the
   // .sync.aligned TMEM loads (threads can leave the mbarrier spin at different times).
@@ -863,6 +881,26 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
   TC_T(if (tid == 0 && (blockIdx.x % 149 == 0)) printf("TCT cta %d mma_cycles %lld total %llu mma_done %llu issue_end %llu wait_strip %llu wait_full %llu wait_empty %llu\n", blockIdx.x, c_mma - c_start, (unsigned long long)(gtimer() - t_start), (unsigned long long)(t_mma - t_start), (unsigned long long)(t_issue - t_start), (unsigned long long)w_strip, (unsigned long long)w_full, (unsigned long long)w_empty);)
 }
 
+// The B tile of every (strip st, pair i), as the producers would build it: row n = (d,
+// pb, t), half h: bytes T8[pb][2i+d][TPAD + 32 st + 16h - (t - hw) + x], zero rows for
+// t >= W; core-matrix layout (n>>3)*256 + h*128 + (n&7)*16.
+__global__ void k_tc_btab(const uint8_t *__restrict__ T8, TcGeom g, uint8_t *__restrict__ tab) {
+  const int tile = g.N * 32;
+  const int64_t total = (int64_t)g.nstrips * g.npairs * tile;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int off = (int)(e % tile);
+    const int64_t ti_ = e / tile;
+    const int st = (int)(ti_ / g.npairs), i = (int)(ti_ % g.npairs);
+    const int n = (off >> 8) * 8 + ((off & 127) >> 4), h = (off >> 7) & 1, x = off & 15;
+    const int d = n >= g.N1 ? 1 : 0, r = n - d * g.N1;
+    const int pb = r >= g.Wt ? 1 : 0, t = r - pb * g.Wt;
+    uint8_t v = 0;
+    if (t < g.W)
+      v = T8[(int64_t)pb * (g.mc + 2) * g.TP + (int64_t)(2 * i + d) * g.TP + 32 * st + 16 * h - (t - g.hw) + g.TPAD + x];
+    tab[e] = v;
+  }
+}
+
 // template parts for the B operand, zero-padded rows: T8[pb][i][TPAD + j] =
 // (b >> 7, b & 127)[pb] for j in [0, nc), 0 in the pads
 __global__ void k_tc_template(const uint16_t *__restrict__ b, int pitch, int mc, int nc, int TPAD, int TP,
@@ -973,6 +1011,13 @@ inline int tc_init(TcPlan *tc, int w, int mc, int nc, int L, int64_t cap) {
     tc->ga2 = nullptr;
   }
   if (cudaMalloc(&tc->T8, (size_t)2 * (mc + 2) * g.TP) != cudaSuccess) return -1;
+  // precomputed B tiles (MOCO_TC_BTAB=0: the producer warps build them per CTA)
+  const char *bt = getenv("MOCO_TC_BTAB");
+  if (!(bt && atoi(bt) == 0) &&
+      cudaMalloc(&tc->Btab, (size_t)g.nstrips * g.npairs * g.N * 32) != cudaSuccess) {
+    cudaGetLastError();
+    tc->Btab = nullptr;
+  }
   if (cudaFuncSetAttribute(k_tc_coarse<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_tc_coarse<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_tc_coarse<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
@@ -993,6 +1038,7 @@ inline int tc_init(TcPlan *tc, int w, int mc, int nc, int L, int64_t cap) {
 inline int tc_set_template(TcPlan *tc, const uint16_t *tpl_coarse, int pitch, cudaStream_t st) {
   const TcGeom &g = tc->g;
   k_tc_template<<<128, 256, 0, st>>>(tpl_coarse, pitch, g.mc, g.nc, g.TPAD, g.TP, tc->T8);
+  if (tc->Btab) k_tc_btab<<<512, 256, 0, st>>>(tc->T8, g, tc->Btab);
   if (cudaGetLastError() != cudaSuccess) return -1;
   tc->tpl_ready = true;
   return 0;
@@ -1005,7 +1051,8 @@ inline void tc_free(TcPlan *tc) {
   if (tc->ga2) cudaFree(tc->ga2);
   tc->G2 = nullptr; tc->ga2 = nullptr;
   if (tc->T8) cudaFree(tc->T8);
-  tc->G = nullptr; tc->ga = nullptr; tc->T8 = nullptr;
+  if (tc->Btab) cudaFree(tc->Btab);
+  tc->G = nullptr; tc->ga = nullptr; tc->T8 = nullptr; tc->Btab = nullptr;
   tc->ready = tc->tpl_ready = false;
 }
 

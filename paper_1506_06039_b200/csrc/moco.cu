@@ -847,7 +847,7 @@ static int launch_tc_coarse(moco_plan *p, int64_t B, const uint8_t *G, const u64
   const TcGeom &g = p->tc.g;
   const int64_t groups = (B + g.F - 1) / g.F;
   TcArgs ta;
-  ta.G = G; ta.T8 = p->tc.T8; ta.ga = ga; ta.gb = (const u64 *)p->gb; ta.g = g;
+  ta.G = G; ta.T8 = p->tc.T8; ta.Btab = p->tc.Btab; ta.ga = ga; ta.gb = (const u64 *)p->gb; ta.g = g;
   ta.scale = (double)(1u << (4 * p->levels)); ta.B = (int)B;
   ta.shift_out = shift_out; ta.f_out = f_out; ta.flags = flags; ta.grid_out = grid_out;
   {
