@@ -370,7 +370,10 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
         const int f = cw + fk * RTC_CW;
         if (f >= nf) continue;
         const unsigned char *st = stg + s * RTC_STAGE + f * RTC_SLOT;
-        for (int rb = 0; rb < nrow; rb += 8) {
+#pragma unroll
+        for (int rq = 0; rq < RTC_R / 8; ++rq) {   // fixed trip count: loads of all row blocks in flight
+          const int rb = rq * 8;
+          if (rb >= nrow) break;
           const int rr = rb + lr;
           const int pr = r_lo + rr;
           const int rc = pr < 2 ? pr : (pr >= g.ml ? pr - g.ml + 2 : 4);
