@@ -932,11 +932,12 @@ inline bool tc_make_geom(TcGeom *gp, int w, int mc, int nc, int L) {
   const char *ce = getenv("MOCO_TC_CTAS");   // tuning experiments: CTAs per SM target
   const int ctas = ce ? std::max(1, atoi(ce)) : 1;
   const int smem_cap = (228 * 1024) / ctas - 1024, tmem_cap = 512 / ctas;
-  // frames per group: the fewest padded lag rows with NT*N within TMEM; ties -> F = 2
-  // (one M tile per group: every MMA of a pair step shares the B tile)
+  // frames per group: the fewest padded lag rows with NT*N within TMEM; ties -> F = 1
+  // (measured with B tiles from the per-template table: C1 1.027 -> 1.048 M, C3 868 -> 921 k
+  // frames/s over F = 2)
   int bestF = 0, bestRows = 1 << 30;
   const char *fe = getenv("MOCO_TC_F");   // tuning experiments
-  for (int F : {2, 4, 1}) {
+  for (int F : {1, 2, 4}) {
     if (fe && atoi(fe) != F) continue;
     const int ST = 64 / F, NT = (lagrows + ST - 1) / ST;
     if (NT * g.N > tmem_cap) continue;
