@@ -53,6 +53,7 @@ struct TcGeom {
   int stripB;   // 2 planes
   int TPAD, TP; // padded template parts: TP = nc + 2*TPAD bytes per row, zeros in the pads
   int SEGB;     // bytes of one template part row a strip's B tiles read: 32 + 2*TPAD
+  int stg;      // 1: the producers build B tiles from a staged template band (no tile table)
   int TS;       // TMEM columns between accumulator tiles (N, or 256 when there is room)
   int ICH;      // template-row pairs per super-stage (one ring slot per producer warp)
   int ctas;     // CTAs per SM the geometry is sized for
@@ -551,8 +552,8 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
   unsigned char *As = smem;                                   // [GG] strips of 2 planes
   unsigned char *Bring = As + GG * g.stripB;                  // [NSS][ICH][N*32]
   const int SEGB = g.SEGB, PAIRB = 4 * SEGB;
-  unsigned char *Stg = Bring + NSS * ICH * N * 32;            // [NSS][2][ICH][pb][d][SEGB]
-  uint64_t *bars = reinterpret_cast<uint64_t *>(Stg + NSS * 2 * ICH * PAIRB);
+  unsigned char *Stg = Bring + NSS * ICH * N * 32;            // [NSS][2][ICH][pb][d][SEGB] (g.stg only)
+  uint64_t *bars = reinterpret_cast<uint64_t *>(Stg + (g.stg ? NSS * 2 * ICH * PAIRB : 0));
   uint64_t *full = bars, *empty = bars + NSS, *aload = bars + 2 * NSS;
   uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * NSS + 1);
   const int grp0 = blockIdx.x * GG;
@@ -953,8 +954,11 @@ inline bool tc_make_geom(TcGeom *gp, int w, int mc, int nc, int L) {
   g.TP = nc + 2 * g.TPAD;
   g.npairs = (mc + 1) / 2;
   g.SEGB = 32 + 2 * g.TPAD;
+  // B tiles from the per-template table unless MOCO_TC_BTAB=0 (then the band staging area)
+  const char *bte = getenv("MOCO_TC_BTAB");
+  g.stg = (bte && atoi(bte) == 0) ? 1 : 0;
   auto smem_for = [&](int GG, int ICH) {
-    return 1024 + GG * g.stripB + TC_PRODUCERS * ICH * g.N * 32 + TC_PRODUCERS * 2 * ICH * 4 * g.SEGB +
+    return 1024 + GG * g.stripB + TC_PRODUCERS * ICH * g.N * 32 + g.stg * TC_PRODUCERS * 2 * ICH * 4 * g.SEGB +
            (2 * TC_PRODUCERS + 1) * 8 + 16;
   };
   // two CTAs per SM (one loads its next strip while the other computes): as many
@@ -1013,12 +1017,7 @@ inline int tc_init(TcPlan *tc, int w, int mc, int nc, int L, int64_t cap) {
   }
   if (cudaMalloc(&tc->T8, (size_t)2 * (mc + 2) * g.TP) != cudaSuccess) return -1;
   // precomputed B tiles (MOCO_TC_BTAB=0: the producer warps build them per CTA)
-  const char *bt = getenv("MOCO_TC_BTAB");
-  if (!(bt && atoi(bt) == 0) &&
-      cudaMalloc(&tc->Btab, (size_t)g.nstrips * g.npairs * g.N * 32) != cudaSuccess) {
-    cudaGetLastError();
-    tc->Btab = nullptr;
-  }
+  if (!g.stg && cudaMalloc(&tc->Btab, (size_t)g.nstrips * g.npairs * g.N * 32) != cudaSuccess) return -1;
   if (cudaFuncSetAttribute(k_tc_coarse<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_tc_coarse<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
       cudaFuncSetAttribute(k_tc_coarse<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
