@@ -108,6 +108,24 @@ def test_tc_equals_direct_whole_stack(c, T):
     assert torch.equal(out["tc"][2], out["direct"][2])
 
 
+@pytest.mark.parametrize("c,T", [(1, 300), (2, 600), (3, 150)])
+def test_tc_btile_table_equals_in_cta_build(c, T, monkeypatch):
+    """TC search with B tiles bulk-copied from the per-template table (default) and built
+    in every CTA from the staged template band (MOCO_TC_BTAB=0, other super-stage sizes):
+    identical shifts, f_min and edge flags."""
+    spec = config_spec(c, T=T)
+    st = make_stack(spec, 0, T, device=DEV)
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("MOCO_TC_BTAB", mode)
+        p = _plan_for(spec, "tc")
+        p.set_template(st.template)
+        sh, fm, _, fl = p.align(st.frames, corrected=False, flags=True)
+        out[mode] = (sh, fm, fl)
+    for a, b in zip(out["1"], out["0"]):
+        assert torch.equal(a, b)
+
+
 @pytest.mark.parametrize("c,T", [(2, 2100), (4, 24)])
 def test_fused_refine_equals_simple_refine(c, T, monkeypatch):
     """The fused, register-blocked refine+apply kernel and the simple one-candidate-
