@@ -54,6 +54,7 @@ struct TcGeom {
   int TPAD, TP; // padded template parts: TP = nc + 2*TPAD bytes per row, zeros in the pads
   int SEGB;     // bytes of one template part row a strip's B tiles read: 32 + 2*TPAD
   int stg;      // 1: the producers build B tiles from a staged template band (no tile table)
+  int nss;      // ring slots (= active producer warps): 7 when building, TC_TSLOTS when copying
   int TS;       // TMEM columns between accumulator tiles (N, or 256 when there is room)
   int ICH;      // template-row pairs per super-stage (one ring slot per producer warp)
   int ctas;     // CTAs per SM the geometry is sized for
@@ -529,6 +530,7 @@ __device__ __forceinline__ uint64_t gtimer() {
 #endif
 constexpr int TC_THREADS = 256;
 constexpr int TC_PRODUCERS = 7;
+constexpr int TC_TSLOTS = 4;   // ring slots with the B-tile table (copies are cheap; fewer slots, larger super-stages)
 
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
@@ -547,7 +549,7 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
   unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int F = g.F, hw = g.hw, mc = g.mc, nc = g.nc, N = g.N, N1 = g.N1, NT = g.NT, GG = g.GG;
-  constexpr int NSS = TC_PRODUCERS;                            // one ring slot per producer warp
+  const int NSS = g.nss;                                       // one ring slot per active producer warp
   const int ICH = g.ICH;
   unsigned char *As = smem;                                   // [GG] strips of 2 planes
   unsigned char *Bring = As + GG * g.stripB;                  // [NSS][ICH][N*32]
@@ -677,14 +679,14 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
       // B tiles precomputed per template: one bulk copy of the super-stage's ICH tiles
       const uint32_t bytes = (uint32_t)(ICH * N * 32);
       int round = 0;
-      for (int u = p; u < nsuper; u += TC_PRODUCERS, ++round) {
+      for (int u = p; p < NSS && u < nsuper; u += NSS, ++round) {
         if (round > 0) mbar_wait(&empty[ss], (round - 1) & 1);
         if (lane == 0) {
           mbar_arrive_expect_tx(&full[ss], bytes);
           bulk_g2s(Bring + ss * ICH * N * 32, a.Btab + ((int64_t)st * g.npairs + i0) * (N * 32), bytes, &full[ss]);
         }
         __syncwarp();
-        i0 += TC_PRODUCERS * ICH;
+        i0 += NSS * ICH;
         while (i0 >= g.npairs) { i0 -= g.npairs; ++st; }
       }
     } else {
@@ -957,9 +959,11 @@ inline bool tc_make_geom(TcGeom *gp, int w, int mc, int nc, int L) {
   // B tiles from the per-template table unless MOCO_TC_BTAB=0 (then the band staging area)
   const char *bte = getenv("MOCO_TC_BTAB");
   g.stg = (bte && atoi(bte) == 0) ? 1 : 0;
+  const char *nse = getenv("MOCO_TC_SLOTS");   // tuning: ring slots when copying tiles
+  g.nss = g.stg ? TC_PRODUCERS : (nse ? std::max(2, std::min(TC_PRODUCERS, atoi(nse))) : TC_TSLOTS);
   auto smem_for = [&](int GG, int ICH) {
-    return 1024 + GG * g.stripB + TC_PRODUCERS * ICH * g.N * 32 + g.stg * TC_PRODUCERS * 2 * ICH * 4 * g.SEGB +
-           (2 * TC_PRODUCERS + 1) * 8 + 16;
+    return 1024 + GG * g.stripB + g.nss * ICH * g.N * 32 + g.stg * TC_PRODUCERS * 2 * ICH * 4 * g.SEGB +
+           (2 * g.nss + 1) * 8 + 16;
   };
   // two CTAs per SM (one loads its next strip while the other computes): as many
   // groups per CTA as half of shared memory and half of TMEM allow, then the largest
@@ -969,7 +973,7 @@ inline bool tc_make_geom(TcGeom *gp, int w, int mc, int nc, int L) {
   g.ctas = ctas;
   for (int GG = 4; GG >= 1 && !g.GG; --GG) {
     if (GG * g.NT * g.N > tmem_cap || GG * g.NT > 4) continue;
-    for (int ICH = 4; ICH >= 1; ICH /= 2) {
+    for (int ICH = 8; ICH >= 1; ICH /= 2) {
       const int sm = smem_for(GG, ICH);
       if (g.npairs % ICH == 0 && sm <= smem_cap && GG * g.NT * 128 * 132 + GG * 128 * 16 + GG * g.F * g.W * g.W * 8 <= sm - 1024 - 256) {
         g.GG = GG;
