@@ -16,10 +16,11 @@
 // (A-row lags s' in [-(w-1), w]).  Pairing halves the MMA instructions and the A-operand
 // shared-memory reads per multiply-accumulate.
 //
-// Exactness: coarse values are < 2^14 (bits + 2L <= 14); each is split
-// into two 7-bit parts v = 128*hi + lo, both in [0,127], so every int8 product is exact
-// and every int32 accumulator stays below 127^2 * m_c * n_c < 2^31.  The epilogue
-// recombines h = 2^14 D_hh + 2^7 (D_hl + D_lh) + D_ll in 64-bit integers, so
+// Exactness: coarse values < 2^14 (bits + 2L <= 14) are split into two
+// 7-bit parts v = 128*hi + lo, values < 2^16 into their two bytes (sb = 8), so every u8
+// product is exact and every int32 accumulator (one product per template-row pair and
+// column) stays below (2^sb - 1)^2 * ceil(m_c/2) * n_c < 2^31.  The epilogue recombines
+// h = 2^(2 sb) D_hh + 2^sb (D_hl + D_lh) + D_ll in 64-bit integers, so
 // N = g_a + g_b - 2h is EXACT and f = fl(N / (16^L A)) is bit-identical to the
 // oracle's -- no certification step is needed.
 //
@@ -55,6 +56,7 @@ struct TcGeom {
   int SEGB;     // bytes of one template part row a strip's B tiles read: 32 + 2*TPAD
   int stg;      // 1: the producers build B tiles from a staged template band (no tile table)
   int nss;      // ring slots (= active producer warps): 7 when building, TC_TSLOTS when copying
+  int sb;       // bits per operand part: 7 (coarse values < 2^14) or 8 (< 2^16)
   int TS;       // TMEM columns between accumulator tiles (N, or 256 when there is room)
   int ICH;      // template-row pairs per super-stage (one ring slot per producer warp)
   int ctas;     // CTAs per SM the geometry is sized for
@@ -332,7 +334,7 @@ __global__ void __launch_bounds__(256, TC_PREP_MINB) k_tc_prep(TcPrepArgs a) {
   // coarse rows of <= 256 values: each lane owns one 8-column chunk, so its edge-column
   // squares (< 2^28 each: coarse values < 2^14) accumulate in 32-bit registers and are
   // flushed to the warp's shared sums every 16 rows
-  const bool one_chunk = nchunk <= 32;
+  const bool one_chunk = nchunk <= 32 && g.sb == 7;   // 32-bit edge accumulators: 14-bit values only
   uint32_t eacc[8];
 #pragma unroll
   for (int x = 0; x < 8; ++x) eacc[x] = 0;
@@ -350,11 +352,13 @@ __global__ void __launch_bounds__(256, TC_PREP_MINB) k_tc_prep(TcPrepArgs a) {
   };
   auto item = [&](int pr, const uint32_t (&P)[4], int cc, bool live, u64 &rs) {
     const int cr = pr - hw;
-    const uint32_t h0 = (P[0] >> 7) & 0x007F007Fu, h1 = (P[1] >> 7) & 0x007F007Fu;
-    const uint32_t h2 = (P[2] >> 7) & 0x007F007Fu, h3 = (P[3] >> 7) & 0x007F007Fu;
+    // parts of g.sb bits (7: v = 128 hi + lo; 8: the two bytes of a 16-bit coarse value)
+    const uint32_t pm = g.sb == 7 ? 0x007F007Fu : 0x00FF00FFu, sb = (uint32_t)g.sb;
+    const uint32_t h0 = (P[0] >> sb) & pm, h1 = (P[1] >> sb) & pm;
+    const uint32_t h2 = (P[2] >> sb) & pm, h3 = (P[3] >> sb) & pm;
     const uint2 hi = make_uint2(__byte_perm(h0, h1, 0x6420), __byte_perm(h2, h3, 0x6420));
-    const uint2 lo = make_uint2(__byte_perm(P[0] & 0x007F007Fu, P[1] & 0x007F007Fu, 0x6420),
-                                __byte_perm(P[2] & 0x007F007Fu, P[3] & 0x007F007Fu, 0x6420));
+    const uint2 lo = make_uint2(__byte_perm(P[0] & pm, P[1] & pm, 0x6420),
+                                __byte_perm(P[2] & pm, P[3] & pm, 0x6420));
     uint8_t *dst = a.G + ((((int64_t)grp * g.nstrips + (cc >> 2)) * 2 + ((cc >> 1) & 1)) * g.R + pr) * (32 * F) +
                    f * 32 + (cc & 1) * 8;
     *reinterpret_cast<uint2 *>(dst) = hi;
@@ -363,10 +367,15 @@ __global__ void __launch_bounds__(256, TC_PREP_MINB) k_tc_prep(TcPrepArgs a) {
     uint32_t v[8];
 #pragma unroll
     for (int k = 0; k < 4; ++k) { v[2 * k] = P[k] & 0xffffu; v[2 * k + 1] = P[k] >> 16; }
-    uint32_t cs = 0;
+    if (g.sb == 7) {
+      uint32_t cs = 0;
 #pragma unroll
-    for (int x = 0; x < 8; ++x) cs += v[x] * v[x];   // 8 terms < 2^28: < 2^31
-    rs += cs;
+      for (int x = 0; x < 8; ++x) cs += v[x] * v[x];   // 8 terms < 2^28: < 2^31
+      rs += cs;
+    } else {
+#pragma unroll
+      for (int x = 0; x < 8; ++x) rs += (u64)(v[x] * v[x]);   // each < 2^32
+    }
     const int c0 = cc * 8;
     const bool eL = c0 < hw, eR = c0 + 8 > nc - hw;
     if (!(eL || eR)) return;
@@ -840,8 +849,9 @@ __global__ void __launch_bounds__(TC_THREADS, 3) k_tc_coarse(TcArgs a) {   // <=
           const uint32_t pl = __shfl_xor_sync(0xffffffffu, pa ? xl[j] : xl[j + 8], 1);
           const int ti = c + j + (pa ? 8 : 0);
           if (!valid || ti >= W) continue;
-          const u64 h = pa == 0 ? ((u64)mh << 14) + (((u64)ml + (u64)ph) << 7) + (u64)pl
-                                : ((u64)ph << 14) + (((u64)pl + (u64)mh) << 7) + (u64)ml;
+          const int sb = g.sb;   // h = 2^(2 sb) D_hh + 2^sb (D_hl + D_lh) + D_ll
+          const u64 h = pa == 0 ? ((u64)mh << (2 * sb)) + (((u64)ml + (u64)ph) << sb) + (u64)pl
+                                : ((u64)ph << (2 * sb)) + (((u64)pl + (u64)mh) << sb) + (u64)ml;
           const int lag = (s + hw) * W + ti;
           const u64 Nn = gas[(fi - fi0) * W * W + lag] + a.gb[lag] - 2 * h;
           const int t = ti - hw;
@@ -905,8 +915,8 @@ __global__ void k_tc_btab(const uint8_t *__restrict__ T8, TcGeom g, uint8_t *__r
 }
 
 // template parts for the B operand, zero-padded rows: T8[pb][i][TPAD + j] =
-// (b >> 7, b & 127)[pb] for j in [0, nc), 0 in the pads
-__global__ void k_tc_template(const uint16_t *__restrict__ b, int pitch, int mc, int nc, int TPAD, int TP,
+// (b >> sb, b & (2^sb - 1))[pb] for j in [0, nc), 0 in the pads
+__global__ void k_tc_template(const uint16_t *__restrict__ b, int pitch, int mc, int nc, int TPAD, int TP, int sb,
                               uint8_t *T8) {
   const int rows = mc + 2;   // zero rows past the template (second row of an odd-mc pair)
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 2 * rows * TP; e += gridDim.x * blockDim.x) {
@@ -915,16 +925,17 @@ __global__ void k_tc_template(const uint16_t *__restrict__ b, int pitch, int mc,
     uint8_t v = 0;
     if (j >= 0 && j < nc && i < mc) {
       const uint32_t x = b[(int64_t)i * pitch + j];
-      v = (uint8_t)(pb == 0 ? (x >> 7) : (x & 127u));
+      v = (uint8_t)(pb == 0 ? (x >> sb) : (x & ((1u << sb) - 1u)));
     }
     T8[e] = v;
   }
 }
 
 // ---------------------------------------------------------------- host side
-inline bool tc_make_geom(TcGeom *gp, int w, int mc, int nc, int L) {
+inline bool tc_make_geom(TcGeom *gp, int w, int mc, int nc, int L, int vb) {
   TcGeom g{};
   g.mc = mc; g.nc = nc; g.w = w; g.hw = w - 1; g.W = 2 * w - 1; g.L = L;
+  g.sb = vb <= 14 ? 7 : 8;
   g.Wt = (g.W + 15) / 16 * 16;
   g.N1 = 2 * g.Wt;
   g.N = 2 * g.N1;
@@ -994,10 +1005,13 @@ inline bool tc_make_geom(TcGeom *gp, int w, int mc, int nc, int L) {
 }
 
 inline bool tc_supported(int dtype, int bits, int levels, int w, int mc, int nc) {
-  if (dtype != 1 /*MOCO_U16*/ || bits + 2 * levels > 14) return false;
-  if (nc % 32 != 0 || (int64_t)mc * nc * 127 * 127 >= ((int64_t)1 << 31)) return false;
+  const int vb = bits + 2 * levels;
+  if (dtype != 1 /*MOCO_U16*/ || vb > 16) return false;
+  // an int32 accumulator adds one part product per template-row pair and column
+  const int64_t pmax = vb <= 14 ? 127 : 255;
+  if (nc % 32 != 0 || (int64_t)((mc + 1) / 2) * nc * pmax * pmax >= ((int64_t)1 << 31)) return false;
   TcGeom g;
-  return tc_make_geom(&g, w, mc, nc, levels);
+  return tc_make_geom(&g, w, mc, nc, levels, vb);
 }
 // AUTO policy (from measurement): the tensor-core search wherever it is
 // supported; otherwise the FFT path for 16-bit data (exact after certification), with
@@ -1005,8 +1019,8 @@ inline bool tc_supported(int dtype, int bits, int levels, int w, int mc, int nc)
 inline bool tc_auto_prefers(int w) { (void)w; return true; }
 inline bool fft_auto_prefers(int w, bool tc_ok) { (void)w; return !tc_ok; }
 
-inline int tc_init(TcPlan *tc, int w, int mc, int nc, int L, int64_t cap) {
-  if (!tc_make_geom(&tc->g, w, mc, nc, L)) return -1;
+inline int tc_init(TcPlan *tc, int w, int mc, int nc, int L, int vb, int64_t cap) {
+  if (!tc_make_geom(&tc->g, w, mc, nc, L, vb)) return -1;
   const TcGeom &g = tc->g;
   tc->cap = cap;
   const int64_t groups = (cap + g.F - 1) / g.F;
@@ -1041,7 +1055,7 @@ inline int tc_init(TcPlan *tc, int w, int mc, int nc, int L, int64_t cap) {
 
 inline int tc_set_template(TcPlan *tc, const uint16_t *tpl_coarse, int pitch, cudaStream_t st) {
   const TcGeom &g = tc->g;
-  k_tc_template<<<128, 256, 0, st>>>(tpl_coarse, pitch, g.mc, g.nc, g.TPAD, g.TP, tc->T8);
+  k_tc_template<<<128, 256, 0, st>>>(tpl_coarse, pitch, g.mc, g.nc, g.TPAD, g.TP, g.sb, tc->T8);
   if (tc->Btab) k_tc_btab<<<512, 256, 0, st>>>(tc->T8, g, tc->Btab);
   if (cudaGetLastError() != cudaSuccess) return -1;
   tc->tpl_ready = true;

@@ -482,7 +482,7 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
   p->algo = MOCO_ALGO_DIRECT;
   const bool tc_ok = tc_supported(p->dtype, p->bits, p->levels, p->w, p->ml[levels], p->nl[levels]);
   if (tc_ok && tc_auto_prefers(p->w)) {
-    if (tc_init(&p->tc, p->w, p->ml[levels], p->nl[levels], levels, p->cap) == 0) {
+    if (tc_init(&p->tc, p->w, p->ml[levels], p->nl[levels], levels, p->bits + 2 * levels, p->cap) == 0) {
       p->algo = MOCO_ALGO_TC;
       // whole waves of the tensor-core search per internal batch (CTAs/SM x GG*F frames)
       const int64_t wave = (int64_t)nsm * p->tc.g.ctas * p->tc.g.GG * p->tc.g.F;
@@ -533,7 +533,7 @@ int moco_plan_set_algo(moco_plan *p, int algo) {
     }
     if (!ok) return MOCO_EINVAL;
     CK(cudaSetDevice(p->device));
-    if (!p->tc.ready && tc_init(&p->tc, p->w, p->ml[L], p->nl[L], L, p->cap) != 0) return MOCO_ENOMEM;
+    if (!p->tc.ready && tc_init(&p->tc, p->w, p->ml[L], p->nl[L], L, p->bits + 2 * L, p->cap) != 0) return MOCO_ENOMEM;
     if (p->has_tpl && !p->tc.tpl_ready) {
       if (tc_set_template(&p->tc, (const uint16_t *)p->tpl[L], p->pitch[L], 0) != 0)
         return set_cuda_err(cudaGetLastError(), "tc_set_template");

@@ -91,7 +91,7 @@ def _run_config(c, T, sample, device_gen=True, algo=None, **over):
     return spec, st, sh, fm, fl, kinds, p
 
 
-@pytest.mark.parametrize("c,T", [(1, 1000), (2, 2100), (3, 300)])
+@pytest.mark.parametrize("c,T", [(1, 1000), (2, 2100), (3, 300), (4, 40)])
 def test_tc_equals_direct_whole_stack(c, T):
     """Tensor-core and CUDA-core coarse searches agree bit for bit on every frame
     (both are exact integer evaluations of the same N_{s,t})."""
