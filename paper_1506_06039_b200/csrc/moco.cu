@@ -90,6 +90,8 @@ struct moco_plan {
   cudaStream_t ps[3];
   cudaEvent_t pe_prep[2], pe_free[2], pe_sums[2], pe_pick[2], pe_start, pe_end, pe_end2;
   int32_t *sh1b;              // second level-1 shift buffer (pipeline)
+  int32_t *sh2b[2];           // coarse shifts at level 2 (pipeline, levels = 2)
+  void *scratch1b;            // second level-1 image buffer (pipeline, levels = 2)
   u64 *racc2;                 // second refine accumulator buffer (pipeline)
   // end-to-end staging
   bool host_ready;
@@ -213,6 +215,9 @@ static void plan_free(moco_plan *p) {
   for (cudaEvent_t e : {p->pe_start, p->pe_end, p->pe_end2})
     if (e) cudaEventDestroy(e);
   if (p->sh1b) cudaFree(p->sh1b);
+  for (int k = 0; k < 2; ++k)
+    if (p->sh2b[k]) cudaFree(p->sh2b[k]);
+  if (p->scratch1b) cudaFree(p->scratch1b);
   if (p->racc2) cudaFree(p->racc2);
   for (auto &r : p->prof_live) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : p->prof_pool) cudaEventDestroy(e);
@@ -427,6 +432,10 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
     alloc((void **)&p->racc, (size_t)p->cap * 18 * sizeof(u64));
     alloc((void **)&p->racc2, (size_t)p->cap * 18 * sizeof(u64));
     alloc((void **)&p->sh1b, (size_t)p->cap * 2 * sizeof(int32_t));
+    if (levels == 2) {   // align_tc_pipelined at two levels: coarse shifts, level-1 images
+      for (int k = 0; k < 2; ++k) alloc((void **)&p->sh2b[k], (size_t)p->cap * 2 * sizeof(int32_t));
+      alloc(&p->scratch1b, (size_t)p->cap * p->ml[1] * p->pitch[1] * p->esz[1]);
+    }
     if (rc == MOCO_OK && (cudaMemset(p->racc, 0, (size_t)p->cap * 18 * sizeof(u64)) != cudaSuccess ||
                           cudaMemset(p->racc2, 0, (size_t)p->cap * 18 * sizeof(u64)) != cudaSuccess))
       rc = MOCO_ENOMEM;
@@ -972,6 +981,12 @@ static int align_tc_pipelined(moco_plan *p, const void *d_frames, int64_t T, int
   u64 *ga[2] = {p->tc.ga, p->tc.ga2};
   int32_t *sh1[2] = {p->sh[1], p->sh1b};
   u64 *racc[2] = {p->racc, p->racc2};
+  // levels = 2: the coarse search lands at level 2 (sh2b), the level-1 image of the batch
+  // is downsampled on the prep stream (scratch[1] / scratch1b) and refined on the main
+  // stream (its pick too, since the level-0 refine reads its shifts) into sh1
+  const bool two = p->levels == 2;
+  void *img1[2] = {p->scratch[1], p->scratch1b};
+  const int64_t fs1 = (int64_t)p->ml[1] * p->pitch[1];
   int64_t k = 0;
   for (int64_t f0 = 0; f0 < T; f0 += p->cap, ++k) {
     const int64_t B = std::min<int64_t>(p->cap, T - f0);
@@ -980,11 +995,20 @@ static int align_tc_pipelined(moco_plan *p, const void *d_frames, int64_t T, int
     if (k >= 2) CK(cudaStreamWaitEvent(sp, p->pe_free[buf], 0));
     int rc = launch_tc_prep(p, fr, B, G[buf], ga[buf], sp);
     if (rc) return rc;
+    if (two) {
+      rc = launch_downsample(p, 0, fr, (int64_t)p->m * p->n, img1[buf], B, sp);
+      if (rc) return rc;
+    }
     CK(cudaEventRecord(p->pe_prep[buf], sp));
     CK(cudaStreamWaitEvent(sm, p->pe_prep[buf], 0));
     if (k >= 2) CK(cudaStreamWaitEvent(sm, p->pe_pick[buf], 0));   // sh1/racc of batch k-2 consumed
-    rc = launch_tc_coarse(p, B, G[buf], ga[buf], sh1[buf], nullptr, d_flags ? d_flags + f0 : nullptr, nullptr, sm);
+    int32_t *sc = two ? p->sh2b[buf] : sh1[buf];
+    rc = launch_tc_coarse(p, B, G[buf], ga[buf], sc, nullptr, d_flags ? d_flags + f0 : nullptr, nullptr, sm);
     if (rc) return rc;
+    if (two) {
+      rc = launch_refine_h(p, 1, img1[buf], fs1, B, sc, sh1[buf], nullptr, nullptr, sm, racc[buf]);
+      if (rc) return rc;
+    }
     CK(cudaEventRecord(p->pe_free[buf], sm));
     rc = launch_refine_h(p, 0, fr, (int64_t)p->m * p->n, B, sh1[buf], d_shifts + 2 * f0, d_fmin + f0,
                          d_corrected ? (char *)d_corrected + f0 * fbytes : nullptr, sm, racc[buf], sa,
@@ -1021,8 +1045,8 @@ int moco_align_batch(moco_plan *p, const void *d_frames, int64_t T, int32_t *d_s
     p->algo = MOCO_ALGO_TC;
     return rc;
   }
-  if (p->algo == MOCO_ALGO_TC && p->levels == 1 && T > p->cap && p->tc.G2 && p->racc2 && p->sh1b &&
-      fused_ok(p, 0) && !getenv("MOCO_NOPIPE"))
+  if (p->algo == MOCO_ALGO_TC && T > p->cap && p->tc.G2 && p->racc2 && p->sh1b && fused_ok(p, 0) &&
+      (p->levels == 1 || (p->levels == 2 && p->scratch1b && p->sh2b[1] && fused_ok(p, 1))) && !getenv("MOCO_NOPIPE"))
     return align_tc_pipelined(p, d_frames, T, d_shifts, d_fmin, d_corrected, d_flags, (cudaStream_t)stream);
   for (int64_t f0 = 0; f0 < T; f0 += p->cap) {
     const int64_t B = std::min<int64_t>(p->cap, T - f0);

@@ -192,6 +192,29 @@ def test_tensor_core_refine_ragged_shapes(m, n, levels, w, T, monkeypatch):
         assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("c,T,rtc", [(2, 800, "1"), (4, 200, "1"), (4, 200, "0")])
+def test_pipelined_batches_equal_sequential(c, T, rtc, monkeypatch):
+    """The three-stream batch pipeline (align_tc_pipelined: operand prep and, at two
+    levels, the level-1 downsample of batch k+1 beside the search and refines of batch k)
+    gives bit-identical shifts, f_min and corrected frames to the sequential batches
+    (MOCO_NOPIPE); a 64 MB scratch budget forces several internal batches with a
+    ragged last one."""
+    spec = config_spec(c, T=T)
+    st = make_stack(spec, 0, T, device=DEV)
+    monkeypatch.setenv("MOCO_BATCH_MB", "64")
+    monkeypatch.setenv("MOCO_RTC", rtc)
+    out = {}
+    for mode in ("pipe", "seq"):
+        if mode == "seq":
+            monkeypatch.setenv("MOCO_NOPIPE", "1")
+        p = _plan_for(spec)
+        p.set_template(st.template)
+        sh, fm, co, _ = p.align(st.frames, corrected=True)
+        out[mode] = (sh, fm, co.view(torch.int16))
+    for a, b in zip(out["pipe"], out["seq"]):
+        assert torch.equal(a, b)
+
+
 def test_refine_all_alignments():
     """Refine+apply at every column misalignment of the doubled shift (the fused
     kernel specialises on (T-1) mod 8): exact translates with dx = -9..9."""
