@@ -365,11 +365,43 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
       mbar_wait(&full[s], rnd & 1);
       RT_T(w_a += gtimer() - t0;)
       const int nrow = r_hi - r_lo, nch = 2 * kc;
+      // interior stage (no grid row 0, 1, ml, ml+1 and no edge column: about 2/3 of the
+      // stages at C2): no per-chunk tests; a^2 = a * a_lo + 2^8 a * a_hi as two 16x8-bit
+      // dot products per word (bytes regrouped by one PRMT); per stage and lane 32 words,
+      // each product pair < 2^23 for a < 2^14, so the 32-bit sums cannot wrap
+      const bool fast = kc == RTC_KS && r_lo >= 2 && r_hi <= g.ml && 16 * j0 - o > 1 &&
+                        16 * j0 + 8 * RTC_CH - o <= g.nl;
 #pragma unroll
       for (int fk = 0; fk < FPW; ++fk) {
         const int f = cw + fk * RTC_CW;
         if (f >= nf) continue;
         const unsigned char *st = stg + s * RTC_STAGE + f * RTC_SLOT;
+        if (fast) {
+          uint4 q4[RTC_R / 8][RTC_CH / 4];
+#pragma unroll
+          for (int rq = 0; rq < RTC_R / 8; ++rq) {
+            const int br = rq * 8 + lr;   // box row = grid row - r_lo (r_lo = 6 gb)
+#pragma unroll
+            for (int cb = 0; cb < RTC_CH / 4; ++cb)
+              q4[rq][cb] = br < nrow ? *reinterpret_cast<const uint4 *>(st + br * 128 + (((cb * 4 + lc) ^ lr) << 4))
+                                     : make_uint4(0, 0, 0, 0);
+          }
+          uint32_t slo = 0, shi = 0;
+#pragma unroll
+          for (int rq = 0; rq < RTC_R / 8; ++rq)
+#pragma unroll
+            for (int cb = 0; cb < RTC_CH / 4; ++cb) {
+              const uint32_t wv[4] = {q4[rq][cb].x, q4[rq][cb].y, q4[rq][cb].z, q4[rq][cb].w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const uint32_t pb = __byte_perm(wv[q], 0, 0x3120);   // (lo0, lo1, hi0, hi1)
+                slo = __dp2a_lo(wv[q], pb, slo);
+                shi = __dp2a_hi(wv[q], pb, shi);
+              }
+            }
+          tot[fk] += (u64)slo + ((u64)shi << 8);
+          continue;
+        }
 #pragma unroll
         for (int rq = 0; rq < RTC_R / 8; ++rq) {   // fixed trip count: loads of all row blocks in flight
           const int rb = rq * 8;
