@@ -322,7 +322,11 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
       tc_fence_after();
       const uint32_t alo = (uint32_t)ad0 + (uint32_t)(s * RTC_STAGE >> 4);
       const uint32_t blo = (uint32_t)bd0 + (uint32_t)(s * RTC_STAGE >> 4);
+#ifndef RTC_DIAG_NOMMA   // (diagnostic builds, results wrong: tools/rtc_diag.sh)
       for (int q = 0; q < ngr; ++q) {
+#else
+      for (int q = 0; q < 0; ++q) {
+#endif
         const int G = gb + q, Gr = G - G0;
         // sets by the part-relative group index: the epilogue reads sets 0 .. nsets_used-1
         const uint32_t d = taddr + (uint32_t)((Gr & (g.nsets - 1)) * 64);
@@ -364,7 +368,11 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
       RT_T(t0 = gtimer();)
       mbar_wait(&full[s], rnd & 1);
       RT_T(w_a += gtimer() - t0;)
+#ifndef RTC_DIAG_NOGA
       const int nrow = r_hi - r_lo, nch = 2 * kc;
+#else
+      const int nrow = 0, nch = 0;
+#endif
       // interior stage (no grid row 0, 1, ml, ml+1 and no edge column: about 2/3 of the
       // stages at C2): no per-chunk tests; a^2 = a * a_lo + 2^8 a * a_hi as two 16x8-bit
       // dot products per word (bytes regrouped by one PRMT); per stage and lane 32 words,
