@@ -115,8 +115,16 @@ class ClockSampler:
                  "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()   # nvidia-smi can take seconds to start on a fresh box
+            while not self.lines and time.time() - t0 < 15 and self.proc.poll() is None:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
+        self.i0 = 0
+
+    def mark(self):
+        """Start of the timed region: samples before it are dropped."""
+        self.i0 = len(self.lines)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -132,7 +140,8 @@ class ClockSampler:
             self.proc.kill()
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        # the samples taken during the timed region (at least the first one after it)
+        for ln in self.lines[self.i0:] or self.lines[-1:]:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -279,6 +288,7 @@ def main():
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    clk.mark()
     e0.record()
     for _ in range(args.steps):
         step()

@@ -248,6 +248,9 @@ struct TcPrepArgs {
   TcGeom g;
   uint8_t *G;               // [groups][nstrips][2][R][F][2][16]
   u64 *ga;                  // [B][W*W]
+  uint16_t *img1;           // L = 2: also write the level-1 image (2x2 sums) here, or null
+  int64_t fs1;              // its frame stride and row pitch (elements)
+  int p1;
 };
 
 // 8 consecutive coarse values (2^L x 2^L block sums) of one coarse row as 4 pair-words.
@@ -289,6 +292,40 @@ __device__ __forceinline__ void coarse8(const uint16_t *base, int n, uint32_t (&
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) P[k] = c[2 * k] | (c[2 * k + 1] << 16);
+  }
+}
+
+// L = 2 with the level-1 image written on the way (replaces the separate level 0 -> 1
+// downsample, which read the frames a second time): raw rows 0-1 and 2-3 of the 4-row band
+// summed apart; level-1 value j of each row pair = both halves of pair word j (< 2^14);
+// the 4x4 coarse value k = both halves of the sum of the two level-1 pair words 2k', 2k'+1
+// (each half < 2^15, the coarse value < 2^16) -- the same sums, regrouped.
+__device__ __forceinline__ void coarse8_l2_emit(const uint16_t *base, int n, uint16_t *o1, int p1,
+                                                uint32_t (&P)[4]) {
+  uint32_t sa[16], sb[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) sa[k] = sb[k] = 0;
+#pragma unroll
+  for (int dy = 0; dy < 4; ++dy)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 u = __ldcs(reinterpret_cast<const uint4 *>(base + (int64_t)dy * n + q * 8));
+      uint32_t *s = dy < 2 ? sa : sb;
+      s[4 * q + 0] += u.x; s[4 * q + 1] += u.y; s[4 * q + 2] += u.z; s[4 * q + 3] += u.w;
+    }
+  uint32_t wa[8], wb[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    wa[k] = __byte_perm(sa[2 * k], sa[2 * k + 1], 0x5410) + __byte_perm(sa[2 * k], sa[2 * k + 1], 0x7632);
+    wb[k] = __byte_perm(sb[2 * k], sb[2 * k + 1], 0x5410) + __byte_perm(sb[2 * k], sb[2 * k + 1], 0x7632);
+  }
+  uint4 *ra = reinterpret_cast<uint4 *>(o1), *rb = reinterpret_cast<uint4 *>(o1 + p1);
+  ra[0] = make_uint4(wa[0], wa[1], wa[2], wa[3]); ra[1] = make_uint4(wa[4], wa[5], wa[6], wa[7]);
+  rb[0] = make_uint4(wb[0], wb[1], wb[2], wb[3]); rb[1] = make_uint4(wb[4], wb[5], wb[6], wb[7]);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t x0 = wa[2 * k] + wb[2 * k], x1 = wa[2 * k + 1] + wb[2 * k + 1];
+    P[k] = __byte_perm(x0, x1, 0x5410) + __byte_perm(x0, x1, 0x7632);
   }
 }
 
@@ -441,7 +478,17 @@ __global__ void __launch_bounds__(256, TC_PREP_MINB) k_tc_prep(TcPrepArgs a) {
       for (int q = 0; q < TC_PREP_RPP; ++q) {
         const int pr = pr0 + q * pstep;
         P[q][0] = P[q][1] = P[q][2] = P[q][3] = 0;
-        if (live[q]) coarse8<L>(frame + (int64_t)((pr - hw) << L) * a.n + ((cc * 8) << L), a.n, P[q]);
+        if (!live[q]) continue;
+        const uint16_t *src = frame + (int64_t)((pr - hw) << L) * a.n + ((cc * 8) << L);
+        if constexpr (L == 2) {
+          if (a.img1)
+            coarse8_l2_emit(src, a.n, a.img1 + (int64_t)fi * a.fs1 + (int64_t)(2 * (pr - hw)) * a.p1 + cc * 16, a.p1,
+                            P[q]);
+          else
+            coarse8<L>(src, a.n, P[q]);
+        } else {
+          coarse8<L>(src, a.n, P[q]);
+        }
       }
 #pragma unroll
       for (int q = 0; q < TC_PREP_RPP; ++q) {

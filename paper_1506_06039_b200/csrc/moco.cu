@@ -834,12 +834,21 @@ static int check_align_args(moco_plan *p, const void *frames, int64_t T) {
 
 // Tensor-core coarse search (kernels_tc.cuh) straight from the level-0 frames:
 // K_prep (operand planes G + lag energies ga) then K_tc.
-static int launch_tc_prep(moco_plan *p, const void *frames_b, int64_t B, uint8_t *G, u64 *ga, cudaStream_t st) {
+// levels = 2: the operand preparation also writes the level-1 image (the refine at level
+// 1 reads it) when the level-2 band covers it exactly
+static bool prep_emits_l1(const moco_plan *p) {
+  if (p->levels != 2 || p->dtype != MOCO_U16 || getenv("MOCO_NOFUSE_DS")) return false;
+  return p->ml[1] == 2 * p->ml[2] && p->nl[1] == 2 * p->nl[2] && p->nl[2] % 8 == 0 && p->pitch[1] % 8 == 0;
+}
+
+static int launch_tc_prep(moco_plan *p, const void *frames_b, int64_t B, uint8_t *G, u64 *ga, cudaStream_t st,
+                          void *img1 = nullptr) {
   const TcGeom &g = p->tc.g;
   const int64_t groups = (B + g.F - 1) / g.F;
   TcPrepArgs pa;
   pa.frames = (const uint16_t *)frames_b; pa.fstride = (int64_t)p->m * p->n; pa.n = p->n;
   pa.B = (int)B; pa.g = g; pa.G = G; pa.ga = ga;
+  pa.img1 = (uint16_t *)img1; pa.fs1 = (int64_t)p->ml[1] * p->pitch[1]; pa.p1 = p->pitch[1];
   {
     ProfScope ps(p, MOCO_K_PREP, st);
     if (p->levels == 0) k_tc_prep<0><<<(unsigned)groups, 256, g.prep_smem, st>>>(pa);
@@ -879,8 +888,8 @@ static int launch_tc_coarse(moco_plan *p, int64_t B, const uint8_t *G, const u64
 }
 
 static int launch_tc(moco_plan *p, const void *frames_b, int64_t B, int32_t *shift_out, double *f_out,
-                     uint8_t *flags, double *grid_out, cudaStream_t st) {
-  int rc = launch_tc_prep(p, frames_b, B, p->tc.G, p->tc.ga, st);
+                     uint8_t *flags, double *grid_out, cudaStream_t st, void *img1 = nullptr) {
+  int rc = launch_tc_prep(p, frames_b, B, p->tc.G, p->tc.ga, st, img1);
   if (rc) return rc;
   return launch_tc_coarse(p, B, p->tc.G, p->tc.ga, shift_out, f_out, flags, grid_out, st);
 }
@@ -920,14 +929,16 @@ static int run_batch(moco_plan *p, const void *frames_b, int64_t B, int32_t *shi
   const bool tc = p->algo == MOCO_ALGO_TC;
   // the tensor-core search block-sums the level-0 frames itself; only the levels the
   // refine steps read (1..L-1) are materialised
+  const bool emit1 = tc && !grid_b && prep_emits_l1(p);   // level 1 written by the operand prep
   for (int l = 0; l < (tc ? L - 1 : L); ++l) {
+    if (emit1) break;
     int rc = launch_downsample(p, l, img[l], fstride[l], p->scratch[l + 1], B, st);
     if (rc) return rc;
   }
   if (tc) {
     int rc = grid_b ? launch_tc(p, frames_b, B, nullptr, nullptr, nullptr, grid_b, st)
                     : launch_tc(p, frames_b, B, L == 0 ? shifts_b : p->sh[L], L == 0 ? fmin_b : nullptr,
-                                flags_b, nullptr, st);
+                                flags_b, nullptr, st, emit1 ? p->scratch[1] : nullptr);
     if (rc || grid_b) return rc;
     return refine_levels(p, img, fstride, B, shifts_b, fmin_b, corr_b, st);
   }
@@ -993,9 +1004,10 @@ static int align_tc_pipelined(moco_plan *p, const void *d_frames, int64_t T, int
     const int buf = (int)(k & 1);
     const char *fr = (const char *)d_frames + f0 * fbytes;
     if (k >= 2) CK(cudaStreamWaitEvent(sp, p->pe_free[buf], 0));
-    int rc = launch_tc_prep(p, fr, B, G[buf], ga[buf], sp);
+    const bool emit1 = two && prep_emits_l1(p);
+    int rc = launch_tc_prep(p, fr, B, G[buf], ga[buf], sp, emit1 ? img1[buf] : nullptr);
     if (rc) return rc;
-    if (two) {
+    if (two && !emit1) {
       rc = launch_downsample(p, 0, fr, (int64_t)p->m * p->n, img1[buf], B, sp);
       if (rc) return rc;
     }

@@ -215,6 +215,32 @@ def test_pipelined_batches_equal_sequential(c, T, rtc, monkeypatch):
         assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("m,n,w,T", [(1024, 1024, 24, 40), (256, 384, 6, 21), (262, 256, 5, 9)])
+def test_prep_emitted_level1_equals_downsample(m, n, w, T, monkeypatch):
+    """Two pyramid levels on the tensor-core path: the operand preparation writes the
+    level-1 image on its way to the 4x4 sums (prep_emits_l1); shifts, f_min and corrected
+    frames equal those with the separate level 0 -> 1 downsample (MOCO_NOFUSE_DS); the
+    262-row case has a level-1 row count that is not twice the level-2 one (not fused)."""
+    rng = np.random.default_rng(m + n + w)
+    tp = rng.integers(0, 4096, size=(m, n)).astype(np.uint16)
+    fr = rng.integers(0, 4096, size=(T, m, n)).astype(np.uint16)
+    for k in range(min(T, 6)):
+        fr[k] = pf.translate_zero_fill(tp, 4 * k - 8, 8 - 4 * k)   # exact at every level
+    frames = torch.from_numpy(fr).to(DEV)
+    out = {}
+    for mode in ("fused", "separate"):
+        if mode == "separate":
+            monkeypatch.setenv("MOCO_NOFUSE_DS", "1")
+        p = Plan(m, n, w, 2, "u16", 12, device=0)
+        p.set_algo("tc")
+        p.set_template(torch.from_numpy(tp).to(DEV))
+        sh, fm, co, _ = p.align(frames, corrected=True)
+        out[mode] = (sh, fm, co.view(torch.int16))
+    for a, b in zip(out["fused"], out["separate"]):
+        assert torch.equal(a, b)
+    assert _np(out["fused"][0])[:min(T, 6)].tolist() == [[4 * k - 8, 8 - 4 * k] for k in range(min(T, 6))]
+
+
 def test_refine_all_alignments():
     """Refine+apply at every column misalignment of the doubled shift (the fused
     kernel specialises on (T-1) mod 8): exact translates with dx = -9..9."""

@@ -14,6 +14,10 @@ timeout 120 python tools/profile_run.py --frames 2368 --iters 1 > $O/plain_c2.lo
     python tools/profile_run.py --frames 2368 --iters 1 > $O/ncu_c2.log 2>&1
 timeout 120 python tools/profile_run.py --config 4 --frames 256 --iters 1 > $O/plain_c4.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_energy_u16|k_fft_rows|k_fft_cols|k_fft_score" -c 4 -o $O/prof_c4 \
+    -k regex:"k_tc_prep|k_tc_coarse|k_refine_tc|k_refine_pick|k_downsample" -c 6 -o $O/prof_c4 \
     python tools/profile_run.py --config 4 --frames 256 --iters 1 > $O/ncu_c4.log 2>&1
+for c in 0 1 2 3 4; do
+  timeout 300 python bench.py --config $c --steps 5 --warmup 3 --no-e2e --no-cpu --no-paper 2>/dev/null | tail -1 > $O/bench_c$c.json
+done
+timeout 300 python bench.py --impl reference --steps 2 --warmup 1 2>/dev/null | tail -1 > $O/bench_reference.json
 ls -la $O
