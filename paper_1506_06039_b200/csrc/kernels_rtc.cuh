@@ -377,8 +377,12 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
       // stages at C2): no per-chunk tests; a^2 = a * a_lo + 2^8 a * a_hi as two 16x8-bit
       // dot products per word (bytes regrouped by one PRMT); per stage and lane 32 words,
       // each product pair < 2^23 for a < 2^14, so the 32-bit sums cannot wrap
+#ifndef RTC_DIAG_FASTONLY
       const bool fast = kc == RTC_KS && r_lo >= 2 && r_hi <= g.ml && 16 * j0 - o > 1 &&
                         16 * j0 + 8 * RTC_CH - o <= g.nl;
+#else
+      const bool fast = true;   // (diagnostic: edge stages summed as interior ones)
+#endif
 #pragma unroll
       for (int fk = 0; fk < FPW; ++fk) {
         const int f = cw + fk * RTC_CW;
