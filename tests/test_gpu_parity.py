@@ -282,6 +282,19 @@ def test_config2_full_stack_sampled():
     assert (sh == st.shifts).mean() > 0.95
 
 
+def test_config4_full_stack_sampled():
+    """C4 as bench.py runs it: all 2,000 frames of 1024x1024 in one moco_align_batch call
+    (two pyramid levels: TC search on the 16-bit level-2 sums, the level-1 image written
+    by the operand prep, both refines on the tensor cores, three-stream batch pipeline);
+    frames spread over the stack, on both sides of the likely internal batch
+    boundaries (multiples of 148 x 2^k), checked bit-exactly against the oracle."""
+    spec = config_spec(4)
+    sample = [0, 1, 2, 295, 296, 591, 592, 1023, 1024, 1183, 1184, 1479, 1480, 1776, 1998, 1999]
+    spec, st, sh, fm, fl, kinds, p = _run_config(4, spec.T, sample)
+    assert kinds == ["exact"] * len(sample)
+    assert (sh == st.shifts).mean() > 0.95
+
+
 def test_config3_stripes_sampled():
     spec = config_spec(3, T=64)
     st = make_stack(spec, 0, 64, device=DEV)
