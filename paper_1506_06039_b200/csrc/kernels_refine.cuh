@@ -372,7 +372,86 @@ struct RefinePickArgs {
   double *f_out;            // [B] or null
   uint16_t *corrected;      // [B][ml][nl] or null (level 0)
   int parts;                // CTAs per frame (apply rows split among them)
+  int ga_total;             // 1: acc[9] holds the tensor-core refine's a^2 sum over its staged
+                            // pixels (grid rows [0, ml+2), grid columns [-o, kw-o)); the
+                            // nine GA are completed here (ga_pieces).  0: acc[9..17] are GA
+  int kw;                   // 16 n_k: staged columns per grid row (ga_total)
 };
+
+// GA pieces of frame f for ga_total (kernels_rtc.cuh, RTC_GA_TOTAL): on the extended grid
+// A[p_r][p_c] = a[p_r+S-1][p_c+T-1] (0 outside the frame), o = (T-1) mod 8,
+//   bins[rc][0]   = sum of A^2 over grid row class rc (0: row 0, 1: row 1, 2: row ml,
+//                   3: row ml+1, 4: rows 2..ml-1) and grid columns [0, nl+2),
+//   bins[rc][1+k] = A^2 at grid column (0, 1, nl, nl+1)[k] summed over the rows of class rc;
+// the interior total is the staged sum minus the staged columns outside [0, nl+2) minus
+// the four class rows.  Reads rows 0, 1, ml, ml+1 and, per grid row, the two 16-byte chunks
+// at the left edge and the (kw - nl)/8 chunks at the right edge.
+__device__ __forceinline__ void ga_pieces(const RefinePickArgs &a, int64_t f, int S, int T, u64 total,
+                                          u64 *bins /* smem [26] */) {
+  const int tid = threadIdx.x, nth = blockDim.x, ml = a.ml, nl = a.nl, nl2 = nl + 2;
+  if (tid < 26) bins[tid] = 0;
+  __syncthreads();
+  const uint16_t *A = a.frames + f * a.fstride;
+  const int o = (T - 1) & 7, x0 = (T - 1) - o;   // frame column of staged column 0 (grid column -o)
+  // (1) the four class rows over grid columns [0, nl+2)
+  u64 r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+  for (int k = tid; k < 4 * nl2; k += nth) {
+    const int r = k / nl2, pc = k - r * nl2;
+    const int fr = (r < 2 ? r : ml + r - 2) + S - 1, fc = pc + T - 1;
+    if (fr < 0 || fr >= ml || fc < 0 || fc >= nl) continue;
+    const u64 v = A[(int64_t)fr * a.pitch + fc], q = v * v;
+    if (r == 0) r0 += q; else if (r == 1) r1 += q; else if (r == 2) r2 += q; else r3 += q;
+  }
+  // (2) per grid row: staged columns outside [0, nl+2) and the four edge columns
+  u64 X = 0, i0 = 0, i1 = 0, i2 = 0, i3 = 0;
+  const int cr0 = max(2, nl >> 3), ncs = a.kw >> 3;   // right-edge chunks [cr0, ncs), left [0, 2)
+  for (int pr = tid; pr < ml + 2; pr += nth) {
+    const int fr = pr + S - 1;
+    if (fr < 0 || fr >= ml) continue;
+    const uint16_t *row = A + (int64_t)fr * a.pitch;
+    const int rc = pr < 2 ? pr : (pr >= ml ? pr - ml + 2 : 4);
+    u64 c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+    for (int q = 0; q < 2 + 3; ++q) {
+      const int ch = q < 2 ? q : cr0 + q - 2;
+      if (ch >= ncs || (q >= 2 && ch < 2)) continue;
+      const int fc0 = x0 + 8 * ch;
+      if (fc0 < 0 || fc0 >= nl) continue;   // 8-aligned: the chunk is wholly in or out of the row
+      const uint4 u = *reinterpret_cast<const uint4 *>(row + fc0);
+      const uint32_t wv[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int x = 0; x < 8; ++x) {
+        const u64 v = (x & 1) ? (wv[x >> 1] >> 16) : (wv[x >> 1] & 0xffffu), sq = v * v;
+        const int pc = 8 * ch + x - o;
+        if (pc < 0 || pc >= nl2) X += sq;
+        else if (pc == 0) c0 += sq;
+        else if (pc == 1) c1 += sq;
+        else if (pc == nl) c2 += sq;
+        else if (pc == nl + 1) c3 += sq;
+      }
+    }
+    if (rc == 4) {
+      i0 += c0; i1 += c1; i2 += c2; i3 += c3;
+    } else {
+      atomicAdd(reinterpret_cast<unsigned long long *>(bins + rc * 5 + 1), (unsigned long long)c0);
+      atomicAdd(reinterpret_cast<unsigned long long *>(bins + rc * 5 + 2), (unsigned long long)c1);
+      atomicAdd(reinterpret_cast<unsigned long long *>(bins + rc * 5 + 3), (unsigned long long)c2);
+      atomicAdd(reinterpret_cast<unsigned long long *>(bins + rc * 5 + 4), (unsigned long long)c3);
+    }
+  }
+  r0 = warp_sum(r0); r1 = warp_sum(r1); r2 = warp_sum(r2); r3 = warp_sum(r3);
+  X = warp_sum(X); i0 = warp_sum(i0); i1 = warp_sum(i1); i2 = warp_sum(i2); i3 = warp_sum(i3);
+  if ((tid & 31) == 0) {
+    unsigned long long *b = reinterpret_cast<unsigned long long *>(bins);
+    atomicAdd(b + 0, (unsigned long long)r0); atomicAdd(b + 5, (unsigned long long)r1);
+    atomicAdd(b + 10, (unsigned long long)r2); atomicAdd(b + 15, (unsigned long long)r3);
+    atomicAdd(b + 25, (unsigned long long)X);
+    atomicAdd(b + 21, (unsigned long long)i0); atomicAdd(b + 22, (unsigned long long)i1);
+    atomicAdd(b + 23, (unsigned long long)i2); atomicAdd(b + 24, (unsigned long long)i3);
+  }
+  __syncthreads();
+  if (tid == 0) bins[20] = total - bins[25] - bins[0] - bins[5] - bins[10] - bins[15];
+  __syncthreads();
+}
 
 template <int SH>
 __device__ __forceinline__ void pick_apply_rows(const uint16_t *A, uint16_t *O, int pitch, int s, int t, int ml,
@@ -455,18 +534,31 @@ __device__ __forceinline__ void pick_apply_rows(const uint16_t *A, uint16_t *O, 
 // corrected frame -- small batches (the closed-loop case) spread one frame over many SMs.
 __global__ void __launch_bounds__(256) k_refine_pick(RefinePickArgs a) {
   __shared__ int res[2];
+  __shared__ u64 gbins[26];
   const int parts = a.parts;
   const int64_t f = blockIdx.x / parts;
   const int part = blockIdx.x % parts;
   const int S = 2 * a.shift_in[2 * f], T = 2 * a.shift_in[2 * f + 1];
   const int ml = a.ml, nl = a.nl;
+  if (a.ga_total) ga_pieces(a, f, S, T, a.acc[f * 18 + 9], gbins);
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     u64 *acc = a.acc + f * 18;
     Key k{~0ull, ~0u};
     if (lane < 9) {
       const int c = lane;
-      const u64 h = acc[c], ga = acc[9 + c];
+      const u64 h = acc[c];
+      u64 ga;
+      if (a.ga_total) {
+        // row classes of u' (0: rows 0, 1, interior; 1: 1, interior, ml; 2: interior, ml,
+        // ml+1) minus the two grid columns outside [v', v'+nl) (0: nl, nl+1; 1: 0, nl+1; 2: 0, 1)
+        const int up = c / 3, vp = c % 3, ex1 = vp == 0 ? 3 : 1, ex2 = vp == 2 ? 2 : 4;
+        const int q0 = up == 0 ? 0 : (up == 1 ? 1 : 4), q1 = up == 0 ? 1 : (up == 1 ? 4 : 2), q2 = up == 0 ? 4 : (up == 1 ? 2 : 3);
+        ga = gbins[q0 * 5] - gbins[q0 * 5 + ex1] - gbins[q0 * 5 + ex2] + gbins[q1 * 5] - gbins[q1 * 5 + ex1] -
+             gbins[q1 * 5 + ex2] + gbins[q2 * 5] - gbins[q2 * 5 + ex1] - gbins[q2 * 5 + ex2];
+      } else {
+        ga = acc[9 + c];
+      }
       const int s = S + c / 3 - 1, t = T + c % 3 - 1, n1 = nl + 1;
       const int i0 = max(0, -s), i1 = ml - max(0, s), j0 = max(0, -t), j1 = nl - max(0, t);
       const u64 gb = a.pb2[(int64_t)i1 * n1 + j1] - a.pb2[(int64_t)i0 * n1 + j1] -

@@ -74,6 +74,14 @@ constexpr int RTC_CH = 2 * RTC_KS;         // 8-pixel chunks per stage box
 #ifndef RTC_GA_WARPS
 #define RTC_GA_WARPS 16
 #endif
+// GA split: 1 = the GA warps sum a^2 over every staged pixel (grid rows [0, ml+2), box
+// columns [0, 16 nk), i.e. grid columns [-o, 16 nk - o)) with one uniform path, and the
+// pick kernel (k_refine_pick, ga_total) subtracts the columns outside the grid and
+// separates the rows 0, 1, ml, ml+1 and the columns 0, 1, nl, nl+1 from the frame itself
+// (a few hundred pixels per frame); 0 = row-class bins and edge columns here
+#ifndef RTC_GA_TOTAL
+#define RTC_GA_TOTAL 1
+#endif
 constexpr int RTC_CW = RTC_GA_WARPS;       // GA warps (16 / RTC_CW frames each)
 constexpr int RTC_THREADS = 32 * (2 + RTC_CW);
 constexpr int RTC_SLOT = RTC_R * 128;                        // bytes per frame box: R rows of 128 B (SW128)
@@ -388,6 +396,36 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
         const int f = cw + fk * RTC_CW;
         if (f >= nf) continue;
         const unsigned char *st = stg + s * RTC_STAGE + f * RTC_SLOT;
+#if RTC_GA_TOTAL
+        (void)fast;
+        {
+          uint4 q4[RTC_R / 8][RTC_CH / 4];
+#pragma unroll
+          for (int rq = 0; rq < RTC_R / 8; ++rq) {
+            const int br = rq * 8 + lr;
+#pragma unroll
+            for (int cb = 0; cb < RTC_CH / 4; ++cb)
+              q4[rq][cb] = (br < nrow && cb * 4 + lc < nch)
+                               ? *reinterpret_cast<const uint4 *>(st + br * 128 + (((cb * 4 + lc) ^ lr) << 4))
+                               : make_uint4(0, 0, 0, 0);
+          }
+          uint32_t slo = 0, shi = 0;
+#pragma unroll
+          for (int rq = 0; rq < RTC_R / 8; ++rq)
+#pragma unroll
+            for (int cb = 0; cb < RTC_CH / 4; ++cb) {
+              const uint32_t wv[4] = {q4[rq][cb].x, q4[rq][cb].y, q4[rq][cb].z, q4[rq][cb].w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const uint32_t pb = __byte_perm(wv[q], 0, 0x3120);
+                slo = __dp2a_lo(wv[q], pb, slo);
+                shi = __dp2a_hi(wv[q], pb, shi);
+              }
+            }
+          tot[fk] += (u64)slo + ((u64)shi << 8);
+          continue;
+        }
+#endif
         if (fast) {
           uint4 q4[RTC_R / 8][RTC_CH / 4];
 #pragma unroll
@@ -480,6 +518,16 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
+#if RTC_GA_TOTAL
+#pragma unroll
+    for (int fk = 0; fk < FPW; ++fk) {
+      const int f = cw + fk * RTC_CW;
+      const u64 t = warp_sum(tot[fk]);
+      if (f < nf && lane == 0)
+        atomicAdd(reinterpret_cast<unsigned long long *>(a.acc + (int64_t)Fid[f] * 18 + 9), (unsigned long long)t);
+    }
+    (void)e0; (void)e1; (void)e2; (void)e3;
+#else
 #pragma unroll
     for (int fk = 0; fk < FPW; ++fk) {
       const int f = cw + fk * RTC_CW;
@@ -494,6 +542,7 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
         atomicAdd(reinterpret_cast<unsigned long long *>(bn + 4), (unsigned long long)a3);
       }
     }
+#endif
   }
 
   // ---------------- epilogue: TMEM lane m = f*8 + r_rel; warp (m / 32) reads 32 lanes
@@ -560,6 +609,7 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
   // GA per candidate from the bins: row classes of u' (0: rows 0,1,int; 1: 1,int,ml;
   // 2: int,ml,ml+1), minus the two grid columns outside [v', v'+nl) (0: nl,nl+1;
   // 1: 0,nl+1; 2: 0,1)
+#if !RTC_GA_TOTAL
   for (int k = tid; k < RTC_F * 9; k += RTC_THREADS) {
     const int ff = k / 9, c = k % 9;
     if (ff >= nf) continue;
@@ -575,6 +625,7 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
     }
     atomicAdd(reinterpret_cast<unsigned long long *>(a.acc + (int64_t)Fid[ff] * 18 + 9 + c), (unsigned long long)GA);
   }
+#endif
   tc_fence_before();
   __syncthreads();
   tc_fence_after();

@@ -707,12 +707,16 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
   // cleared by a memset after the pick instead of by the single CTA)
   b.parts = (int)std::max<int64_t>(1, std::min<int64_t>(16, p->nsm / std::max<int64_t>(1, B)));
   if (!corr) b.parts = 1;
+  b.ga_total = 0;
+  b.kw = 0;
   if (rtc) {
     ProfScope ps(p, MOCO_K_REFINE, st);
     k_rtc_bucket<<<1, 1024, 0, st>>>(sin, (int)B, p->rperm, p->rmeta);
     RtcArgs r;
     r.tab = p->rtab[l]; r.acc = racc; r.shift_in = sin; r.perm = p->rperm; r.meta = p->rmeta;
     r.B = (int)B; r.g = p->rtc[l];
+    b.ga_total = RTC_GA_TOTAL;   // the pick completes GA from the staged-pixel total
+    b.kw = 16 * p->rtc[l].nk;
     // row-group ranges per 16-frame group (whole stages): the fewest that bring the last
     // wave near full
     const int64_t groups = (B + RTC_F - 1) / RTC_F + 4;   // upper bound over the 4 classes
