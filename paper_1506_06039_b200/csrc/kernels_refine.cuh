@@ -394,13 +394,25 @@ __device__ __forceinline__ void ga_pieces(const RefinePickArgs &a, int64_t f, in
   const uint16_t *A = a.frames + f * a.fstride;
   const int o = (T - 1) & 7, x0 = (T - 1) - o;   // frame column of staged column 0 (grid column -o)
   // (1) the four class rows over grid columns [0, nl+2)
+  // (16-byte chunks from x0: chunk k holds grid columns 8k-o .. 8k-o+7)
   u64 r0 = 0, r1 = 0, r2 = 0, r3 = 0;
-  for (int k = tid; k < 4 * nl2; k += nth) {
-    const int r = k / nl2, pc = k - r * nl2;
-    const int fr = (r < 2 ? r : ml + r - 2) + S - 1, fc = pc + T - 1;
-    if (fr < 0 || fr >= ml || fc < 0 || fc >= nl) continue;
-    const u64 v = A[(int64_t)fr * a.pitch + fc], q = v * v;
-    if (r == 0) r0 += q; else if (r == 1) r1 += q; else if (r == 2) r2 += q; else r3 += q;
+  const int nchk = (nl2 + o + 7) >> 3;
+  for (int k = tid; k < 4 * nchk; k += nth) {
+    const int r = k / nchk, ch = k - r * nchk;
+    const int fr = (r < 2 ? r : ml + r - 2) + S - 1, fc0 = x0 + 8 * ch;
+    if (fr < 0 || fr >= ml || fc0 < 0 || fc0 >= nl) continue;
+    const uint4 u = *reinterpret_cast<const uint4 *>(A + (int64_t)fr * a.pitch + fc0);
+    const uint32_t wv[4] = {u.x, u.y, u.z, u.w};
+    uint32_t q = 0;   // eight squares of < 2^16 values would overflow: 32-bit per pair below
+    u64 qs = 0;
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+      const uint32_t v = (x & 1) ? (wv[x >> 1] >> 16) : (wv[x >> 1] & 0xffffu);
+      const int pc = 8 * ch + x - o;
+      q = (pc >= 0 && pc < nl2) ? v * v : 0u;
+      qs += q;
+    }
+    if (r == 0) r0 += qs; else if (r == 1) r1 += qs; else if (r == 2) r2 += qs; else r3 += qs;
   }
   // (2) per grid row: staged columns outside [0, nl+2) and the four edge columns
   u64 X = 0, i0 = 0, i1 = 0, i2 = 0, i3 = 0;
