@@ -376,6 +376,7 @@ struct RefinePickArgs {
                             // pixels (grid rows [0, ml+2), grid columns [-o, kw-o)); the
                             // nine GA are completed here (ga_pieces).  0: acc[9..17] are GA
   int kw;                   // 16 n_k: staged columns per grid row (ga_total)
+  const u64 *gbin;          // ga_total: [B][26] pieces from k_ga_pieces, or null (computed here)
 };
 
 // GA pieces of frame f for ga_total (kernels_rtc.cuh, RTC_GA_TOTAL): on the extended grid
@@ -386,7 +387,8 @@ struct RefinePickArgs {
 // the interior total is the staged sum minus the staged columns outside [0, nl+2) minus
 // the four class rows.  Reads rows 0, 1, ml, ml+1 and, per grid row, the two 16-byte chunks
 // at the left edge and the (kw - nl)/8 chunks at the right edge.
-__device__ __forceinline__ void ga_pieces(const RefinePickArgs &a, int64_t f, int S, int T, u64 total,
+// (bins[20], the interior-row total, needs the refine's sum: ga_finish)
+__device__ __forceinline__ void ga_pieces(const RefinePickArgs &a, int64_t f, int S, int T,
                                           u64 *bins /* smem [26] */) {
   const int tid = threadIdx.x, nth = blockDim.x, ml = a.ml, nl = a.nl, nl2 = nl + 2;
   if (tid < 26) bins[tid] = 0;
@@ -461,8 +463,20 @@ __device__ __forceinline__ void ga_pieces(const RefinePickArgs &a, int64_t f, in
     atomicAdd(b + 23, (unsigned long long)i2); atomicAdd(b + 24, (unsigned long long)i3);
   }
   __syncthreads();
-  if (tid == 0) bins[20] = total - bins[25] - bins[0] - bins[5] - bins[10] - bins[15];
+}
+__device__ __forceinline__ void ga_finish(u64 *bins, u64 total) {
+  if (threadIdx.x == 0) bins[20] = total - bins[25] - bins[0] - bins[5] - bins[10] - bins[15];
   __syncthreads();
+}
+
+// The GA pieces of a batch ahead of the pick (align_tc_pipelined: on the pick stream once
+// the shifts the refine starts from exist, so it runs beside the refine sums).
+__global__ void __launch_bounds__(128) k_ga_pieces(RefinePickArgs a, u64 *out) {
+  __shared__ u64 bins[26];
+  const int64_t f = blockIdx.x;
+  const int S = 2 * a.shift_in[2 * f], T = 2 * a.shift_in[2 * f + 1];
+  ga_pieces(a, f, S, T, bins);
+  if (threadIdx.x < 26) out[f * 26 + threadIdx.x] = bins[threadIdx.x];
 }
 
 template <int SH>
@@ -552,7 +566,15 @@ __global__ void __launch_bounds__(256) k_refine_pick(RefinePickArgs a) {
   const int part = blockIdx.x % parts;
   const int S = 2 * a.shift_in[2 * f], T = 2 * a.shift_in[2 * f + 1];
   const int ml = a.ml, nl = a.nl;
-  if (a.ga_total) ga_pieces(a, f, S, T, a.acc[f * 18 + 9], gbins);
+  if (a.ga_total) {
+    if (a.gbin) {
+      if (threadIdx.x < 26) gbins[threadIdx.x] = a.gbin[f * 26 + threadIdx.x];
+      __syncthreads();
+    } else {
+      ga_pieces(a, f, S, T, gbins);
+    }
+    ga_finish(gbins, a.acc[f * 18 + 9]);
+  }
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     u64 *acc = a.acc + f * 18;

@@ -93,6 +93,7 @@ struct moco_plan {
   int32_t *sh2b[2];           // coarse shifts at level 2 (pipeline, levels = 2)
   void *scratch1b;            // second level-1 image buffer (pipeline, levels = 2)
   u64 *racc2;                 // second refine accumulator buffer (pipeline)
+  u64 *gbin[2];               // GA pieces per frame [cap][26] (pipeline, k_ga_pieces)
   // end-to-end staging
   bool host_ready;
   int64_t host_ch;
@@ -219,6 +220,8 @@ static void plan_free(moco_plan *p) {
     if (p->sh2b[k]) cudaFree(p->sh2b[k]);
   if (p->scratch1b) cudaFree(p->scratch1b);
   if (p->racc2) cudaFree(p->racc2);
+  for (int k = 0; k < 2; ++k)
+    if (p->gbin[k]) cudaFree(p->gbin[k]);
   for (auto &r : p->prof_live) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : p->prof_pool) cudaEventDestroy(e);
   delete p;
@@ -432,6 +435,7 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
     alloc((void **)&p->racc, (size_t)p->cap * 18 * sizeof(u64));
     alloc((void **)&p->racc2, (size_t)p->cap * 18 * sizeof(u64));
     alloc((void **)&p->sh1b, (size_t)p->cap * 2 * sizeof(int32_t));
+    for (int k = 0; k < 2; ++k) alloc((void **)&p->gbin[k], (size_t)p->cap * 26 * sizeof(u64));
     if (levels == 2) {   // align_tc_pipelined at two levels: coarse shifts, level-1 images
       for (int k = 0; k < 2; ++k) alloc((void **)&p->sh2b[k], (size_t)p->cap * 2 * sizeof(int32_t));
       alloc(&p->scratch1b, (size_t)p->cap * p->ml[1] * p->pitch[1] * p->esz[1]);
@@ -669,9 +673,33 @@ static int launch_refine(moco_plan *p, int l, const void *img, int64_t fstride, 
 
 // K6 (+K7 at level 0): template-stationary u16 refine (kernels_refine.cuh):
 // k_refine_sums (per-frame sums) then k_refine_pick (argmin + apply).
+// the tensor-core refine sums serve batches of >= 256 frames (the CUDA-core kernel's 148
+// template tiles spread small ones better; MOCO_RTC=1 forces it at any size: parity tests)
+static bool use_rtc(const moco_plan *p, int l, int64_t B) {
+  const char *rf = getenv("MOCO_RTC");
+  return p->rtab[l] != nullptr && (B >= 256 || (rf && atoi(rf) == 1));
+}
+
+// GA pieces of a batch (k_ga_pieces) for the tensor-core refine at level l.
+static int launch_ga_pieces(moco_plan *p, int l, const void *img, int64_t fstride, int64_t B, const int32_t *sin,
+                            u64 *out, cudaStream_t st) {
+  RefinePickArgs b{};
+  b.frames = (const uint16_t *)img; b.fstride = fstride; b.pitch = p->pitch[l];
+  b.ml = p->ml[l]; b.nl = p->nl[l]; b.B = (int)B; b.shift_in = sin;
+  b.ga_total = 1; b.kw = 16 * p->rtc[l].nk;
+  {
+    ProfScope ps(p, MOCO_K_APPLY, st);
+    k_ga_pieces<<<(unsigned)B, 128, 0, st>>>(b, out);
+  }
+  p->launches++;
+  CKL("k_ga_pieces");
+  return MOCO_OK;
+}
+
 static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride, int64_t B,
                            const int32_t *sin, int32_t *sout, double *fout, void *corr, cudaStream_t st,
-                           u64 *racc = nullptr, cudaStream_t st_pick = nullptr, cudaEvent_t ev_sums = nullptr) {
+                           u64 *racc = nullptr, cudaStream_t st_pick = nullptr, cudaEvent_t ev_sums = nullptr,
+                           const u64 *gbin = nullptr) {
   const int vb = p->bits + 2 * l;
   if (!racc) racc = p->racc;
   RefineSumArgs a;
@@ -690,8 +718,7 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
   // the tensor-core kernel parallelises over 16-frame groups: small batches (the closed
   // loop) keep the CUDA-core kernel, whose 148 template tiles spread even one frame
   // (MOCO_RTC=1 forces the tensor-core kernel at any size: parity tests)
-  const char *rf = getenv("MOCO_RTC");
-  const bool rtc = p->rtab[l] != nullptr && (B >= 256 || (rf && atoi(rf) == 1));
+  const bool rtc = use_rtc(p, l, B);
   if (rtc ? !tmap_u16_sw128(&tmF, img, a.nl, a.ml, B, p->pitch[l], fstride, RTC_R)
           : !tmap_u16_3d(&tmF, img, a.nl, a.ml, B, p->pitch[l], fstride, RS_BOX, a.rt + 2)) {
     snprintf(g_err, sizeof(g_err), "cuTensorMapEncodeTiled failed (refine level %d)", l);
@@ -709,6 +736,7 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
   if (!corr) b.parts = 1;
   b.ga_total = 0;
   b.kw = 0;
+  b.gbin = nullptr;
   if (rtc) {
     ProfScope ps(p, MOCO_K_REFINE, st);
     k_rtc_bucket<<<1, 1024, 0, st>>>(sin, (int)B, p->rperm, p->rmeta);
@@ -717,6 +745,7 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
     r.B = (int)B; r.g = p->rtc[l];
     b.ga_total = RTC_GA_TOTAL;   // the pick completes GA from the staged-pixel total
     b.kw = 16 * p->rtc[l].nk;
+    b.gbin = gbin;
     // row-group ranges per 16-frame group (whole stages): the fewest that bring the last
     // wave near full
     const int64_t groups = (B + RTC_F - 1) / RTC_F + 4;   // upper bound over the 4 classes
@@ -1026,9 +1055,17 @@ static int align_tc_pipelined(moco_plan *p, const void *d_frames, int64_t T, int
       if (rc) return rc;
     }
     CK(cudaEventRecord(p->pe_free[buf], sm));
+    // the pick's GA pieces on the pick stream, beside the refine sums
+    const u64 *gb = nullptr;
+    if (use_rtc(p, 0, B) && p->gbin[buf] && RTC_GA_TOTAL && !getenv("MOCO_GA_INPICK")) {
+      CK(cudaStreamWaitEvent(sa, p->pe_free[buf], 0));
+      rc = launch_ga_pieces(p, 0, fr, (int64_t)p->m * p->n, B, sh1[buf], p->gbin[buf], sa);
+      if (rc) return rc;
+      gb = p->gbin[buf];
+    }
     rc = launch_refine_h(p, 0, fr, (int64_t)p->m * p->n, B, sh1[buf], d_shifts + 2 * f0, d_fmin + f0,
                          d_corrected ? (char *)d_corrected + f0 * fbytes : nullptr, sm, racc[buf], sa,
-                         p->pe_sums[buf]);
+                         p->pe_sums[buf], gb);
     if (rc) return rc;
     CK(cudaEventRecord(p->pe_pick[buf], sa));
   }
