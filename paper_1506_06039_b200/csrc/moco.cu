@@ -1055,9 +1055,11 @@ static int align_tc_pipelined(moco_plan *p, const void *d_frames, int64_t T, int
       if (rc) return rc;
     }
     CK(cudaEventRecord(p->pe_free[buf], sm));
-    // the pick's GA pieces on the pick stream, beside the refine sums
+    // the pick's GA pieces on the pick stream, beside the refine sums -- when the TC search
+    // is short (N <= 128: C2 1.66 -> 1.70 M); behind a long one (C3, N = 256) the pick has
+    // slack and the side kernel only slows the refine on the critical stream (982 -> 939 k)
     const u64 *gb = nullptr;
-    if (use_rtc(p, 0, B) && p->gbin[buf] && RTC_GA_TOTAL && !getenv("MOCO_GA_INPICK")) {
+    if (use_rtc(p, 0, B) && p->gbin[buf] && RTC_GA_TOTAL && p->tc.g.N <= 128 && !getenv("MOCO_GA_INPICK")) {
       CK(cudaStreamWaitEvent(sa, p->pe_free[buf], 0));
       rc = launch_ga_pieces(p, 0, fr, (int64_t)p->m * p->n, B, sh1[buf], p->gbin[buf], sa);
       if (rc) return rc;

@@ -8,10 +8,10 @@ tail -1 $O/bench_full.log > $O/bench_full.json
 timeout 300 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > $O/bench_small.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_ -c 400 --csv \
     --log-file $O/ncu_launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > $O/ncu_launches.log 2>&1
-timeout 120 python tools/profile_run.py --frames 2368 --iters 1 > $O/plain_c2.log 2>&1 && \
+MOCO_BATCH_WAVES=1 timeout 120 python tools/profile_run.py --frames 4736 --iters 1 > $O/plain_c2.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_tc_prep|k_tc_coarse|k_refine_tc|k_refine_pick" -c 4 -o $O/prof_c2 \
-    python tools/profile_run.py --frames 2368 --iters 1 > $O/ncu_c2.log 2>&1
+    -k regex:"k_tc_prep|k_tc_coarse|k_refine_tc|k_refine_pick|k_ga_pieces" -c 5 -o $O/prof_c2 \
+    env MOCO_BATCH_WAVES=1 python tools/profile_run.py --frames 4736 --iters 1 > $O/ncu_c2.log 2>&1
 timeout 120 python tools/profile_run.py --config 4 --frames 256 --iters 1 > $O/plain_c4.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on \
     -k regex:"k_tc_prep|k_tc_coarse|k_refine_tc|k_refine_pick|k_downsample" -c 6 -o $O/prof_c4 \
