@@ -275,7 +275,8 @@ def test_config2_full_stack_sampled():
     batch boundaries checked bit-exactly against the oracle."""
     spec = config_spec(2)
     p = _plan_for(spec)
-    # internal batches are whole TC waves (2 368 frames at C2): both sides of each boundary
+    # internal batches are whole TC waves (one wave = 1 184 frames at C2): both sides of
+    # each boundary
     sample = [0, 1, 2047, 2048, 2367, 2368, 4735, 4736, 5000, 7103, 7104, 8191, 8192, 9471, 9472, 9999]
     spec, st, sh, fm, fl, kinds, p = _run_config(2, spec.T, sample)
     assert kinds == ["exact"] * len(sample)
