@@ -192,7 +192,7 @@ def test_tensor_core_refine_ragged_shapes(m, n, levels, w, T, monkeypatch):
         assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("c,T,rtc", [(2, 800, "1"), (4, 200, "1"), (4, 200, "0")])
+@pytest.mark.parametrize("c,T,rtc", [(2, 800, "1"), (4, 200, "1"), (4, 200, "0"), (2, 1284, None)])
 def test_pipelined_batches_equal_sequential(c, T, rtc, monkeypatch):
     """The three-stream batch pipeline (align_tc_pipelined: operand prep and, at two
     levels, the level-1 downsample of batch k+1 beside the search and refines of batch k)
@@ -201,8 +201,11 @@ def test_pipelined_batches_equal_sequential(c, T, rtc, monkeypatch):
     ragged last one."""
     spec = config_spec(c, T=T)
     st = make_stack(spec, 0, T, device=DEV)
-    monkeypatch.setenv("MOCO_BATCH_MB", "64")
-    monkeypatch.setenv("MOCO_RTC", rtc)
+    if rtc is not None:
+        monkeypatch.setenv("MOCO_BATCH_MB", "64")
+        monkeypatch.setenv("MOCO_RTC", rtc)
+    # (rtc None: default plan -- one 1 184-frame wave with the tensor-core refine and the
+    # GA-pieces kernel, then a 100-frame batch on the CUDA-core refine)
     out = {}
     for mode in ("pipe", "seq"):
         if mode == "seq":
