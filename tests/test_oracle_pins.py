@@ -276,3 +276,88 @@ def test_acceptable_results_contains_winner():
     r = oracle.align_frame(a, b, 5, 1)
     acc = oracle.acceptable_results(a, b, 5, 1)
     assert (r.s, r.t) in acc and acc[(r.s, r.t)] == r.fmin
+
+
+# ------------------------------------------- refine neighbourhood, R10
+@pytest.mark.parametrize("u", [-1, 0, 1])
+@pytest.mark.parametrize("v", [-1, 0, 1])
+def test_refine_reaches_every_neighbour(u, v):
+    """the finer-level search covers f_{2s+u,2t+v} for EVERY u,v in
+    {0,-1,1}.  A frame that is an exact zero-filled translate of b by
+    (2s+u, 2t+v) must make refine(s,t) return that shift with f = 0 exactly.
+    Catches: a dropped +1 or -1 neighbour, or u/v swapped."""
+    rng = np.random.default_rng(100 + 3 * (u + 1) + (v + 1))
+    b = _rand_int(rng, 30, 26).astype(np.uint16)
+    s, t = 2, -3
+    a = pf.translate_zero_fill(b, 2 * s + u, 2 * t + v)
+    r = oracle.refine(a.astype(np.float64), b.astype(np.float64), s, t)
+    assert (r.s, r.t, r.f) == (2 * s + u, 2 * t + v, 0.0)
+
+
+@pytest.mark.parametrize("dy,dx", [(5, -3), (-7, 9), (3, 3), (-1, -5)])
+def test_exact_translate_levels1_odd(dy, dx):
+    """Odd translates at one pyramid level: whichever coarse neighbour the
+    half-integer shift rounds to, the +-1 refine must land on (dy,dx)
+    with f = 0 (P:29-30)."""
+    rng = np.random.default_rng(16)
+    b = _rand_int(rng, 40, 44).astype(np.uint16)
+    a = pf.translate_zero_fill(b, dy, dx)
+    r = oracle.align_frame(a, b, 7, 1)
+    assert (r.s, r.t, r.fmin) == (dy, dx, 0.0)
+    assert abs(2 * r.trace[0].s - dy) == 1 and abs(2 * r.trace[0].t - dx) == 1
+
+
+@pytest.mark.parametrize("dy,dx", [(6, -10), (-2, 7), (5, -9)])
+def test_exact_translate_levels2_not_mod4(dy, dx):
+    """Two levels with components not = 0 mod 4: both refine steps must reach
+    the true shift (P:45 'repeated per level')."""
+    rng = np.random.default_rng(17)
+    b = _rand_int(rng, 56, 52).astype(np.uint16)
+    a = pf.translate_zero_fill(b, dy, dx)
+    r = oracle.align_frame(a, b, 5, 2)
+    assert (r.s, r.t, r.fmin) == (dy, dx, 0.0)
+
+
+# ---------------------------------------------- near-tie threshold (north star)
+def test_select_near_tie_boundary():
+    """BASELINE.json north_star: near-tie = best two f differing by less than
+    1e-4 relative.  f1(1+0.9e-4) is inside the set, f1(1+1.1e-4) outside.
+    Catches a loosened or tightened threshold."""
+    f1 = 1000.0
+    r = oracle.select([(f1, 0, 0), (f1 * (1 + 0.9e-4), 1, 0), (f1 * (1 + 1.1e-4), -1, 0)])
+    assert (r.s, r.t) == (0, 0)
+    assert r.near_ties == [(0, 0), (1, 0)]
+    r = oracle.select([(f1, 0, 0), (f1 * (1 + 1.1e-4), 1, 0)])
+    assert r.near_ties == [(0, 0)] and r.f2 == f1 * (1 + 1.1e-4)
+    # an exact tie always is one, the winner by (s,t)
+    r = oracle.select([(5.0, 3, 1), (5.0, 3, -1)])
+    assert (r.s, r.t) == (3, -1) and r.near_ties == [(3, -1), (3, 1)]
+
+
+# --------------------------------------------- acceptable set, by hand (R15)
+def test_acceptable_results_branches_every_level():
+    """Constant frame = constant template: every f at every level is 0, so
+    every coarse lag |s|,|t| <= w-1 is a near-tie and each branches into its
+    nine refine candidates (all f = 0).  By hand, the acceptable final shifts
+    at levels = 1 are exactly {(S,T) : |S|,|T| <= 2w-1}, each with f = 0;
+    at levels = 2 they are {|S|,|T| <= 4w-1}.  Catches: following only the
+    winner instead of the whole near-tie frontier."""
+    w = 3
+    a = np.full((24, 28), 11, np.uint16)
+    acc = oracle.acceptable_results(a, a, w, 1)
+    want = {(S, T) for S in range(-(2 * w - 1), 2 * w) for T in range(-(2 * w - 1), 2 * w)}
+    assert set(acc) == want and all(f == 0.0 for f in acc.values())
+    a2 = np.full((40, 44), 11, np.uint16)
+    acc2 = oracle.acceptable_results(a2, a2, 2, 2)
+    want2 = {(S, T) for S in range(-7, 8) for T in range(-7, 8)}
+    assert set(acc2) == want2
+
+
+def test_acceptable_results_unique_without_ties():
+    """With no near-tie at any level the acceptable set is the oracle's single
+    answer (exact translate: f = 0 only at the true shift)."""
+    rng = np.random.default_rng(18)
+    b = _rand_int(rng, 32, 36).astype(np.uint16)
+    a = pf.translate_zero_fill(b, 4, -6)
+    acc = oracle.acceptable_results(a, b, 5, 1)
+    assert acc == {(4, -6): 0.0}
