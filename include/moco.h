@@ -20,7 +20,10 @@
  *   - Returned shifts are full-resolution pixels; f_min is f at level 0 (R11).
  *   - Odd dimensions: the trailing row/column is dropped at each level (R1).
  *
- * Data layout: every image is row-major, rows of n elements, no padding.
+ * Data layout: every image is row-major, rows of n elements, no padding.  Rows
+ *   whose byte length is not a multiple of 16 (e.g. the paper's 416x460 video,
+ *   P:62) are accepted: such plans stage each internal batch through a
+ *   padded-pitch device buffer with stream-ordered 2-D copies.
  *   Frames: T consecutive m*n images.  MOCO_U16: uint16 samples holding
  *   integers < 2^bits.  MOCO_F32: float32 samples.
  *
@@ -82,11 +85,25 @@ enum moco_algo { MOCO_ALGO_AUTO = 0, MOCO_ALGO_DIRECT = 1, MOCO_ALGO_TC = 2, MOC
  *   device  CUDA device ordinal the plan lives on.
  * EINVAL when: out == NULL; levels not in {0,1,2}; m or n < 2^(levels+1);
  *   w < 1 or w >= min(m_L, n_L) with m_L = floor(m / 2^levels); unknown dtype;
- *   bits out of range; n * sizeof(sample) not a multiple of 16 bytes.
- * ENOMEM when workspace allocation fails.  No kernel is launched.
+ *   bits out of range.
+ * ENOMEM when workspace allocation fails.  No kernel is launched; every stream,
+ * event and buffer moco_align_batch uses is created here.
  */
 int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype,
                      int bits, int device);
+
+/*
+ * moco_auto_config -- the paper's default settings for an m x n video (P:49,
+ * section 3): "If the images are larger than 256x256, we downsample once,
+ * otherwise, we do not downsample" -> *levels = 1 if m > 256 or n > 256, else 0;
+ * "a maximum translation width of min(m,n)/3" -> *w = floor(min(m_L, n_L) / 3)
+ * at the coarsest level (m_L = floor(m / 2^levels); reading R16: w is
+ * the coarse-level bound, R2).  The paper's template is "the first image in the
+ * video": pass the first frame as d_template to moco_set_template.
+ * Host-only arithmetic.  EINVAL on NULL outputs or when no w >= 1 fits
+ * (min(m_L, n_L) < 3).
+ */
+int moco_auto_config(int m, int n, int *w, int *levels);
 
 /* Force the coarse-search algorithm (tests/benchmarks); EINVAL if unsupported
  * for this plan (MOCO_ALGO_TC needs MOCO_U16 with bits + 2*levels <= 14;

@@ -4,6 +4,7 @@ shift-apply, as hand-written sm_100a CUDA kernels behind the C-ABI in
 include/moco.h.  This package is the thin Python binding (``Plan``) plus the
 build helper and the multi-GPU driver; it never imports ``oracle/``.
 """
-from ._lib import (FLAG_EDGE, FLAG_FULL, LIB_PATH, MocoError, Plan, exported_symbols, load)  # noqa: F401
+from ._lib import (FLAG_EDGE, FLAG_FULL, LIB_PATH, MocoError, Plan, auto_config, exported_symbols,  # noqa: F401
+                   load)
 
-__all__ = ["Plan", "MocoError", "load", "LIB_PATH", "FLAG_EDGE", "FLAG_FULL", "exported_symbols"]
+__all__ = ["Plan", "MocoError", "auto_config", "load", "LIB_PATH", "FLAG_EDGE", "FLAG_FULL", "exported_symbols"]

@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("MOCO_LIB") or os.path.join(_HERE, "libmoco.so")
+LIB_PATH = os.path.join(_HERE, "libmoco.so")
 
 MOCO_U16, MOCO_F32 = 1, 2
 MOCO_ALGO_AUTO, MOCO_ALGO_DIRECT, MOCO_ALGO_TC, MOCO_ALGO_FFT = 0, 1, 2, 3
@@ -29,6 +29,7 @@ _I = ctypes.c_int
 _I64 = ctypes.c_int64
 SIGNATURES = [
     ("moco_plan_create", _I, [ctypes.POINTER(_P), _I, _I, _I, _I, _I, _I, _I]),
+    ("moco_auto_config", _I, [_I, _I, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
     ("moco_plan_set_algo", _I, [_P, _I]),
     ("moco_plan_get_algo", _I, [_P]),
     ("moco_set_template", _I, [_P, _P, _P]),
@@ -109,6 +110,16 @@ class Plan:
         self._h = h
         if algo is not None:
             self.set_algo(algo)
+
+    @classmethod
+    def auto(cls, frames: torch.Tensor, bits: int = 12, algo: Optional[str] = None) -> "Plan":
+        """The paper's settings: w and levels from moco_auto_config, template =
+        the first frame of `frames` (a device tensor (T, m, n))."""
+        T, m, n = frames.shape
+        w, levels = auto_config(m, n)
+        dt = "u16" if frames.dtype == torch.uint16 else "f32"
+        plan = cls(m, n, w, levels, dt, bits, device=frames.device.index, algo=algo)
+        return plan.set_template(frames[0])
 
     # -- algorithm selection (tests/bench)
     def set_algo(self, algo: str):
@@ -216,6 +227,13 @@ class Plan:
             self.close()
         except Exception:
             pass
+
+
+def auto_config(m: int, n: int) -> Tuple[int, int]:
+    """The paper's default (w, levels) for m x n frames (moco_auto_config)."""
+    w, lv = _I(), _I()
+    _check(load().moco_auto_config(m, n, ctypes.byref(w), ctypes.byref(lv)), "moco_auto_config")
+    return w.value, lv.value
 
 
 def exported_symbols():

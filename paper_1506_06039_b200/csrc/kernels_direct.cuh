@@ -16,11 +16,33 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
 #include <type_traits>
+#include <utility>
 
 namespace moco {
 
 typedef unsigned long long u64;
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a property of the function on a device,
+// shared by every plan of the process: only ever RAISE it (a plan with a smaller geometry
+// created later must not lower the limit under an earlier plan's launches).
+inline cudaError_t smem_attr(const void *fn, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void *>, int> set;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  int &cur = set[{dev, fn}];
+  if (bytes <= cur) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
+template <class K>
+inline cudaError_t smem_attr(K *fn, int bytes) { return smem_attr((const void *)fn, bytes); }
 
 // ---------------------------------------------------------------- key helpers
 // f >= 0, so the IEEE-754 bit pattern of the double orders like an unsigned
@@ -530,11 +552,12 @@ __global__ void __launch_bounds__(256) k_refine(RefineArgs a) {
 
 // ------------------------------------------------------------------------- K7
 // corrected[i][j] = a[i+s][j+t] if in range else 0, 16 bytes of output per thread.
+// Rows are `pitch` elements apart (a multiple of 16 bytes); columns >= n are written as 0.
 template <class E>
-__global__ void k_apply(const E *__restrict__ in, E *__restrict__ out, int m, int n,
+__global__ void k_apply(const E *__restrict__ in, E *__restrict__ out, int m, int n, int pitch,
                         const int32_t *__restrict__ shifts, int B) {
   constexpr int V = 16 / sizeof(E);
-  const int groups = n / V;   // n * sizeof(E) is a multiple of 16 (plan validation)
+  const int groups = pitch / V;
   const int64_t total = (int64_t)B * m * groups;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
        g += (int64_t)gridDim.x * blockDim.x) {
@@ -549,14 +572,14 @@ __global__ void k_apply(const E *__restrict__ in, E *__restrict__ out, int m, in
 #pragma unroll
       for (int k = 0; k < V; ++k) o[k] = (E)0;
     } else {
-      const E *src = in + f * (int64_t)m * n + (int64_t)r * n;
+      const E *src = in + f * (int64_t)m * pitch + (int64_t)r * pitch;
 #pragma unroll
       for (int k = 0; k < V; ++k) {
         const int c = cg * V + k + t;
-        o[k] = (c >= 0 && c < n) ? src[c] : (E)0;
+        o[k] = (c >= 0 && c < n && cg * V + k < n) ? src[c] : (E)0;
       }
     }
-    *reinterpret_cast<uint4 *>(out + f * (int64_t)m * n + (int64_t)i * n + cg * V) =
+    *reinterpret_cast<uint4 *>(out + f * (int64_t)m * pitch + (int64_t)i * pitch + cg * V) =
         *reinterpret_cast<const uint4 *>(o);
   }
 }

@@ -1083,18 +1083,18 @@ inline int tc_init(TcPlan *tc, int w, int mc, int nc, int L, int vb, int64_t cap
   if (cudaMalloc(&tc->T8, (size_t)2 * (mc + 2) * g.TP) != cudaSuccess) return -1;
   // precomputed B tiles (MOCO_TC_BTAB=0: the producer warps build them per CTA)
   if (!g.stg && cudaMalloc(&tc->Btab, (size_t)g.nstrips * g.npairs * g.N * 32) != cudaSuccess) return -1;
-  if (cudaFuncSetAttribute(k_tc_coarse<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
-      cudaFuncSetAttribute(k_tc_coarse<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
-      cudaFuncSetAttribute(k_tc_coarse<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
-      cudaFuncSetAttribute(k_tc_coarse<14>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
-      cudaFuncSetAttribute(k_tc_coarse<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
-      cudaFuncSetAttribute(k_tc_coarse<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
-      cudaFuncSetAttribute(k_tc_coarse<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess ||
-      cudaFuncSetAttribute(k_tc_coarse<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) != cudaSuccess)
+  if (smem_attr(k_tc_coarse<2>, g.smem) != cudaSuccess ||
+      smem_attr(k_tc_coarse<4>, g.smem) != cudaSuccess ||
+      smem_attr(k_tc_coarse<10>, g.smem) != cudaSuccess ||
+      smem_attr(k_tc_coarse<14>, g.smem) != cudaSuccess ||
+      smem_attr(k_tc_coarse<6>, g.smem) != cudaSuccess ||
+      smem_attr(k_tc_coarse<8>, g.smem) != cudaSuccess ||
+      smem_attr(k_tc_coarse<12>, g.smem) != cudaSuccess ||
+      smem_attr(k_tc_coarse<16>, g.smem) != cudaSuccess)
     return -1;
-  if (cudaFuncSetAttribute(k_tc_prep<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.prep_smem) != cudaSuccess ||
-      cudaFuncSetAttribute(k_tc_prep<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.prep_smem) != cudaSuccess ||
-      cudaFuncSetAttribute(k_tc_prep<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.prep_smem) != cudaSuccess)
+  if (smem_attr(k_tc_prep<0>, g.prep_smem) != cudaSuccess ||
+      smem_attr(k_tc_prep<1>, g.prep_smem) != cudaSuccess ||
+      smem_attr(k_tc_prep<2>, g.prep_smem) != cudaSuccess)
     return -1;
   tc->ready = true;
   return 0;

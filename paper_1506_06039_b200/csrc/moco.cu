@@ -61,6 +61,17 @@ struct moco_plan {
   void *scratch[3];           // frame pyramid levels 1..L for one batch
   int32_t *sh[3];             // per-level shifts for one batch
   bool has_tpl;
+  // rows of n samples that are not a multiple of 16 bytes: frames are staged through
+  // buffers with the padded level-0 pitch (pitch[0] > n)
+  bool stage;
+  void *stage_in, *stage_out;
+  // tuning / cross-check switches, read from the environment ONCE at plan creation
+  // (DESIGN.md §8 table) -- no getenv on the per-batch launch path
+  struct {
+    int rtc = -1;          // MOCO_RTC: -1 default, 0 CUDA-core refine sums, 1 force tensor cores
+    int rtc_parts = 0;     // MOCO_RTC_PARTS (0: cost model)
+    bool nofuse_ds = false, ga_inpick = false, nopipe = false;
+  } knob;
   bool simple_refine;         // MOCO_REFINE=simple: unfused K6/K7 (cross-check in tests)
   int simple_level;           // MOCO_REFINE=simpleN: simple K6 at level N only (debug)
   int64_t launches;
@@ -159,6 +170,16 @@ static size_t coarse_smem(const moco_plan *p, int sc, int br, int fpitch) {
 
 int moco_abi_version(void) { return MOCO_ABI_VERSION; }
 
+int moco_auto_config(int m, int n, int *w, int *levels) {
+  if (!w || !levels || m < 1 || n < 1) return MOCO_EINVAL;
+  const int L = (m > 256 || n > 256) ? 1 : 0;
+  const int wc = std::min(m >> L, n >> L) / 3;  // P:49 min(m,n)/3, at the coarse level (R16)
+  if (wc < 1) return MOCO_EINVAL;
+  *w = wc;
+  *levels = L;
+  return MOCO_OK;
+}
+
 const char *moco_strerror(int code) {
   switch (code) {
     case MOCO_OK: return "ok";
@@ -188,6 +209,8 @@ static void plan_free(moco_plan *p) {
     if (p->rtab[l]) cudaFree(p->rtab[l]);
   }
   if (p->rperm) cudaFree(p->rperm);
+  if (p->stage_in) cudaFree(p->stage_in);
+  if (p->stage_out) cudaFree(p->stage_out);
   if (p->rmeta) cudaFree(p->rmeta);
   tc_free(&p->tc);
   for (void *q : {(void *)p->fft.twr, (void *)p->fft.twc, (void *)p->fft.Bc, (void *)p->fft.S, (void *)p->fft.P,
@@ -269,11 +292,11 @@ static int fft_init(moco_plan *p) {
   F.smem_score = (Mc + 2 * FFT_ROWS_PAIRS * Mc) * 8 + ((g.W * g.W + 1) & ~1) * 4 + 2 * g.W * 8;
   F.smem_energy = (4 * g.hw + g.w * g.w + 1) * 8;
   if (F.smem_score > 227 * 1024 || F.smem_energy > 227 * 1024) return MOCO_EINVAL;
-  CK(cudaFuncSetAttribute(k_fft_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, F.smem_rows));
-  CK(cudaFuncSetAttribute(k_fft_score_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, F.smem_rows));
-  CK(cudaFuncSetAttribute(k_fft_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, F.smem_cols));
-  CK(cudaFuncSetAttribute(k_fft_score, cudaFuncAttributeMaxDynamicSharedMemorySize, F.smem_score));
-  CK(cudaFuncSetAttribute(k_energy_u16, cudaFuncAttributeMaxDynamicSharedMemorySize, F.smem_energy));
+  CK(smem_attr(k_fft_rows, F.smem_rows));
+  CK(smem_attr(k_fft_score_rows, F.smem_rows));
+  CK(smem_attr(k_fft_cols, F.smem_cols));
+  CK(smem_attr(k_fft_score, F.smem_score));
+  CK(smem_attr(k_energy_u16, F.smem_energy));
   k_fft_twiddles<<<(Mr + 255) / 256, 256>>>(F.twr, Mr);
   k_fft_twiddles<<<(Mc + 255) / 256, 256>>>(F.twc, Mc);
   CKL("k_fft_twiddles");
@@ -366,6 +389,21 @@ static int launch_fft(moco_plan *p, const void *img, int64_t fstride, int pitch,
   return MOCO_OK;
 }
 
+static int pipe_create(moco_plan *p) {
+  for (int k = 0; k < 3; ++k) CK(cudaStreamCreateWithFlags(&p->ps[k], cudaStreamNonBlocking));
+  for (int k = 0; k < 2; ++k) {
+    CK(cudaEventCreateWithFlags(&p->pe_prep[k], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&p->pe_free[k], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&p->pe_sums[k], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&p->pe_pick[k], cudaEventDisableTiming));
+  }
+  CK(cudaEventCreateWithFlags(&p->pe_start, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&p->pe_end, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&p->pe_end2, cudaEventDisableTiming));
+  p->pipe_ready = true;
+  return MOCO_OK;
+}
+
 int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype, int bits,
                      int device) {
   if (!out) return MOCO_EINVAL;
@@ -375,7 +413,6 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
   if (dtype == MOCO_U16 && (bits < 1 || bits > 16 || bits + 2 * levels > 16)) return MOCO_EINVAL;
   if (m < (2 << levels) || n < (2 << levels)) return MOCO_EINVAL;
   const size_t e0 = dtype == MOCO_U16 ? 2 : 4;
-  if ((n * e0) % 16 != 0) return MOCO_EINVAL;
   const int mL = m >> levels, nL = n >> levels;
   if (w < 1 || w >= std::min(mL, nL)) return MOCO_EINVAL;
   if (w > 64 && dtype != MOCO_U16) return MOCO_EINVAL;   // w > 64: FFT path only
@@ -396,11 +433,16 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
     const char *e = getenv("MOCO_REFINE");
     p->simple_refine = e && strcmp(e, "simple") == 0;
     p->simple_level = (e && strncmp(e, "simple", 6) == 0 && e[6] >= '0' && e[6] <= '9') ? e[6] - '0' : -1;
+    if (const char *v = getenv("MOCO_RTC")) p->knob.rtc = atoi(v) ? 1 : 0;
+    if (const char *v = getenv("MOCO_RTC_PARTS")) p->knob.rtc_parts = std::max(0, atoi(v));
+    p->knob.nofuse_ds = getenv("MOCO_NOFUSE_DS") != nullptr;
+    p->knob.ga_inpick = getenv("MOCO_GA_INPICK") != nullptr;
+    p->knob.nopipe = getenv("MOCO_NOPIPE") != nullptr;
   }
   for (int l = 0; l <= levels; ++l) {
     p->ml[l] = m >> l;
     p->nl[l] = n >> l;
-    p->pitch[l] = l == 0 ? n : round_up(p->nl[l], 8);
+    p->pitch[l] = l == 0 ? round_up(n, (int)(16 / e0)) : round_up(p->nl[l], 8);
     p->esz[l] = dtype == MOCO_U16 ? 2 : (l == 0 ? 4 : 8);
   }
   // coarse kernel geometry (K3+K4d+K5)
@@ -422,6 +464,8 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
   alloc(&p->gb, (size_t)W * W * 8);
   size_t per_frame = 0;
   for (int l = 1; l <= levels; ++l) per_frame += (size_t)p->ml[l] * p->pitch[l] * p->esz[l];
+  p->stage = p->pitch[0] != n;
+  if (p->stage) per_frame += (size_t)2 * m * p->pitch[0] * e0;
   // tensor-core operand planes + lag energies (upper bound: rows <= m_L + 128, int8 hi/lo)
   if (dtype == MOCO_U16) per_frame += (size_t)2 * (p->ml[levels] + 128) * p->nl[levels] + (size_t)W * W * 8;
   size_t budget = (size_t)1 << 30;   // internal batch scratch (B200: 180 GB HBM)
@@ -431,6 +475,10 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
   for (int l = 1; l <= levels; ++l)
     alloc(&p->scratch[l], (size_t)p->cap * p->ml[l] * p->pitch[l] * p->esz[l]);
   for (int l = 0; l <= levels; ++l) alloc((void **)&p->sh[l], (size_t)p->cap * 2 * sizeof(int32_t));
+  if (p->stage) {
+    alloc(&p->stage_in, (size_t)p->cap * m * p->pitch[0] * e0);
+    alloc(&p->stage_out, (size_t)p->cap * m * p->pitch[0] * e0);
+  }
   if (dtype == MOCO_U16 && levels > 0) {
     alloc((void **)&p->racc, (size_t)p->cap * 18 * sizeof(u64));
     alloc((void **)&p->racc2, (size_t)p->cap * 18 * sizeof(u64));
@@ -462,8 +510,7 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
       p->rstages[l] = std::min(32, (150 * 1024 - rs_smem_bytes(rt, 0)) / rs_stage_bytes(rt));
       // tensor-core refine sums (kernels_rtc.cuh) where they apply; MOCO_RTC=0 selects the
       // CUDA-core kernel (parity cross-check)
-      const char *re = getenv("MOCO_RTC");
-      if (!(re && atoi(re) == 0) && rtc_make(&p->rtc[l], p->ml[l], p->nl[l], bits + 2 * l)) {
+      if (p->knob.rtc != 0 && rtc_make(&p->rtc[l], p->ml[l], p->nl[l], bits + 2 * l)) {
         const size_t tb = rtc_table_bytes(p->rtc[l]);
         if (cudaMalloc((void **)&p->rtab[l], tb) != cudaSuccess ||
             (!p->rperm && (cudaMalloc((void **)&p->rperm, (size_t)p->cap * sizeof(int)) != cudaSuccess ||
@@ -484,10 +531,10 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
       smem = std::max(smem, rs_smem_bytes(p->rrt[l], p->rstages[l]));
       any_rtc = any_rtc || p->rtab[l] != nullptr;
     }
-    if (cudaFuncSetAttribute(k_refine_sums<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
-        cudaFuncSetAttribute(k_refine_sums<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+    if (smem_attr(k_refine_sums<false>, smem) != cudaSuccess ||
+        smem_attr(k_refine_sums<true>, smem) != cudaSuccess ||
         (any_rtc &&
-         cudaFuncSetAttribute(k_refine_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, RTC_SMEM) != cudaSuccess)) {
+         smem_attr(k_refine_tc, RTC_SMEM) != cudaSuccess)) {
       plan_free(p);
       return set_cuda_err(cudaGetLastError(), "refine kernel attributes");
     }
@@ -517,6 +564,12 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
     if (fft_init(p) != MOCO_OK) cudaGetLastError();   // latency route for small calls (optional)
   }
   if (w > 64 && p->algo != MOCO_ALGO_FFT) { plan_free(p); return MOCO_EINVAL; }
+  // streams and events of the batch pipeline (align_tc_pipelined) are created here, so
+  // that moco_align_batch never allocates (moco.h) and can be captured in a CUDA graph
+  if (dtype == MOCO_U16 && levels > 0) {
+    const int prc = pipe_create(p);
+    if (prc) { plan_free(p); return prc; }
+  }
   *out = p;
   return MOCO_OK;
 }
@@ -629,8 +682,7 @@ template <class In, bool WIDE>
 static int launch_coarse_t(moco_plan *p, const CoarseArgs &a, cudaStream_t st) {
   static bool attr_done[8] = {false};   // per-device attribute is set once per process
   (void)attr_done;
-  CK(cudaFuncSetAttribute(k_coarse<In, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)p->c_smem));
+  CK(smem_attr(k_coarse<In, WIDE>, (int)p->c_smem));
   ProfScope ps(p, MOCO_K_COARSE, st);
   k_coarse<In, WIDE><<<a.B, p->c_threads, p->c_smem, st>>>(a);
   p->launches++;
@@ -680,8 +732,7 @@ static int launch_refine(moco_plan *p, int l, const void *img, int64_t fstride, 
 // the tensor-core refine sums serve batches of >= 256 frames (the CUDA-core kernel's 148
 // template tiles spread small ones better; MOCO_RTC=1 forces it at any size: parity tests)
 static bool use_rtc(const moco_plan *p, int l, int64_t B) {
-  const char *rf = getenv("MOCO_RTC");
-  return p->rtab[l] != nullptr && (B >= 256 || (rf && atoi(rf) == 1));
+  return p->rtab[l] != nullptr && (B >= 256 || p->knob.rtc == 1);
 }
 
 // GA pieces of a batch (k_ga_pieces) for the tensor-core refine at level l.
@@ -763,7 +814,7 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
       const double cost = waves * (0.08 + 1.0 / parts);
       if (cost < bestc) { bestc = cost; best = parts; }
     }
-    if (const char *pe = getenv("MOCO_RTC_PARTS")) best = std::max(1, std::min(nblk, atoi(pe)));   // tuning
+    if (p->knob.rtc_parts) best = std::min(nblk, p->knob.rtc_parts);   // tuning
     r.groups_per_part = (nblk + best - 1) / best * RTC_RG;
     r.parts = (p->rtc[l].ng + r.groups_per_part - 1) / r.groups_per_part;
     k_refine_tc<<<(unsigned)(groups * r.parts), RTC_THREADS, RTC_SMEM, st>>>(tmF, r);
@@ -803,13 +854,13 @@ static int launch_apply(moco_plan *p, const void *in, void *out, const int32_t *
                         cudaStream_t st) {
   ProfScope ps(p, MOCO_K_APPLY, st);
   if (p->dtype == MOCO_U16) {
-    const int64_t work = B * p->m * (p->n / 8);
+    const int64_t work = B * p->m * (p->pitch[0] / 8);
     k_apply<uint16_t><<<grid_for(work, 256), 256, 0, st>>>((const uint16_t *)in, (uint16_t *)out,
-                                                           p->m, p->n, sh, (int)B);
+                                                           p->m, p->n, p->pitch[0], sh, (int)B);
   } else {
-    const int64_t work = B * p->m * (p->n / 4);
+    const int64_t work = B * p->m * (p->pitch[0] / 4);
     k_apply<float><<<grid_for(work, 256), 256, 0, st>>>((const float *)in, (float *)out, p->m,
-                                                        p->n, sh, (int)B);
+                                                        p->n, p->pitch[0], sh, (int)B);
   }
   p->launches++;
   CKL("k_apply");
@@ -820,8 +871,9 @@ int moco_set_template(moco_plan *p, const void *d_template, moco_stream_t stream
   if (!p || !d_template) return MOCO_EINVAL;
   CK(cudaSetDevice(p->device));
   cudaStream_t st = (cudaStream_t)stream;
-  const size_t bytes0 = (size_t)p->m * p->n * p->esz[0];
-  CK(cudaMemcpyAsync(p->tpl[0], d_template, bytes0, cudaMemcpyDeviceToDevice, st));
+  const size_t row0 = (size_t)p->n * p->esz[0];
+  CK(cudaMemcpy2DAsync(p->tpl[0], (size_t)p->pitch[0] * p->esz[0], d_template, row0, row0, p->m,
+                       cudaMemcpyDeviceToDevice, st));
   for (int l = 0; l < p->levels; ++l) {
     int rc = launch_downsample(p, l, p->tpl[l], 0, p->tpl[l + 1], 1, st);
     if (rc) return rc;
@@ -874,7 +926,7 @@ static int check_align_args(moco_plan *p, const void *frames, int64_t T) {
 // levels = 2: the operand preparation also writes the level-1 image (the refine at level
 // 1 reads it) when the level-2 band covers it exactly
 static bool prep_emits_l1(const moco_plan *p) {
-  if (p->levels != 2 || p->dtype != MOCO_U16 || getenv("MOCO_NOFUSE_DS")) return false;
+  if (p->levels != 2 || p->dtype != MOCO_U16 || p->knob.nofuse_ds) return false;
   return p->ml[1] == 2 * p->ml[2] && p->nl[1] == 2 * p->nl[2] && p->nl[2] % 8 == 0 && p->pitch[1] % 8 == 0;
 }
 
@@ -958,7 +1010,7 @@ static int run_batch(moco_plan *p, const void *frames_b, int64_t B, int32_t *shi
   const void *img[3];
   int64_t fstride[3];
   img[0] = frames_b;
-  fstride[0] = (int64_t)p->m * p->n;
+  fstride[0] = (int64_t)p->m * p->pitch[0];
   for (int l = 1; l <= L; ++l) {
     img[l] = p->scratch[l];
     fstride[l] = (int64_t)p->ml[l] * p->pitch[l];
@@ -996,6 +1048,31 @@ static int run_batch(moco_plan *p, const void *frames_b, int64_t B, int32_t *shi
   return refine_levels(p, img, fstride, B, shifts_b, fmin_b, corr_b, st);
 }
 
+// run_batch on caller frames with unpadded rows: plans whose rows are not a multiple of
+// 16 bytes (p->stage) copy the batch into the padded-pitch staging buffer first and the
+// corrected frames back out (stream-ordered 2-D copies); otherwise a plain run_batch.
+static const void *stage_frames(moco_plan *p, const void *frames_b, int64_t B, cudaStream_t st, int *rc) {
+  *rc = MOCO_OK;
+  if (!p->stage) return frames_b;
+  const size_t row = (size_t)p->n * p->esz[0], dpitch = (size_t)p->pitch[0] * p->esz[0];
+  cudaError_t e = cudaMemcpy2DAsync(p->stage_in, dpitch, frames_b, row, row, (size_t)B * p->m,
+                                    cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) *rc = set_cuda_err(e, "stage frames in");
+  return p->stage_in;
+}
+
+static int run_batch_user(moco_plan *p, const void *frames_b, int64_t B, int32_t *shifts_b, double *fmin_b,
+                          void *corr_b, uint8_t *flags_b, double *grid_b, cudaStream_t st) {
+  int rc;
+  const void *src = stage_frames(p, frames_b, B, st, &rc);
+  if (rc) return rc;
+  rc = run_batch(p, src, B, shifts_b, fmin_b, (p->stage && corr_b) ? p->stage_out : corr_b, flags_b, grid_b, st);
+  if (rc || !p->stage || !corr_b) return rc;
+  const size_t row = (size_t)p->n * p->esz[0], spitch = (size_t)p->pitch[0] * p->esz[0];
+  CK(cudaMemcpy2DAsync(corr_b, row, p->stage_out, spitch, row, (size_t)B * p->m, cudaMemcpyDeviceToDevice, st));
+  return MOCO_OK;
+}
+
 // Several internal batches on the tensor-core path (levels = 1): the HBM-bound operand
 // preparation of batch k+1 runs on a second stream into the other G/ga buffer while the
 // tensor-core search, refine and apply of batch k run on the main stream, so the
@@ -1005,19 +1082,7 @@ constexpr int64_t LAT_T = 16;   // calls with at most this many frames take the 
 
 static int align_tc_pipelined(moco_plan *p, const void *d_frames, int64_t T, int32_t *d_shifts, double *d_fmin,
                               void *d_corrected, uint8_t *d_flags, cudaStream_t user) {
-  if (!p->pipe_ready) {
-    for (int k = 0; k < 3; ++k) CK(cudaStreamCreateWithFlags(&p->ps[k], cudaStreamNonBlocking));
-    for (int k = 0; k < 2; ++k) {
-      CK(cudaEventCreateWithFlags(&p->pe_prep[k], cudaEventDisableTiming));
-      CK(cudaEventCreateWithFlags(&p->pe_free[k], cudaEventDisableTiming));
-      CK(cudaEventCreateWithFlags(&p->pe_sums[k], cudaEventDisableTiming));
-      CK(cudaEventCreateWithFlags(&p->pe_pick[k], cudaEventDisableTiming));
-    }
-    CK(cudaEventCreateWithFlags(&p->pe_start, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&p->pe_end, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&p->pe_end2, cudaEventDisableTiming));
-    p->pipe_ready = true;
-  }
+  if (!p->pipe_ready) return MOCO_ESTATE;   // created by moco_plan_create
   // prep stream | main stream (TC search, refine sums) | pick/apply stream.  Per batch
   // parity: operand planes G/ga, coarse shifts and refine accumulators are double-
   // buffered; a buffer is reused two batches later, after the events below.
@@ -1063,7 +1128,7 @@ static int align_tc_pipelined(moco_plan *p, const void *d_frames, int64_t T, int
     // is short (N <= 128: C2 1.66 -> 1.70 M); behind a long one (C3, N = 256) the pick has
     // slack and the side kernel only slows the refine on the critical stream (982 -> 939 k)
     const u64 *gb = nullptr;
-    if (use_rtc(p, 0, B) && p->gbin[buf] && RTC_GA_TOTAL && p->tc.g.N <= 128 && !getenv("MOCO_GA_INPICK")) {
+    if (use_rtc(p, 0, B) && p->gbin[buf] && RTC_GA_TOTAL && p->tc.g.N <= 128 && !p->knob.ga_inpick) {
       CK(cudaStreamWaitEvent(sa, p->pe_free[buf], 0));
       rc = launch_ga_pieces(p, 0, fr, (int64_t)p->m * p->n, B, sh1[buf], p->gbin[buf], sa);
       if (rc) return rc;
@@ -1097,7 +1162,7 @@ int moco_align_batch(moco_plan *p, const void *d_frames, int64_t T, int32_t *d_s
     p->algo = MOCO_ALGO_FFT;
     for (int64_t f0 = 0; f0 < T && rc == MOCO_OK; f0 += p->cap) {
       const int64_t B = std::min<int64_t>(p->cap, T - f0);
-      rc = run_batch(p, (const char *)d_frames + f0 * fbytes, B, d_shifts + 2 * f0, d_fmin + f0,
+      rc = run_batch_user(p, (const char *)d_frames + f0 * fbytes, B, d_shifts + 2 * f0, d_fmin + f0,
                      d_corrected ? (char *)d_corrected + f0 * fbytes : nullptr,
                      d_flags ? d_flags + f0 : nullptr, nullptr, (cudaStream_t)stream);
     }
@@ -1105,11 +1170,11 @@ int moco_align_batch(moco_plan *p, const void *d_frames, int64_t T, int32_t *d_s
     return rc;
   }
   if (p->algo == MOCO_ALGO_TC && T > p->cap && p->tc.G2 && p->racc2 && p->sh1b && fused_ok(p, 0) &&
-      (p->levels == 1 || (p->levels == 2 && p->scratch1b && p->sh2b[1] && fused_ok(p, 1))) && !getenv("MOCO_NOPIPE"))
+      (p->levels == 1 || (p->levels == 2 && p->scratch1b && p->sh2b[1] && fused_ok(p, 1))) && !p->knob.nopipe)
     return align_tc_pipelined(p, d_frames, T, d_shifts, d_fmin, d_corrected, d_flags, (cudaStream_t)stream);
   for (int64_t f0 = 0; f0 < T; f0 += p->cap) {
     const int64_t B = std::min<int64_t>(p->cap, T - f0);
-    rc = run_batch(p, (const char *)d_frames + f0 * fbytes, B, d_shifts + 2 * f0, d_fmin + f0,
+    rc = run_batch_user(p, (const char *)d_frames + f0 * fbytes, B, d_shifts + 2 * f0, d_fmin + f0,
                    d_corrected ? (char *)d_corrected + f0 * fbytes : nullptr,
                    d_flags ? d_flags + f0 : nullptr, nullptr, (cudaStream_t)stream);
     if (rc) return rc;
@@ -1128,7 +1193,7 @@ int moco_score_grid(moco_plan *p, const void *d_frames, int64_t T, double *d_f,
   const int64_t WW = (int64_t)p->W * p->W;
   for (int64_t f0 = 0; f0 < T; f0 += p->cap) {
     const int64_t B = std::min<int64_t>(p->cap, T - f0);
-    rc = run_batch(p, (const char *)d_frames + f0 * fbytes, B, nullptr, nullptr, nullptr, nullptr,
+    rc = run_batch_user(p, (const char *)d_frames + f0 * fbytes, B, nullptr, nullptr, nullptr, nullptr,
                    d_f + f0 * WW, (cudaStream_t)stream);
     if (rc) return rc;
   }
@@ -1155,8 +1220,9 @@ int moco_fft_cross(moco_plan *p, const void *d_frames, int64_t T, float *d_h, in
   const int64_t WW = (int64_t)p->W * p->W;
   for (int64_t f0 = 0; f0 < T; f0 += p->cap) {
     const int64_t B = std::min<int64_t>(p->cap, T - f0);
-    const void *img = (const char *)d_frames + f0 * fbytes;
-    int64_t fs = (int64_t)p->m * p->n;
+    const void *img = stage_frames(p, (const char *)d_frames + f0 * fbytes, B, st, &rc);
+    if (rc) return rc;
+    int64_t fs = (int64_t)p->m * p->pitch[0];
     for (int l = 0; l < L; ++l) {
       rc = launch_downsample(p, l, img, fs, p->scratch[l + 1], B, st);
       if (rc) return rc;

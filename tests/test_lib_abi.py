@@ -54,7 +54,6 @@ def test_abi_version_and_strerror(lib):
     (512, 512, 16, -1, 1, 12, 0),
     (64, 64, 32, 1, 1, 12, 0),      # w >= m_L
     (64, 64, 0, 0, 1, 12, 0),       # w < 1
-    (64, 60, 8, 0, 1, 12, 0),       # row not a 16-byte multiple
     (64, 64, 8, 0, 3, 12, 0),       # unknown dtype
     (64, 64, 8, 2, 1, 14, 0),       # bits + 2*levels > 16
     (3, 64, 1, 1, 1, 12, 0),        # m < 2^(levels+1)
@@ -91,3 +90,19 @@ def test_sass_is_sm100a(lib):
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", LIB_PATH],
                          capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("m,n,want", [((512), 512, (85, 1)), (256, 256, (85, 0)), (416, 460, (69, 1)),
+                                      (3, 3, (1, 0)), (257, 100, (16, 1)), (1024, 1024, (170, 1))])
+def test_auto_config_paper_defaults(lib, m, n, want):
+    """downsample once iff the frame is larger than 256x256; w = min(m,n)/3, taken
+    at the coarse level (reading R16).  Host arithmetic, no device needed."""
+    w, lv = ctypes.c_int(), ctypes.c_int()
+    assert lib.moco_auto_config(m, n, ctypes.byref(w), ctypes.byref(lv)) == 0
+    assert (w.value, lv.value) == want
+
+
+def test_auto_config_rejects_tiny(lib):
+    w, lv = ctypes.c_int(), ctypes.c_int()
+    assert lib.moco_auto_config(2, 2, ctypes.byref(w), ctypes.byref(lv)) == -1
+    assert lib.moco_auto_config(64, 64, None, ctypes.byref(lv)) == -1
