@@ -68,7 +68,7 @@ def test_score_grid_full_coarse_size(c):
     p = Plan(spec.m, spec.n, spec.w, spec.levels, "u16", 12, device=0)
     assert p.algo == "tc"
     p.set_template(st.template)
-    g = _np(p.score_grid(st.frames[ks].contiguous()))
+    g = _np(p.score_grid(torch.stack([st.frames[k] for k in ks])))
     B = oracle.pyramid(_np(st.template), spec.levels)[spec.levels]
     for j, k in enumerate(ks):
         A = oracle.pyramid(_np(st.frames[k]), spec.levels)[spec.levels]
