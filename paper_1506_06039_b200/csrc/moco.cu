@@ -21,6 +21,7 @@
 #include "kernels_refine.cuh"
 #include "kernels_rtc.cuh"
 #include "kernels_fft.cuh"
+#include "kernels_fra.cuh"
 
 using namespace moco;
 
@@ -54,6 +55,8 @@ struct moco_plan {
   int rrt[3], rnrt[3];        // refine levels: template rows per tile, row tiles
   u64 *racc;                  // refine accumulators [cap][18] (kept zero between calls)
   RtcGeom rtc[3];             // tensor-core refine geometry per level (kernels_rtc.cuh)
+  FraGeom fra;                // frame-resident refine + pick + apply at level 0 (kernels_fra.cuh)
+  bool fra_ok;
   uint8_t *rtab[3];           // its template candidate tiles, or null: CUDA-core refine
   int *rperm, *rmeta;         // its per-batch alignment-class bucketing
   int nsm;                    // multiprocessors of the plan's device
@@ -70,6 +73,9 @@ struct moco_plan {
   struct {
     int rtc = -1;          // MOCO_RTC: -1 default, 0 CUDA-core refine sums, 1 force tensor cores
     int rtc_parts = 0;     // MOCO_RTC_PARTS (0: cost model)
+    int fra = 1;           // MOCO_FRA=0: level-0 refine by k_refine_tc + k_refine_pick instead of
+                           // the frame-resident cluster kernel k_refine_frame
+    int fra_min = 64;      // MOCO_FRA_MIN: smallest batch for k_refine_frame
     bool nofuse_ds = false, ga_inpick = false, nopipe = false;
   } knob;
   bool simple_refine;         // MOCO_REFINE=simple: unfused K6/K7 (cross-check in tests)
@@ -438,6 +444,8 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
     p->knob.nofuse_ds = getenv("MOCO_NOFUSE_DS") != nullptr;
     p->knob.ga_inpick = getenv("MOCO_GA_INPICK") != nullptr;
     p->knob.nopipe = getenv("MOCO_NOPIPE") != nullptr;
+    if (const char *v = getenv("MOCO_FRA")) p->knob.fra = atoi(v);
+    if (const char *v = getenv("MOCO_FRA_MIN")) p->knob.fra_min = std::max(1, atoi(v));
   }
   for (int l = 0; l <= levels; ++l) {
     p->ml[l] = m >> l;
@@ -538,6 +546,28 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
       plan_free(p);
       return set_cuda_err(cudaGetLastError(), "refine kernel attributes");
     }
+  }
+  // frame-resident level-0 refine + apply (kernels_fra.cuh): clusters of Q CTAs, as many
+  // as can be co-resident (occupancy query with the cluster launch configuration)
+  if (dtype == MOCO_U16 && levels > 0 && !p->stage && p->knob.fra &&
+      fra_make(&p->fra, p->ml[0], p->nl[0], p->pitch[0], p->pitch[0], bits)) {
+    if (smem_attr(k_refine_frame, p->fra.smem) == cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = p->fra.Q; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(p->fra.Q * nsm / p->fra.Q);
+      cfg.blockDim = dim3(FRA_THREADS);
+      cfg.dynamicSmemBytes = p->fra.smem;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int ncl = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl, k_refine_frame, &cfg) == cudaSuccess && ncl > 0) {
+        p->fra.ncl = ncl;
+        p->fra_ok = true;
+      }
+    }
+    cudaGetLastError();
   }
   p->algo = MOCO_ALGO_DIRECT;
   const bool tc_ok = tc_supported(p->dtype, p->bits, p->levels, p->w, p->ml[levels], p->nl[levels]);
@@ -983,6 +1013,40 @@ static int launch_tc(moco_plan *p, const void *frames_b, int64_t B, int32_t *shi
   return launch_tc_coarse(p, B, p->tc.G, p->tc.ga, shift_out, f_out, flags, grid_out, st);
 }
 
+// Level-0 refine + pick + apply with the frame resident in a thread-block cluster.
+static bool use_fra(const moco_plan *p, int l, int64_t B) {
+  return l == 0 && p->fra_ok && B >= p->knob.fra_min && fused_ok(p, 0);
+}
+
+static int launch_fra(moco_plan *p, const void *img, int64_t fstride, int64_t B, const int32_t *sin, int32_t *sout,
+                      double *fout, void *corr, cudaStream_t st) {
+  FraArgs a;
+  a.frames = (const uint16_t *)img; a.fstride = fstride; a.pitch = p->pitch[0];
+  a.tpl = (const uint16_t *)p->tpl[0]; a.tpitch = p->pitch[0];
+  a.pb2 = p->pb2[0]; a.ml = p->ml[0]; a.nl = p->nl[0]; a.scale = 1.0;
+  a.B = (int)B; a.shift_in = sin; a.shift_out = sout; a.f_out = fout;
+  a.corrected = (uint16_t *)corr;
+  a.g = p->fra;
+  a.g.ncl = (int)std::min<int64_t>(p->fra.ncl, B);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = p->fra.Q; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3((unsigned)(a.g.ncl * p->fra.Q));
+  cfg.blockDim = dim3(FRA_THREADS);
+  cfg.dynamicSmemBytes = p->fra.smem;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  {
+    ProfScope ps(p, MOCO_K_APPLY, st);
+    CK(cudaLaunchKernelEx(&cfg, k_refine_frame, a));
+  }
+  p->launches++;
+  CKL("k_refine_frame");
+  return MOCO_OK;
+}
+
 // S5 refine at levels L-1..0, then S6 apply (fused into the level-0 refine when possible).
 static int refine_levels(moco_plan *p, const void *const *img, const int64_t *fstride, int64_t B,
                          int32_t *shifts_b, double *fmin_b, void *corr_b, cudaStream_t st) {
@@ -992,7 +1056,9 @@ static int refine_levels(moco_plan *p, const void *const *img, const int64_t *fs
     int32_t *so = l == 0 ? shifts_b : p->sh[l];
     double *fo = l == 0 ? fmin_b : nullptr;
     int rc;
-    if (fused_ok(p, l))
+    if (use_fra(p, l, B))
+      rc = launch_fra(p, img[0], fstride[0], B, p->sh[1], so, fo, corr_b, st);
+    else if (fused_ok(p, l))
       rc = launch_refine_h(p, l, img[l], fstride[l], B, p->sh[l + 1], so, fo, l == 0 ? corr_b : nullptr, st);
     else
       rc = launch_refine(p, l, img[l], fstride[l], B, p->sh[l + 1], so, fo, st);
@@ -1127,6 +1193,15 @@ static int align_tc_pipelined(moco_plan *p, const void *d_frames, int64_t T, int
     // the pick's GA pieces on the pick stream, beside the refine sums -- when the TC search
     // is short (N <= 128: C2 1.66 -> 1.70 M); behind a long one (C3, N = 256) the pick has
     // slack and the side kernel only slows the refine on the critical stream (982 -> 939 k)
+    if (use_fra(p, 0, B)) {
+      rc = launch_fra(p, fr, (int64_t)p->m * p->n, B, sh1[buf], d_shifts + 2 * f0, d_fmin + f0,
+                      d_corrected ? (char *)d_corrected + f0 * fbytes : nullptr, sm);
+      if (rc) return rc;
+      CK(cudaEventRecord(p->pe_sums[buf], sm));
+      CK(cudaStreamWaitEvent(sa, p->pe_sums[buf], 0));
+      CK(cudaEventRecord(p->pe_pick[buf], sa));
+      continue;
+    }
     const u64 *gb = nullptr;
     if (use_rtc(p, 0, B) && p->gbin[buf] && RTC_GA_TOTAL && p->tc.g.N <= 128 && !p->knob.ga_inpick) {
       CK(cudaStreamWaitEvent(sa, p->pe_free[buf], 0));
