@@ -426,3 +426,47 @@ def test_errors():
     with pytest.raises(MocoError) as e:
         p.align(fr)                                         # before set_template
     assert e.value.code == -4
+
+
+@pytest.mark.parametrize("c,T", [(2, 1300), (3, 700)])
+def test_frame_resident_refine_equals_tc_refine(c, T, monkeypatch):
+    """The frame-resident cluster kernel (k_refine_frame: level-0 refine sums, argmin and
+    apply with the frame's rows held in the shared memory of a 4-CTA cluster) gives
+    bit-identical shifts, f_min and corrected frames to the tensor-core refine + pick
+    (MOCO_FRA=0), through the pipelined multi-batch path."""
+    spec = config_spec(c, T=T)
+    st = make_stack(spec, 0, T, device=DEV)
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("MOCO_FRA", mode)
+        monkeypatch.setenv("MOCO_BATCH_MB", "128")
+        p = _plan_for(spec)
+        p.set_template(st.template)
+        sh, fm, co, _ = p.align(st.frames, corrected=True)
+        sh2, fm2, _, _ = p.align(st.frames, corrected=False)
+        assert torch.equal(sh, sh2) and torch.equal(fm, fm2)
+        out[mode] = (sh, fm, co.view(torch.int16))
+    for a, b in zip(out["1"], out["0"]):
+        assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("m,n,w,T", [(200, 136, 9, 70), (98, 72, 5, 66), (384, 256, 12, 80), (512, 512, 30, 65),
+                                     (64, 64, 4, 64)])
+def test_frame_resident_refine_ragged_vs_oracle(m, n, w, T, monkeypatch):
+    """k_refine_frame on ragged shapes (1-, 2- and 4-CTA clusters, partial chunks and ring
+    slots, 17-chunk rows) with exact translates up to the window edge (large S: slice chunks
+    with no needed rows) and random frames: bit-exact vs the oracle on every frame."""
+    monkeypatch.setenv("MOCO_FRA_MIN", "1")
+    rng = np.random.default_rng(m * 3 + n + w)
+    tp = rng.integers(0, 4096, size=(m, n)).astype(np.uint16)
+    fr = rng.integers(0, 4096, size=(T, m, n)).astype(np.uint16)
+    lim = 2 * w - 1
+    for k in range(T // 2):
+        fr[k] = pf.translate_zero_fill(tp, int(rng.integers(-lim, lim + 1)), int(rng.integers(-lim, lim + 1)))
+    p = Plan(m, n, w, 1, "u16", 12, device=0)
+    p.set_template(torch.from_numpy(tp).to(DEV))
+    sh, fm, co, _ = p.align(torch.from_numpy(fr).to(DEV), corrected=True)
+    torch.cuda.synchronize()
+    sh, fm = _np(sh), _np(fm)
+    for k in list(range(0, T, 3)):
+        check_frame(fr[k], tp, w, 1, sh[k], fm[k], _np(co[k]))
