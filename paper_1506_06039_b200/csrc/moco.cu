@@ -73,8 +73,10 @@ struct moco_plan {
   struct {
     int rtc = -1;          // MOCO_RTC: -1 default, 0 CUDA-core refine sums, 1 force tensor cores
     int rtc_parts = 0;     // MOCO_RTC_PARTS (0: cost model)
-    int fra = 1;           // MOCO_FRA=0: level-0 refine by k_refine_tc + k_refine_pick instead of
-                           // the frame-resident cluster kernel k_refine_frame
+    int fra = 0;           // MOCO_FRA=1: level-0 refine + pick + apply by the frame-resident
+                           // cluster kernel k_refine_frame (one HBM read per frame, but CUDA-core
+                           // bound: 0.68 us/frame alone vs 0.30 for k_refine_tc + k_refine_pick,
+                           // DESIGN.md section 11) instead of the tensor-core refine + pick
     int fra_min = 64;      // MOCO_FRA_MIN: smallest batch for k_refine_frame
     bool nofuse_ds = false, ga_inpick = false, nopipe = false;
   } knob;

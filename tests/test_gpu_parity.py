@@ -433,7 +433,7 @@ def test_frame_resident_refine_equals_tc_refine(c, T, monkeypatch):
     """The frame-resident cluster kernel (k_refine_frame: level-0 refine sums, argmin and
     apply with the frame's rows held in the shared memory of a 4-CTA cluster) gives
     bit-identical shifts, f_min and corrected frames to the tensor-core refine + pick
-    (MOCO_FRA=0), through the pipelined multi-batch path."""
+    (MOCO_FRA=0, the default), through the pipelined multi-batch path."""
     spec = config_spec(c, T=T)
     st = make_stack(spec, 0, T, device=DEV)
     out = {}
@@ -457,6 +457,7 @@ def test_frame_resident_refine_ragged_vs_oracle(m, n, w, T, monkeypatch):
     slots, 17-chunk rows) with exact translates up to the window edge (large S: slice chunks
     with no needed rows) and random frames: bit-exact vs the oracle on every frame."""
     monkeypatch.setenv("MOCO_FRA_MIN", "1")
+    monkeypatch.setenv("MOCO_FRA", "1")
     rng = np.random.default_rng(m * 3 + n + w)
     tp = rng.integers(0, 4096, size=(m, n)).astype(np.uint16)
     fr = rng.integers(0, 4096, size=(T, m, n)).astype(np.uint16)
