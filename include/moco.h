@@ -168,6 +168,16 @@ int moco_score_grid(moco_plan *p, const void *d_frames, int64_t T, double *d_f,
 int moco_fft_cross(moco_plan *p, const void *d_frames, int64_t T, float *d_h, int32_t *d_shifts,
                    int32_t *d_qcount, moco_stream_t stream);
 
+/*
+ * moco_probe_peaks -- measured arithmetic throughput of `device` (not part of the hot
+ * path; the ALU roofs bench.py reports, SURVEY.md section 2.5 "MB"): out[0] FFMA
+ * flop/s, out[1] IMAD int ops/s, out[2] IDP.2A (16x8-bit dot product) ops/s,
+ * out[3] DFMA flop/s, each from a saturating microbenchmark (8 chains per thread, 8
+ * CTAs of 256 threads per SM, best of 2 timed runs).  Fills min(n, 4) entries;
+ * synchronous.  EINVAL on NULL out, ECUDA on a device error.
+ */
+int moco_probe_peaks(int device, double *out, int n);
+
 /* Number of kernel launches the last moco_align_batch/moco_score_grid issued. */
 int64_t moco_last_launch_count(const moco_plan *p);
 

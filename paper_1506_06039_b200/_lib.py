@@ -37,6 +37,7 @@ SIGNATURES = [
     ("moco_align_host", _I, [_P, _P, _I64, _P, _P, _P, _P]),
     ("moco_score_grid", _I, [_P, _P, _I64, _P, _P]),
     ("moco_fft_cross", _I, [_P, _P, _I64, _P, _P, _P, _P]),
+    ("moco_probe_peaks", _I, [_I, ctypes.POINTER(ctypes.c_double), _I]),
     ("moco_last_launch_count", _I64, [_P]),
     ("moco_profile_enable", _I, [_P, _I]),
     ("moco_profile_read", _I, [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64), _I]),
@@ -234,6 +235,14 @@ def auto_config(m: int, n: int) -> Tuple[int, int]:
     w, lv = _I(), _I()
     _check(load().moco_auto_config(m, n, ctypes.byref(w), ctypes.byref(lv)), "moco_auto_config")
     return w.value, lv.value
+
+
+def probe_peaks(device: int = 0) -> dict:
+    """Measured FFMA / IMAD / IDP.2A / DFMA throughput of a device (moco_probe_peaks)."""
+    out = (ctypes.c_double * 4)()
+    _check(load().moco_probe_peaks(device, out, 4), "moco_probe_peaks")
+    return {"ffma_tflops": out[0] / 1e12, "imad_tops": out[1] / 1e12, "idp2a_tops": out[2] / 1e12,
+            "dfma_tflops": out[3] / 1e12}
 
 
 def exported_symbols():

@@ -585,3 +585,60 @@ __global__ void k_apply(const E *__restrict__ in, E *__restrict__ out, int m, in
 }
 
 }  // namespace moco
+
+namespace moco {
+// ---------------------------------------------------------------- peak probes
+// Throughput microbenchmarks for the ALU roofs bench.py reports (SURVEY.md section 2.5
+// "MB"): every thread runs `iters` x 8 independent dependency chains of one instruction
+// kind; ops are counted as the instruction's arithmetic (FFMA/DFMA = 2 flops, IMAD = 2
+// ops, IDP.2A = 4 ops: two 16x8-bit products and two adds).
+template <int KIND>
+__global__ void __launch_bounds__(256) k_probe(int iters, uint32_t seed, uint32_t *sink) {
+  const uint32_t t = threadIdx.x + seed;
+  if (KIND == 0) {
+    float a[8], b = __uint_as_float(0x3f800001u + (t & 7)), c = 1e-7f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = (float)(t + k);
+    for (int i = 0; i < iters; ++i)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = fmaf(a[k], b, c);
+    float s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += a[k];
+    if (s == 1234.5f) sink[0] = 1;
+  } else if (KIND == 1) {
+    uint32_t a[8], b = 3u + (t & 7), c = t;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = t + k;
+    for (int i = 0; i < iters; ++i)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = a[k] * b + c;
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s ^= a[k];
+    if (s == 0x12345u) sink[0] = s;
+  } else if (KIND == 2) {
+    uint32_t a[8], b = 0x01020304u ^ t, c = t * 7u;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = t + k;
+    for (int i = 0; i < iters; ++i)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = __dp2a_lo(c + k, b, a[k]);
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s ^= a[k];
+    if (s == 0x12345u) sink[0] = s;
+  } else {
+    double a[8], b = 1.0 + 1e-9 * (t & 7), c = 1e-12;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = (double)(t + k);
+    for (int i = 0; i < iters; ++i)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = fma(a[k], b, c);
+    double s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += a[k];
+    if (s == 1234.5) sink[0] = 1;
+  }
+}
+}  // namespace moco

@@ -178,6 +178,44 @@ static size_t coarse_smem(const moco_plan *p, int sc, int br, int fpitch) {
 
 int moco_abi_version(void) { return MOCO_ABI_VERSION; }
 
+int moco_probe_peaks(int device, double *out, int n) {
+  if (!out || n < 0) return MOCO_EINVAL;
+  CK(cudaSetDevice(device));
+  int nsm = 0;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+  uint32_t *sink = nullptr;
+  CK(cudaMalloc(&sink, 16));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  const int iters = 4096, blocks = nsm * 8;
+  const double ops_per_inst[4] = {2.0, 2.0, 4.0, 2.0};
+  int rc = MOCO_OK;
+  for (int k = 0; k < 4 && k < n && rc == MOCO_OK; ++k) {
+    float best = 1e30f;
+    for (int rep = 0; rep < 3; ++rep) {
+      cudaEventRecord(e0);
+      switch (k) {
+        case 0: k_probe<0><<<blocks, 256>>>(iters, rep, sink); break;
+        case 1: k_probe<1><<<blocks, 256>>>(iters, rep, sink); break;
+        case 2: k_probe<2><<<blocks, 256>>>(iters, rep, sink); break;
+        default: k_probe<3><<<blocks, (unsigned)256>>>(iters / 8, rep, sink); break;
+      }
+      cudaEventRecord(e1);
+      if (cudaEventSynchronize(e1) != cudaSuccess) { rc = set_cuda_err(cudaGetLastError(), "k_probe"); break; }
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (rep > 0) best = std::min(best, ms);
+    }
+    const double insts = (double)blocks * 256 * 8 * (k == 3 ? iters / 8 : iters);
+    out[k] = insts * ops_per_inst[k] / (best * 1e-3);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  return rc;
+}
+
 int moco_auto_config(int m, int n, int *w, int *levels) {
   if (!w || !levels || m < 1 || n < 1) return MOCO_EINVAL;
   const int L = (m > 256 || n > 256) ? 1 : 0;
