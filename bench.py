@@ -191,20 +191,25 @@ def parity_report(frames, template, shifts, fmin, corrected, spec, budget_s=25.0
     tp = template.cpu().numpy()
     T = frames.shape[0]
     # pilot: rate on a small sample sizes the parity sample to the time budget
+    def take(x, idx):   # (integer-array indexing is not implemented for uint16 on CUDA)
+        y = x.view(torch.int16) if x.dtype == torch.uint16 else x
+        y = y[torch.as_tensor(idx, device=x.device)].cpu()
+        return (y.view(torch.uint16) if x.dtype == torch.uint16 else y).numpy()
+
     pilot = list(range(0, min(T, 10 * cores), 10))[: max(4, cores)]
     t0 = time.perf_counter()
-    oracle.align_stack(frames[pilot].cpu().numpy(), tp, spec.w, spec.levels, workers=cores)
+    oracle.align_stack(take(frames, pilot), tp, spec.w, spec.levels, workers=cores)
     rate0 = len(pilot) / (time.perf_counter() - t0)
     want = max(len(pilot), int(rate0 * budget_s))
     idx = list(range(0, T, stride))
     if len(idx) > want:
         idx = idx[:: int(math.ceil(len(idx) / want))]
-    fr = frames[idx].cpu().numpy()
+    fr = take(frames, idx)
     t0 = time.perf_counter()
     osh, ofm = oracle.align_stack(fr, tp, spec.w, spec.levels, workers=cores)
     dt = time.perf_counter() - t0
-    sh = shifts[idx].cpu().numpy()
-    fm = fmin[idx].cpu().numpy()
+    sh = take(shifts, idx)
+    fm = take(fmin, idx)
     exact = near = failed = 0
     bad = []
     for j, k in enumerate(idx):

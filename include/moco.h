@@ -169,6 +169,17 @@ int moco_fft_cross(moco_plan *p, const void *d_frames, int64_t T, float *d_h, in
                    int32_t *d_qcount, moco_stream_t stream);
 
 /*
+ * moco_mean_image -- report helper (Fig. 2 caption:
+ * "the mean of every image"): d_mean[i*n + j] = (1/T) sum_k frames[k][i][j] for T device
+ * frames of m x n samples (dtype MOCO_U16 or MOCO_F32, rows of n samples, no padding).
+ * uint16: exact 64-bit sums, one fp64 division per pixel; float32: fp64 sums.  d_mean is
+ * double [m][n], device memory.  Stream-ordered.  EINVAL on T < 1, m or n < 1, NULL
+ * pointers or an unknown dtype.
+ */
+int moco_mean_image(const void *d_frames, int64_t T, int m, int n, int dtype, double *d_mean,
+                    moco_stream_t stream);
+
+/*
  * moco_probe_peaks -- measured arithmetic throughput of `device` (not part of the hot
  * path; the ALU roofs bench.py reports, SURVEY.md section 2.5 "MB"): out[0] FFMA
  * flop/s, out[1] IMAD int ops/s, out[2] IDP.2A (16x8-bit dot product) ops/s,

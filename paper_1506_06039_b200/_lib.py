@@ -38,6 +38,7 @@ SIGNATURES = [
     ("moco_score_grid", _I, [_P, _P, _I64, _P, _P]),
     ("moco_fft_cross", _I, [_P, _P, _I64, _P, _P, _P, _P]),
     ("moco_probe_peaks", _I, [_I, ctypes.POINTER(ctypes.c_double), _I]),
+    ("moco_mean_image", _I, [_P, _I64, _I, _I, _I, _P, _P]),
     ("moco_last_launch_count", _I64, [_P]),
     ("moco_profile_enable", _I, [_P, _I]),
     ("moco_profile_read", _I, [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64), _I]),

@@ -642,3 +642,24 @@ __global__ void __launch_bounds__(256) k_probe(int iters, uint32_t seed, uint32_
   }
 }
 }  // namespace moco
+
+namespace moco {
+// ---------------------------------------------------------------- mean image (reports)
+// mean[p] = (1/T) sum_f frames[f][p] (Fig. 2, "the mean of every image"); exact
+// 64-bit integer sums for uint16, fp64 for float32; one division per pixel.
+template <class E>
+__global__ void __launch_bounds__(256) k_mean_image(const E *__restrict__ fr, int64_t T, int64_t mn,
+                                                    double *__restrict__ out) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < mn; p += (int64_t)gridDim.x * blockDim.x) {
+    if (std::is_same<E, uint16_t>::value) {
+      u64 s = 0;
+      for (int64_t f = 0; f < T; ++f) s += (u64)fr[f * mn + p];
+      out[p] = (double)s / (double)T;
+    } else {
+      double s = 0;
+      for (int64_t f = 0; f < T; ++f) s += (double)fr[f * mn + p];
+      out[p] = s / (double)T;
+    }
+  }
+}
+}  // namespace moco

@@ -216,6 +216,17 @@ int moco_probe_peaks(int device, double *out, int n) {
   return rc;
 }
 
+int moco_mean_image(const void *d_frames, int64_t T, int m, int n, int dtype, double *d_mean, moco_stream_t stream) {
+  if (T < 1 || m < 1 || n < 1 || !d_frames || !d_mean || (dtype != MOCO_U16 && dtype != MOCO_F32)) return MOCO_EINVAL;
+  const int64_t mn = (int64_t)m * n;
+  const unsigned grid = (unsigned)std::min<int64_t>((mn + 255) / 256, 148 * 16);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == MOCO_U16) k_mean_image<uint16_t><<<grid, 256, 0, st>>>((const uint16_t *)d_frames, T, mn, d_mean);
+  else k_mean_image<float><<<grid, 256, 0, st>>>((const float *)d_frames, T, mn, d_mean);
+  CKL("k_mean_image");
+  return MOCO_OK;
+}
+
 int moco_auto_config(int m, int n, int *w, int *levels) {
   if (!w || !levels || m < 1 || n < 1) return MOCO_EINVAL;
   const int L = (m > 256 || n > 256) ? 1 : 0;
