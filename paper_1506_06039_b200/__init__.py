@@ -5,6 +5,6 @@ include/moco.h.  This package is the thin Python binding (``Plan``) plus the
 build helper and the multi-GPU driver; it never imports ``oracle/``.
 """
 from ._lib import (FLAG_EDGE, FLAG_FULL, LIB_PATH, MocoError, Plan, auto_config, exported_symbols,  # noqa: F401
-                   load)
+                   load, probe_peaks)
 
-__all__ = ["Plan", "MocoError", "auto_config", "load", "LIB_PATH", "FLAG_EDGE", "FLAG_FULL", "exported_symbols"]
+__all__ = ["Plan", "MocoError", "auto_config", "probe_peaks", "load", "LIB_PATH", "FLAG_EDGE", "FLAG_FULL", "exported_symbols"]
