@@ -141,9 +141,148 @@ __device__ __forceinline__ void fft_stage(const float2 *x, float2 *y, const floa
   }
 }
 
+// ------------------------------------------------------------ register codelets
+// Small DFTs held in registers, natural order in and out, X[k] = sum_n v[n] e^{SIGN 2 pi i n k / N}
+// (SIGN = -1 forward, +1 inverse); twiddle constants cos/sin(2 pi m / N) to float precision.
+__device__ __forceinline__ float2 mul_i(float2 z, float s) { return make_float2(-s * z.y, s * z.x); }   // (s i) z
+template <int SIGN>
+__device__ __forceinline__ void dft4(float2 &a0, float2 &a1, float2 &a2, float2 &a3) {
+  const float2 t0 = cadd(a0, a2), t1 = csub(a0, a2), t2 = cadd(a1, a3), t3 = mul_i(csub(a1, a3), (float)SIGN);
+  a0 = cadd(t0, t2);
+  a2 = csub(t0, t2);
+  a1 = cadd(t1, t3);
+  a3 = csub(t1, t3);
+}
+template <int SIGN>
+__device__ __forceinline__ void dft3(float2 &a0, float2 &a1, float2 &a2) {
+  const float s1 = (float)SIGN * 0.86602540378443865f;
+  const float2 t = cadd(a1, a2), u = csub(a1, a2);
+  const float2 m = make_float2(a0.x - 0.5f * t.x, a0.y - 0.5f * t.y);
+  const float2 r = mul_i(u, s1);
+  a0 = cadd(a0, t);
+  a1 = cadd(m, r);
+  a2 = csub(m, r);
+}
+// z * e^{SIGN 2 pi i m / N} with the table value (c, s) = (cos, sin)(2 pi m / N)
+template <int SIGN>
+__device__ __forceinline__ float2 rot(float2 z, float c, float s) {
+  const float sn = (float)SIGN * s;
+  return make_float2(z.x * c - z.y * sn, z.x * sn + z.y * c);
+}
+template <int SIGN>
+__device__ __forceinline__ void dft16(float2 (&v)[16]) {
+  constexpr float C[10] = {1.0f, 0.92387953251128674f, 0.70710678118654752f, 0.38268343236508977f, 0.0f,
+                           -0.38268343236508977f, -0.70710678118654752f, -0.92387953251128674f, -1.0f,
+                           -0.92387953251128674f};
+  constexpr float S[10] = {0.0f, 0.38268343236508977f, 0.70710678118654752f, 0.92387953251128674f, 1.0f,
+                           0.92387953251128674f, 0.70710678118654752f, 0.38268343236508977f, 0.0f,
+                           -0.38268343236508977f};
+#pragma unroll
+  for (int n2 = 0; n2 < 4; ++n2) dft4<SIGN>(v[n2], v[4 + n2], v[8 + n2], v[12 + n2]);   // -> y[k1][n2] at v[4 k1 + n2]
+#pragma unroll
+  for (int k1 = 1; k1 < 4; ++k1)
+#pragma unroll
+    for (int n2 = 1; n2 < 4; ++n2) v[4 * k1 + n2] = rot<SIGN>(v[4 * k1 + n2], C[n2 * k1], S[n2 * k1]);
+  float2 o[16];
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) {
+    float2 a = v[4 * k1], b = v[4 * k1 + 1], c = v[4 * k1 + 2], d = v[4 * k1 + 3];
+    dft4<SIGN>(a, b, c, d);
+    o[k1] = a; o[k1 + 4] = b; o[k1 + 8] = c; o[k1 + 12] = d;
+  }
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = o[k];
+}
+template <int SIGN>
+__device__ __forceinline__ void dft9(float2 (&v)[9]) {
+  constexpr float C[5] = {1.0f, 0.76604444311897804f, 0.17364817766693035f, -0.5f, -0.93969262078590838f};
+  constexpr float S[5] = {0.0f, 0.64278760968653933f, 0.98480775301220806f, 0.86602540378443865f,
+                          0.34202014332566873f};
+#pragma unroll
+  for (int n2 = 0; n2 < 3; ++n2) dft3<SIGN>(v[n2], v[3 + n2], v[6 + n2]);   // -> y[k1][n2] at v[3 k1 + n2]
+#pragma unroll
+  for (int k1 = 1; k1 < 3; ++k1)
+#pragma unroll
+    for (int n2 = 1; n2 < 3; ++n2) v[3 * k1 + n2] = rot<SIGN>(v[3 * k1 + n2], C[n2 * k1], S[n2 * k1]);
+  float2 o[9];
+#pragma unroll
+  for (int k1 = 0; k1 < 3; ++k1) {
+    float2 a = v[3 * k1], b = v[3 * k1 + 1], c = v[3 * k1 + 2];
+    dft3<SIGN>(a, b, c);
+    o[k1] = a; o[k1 + 3] = b; o[k1 + 6] = c;
+  }
+#pragma unroll
+  for (int k = 0; k < 9; ++k) v[k] = o[k];
+}
+template <int SIGN>
+__device__ __forceinline__ void dft18(float2 (&v)[18]) {
+  constexpr float C[9] = {1.0f, 0.93969262078590838f, 0.76604444311897804f, 0.5f, 0.17364817766693035f,
+                          -0.17364817766693035f, -0.5f, -0.76604444311897804f, -0.93969262078590838f};
+  constexpr float S[9] = {0.0f, 0.34202014332566873f, 0.64278760968653933f, 0.86602540378443865f,
+                          0.98480775301220806f, 0.98480775301220806f, 0.86602540378443865f,
+                          0.64278760968653933f, 0.34202014332566873f};
+  float2 e[9], od[9];
+#pragma unroll
+  for (int n2 = 0; n2 < 9; ++n2) {   // n = 9 n1 + n2: radix-2 over n1, then twiddle W18^(n2 k1)
+    e[n2] = cadd(v[n2], v[9 + n2]);
+    od[n2] = n2 == 0 ? csub(v[n2], v[9 + n2]) : rot<SIGN>(csub(v[n2], v[9 + n2]), C[n2], S[n2]);
+  }
+  dft9<SIGN>(e);
+  dft9<SIGN>(od);
+#pragma unroll
+  for (int k2 = 0; k2 < 9; ++k2) {
+    v[2 * k2] = e[k2];
+    v[2 * k2 + 1] = od[k2];
+  }
+}
+
+// nfft transforms of length 288 = 16 x 18 (every 256-row/column coarse level with w <= 33):
+// pass 1, one thread per (transform, n2): radix-16 over n1 of x[18 n1 + n2] in registers,
+// times W288^(n2 k1), into y at n2 + 19 k1 (19-element rows: conflict-free pass 2 reads);
+// pass 2, one thread per (transform, k1): radix-18 over n2 -> X[k1 + 16 k2] back into x in
+// natural order.  tw[m] = e^{-2 pi i m / 288}.  y needs nfft * 304 elements.
+constexpr int FFT288_YS = 304;
+template <int SIGN>
+__device__ void fft288(float2 *x, float2 *y, const float2 *tw, int nfft) {
+  for (int task = threadIdx.x; task < nfft * 18; task += blockDim.x) {
+    const int q = task / 18, n2 = task - q * 18;
+    const float2 *in = x + q * 288 + n2;
+    float2 v[16];
+#pragma unroll
+    for (int n1 = 0; n1 < 16; ++n1) v[n1] = in[18 * n1];
+    dft16<SIGN>(v);
+    float2 *out = y + q * FFT288_YS + n2;
+    out[0] = v[0];
+#pragma unroll
+    for (int k1 = 1; k1 < 16; ++k1) {
+      float2 t = tw[n2 * k1];   // n2 k1 <= 255 < 288
+      if (SIGN > 0) t.y = -t.y;
+      out[19 * k1] = cmul(v[k1], t);
+    }
+  }
+  __syncthreads();
+  for (int task = threadIdx.x; task < nfft * 16; task += blockDim.x) {
+    const int q = task >> 4, k1 = task & 15;
+    const float2 *in = y + q * FFT288_YS + 19 * k1;
+    float2 u[18];
+#pragma unroll
+    for (int n2 = 0; n2 < 18; ++n2) u[n2] = in[n2];
+    dft18<SIGN>(u);
+    float2 *out = x + q * 288 + k1;
+#pragma unroll
+    for (int k2 = 0; k2 < 18; ++k2) out[16 * k2] = u[k2];
+  }
+  __syncthreads();
+}
+
 // nfft transforms of length L.N stored contiguously in x; y is scratch of the same
 // size.  Returns the buffer holding the result.  All threads of the block take part.
 __device__ float2 *fft_batch(float2 *x, float2 *y, const float2 *tw, const FftLen &L, int nfft, float sign) {
+  if (L.N == 288) {   // register codelets (x in, x out); y holds nfft * FFT288_YS elements
+    if (sign < 0) fft288<-1>(x, y, tw, nfft);
+    else fft288<1>(x, y, tw, nfft);
+    return x;
+  }
   int Ns = 1;
   for (int st = 0; st < L.nst; ++st) {
     const int R = L.rad[st];
@@ -188,7 +327,7 @@ __global__ void __launch_bounds__(FFT_THREADS) k_fft_rows(const uint16_t *__rest
   extern __shared__ __align__(16) float2 fsm[];
   const int Mc = g.Lc.N;
   float2 *tw = fsm;
-  float2 *x = tw + Mc, *y = x + FFT_ROWS_PAIRS * Mc;
+  float2 *x = tw + Mc, *y = x + FFT_ROWS_PAIRS * Mc;   // y: FFT_ROWS_PAIRS * (Mc + 16)
   const int nrb = (g.mcp / 2 + per - 1) / per;   // per <= FFT_ROWS_PAIRS row pairs per block
   const int f = blockIdx.x / nrb, rb = blockIdx.x % nrb;
   const int p0 = rb * per, np = min(per, g.mcp / 2 - p0);
@@ -371,7 +510,7 @@ __global__ void __launch_bounds__(1024) k_fft_score(FftScoreArgs a) {
   const int Mc = g.Lc.N, W = g.W, hw = g.hw;
   float2 *tw = fsm;
   float2 *x = tw + Mc, *y = x + FFT_ROWS_PAIRS * Mc;
-  float *hb = reinterpret_cast<float *>(y + FFT_ROWS_PAIRS * Mc);   // [W][W] h~
+  float *hb = reinterpret_cast<float *>(y + FFT_ROWS_PAIRS * (Mc + 16));   // [W][W] h~
   __shared__ u64 red[32];
   __shared__ float fmin_hi_s;
   __shared__ int qn;
