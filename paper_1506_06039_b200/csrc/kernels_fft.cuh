@@ -142,147 +142,212 @@ __device__ __forceinline__ void fft_stage(const float2 *x, float2 *y, const floa
 }
 
 // ------------------------------------------------------------ register codelets
-// Small DFTs held in registers, natural order in and out, X[k] = sum_n v[n] e^{SIGN 2 pi i n k / N}
-// (SIGN = -1 forward, +1 inverse); twiddle constants cos/sin(2 pi m / N) to float precision.
+// Small DFTs held in registers, natural order in and out,
+//   X[k] = sum_n v[n] e^{SIGN 2 pi i n k / N}   (SIGN = -1 forward, +1 inverse),
+// N = 2, 3, 4, 5 written out, larger N composed by Cooley-Tukey N = N1 x N2 at compile time
+// (n = N2 n1 + n2, k = k1 + N1 k2) with the twiddles e^{SIGN 2 pi i n2 k1 / N} as float
+// constants (cos, sin)(2 pi m / N) -- every index is a compile-time constant after
+// unrolling, so the tables fold into immediates.
 __device__ __forceinline__ float2 mul_i(float2 z, float s) { return make_float2(-s * z.y, s * z.x); }   // (s i) z
 template <int SIGN>
-__device__ __forceinline__ void dft4(float2 &a0, float2 &a1, float2 &a2, float2 &a3) {
-  const float2 t0 = cadd(a0, a2), t1 = csub(a0, a2), t2 = cadd(a1, a3), t3 = mul_i(csub(a1, a3), (float)SIGN);
-  a0 = cadd(t0, t2);
-  a2 = csub(t0, t2);
-  a1 = cadd(t1, t3);
-  a3 = csub(t1, t3);
+__device__ __forceinline__ float2 rot(float2 z, float2 cs) {   // z * e^{SIGN i theta}, cs = (cos, sin) theta
+  const float sn = (float)SIGN * cs.y;
+  return make_float2(z.x * cs.x - z.y * sn, z.x * sn + z.y * cs.x);
 }
-template <int SIGN>
-__device__ __forceinline__ void dft3(float2 &a0, float2 &a1, float2 &a2) {
-  const float s1 = (float)SIGN * 0.86602540378443865f;
-  const float2 t = cadd(a1, a2), u = csub(a1, a2);
-  const float2 m = make_float2(a0.x - 0.5f * t.x, a0.y - 0.5f * t.y);
-  const float2 r = mul_i(u, s1);
-  a0 = cadd(a0, t);
-  a1 = cadd(m, r);
-  a2 = csub(m, r);
+template <int N>
+__device__ __forceinline__ float2 twk(int m);
+template <>
+__device__ __forceinline__ float2 twk<8>(int m) {
+  constexpr float C[8] = {1.0f, 0.707106781f, 0.0f, -0.707106781f, -1.0f, -0.707106781f, 0.0f, 0.707106781f};
+  constexpr float S[8] = {0.0f, 0.707106781f, 1.0f, 0.707106781f, 0.0f, -0.707106781f, -1.0f, -0.707106781f};
+  return make_float2(C[m], S[m]);
 }
-// z * e^{SIGN 2 pi i m / N} with the table value (c, s) = (cos, sin)(2 pi m / N)
-template <int SIGN>
-__device__ __forceinline__ float2 rot(float2 z, float c, float s) {
-  const float sn = (float)SIGN * s;
-  return make_float2(z.x * c - z.y * sn, z.x * sn + z.y * c);
+template <>
+__device__ __forceinline__ float2 twk<9>(int m) {
+  constexpr float C[9] = {1.0f, 0.766044443f, 0.173648178f, -0.5f, -0.939692621f, -0.939692621f, -0.5f, 0.173648178f, 0.766044443f};
+  constexpr float S[9] = {0.0f, 0.64278761f, 0.984807753f, 0.866025404f, 0.342020143f, -0.342020143f, -0.866025404f, -0.984807753f, -0.64278761f};
+  return make_float2(C[m], S[m]);
 }
-template <int SIGN>
-__device__ __forceinline__ void dft16(float2 (&v)[16]) {
-  constexpr float C[10] = {1.0f, 0.92387953251128674f, 0.70710678118654752f, 0.38268343236508977f, 0.0f,
-                           -0.38268343236508977f, -0.70710678118654752f, -0.92387953251128674f, -1.0f,
-                           -0.92387953251128674f};
-  constexpr float S[10] = {0.0f, 0.38268343236508977f, 0.70710678118654752f, 0.92387953251128674f, 1.0f,
-                           0.92387953251128674f, 0.70710678118654752f, 0.38268343236508977f, 0.0f,
-                           -0.38268343236508977f};
-#pragma unroll
-  for (int n2 = 0; n2 < 4; ++n2) dft4<SIGN>(v[n2], v[4 + n2], v[8 + n2], v[12 + n2]);   // -> y[k1][n2] at v[4 k1 + n2]
-#pragma unroll
-  for (int k1 = 1; k1 < 4; ++k1)
-#pragma unroll
-    for (int n2 = 1; n2 < 4; ++n2) v[4 * k1 + n2] = rot<SIGN>(v[4 * k1 + n2], C[n2 * k1], S[n2 * k1]);
-  float2 o[16];
-#pragma unroll
-  for (int k1 = 0; k1 < 4; ++k1) {
-    float2 a = v[4 * k1], b = v[4 * k1 + 1], c = v[4 * k1 + 2], d = v[4 * k1 + 3];
-    dft4<SIGN>(a, b, c, d);
-    o[k1] = a; o[k1 + 4] = b; o[k1 + 8] = c; o[k1 + 12] = d;
-  }
-#pragma unroll
-  for (int k = 0; k < 16; ++k) v[k] = o[k];
+template <>
+__device__ __forceinline__ float2 twk<12>(int m) {
+  constexpr float C[12] = {1.0f, 0.866025404f, 0.5f, 0.0f, -0.5f, -0.866025404f, -1.0f, -0.866025404f, -0.5f, 0.0f, 0.5f, 0.866025404f};
+  constexpr float S[12] = {0.0f, 0.5f, 0.866025404f, 1.0f, 0.866025404f, 0.5f, 0.0f, -0.5f, -0.866025404f, -1.0f, -0.866025404f, -0.5f};
+  return make_float2(C[m], S[m]);
 }
-template <int SIGN>
-__device__ __forceinline__ void dft9(float2 (&v)[9]) {
-  constexpr float C[5] = {1.0f, 0.76604444311897804f, 0.17364817766693035f, -0.5f, -0.93969262078590838f};
-  constexpr float S[5] = {0.0f, 0.64278760968653933f, 0.98480775301220806f, 0.86602540378443865f,
-                          0.34202014332566873f};
-#pragma unroll
-  for (int n2 = 0; n2 < 3; ++n2) dft3<SIGN>(v[n2], v[3 + n2], v[6 + n2]);   // -> y[k1][n2] at v[3 k1 + n2]
-#pragma unroll
-  for (int k1 = 1; k1 < 3; ++k1)
-#pragma unroll
-    for (int n2 = 1; n2 < 3; ++n2) v[3 * k1 + n2] = rot<SIGN>(v[3 * k1 + n2], C[n2 * k1], S[n2 * k1]);
-  float2 o[9];
-#pragma unroll
-  for (int k1 = 0; k1 < 3; ++k1) {
-    float2 a = v[3 * k1], b = v[3 * k1 + 1], c = v[3 * k1 + 2];
-    dft3<SIGN>(a, b, c);
-    o[k1] = a; o[k1 + 3] = b; o[k1 + 6] = c;
-  }
-#pragma unroll
-  for (int k = 0; k < 9; ++k) v[k] = o[k];
+template <>
+__device__ __forceinline__ float2 twk<15>(int m) {
+  constexpr float C[15] = {1.0f, 0.913545458f, 0.669130606f, 0.309016994f, -0.104528463f, -0.5f, -0.809016994f, -0.978147601f, -0.978147601f, -0.809016994f, -0.5f, -0.104528463f, 0.309016994f, 0.669130606f, 0.913545458f};
+  constexpr float S[15] = {0.0f, 0.406736643f, 0.743144825f, 0.951056516f, 0.994521895f, 0.866025404f, 0.587785252f, 0.207911691f, -0.207911691f, -0.587785252f, -0.866025404f, -0.994521895f, -0.951056516f, -0.743144825f, -0.406736643f};
+  return make_float2(C[m], S[m]);
 }
-template <int SIGN>
-__device__ __forceinline__ void dft18(float2 (&v)[18]) {
-  constexpr float C[9] = {1.0f, 0.93969262078590838f, 0.76604444311897804f, 0.5f, 0.17364817766693035f,
-                          -0.17364817766693035f, -0.5f, -0.76604444311897804f, -0.93969262078590838f};
-  constexpr float S[9] = {0.0f, 0.34202014332566873f, 0.64278760968653933f, 0.86602540378443865f,
-                          0.98480775301220806f, 0.98480775301220806f, 0.86602540378443865f,
-                          0.64278760968653933f, 0.34202014332566873f};
-  float2 e[9], od[9];
-#pragma unroll
-  for (int n2 = 0; n2 < 9; ++n2) {   // n = 9 n1 + n2: radix-2 over n1, then twiddle W18^(n2 k1)
-    e[n2] = cadd(v[n2], v[9 + n2]);
-    od[n2] = n2 == 0 ? csub(v[n2], v[9 + n2]) : rot<SIGN>(csub(v[n2], v[9 + n2]), C[n2], S[n2]);
-  }
-  dft9<SIGN>(e);
-  dft9<SIGN>(od);
-#pragma unroll
-  for (int k2 = 0; k2 < 9; ++k2) {
-    v[2 * k2] = e[k2];
-    v[2 * k2 + 1] = od[k2];
-  }
+template <>
+__device__ __forceinline__ float2 twk<16>(int m) {
+  constexpr float C[16] = {1.0f, 0.923879533f, 0.707106781f, 0.382683432f, 0.0f, -0.382683432f, -0.707106781f, -0.923879533f, -1.0f, -0.923879533f, -0.707106781f, -0.382683432f, 0.0f, 0.382683432f, 0.707106781f, 0.923879533f};
+  constexpr float S[16] = {0.0f, 0.382683432f, 0.707106781f, 0.923879533f, 1.0f, 0.923879533f, 0.707106781f, 0.382683432f, 0.0f, -0.382683432f, -0.707106781f, -0.923879533f, -1.0f, -0.923879533f, -0.707106781f, -0.382683432f};
+  return make_float2(C[m], S[m]);
+}
+template <>
+__device__ __forceinline__ float2 twk<18>(int m) {
+  constexpr float C[18] = {1.0f, 0.939692621f, 0.766044443f, 0.5f, 0.173648178f, -0.173648178f, -0.5f, -0.766044443f, -0.939692621f, -1.0f, -0.939692621f, -0.766044443f, -0.5f, -0.173648178f, 0.173648178f, 0.5f, 0.766044443f, 0.939692621f};
+  constexpr float S[18] = {0.0f, 0.342020143f, 0.64278761f, 0.866025404f, 0.984807753f, 0.984807753f, 0.866025404f, 0.64278761f, 0.342020143f, 0.0f, -0.342020143f, -0.64278761f, -0.866025404f, -0.984807753f, -0.984807753f, -0.866025404f, -0.64278761f, -0.342020143f};
+  return make_float2(C[m], S[m]);
+}
+template <>
+__device__ __forceinline__ float2 twk<20>(int m) {
+  constexpr float C[20] = {1.0f, 0.951056516f, 0.809016994f, 0.587785252f, 0.309016994f, 0.0f, -0.309016994f, -0.587785252f, -0.809016994f, -0.951056516f, -1.0f, -0.951056516f, -0.809016994f, -0.587785252f, -0.309016994f, 0.0f, 0.309016994f, 0.587785252f, 0.809016994f, 0.951056516f};
+  constexpr float S[20] = {0.0f, 0.309016994f, 0.587785252f, 0.809016994f, 0.951056516f, 1.0f, 0.951056516f, 0.809016994f, 0.587785252f, 0.309016994f, 0.0f, -0.309016994f, -0.587785252f, -0.809016994f, -0.951056516f, -1.0f, -0.951056516f, -0.809016994f, -0.587785252f, -0.309016994f};
+  return make_float2(C[m], S[m]);
 }
 
-// nfft transforms of length 288 = 16 x 18 (every 256-row/column coarse level with w <= 33):
-// pass 1, one thread per (transform, n2): radix-16 over n1 of x[18 n1 + n2] in registers,
-// times W288^(n2 k1), into y at n2 + 19 k1 (19-element rows: conflict-free pass 2 reads);
-// pass 2, one thread per (transform, k1): radix-18 over n2 -> X[k1 + 16 k2] back into x in
-// natural order.  tw[m] = e^{-2 pi i m / 288}.  y needs nfft * 304 elements.
-constexpr int FFT288_YS = 304;
+template <int N, int SIGN>
+struct Dft;
 template <int SIGN>
-__device__ void fft288(float2 *x, float2 *y, const float2 *tw, int nfft) {
-  for (int task = threadIdx.x; task < nfft * 18; task += blockDim.x) {
-    const int q = task / 18, n2 = task - q * 18;
-    const float2 *in = x + q * 288 + n2;
-    float2 v[16];
+struct Dft<2, SIGN> {
+  static __device__ __forceinline__ void run(float2 (&v)[2]) {
+    const float2 a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  }
+};
+template <int SIGN>
+struct Dft<3, SIGN> {
+  static __device__ __forceinline__ void run(float2 (&v)[3]) {
+    const float s1 = (float)SIGN * 0.86602540378443865f;
+    const float2 t = cadd(v[1], v[2]), u = csub(v[1], v[2]);
+    const float2 m = make_float2(v[0].x - 0.5f * t.x, v[0].y - 0.5f * t.y);
+    const float2 r = mul_i(u, s1);
+    v[0] = cadd(v[0], t);
+    v[1] = cadd(m, r);
+    v[2] = csub(m, r);
+  }
+};
+template <int SIGN>
+struct Dft<4, SIGN> {
+  static __device__ __forceinline__ void run(float2 (&v)[4]) {
+    const float2 t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]), t2 = cadd(v[1], v[3]);
+    const float2 t3 = mul_i(csub(v[1], v[3]), (float)SIGN);
+    v[0] = cadd(t0, t2);
+    v[2] = csub(t0, t2);
+    v[1] = cadd(t1, t3);
+    v[3] = csub(t1, t3);
+  }
+};
+template <int SIGN>
+struct Dft<5, SIGN> {
+  static __device__ __forceinline__ void run(float2 (&v)[5]) {
+    const float c1 = 0.30901699437494742f, c2 = -0.80901699437494742f;
+    const float s1 = (float)SIGN * 0.95105651629515357f, s2 = (float)SIGN * 0.58778525229247313f;
+    const float2 a = v[0];
+    const float2 t1 = cadd(v[1], v[4]), u1 = csub(v[1], v[4]);
+    const float2 t2 = cadd(v[2], v[3]), u2 = csub(v[2], v[3]);
+    v[0] = cadd(a, cadd(t1, t2));
+    const float2 m1 = make_float2(a.x + c1 * t1.x + c2 * t2.x, a.y + c1 * t1.y + c2 * t2.y);
+    const float2 m2 = make_float2(a.x + c2 * t1.x + c1 * t2.x, a.y + c2 * t1.y + c1 * t2.y);
+    const float2 r1 = make_float2(-(s1 * u1.y + s2 * u2.y), s1 * u1.x + s2 * u2.x);   // i (s1 u1 + s2 u2)
+    const float2 r2 = make_float2(-(s2 * u1.y - s1 * u2.y), s2 * u1.x - s1 * u2.x);   // i (s2 u1 - s1 u2)
+    v[1] = cadd(m1, r1);
+    v[4] = csub(m1, r1);
+    v[2] = cadd(m2, r2);
+    v[3] = csub(m2, r2);
+  }
+};
+template <int N1, int N2, int SIGN>
+struct DftCT {
+  static __device__ __forceinline__ void run(float2 (&v)[N1 * N2]) {
+    constexpr int N = N1 * N2;
+    float2 t[N1][N2];
 #pragma unroll
-    for (int n1 = 0; n1 < 16; ++n1) v[n1] = in[18 * n1];
-    dft16<SIGN>(v);
-    float2 *out = y + q * FFT288_YS + n2;
+    for (int n2 = 0; n2 < N2; ++n2) {
+      float2 u[N1];
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) u[n1] = v[N2 * n1 + n2];
+      Dft<N1, SIGN>::run(u);
+#pragma unroll
+      for (int k1 = 0; k1 < N1; ++k1) t[k1][n2] = (n2 * k1 == 0) ? u[k1] : rot<SIGN>(u[k1], twk<N>((n2 * k1) % N));
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < N1; ++k1) {
+      Dft<N2, SIGN>::run(t[k1]);
+#pragma unroll
+      for (int k2 = 0; k2 < N2; ++k2) v[k1 + N1 * k2] = t[k1][k2];
+    }
+  }
+};
+template <int SIGN> struct Dft<8, SIGN> : DftCT<2, 4, SIGN> {};
+template <int SIGN> struct Dft<9, SIGN> : DftCT<3, 3, SIGN> {};
+template <int SIGN> struct Dft<12, SIGN> : DftCT<3, 4, SIGN> {};
+template <int SIGN> struct Dft<15, SIGN> : DftCT<3, 5, SIGN> {};
+template <int SIGN> struct Dft<16, SIGN> : DftCT<4, 4, SIGN> {};
+template <int SIGN> struct Dft<18, SIGN> : DftCT<2, 9, SIGN> {};
+template <int SIGN> struct Dft<20, SIGN> : DftCT<4, 5, SIGN> {};
+
+// nfft transforms of length N = N1 x N2 in two register passes: pass 1, one thread per
+// (transform, n2): radix-N1 over n1 of x[N2 n1 + n2], times e^{SIGN 2 pi i n2 k1 / N} (the
+// smem table tw[m] = e^{-2 pi i m / N}), into y at n2 + RP k1 (rows padded to RP elements so
+// that pass 2 reads are bank-conflict free); pass 2, one thread per (transform, k1):
+// radix-N2 over n2 -> X[k1 + N1 k2] back into x in natural order.  y holds nfft*(N+FFT_YPAD).
+constexpr int FFT_YPAD = 40;
+template <int N1, int N2, int SIGN>
+__device__ void fft2p(float2 *x, float2 *y, const float2 *tw, int nfft) {
+  constexpr int N = N1 * N2, RP = (N2 & 1) ? N2 + 2 : N2 + 1, YS = N + FFT_YPAD;
+  static_assert(N1 * RP <= YS, "scratch row padding");
+  for (int task = threadIdx.x; task < nfft * N2; task += blockDim.x) {
+    const int q = task / N2, n2 = task - q * N2;
+    const float2 *in = x + q * N + n2;
+    float2 v[N1];
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) v[n1] = in[N2 * n1];
+    Dft<N1, SIGN>::run(v);
+    float2 *out = y + q * YS + n2;
     out[0] = v[0];
 #pragma unroll
-    for (int k1 = 1; k1 < 16; ++k1) {
-      float2 t = tw[n2 * k1];   // n2 k1 <= 255 < 288
+    for (int k1 = 1; k1 < N1; ++k1) {
+      float2 t = tw[n2 * k1];   // n2 k1 <= (N2-1)(N1-1) < N
       if (SIGN > 0) t.y = -t.y;
-      out[19 * k1] = cmul(v[k1], t);
+      out[RP * k1] = cmul(v[k1], t);
     }
   }
   __syncthreads();
-  for (int task = threadIdx.x; task < nfft * 16; task += blockDim.x) {
-    const int q = task >> 4, k1 = task & 15;
-    const float2 *in = y + q * FFT288_YS + 19 * k1;
-    float2 u[18];
+  for (int task = threadIdx.x; task < nfft * N1; task += blockDim.x) {
+    const int q = task / N1, k1 = task - q * N1;
+    const float2 *in = y + q * YS + RP * k1;
+    float2 u[N2];
 #pragma unroll
-    for (int n2 = 0; n2 < 18; ++n2) u[n2] = in[n2];
-    dft18<SIGN>(u);
-    float2 *out = x + q * 288 + k1;
+    for (int n2 = 0; n2 < N2; ++n2) u[n2] = in[n2];
+    Dft<N2, SIGN>::run(u);
+    float2 *out = x + q * N + k1;
 #pragma unroll
-    for (int k2 = 0; k2 < 18; ++k2) out[16 * k2] = u[k2];
+    for (int k2 = 0; k2 < N2; ++k2) out[N1 * k2] = u[k2];
   }
   __syncthreads();
+}
+// the lengths with a two-pass register plan: (N1, N2) from {15, 16, 18, 20}
+__host__ __device__ constexpr int fft2p_code(int N) {
+  return N == 288 ? 1 : N == 360 ? 2 : N == 300 ? 3 : N == 320 ? 4 : N == 240 ? 5 : N == 270 ? 6 : N == 256 ? 7
+       : N == 324 ? 8 : N == 400 ? 9 : N == 225 ? 10 : 0;
+}
+template <int SIGN>
+__device__ __forceinline__ bool fft2p_run(int N, float2 *x, float2 *y, const float2 *tw, int nfft) {
+  switch (fft2p_code(N)) {
+    case 1: fft2p<16, 18, SIGN>(x, y, tw, nfft); return true;
+    case 2: fft2p<20, 18, SIGN>(x, y, tw, nfft); return true;
+    case 3: fft2p<20, 15, SIGN>(x, y, tw, nfft); return true;
+    case 4: fft2p<16, 20, SIGN>(x, y, tw, nfft); return true;
+    case 5: fft2p<16, 15, SIGN>(x, y, tw, nfft); return true;
+    case 6: fft2p<18, 15, SIGN>(x, y, tw, nfft); return true;
+    case 7: fft2p<16, 16, SIGN>(x, y, tw, nfft); return true;
+    case 8: fft2p<18, 18, SIGN>(x, y, tw, nfft); return true;
+    case 9: fft2p<20, 20, SIGN>(x, y, tw, nfft); return true;
+    case 10: fft2p<15, 15, SIGN>(x, y, tw, nfft); return true;
+    default: return false;
+  }
 }
 
 // nfft transforms of length L.N stored contiguously in x; y is scratch of the same
 // size.  Returns the buffer holding the result.  All threads of the block take part.
 __device__ float2 *fft_batch(float2 *x, float2 *y, const float2 *tw, const FftLen &L, int nfft, float sign) {
-  if (L.N == 288) {   // register codelets (x in, x out); y holds nfft * FFT288_YS elements
-    if (sign < 0) fft288<-1>(x, y, tw, nfft);
-    else fft288<1>(x, y, tw, nfft);
-    return x;
-  }
+  // register two-pass plans (x in, x out; y holds nfft * (N + FFT_YPAD) elements)
+  if (sign < 0 ? fft2p_run<-1>(L.N, x, y, tw, nfft) : fft2p_run<1>(L.N, x, y, tw, nfft)) return x;
   int Ns = 1;
   for (int st = 0; st < L.nst; ++st) {
     const int R = L.rad[st];
@@ -327,7 +392,7 @@ __global__ void __launch_bounds__(FFT_THREADS) k_fft_rows(const uint16_t *__rest
   extern __shared__ __align__(16) float2 fsm[];
   const int Mc = g.Lc.N;
   float2 *tw = fsm;
-  float2 *x = tw + Mc, *y = x + FFT_ROWS_PAIRS * Mc;   // y: FFT_ROWS_PAIRS * (Mc + 16)
+  float2 *x = tw + Mc, *y = x + FFT_ROWS_PAIRS * Mc;   // y: FFT_ROWS_PAIRS * (Mc + FFT_YPAD)
   const int nrb = (g.mcp / 2 + per - 1) / per;   // per <= FFT_ROWS_PAIRS row pairs per block
   const int f = blockIdx.x / nrb, rb = blockIdx.x % nrb;
   const int p0 = rb * per, np = min(per, g.mcp / 2 - p0);
@@ -510,7 +575,7 @@ __global__ void __launch_bounds__(1024) k_fft_score(FftScoreArgs a) {
   const int Mc = g.Lc.N, W = g.W, hw = g.hw;
   float2 *tw = fsm;
   float2 *x = tw + Mc, *y = x + FFT_ROWS_PAIRS * Mc;
-  float *hb = reinterpret_cast<float *>(y + FFT_ROWS_PAIRS * (Mc + 16));   // [W][W] h~
+  float *hb = reinterpret_cast<float *>(y + FFT_ROWS_PAIRS * (Mc + FFT_YPAD));   // [W][W] h~
   __shared__ u64 red[32];
   __shared__ float fmin_hi_s;
   __shared__ int qn;

@@ -344,11 +344,11 @@ static int fft_init(moco_plan *p) {
   CK(cudaEventCreateWithFlags(&F.ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&F.ev_join, cudaEventDisableTiming));
   F.eps_rel = RS_FFT_C * std::ldexp(1.0, -24) * std::log2((double)Mr * (double)Mc);
-  // (the scratch half of each transform buffer carries 16 extra elements per transform:
-  // the padded rows of the 288-point register codelets, kernels_fft.cuh fft288)
-  F.smem_rows = (Mc + FFT_ROWS_PAIRS * Mc + FFT_ROWS_PAIRS * (Mc + 16)) * 8;
-  F.smem_cols = (Mr + FFT_COLS * Mr + FFT_COLS * (Mr + 16)) * 8;
-  F.smem_score = (Mc + FFT_ROWS_PAIRS * Mc + FFT_ROWS_PAIRS * (Mc + 16)) * 8 + ((g.W * g.W + 1) & ~1) * 4 + 2 * g.W * 8;
+  // (the scratch half of each transform buffer carries FFT_YPAD extra elements per
+  // transform: the padded rows of the two-pass register plans, kernels_fft.cuh fft2p)
+  F.smem_rows = (Mc + FFT_ROWS_PAIRS * Mc + FFT_ROWS_PAIRS * (Mc + FFT_YPAD)) * 8;
+  F.smem_cols = (Mr + FFT_COLS * Mr + FFT_COLS * (Mr + FFT_YPAD)) * 8;
+  F.smem_score = (Mc + FFT_ROWS_PAIRS * Mc + FFT_ROWS_PAIRS * (Mc + FFT_YPAD)) * 8 + ((g.W * g.W + 1) & ~1) * 4 + 2 * g.W * 8;
   F.smem_energy = (4 * g.hw + g.w * g.w + 1) * 8;
   if (F.smem_score > 227 * 1024 || F.smem_energy > 227 * 1024) return MOCO_EINVAL;
   CK(smem_attr(k_fft_rows, F.smem_rows));
