@@ -321,33 +321,31 @@ __device__ void fft2p(float2 *x, float2 *y, const float2 *tw, int nfft) {
   }
   __syncthreads();
 }
-// the lengths with a two-pass register plan: (N1, N2) from {15, 16, 18, 20}
-__host__ __device__ constexpr int fft2p_code(int N) {
-  return N == 288 ? 1 : N == 360 ? 2 : N == 300 ? 3 : N == 320 ? 4 : N == 240 ? 5 : N == 270 ? 6 : N == 256 ? 7
-       : N == 324 ? 8 : N == 400 ? 9 : N == 225 ? 10 : 0;
+// The lengths with a two-pass register plan, P -> (N1, N2), N1 N2 = N (P = 0: the generic
+// shared-memory Stockham passes).  Each kernel that transforms is instantiated per plan,
+// so a kernel carries the code of one plan only (all of them inlined together thrashed
+// the instruction cache: 288-point rows 363 -> 435 us).
+constexpr int FFT_NPLAN = 7;
+__host__ __device__ constexpr int fft_plan_of(int N) {
+  return N == 288 ? 1 : N == 360 ? 2 : N == 300 ? 3 : N == 320 ? 4 : N == 240 ? 5 : N == 256 ? 6 : 0;
 }
-template <int SIGN>
-__device__ __forceinline__ bool fft2p_run(int N, float2 *x, float2 *y, const float2 *tw, int nfft) {
-  switch (fft2p_code(N)) {
-    case 1: fft2p<16, 18, SIGN>(x, y, tw, nfft); return true;
-    case 2: fft2p<20, 18, SIGN>(x, y, tw, nfft); return true;
-    case 3: fft2p<20, 15, SIGN>(x, y, tw, nfft); return true;
-    case 4: fft2p<16, 20, SIGN>(x, y, tw, nfft); return true;
-    case 5: fft2p<16, 15, SIGN>(x, y, tw, nfft); return true;
-    case 6: fft2p<18, 15, SIGN>(x, y, tw, nfft); return true;
-    case 7: fft2p<16, 16, SIGN>(x, y, tw, nfft); return true;
-    case 8: fft2p<18, 18, SIGN>(x, y, tw, nfft); return true;
-    case 9: fft2p<20, 20, SIGN>(x, y, tw, nfft); return true;
-    case 10: fft2p<15, 15, SIGN>(x, y, tw, nfft); return true;
-    default: return false;
-  }
-}
+template <int P> struct Plan2p { static constexpr int N1 = 1, N2 = 1; };
+template <> struct Plan2p<1> { static constexpr int N1 = 16, N2 = 18; };
+template <> struct Plan2p<2> { static constexpr int N1 = 20, N2 = 18; };
+template <> struct Plan2p<3> { static constexpr int N1 = 20, N2 = 15; };
+template <> struct Plan2p<4> { static constexpr int N1 = 16, N2 = 20; };
+template <> struct Plan2p<5> { static constexpr int N1 = 16, N2 = 15; };
+template <> struct Plan2p<6> { static constexpr int N1 = 16, N2 = 16; };
 
 // nfft transforms of length L.N stored contiguously in x; y is scratch of the same
 // size.  Returns the buffer holding the result.  All threads of the block take part.
+template <int P>
 __device__ float2 *fft_batch(float2 *x, float2 *y, const float2 *tw, const FftLen &L, int nfft, float sign) {
-  // register two-pass plans (x in, x out; y holds nfft * (N + FFT_YPAD) elements)
-  if (sign < 0 ? fft2p_run<-1>(L.N, x, y, tw, nfft) : fft2p_run<1>(L.N, x, y, tw, nfft)) return x;
+  if constexpr (P > 0) {   // register two-pass plan (x in, x out; y holds nfft * (N + FFT_YPAD))
+    if (sign < 0) fft2p<Plan2p<P>::N1, Plan2p<P>::N2, -1>(x, y, tw, nfft);
+    else fft2p<Plan2p<P>::N1, Plan2p<P>::N2, 1>(x, y, tw, nfft);
+    return x;
+  }
   int Ns = 1;
   for (int st = 0; st < L.nst; ++st) {
     const int R = L.rad[st];
@@ -386,6 +384,7 @@ constexpr int FFT_THREADS = 256;
 
 // ---------------------------------------------------------------- forward rows
 // S[f][k][r] = sum_j a_f[r][j] exp(-2 pi i j k / Mc), k in [0, Kc), r in [0, mcp)
+template <int P>
 __global__ void __launch_bounds__(FFT_THREADS) k_fft_rows(const uint16_t *__restrict__ img, int64_t fstride,
                                                           int pitch, FftGeom g, const float2 *__restrict__ twc,
                                                           float2 *__restrict__ S, int per) {
@@ -409,7 +408,7 @@ __global__ void __launch_bounds__(FFT_THREADS) k_fft_rows(const uint16_t *__rest
     x[q * Mc + j] = make_float2(re, im);
   }
   __syncthreads();
-  const float2 *Z = fft_batch(x, y, tw, g.Lc, np, -1.f);
+  const float2 *Z = fft_batch<P>(x, y, tw, g.Lc, np, -1.f);
   // unpack the two real rows' spectra; store column-major S[f][k][row]
   float2 *Sf = S + (int64_t)f * g.Kc * g.mcp;
   for (int e = threadIdx.x; e < g.Kc * np; e += blockDim.x) {
@@ -428,6 +427,7 @@ __global__ void __launch_bounds__(FFT_THREADS) k_fft_rows(const uint16_t *__rest
 // mode 0 (frames): P[f][s+hw][k] = (1/(Mr Mc)) sum_u X[u][k] Bc[k][u] e^{+2 pi i u s / Mr}
 //                  for s in [-hw, hw], X = FFT over rows of S[f][k][*]
 // mode 1 (template): Bc[k][u] = conj(X[u][k]) / (Mr Mc)
+template <int PL>
 __global__ void __launch_bounds__(FFT_THREADS) k_fft_cols(const float2 *__restrict__ S, FftGeom g,
                                                           const float2 *__restrict__ twr, float2 *__restrict__ Bc,
                                                           float2 *__restrict__ P, int mode, int per) {
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(FFT_THREADS) k_fft_cols(const float2 *__restri
     x[q * Mr + u] = u < g.mc ? Sf[(int64_t)(k0 + q) * g.mcp + u] : make_float2(0.f, 0.f);
   }
   __syncthreads();
-  float2 *X = fft_batch(x, y, tw, g.Lr, nk, -1.f);
+  float2 *X = fft_batch<PL>(x, y, tw, g.Lr, nk, -1.f);
   const float scale = 1.0f / ((float)Mr * (float)g.Lc.N);
   if (mode == 1) {
     for (int e = threadIdx.x; e < nk * Mr; e += blockDim.x) {
@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(FFT_THREADS) k_fft_cols(const float2 *__restri
   }
   __syncthreads();
   float2 *other = X == x ? y : x;
-  const float2 *Hc = fft_batch(X, other, tw, g.Lr, nk, +1.f);
+  const float2 *Hc = fft_batch<PL>(X, other, tw, g.Lr, nk, +1.f);
   float2 *Pf = P + (int64_t)f * g.W * g.Kc;
   for (int e = threadIdx.x; e < g.W * nk; e += blockDim.x) {
     const int si = e / nk, q = e - si * nk;
@@ -569,6 +569,7 @@ __device__ __forceinline__ void fft_pick_tail(const FftScoreArgs &a, int64_t f, 
   }
 }
 
+template <int P>
 __global__ void __launch_bounds__(1024) k_fft_score(FftScoreArgs a) {
   extern __shared__ __align__(16) float2 fsm[];
   const FftGeom &g = a.g;
@@ -599,7 +600,7 @@ __global__ void __launch_bounds__(1024) k_fft_score(FftScoreArgs a) {
       x[q * Mc + k] = make_float2(v1.x - v2.y, v1.y + v2.x);
     }
     __syncthreads();
-    const float2 *Hr = fft_batch(x, y, tw, g.Lc, np, +1.f);
+    const float2 *Hr = fft_batch<P>(x, y, tw, g.Lc, np, +1.f);
     for (int e = threadIdx.x; e < np * W; e += blockDim.x) {
       const int q = e / W, ti = e - q * W;
       const int s1 = 2 * (p0 + q), s2 = s1 + 1;
@@ -650,6 +651,7 @@ __global__ void __launch_bounds__(1024) k_fft_score(FftScoreArgs a) {
 // of its lag rows and the certified interval of each of its lags (same arithmetic as
 // k_fft_score): lower bound to a.lb, min of the upper bounds by atomicMin into a.ub[f]
 // (non-negative floats order like their bit patterns).
+template <int P>
 __global__ void __launch_bounds__(FFT_THREADS) k_fft_score_rows(FftScoreArgs a, int per) {
   extern __shared__ __align__(16) float2 fsm[];
   const FftGeom &g = a.g;
@@ -673,7 +675,7 @@ __global__ void __launch_bounds__(FFT_THREADS) k_fft_score_rows(FftScoreArgs a, 
     x[q * Mc + k] = make_float2(v1.x - v2.y, v1.y + v2.x);
   }
   __syncthreads();
-  const float2 *Hr = fft_batch(x, y, tw, g.Lc, np, +1.f);
+  const float2 *Hr = fft_batch<P>(x, y, tw, g.Lc, np, +1.f);
   const u64 *gaf = a.ga + f * W * W;
   const double na = sqrt((double)gaf[hw * W + hw]), nb = sqrt((double)a.gb[hw * W + hw]);
   const double eps2 = 2.0 * a.eps_rel * na * nb;
@@ -776,26 +778,52 @@ __global__ void __launch_bounds__(1024) k_energy_u16(const uint16_t *__restrict_
       esm[k < 4 * hw ? k : 4 * hw + CS] = pf[k];
       pf[k] = 0;
     }
-  }
-  for (int r = warp; r < (part ? 0 : mc); r += nwarp) {
-    u64 rs = 0;
-    const bool top = r < hw, bot = r >= mc - hw;
-    const uint16_t *row = A + (int64_t)r * pitch;
-#pragma unroll 4
-    for (int c = lane; c < nc; c += 32) {
-      const u64 v2 = (u64)row[c] * row[c];
-      rs += v2;
-      if (c < hw) atomicAdd(&colE[c], v2);
-      if (c >= nc - hw) atomicAdd(&colE[hw + (nc - 1 - c)], v2);
+  } else {
+    // row pass: warp per row, lane per 8-column chunk (16-byte loads: the coarse images'
+    // pitch is a multiple of 8 samples); squares of the edge columns accumulate in the
+    // lane's registers (a lane holds at most one left-edge and one right-edge chunk for
+    // hw <= 256) and reach shared memory once per frame
+    const int nchunk = (nc + 7) >> 3;
+    const int cl = lane, cr = lane + 32 * ((nchunk - 1 - lane) >> 5);   // the lane's first / last chunk
+    const bool hasL = lane < nchunk && 8 * cl < hw, hasR = lane < nchunk && 8 * cr + 8 > nc - hw;
+    u64 eL[8], eR[8];
+#pragma unroll
+    for (int x = 0; x < 8; ++x) eL[x] = eR[x] = 0;
+    for (int r = warp; r < mc; r += nwarp) {
+      const uint16_t *row = A + (int64_t)r * pitch;
+      u64 rs = 0;
+      for (int c = lane; c < nchunk; c += 32) {
+        const uint4 q = *reinterpret_cast<const uint4 *>(row + 8 * c);
+        const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
+        uint32_t sq[8];
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+          const uint32_t v = (x & 1) ? (wv[x >> 1] >> 16) : (wv[x >> 1] & 0xffffu);
+          sq[x] = 8 * c + x < nc ? v * v : 0u;   // < 2^32
+          rs += sq[x];
+        }
+        if (c == cl && hasL)
+#pragma unroll
+          for (int x = 0; x < 8; ++x) eL[x] += sq[x];
+        if (c == cr && hasR)
+#pragma unroll
+          for (int x = 0; x < 8; ++x) eR[x] += sq[x];
+      }
+      rs = warp_sum(rs);
+      if (lane == 0) {
+        mytot += rs;
+        if (r < hw) rowE[r] = rs;
+        if (r >= mc - hw) rowE[hw + (mc - 1 - r)] = rs;
+      }
     }
-    rs = warp_sum(rs);
-    if (lane == 0) {
-      mytot += rs;
-      if (top) rowE[r] = rs;
-      if (bot) rowE[hw + (mc - 1 - r)] = rs;
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+      const int c0 = 8 * cl + x, c1 = 8 * cr + x;
+      if (hasL && c0 < hw) atomicAdd(&colE[c0], eL[x]);
+      if (hasR && c1 < nc && c1 >= nc - hw) atomicAdd(&colE[hw + (nc - 1 - c1)], eR[x]);
     }
+    if (lane == 0) atomicAdd(tot, mytot);
   }
-  if (lane == 0 && !part) atomicAdd(tot, mytot);
   __syncthreads();
   if (threadIdx.x < 4) {
     u64 *e = (threadIdx.x & 2) ? colE : rowE;

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <new>
+#include <type_traits>
 #include <vector>
 
 #include "moco.h"
@@ -103,6 +104,7 @@ struct moco_plan {
     int64_t cap = 0;
     double eps_rel = 0;
     int smem_rows = 0, smem_cols = 0, smem_score = 0, smem_energy = 0;
+    int pc = 0, pr = 0;         // register FFT plans of the row (Mc) and column (Mr) lengths
   } fft;
   // two-stream batch pipeline (align_tc_pipelined)
   bool pipe_ready;
@@ -308,8 +310,21 @@ static void plan_free(moco_plan *p) {
 }
 
 // ---------------------------------------------------------------- FFT path (S3 by FFT)
+// call fn(std::integral_constant<int, P>) for the kernel instantiation of FFT plan P
+template <class Fn>
+static void fft_dispatch(int plan, Fn &&fn) {
+  switch (plan) {
+    case 1: fn(std::integral_constant<int, 1>{}); break;
+    case 2: fn(std::integral_constant<int, 2>{}); break;
+    case 3: fn(std::integral_constant<int, 3>{}); break;
+    case 4: fn(std::integral_constant<int, 4>{}); break;
+    case 5: fn(std::integral_constant<int, 5>{}); break;
+    case 6: fn(std::integral_constant<int, 6>{}); break;
+    default: fn(std::integral_constant<int, 0>{}); break;
+  }
+}
 static bool fft_supported(const moco_plan *p) {
-  if (p->dtype != MOCO_U16) return false;
+  if (p->dtype != MOCO_U16 || p->w - 1 > 248) return false;   // (k_energy_u16: edge chunks in one lane round)
   const int L = p->levels;
   FftLen a, b;
   return fft_len_make(p->ml[L] + p->w - 1, &a) && fft_len_make(p->nl[L] + p->w - 1, &b);
@@ -351,10 +366,20 @@ static int fft_init(moco_plan *p) {
   F.smem_score = (Mc + FFT_ROWS_PAIRS * Mc + FFT_ROWS_PAIRS * (Mc + FFT_YPAD)) * 8 + ((g.W * g.W + 1) & ~1) * 4 + 2 * g.W * 8;
   F.smem_energy = (4 * g.hw + g.w * g.w + 1) * 8;
   if (F.smem_score > 227 * 1024 || F.smem_energy > 227 * 1024) return MOCO_EINVAL;
-  CK(smem_attr(k_fft_rows, F.smem_rows));
-  CK(smem_attr(k_fft_score_rows, F.smem_rows));
-  CK(smem_attr(k_fft_cols, F.smem_cols));
-  CK(smem_attr(k_fft_score, F.smem_score));
+  F.pc = fft_plan_of(Mc);
+  F.pr = fft_plan_of(Mr);
+  int rc_attr = MOCO_OK;
+  fft_dispatch(F.pc, [&](auto PC) {
+    constexpr int P = decltype(PC)::value;
+    if (smem_attr(k_fft_rows<P>, F.smem_rows) != cudaSuccess || smem_attr(k_fft_score_rows<P>, F.smem_rows) != cudaSuccess ||
+        smem_attr(k_fft_score<P>, F.smem_score) != cudaSuccess)
+      rc_attr = set_cuda_err(cudaGetLastError(), "fft kernel attributes");
+  });
+  fft_dispatch(F.pr, [&](auto PR) {
+    constexpr int P = decltype(PR)::value;
+    if (smem_attr(k_fft_cols<P>, F.smem_cols) != cudaSuccess) rc_attr = set_cuda_err(cudaGetLastError(), "fft kernel attributes");
+  });
+  if (rc_attr) return rc_attr;
   CK(smem_attr(k_energy_u16, F.smem_energy));
   k_fft_twiddles<<<(Mr + 255) / 256, 256>>>(F.twr, Mr);
   k_fft_twiddles<<<(Mc + 255) / 256, 256>>>(F.twc, Mc);
@@ -371,9 +396,13 @@ static int fft_set_template(moco_plan *p, cudaStream_t st) {
   const FftGeom &g = F.g;
   const int nrb = (g.mcp / 2 + FFT_ROWS_PAIRS - 1) / FFT_ROWS_PAIRS;
   const int ncb = (g.Kc + FFT_COLS - 1) / FFT_COLS;
-  k_fft_rows<<<nrb, FFT_THREADS, F.smem_rows, st>>>((const uint16_t *)p->tpl[L], 0, p->pitch[L], g, F.twc, F.S,
-                                                    FFT_ROWS_PAIRS);
-  k_fft_cols<<<ncb, FFT_THREADS, F.smem_cols, st>>>(F.S, g, F.twr, F.Bc, nullptr, 1, FFT_COLS);
+  fft_dispatch(F.pc, [&](auto PC) {
+    k_fft_rows<decltype(PC)::value><<<nrb, FFT_THREADS, F.smem_rows, st>>>((const uint16_t *)p->tpl[L], 0, p->pitch[L],
+                                                                           g, F.twc, F.S, FFT_ROWS_PAIRS);
+  });
+  fft_dispatch(F.pr, [&](auto PR) {
+    k_fft_cols<decltype(PR)::value><<<ncb, FFT_THREADS, F.smem_cols, st>>>(F.S, g, F.twr, F.Bc, nullptr, 1, FFT_COLS);
+  });
   CKL("fft_set_template");
   F.tpl_ready = true;
   return MOCO_OK;
@@ -419,8 +448,14 @@ static int launch_fft(moco_plan *p, const void *img, int64_t fstride, int pitch,
     if (small) CK(cudaEventRecord(F.ev_join, se));
     {
       ProfScope ps(p, MOCO_K_COARSE, st);
-      k_fft_rows<<<(unsigned)(nb * nrb), FFT_THREADS, F.smem_rows, st>>>(im, fstride, pitch, g, F.twc, F.S, rper);
-      k_fft_cols<<<(unsigned)(nb * ncb), FFT_THREADS, F.smem_cols, st>>>(F.S, g, F.twr, F.Bc, F.P, 0, cper);
+      fft_dispatch(F.pc, [&](auto PC) {
+        k_fft_rows<decltype(PC)::value><<<(unsigned)(nb * nrb), FFT_THREADS, F.smem_rows, st>>>(im, fstride, pitch, g,
+                                                                                               F.twc, F.S, rper);
+      });
+      fft_dispatch(F.pr, [&](auto PR) {
+        k_fft_cols<decltype(PR)::value><<<(unsigned)(nb * ncb), FFT_THREADS, F.smem_cols, st>>>(F.S, g, F.twr, F.Bc,
+                                                                                               F.P, 0, cper);
+      });
     }
     if (small) CK(cudaStreamWaitEvent(st, F.ev_join, 0));
     FftScoreArgs a;
@@ -436,10 +471,14 @@ static int launch_fft(moco_plan *p, const void *img, int64_t fstride, int pitch,
     {
       ProfScope ps(p, MOCO_K_SCORE, st);
       if (small) {
-        k_fft_score_rows<<<(unsigned)(nb * npb), FFT_THREADS, F.smem_rows, st>>>(a, sper);
+        fft_dispatch(F.pc, [&](auto PC) {
+          k_fft_score_rows<decltype(PC)::value><<<(unsigned)(nb * npb), FFT_THREADS, F.smem_rows, st>>>(a, sper);
+        });
         k_fft_score_pick<<<(unsigned)nb, 1024, 0, st>>>(a);
       } else {
-        k_fft_score<<<(unsigned)nb, nb < p->nsm ? 1024 : FFT_THREADS, F.smem_score, st>>>(a);
+        fft_dispatch(F.pc, [&](auto PC) {
+          k_fft_score<decltype(PC)::value><<<(unsigned)nb, nb < p->nsm ? 1024 : FFT_THREADS, F.smem_score, st>>>(a);
+        });
       }
     }
     p->launches += small ? 6 : 4;
