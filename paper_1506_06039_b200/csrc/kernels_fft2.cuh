@@ -1,0 +1,673 @@
+// kernels_fft2.cuh -- the FFT path of S3/S4 (the paper's method) for transform
+// lengths with a two-pass register plan (kernels_fft.cuh Plan2p: 240, 256, 288, 300, 320,
+// 360 -- every BASELINE config and the paper's default w = min(m,n)/3 at 256^2 coarse).
+//
+// Same mathematics as kernels_fft.cuh (H = IFFT2(FFT2(a_pad) . conj(FFT2(b_pad))),
+// h(s,t) = H[s mod Mr][t mod Mc], certified candidate set, exact rescoring), laid out for
+// the SM instead of for generality:
+//
+//   k_fft2_rows<P,L>  one read of the frame (bulk copies into shared memory): 2^L x 2^L
+//                     block sums (S1, exact; L <= 1: levels = 2 runs on the level-1 image
+//                     the level-1 refine reads anyway), the frame-energy partials of
+//                     P:33-35 (row sums, edge columns, the row prefixes of the four corner
+//                     blocks) and the row FFTs of two coarse rows packed per complex
+//                     transform -> S[f][k][row]
+//   k_fft2_cols<P>    per column bin: FFT_Mr, times conj(B^)/(Mr Mc), IFFT_Mr, keep the
+//                     2w-1 lag rows -> P[f][s][k]
+//   k_fft2_score<P>   per group of lag rows: IFFT_Mc of two packed lag rows, g_a of every
+//                     lag from the energy partials (total - strips + corner),
+//                     certified interval of f~; the LAST block of a frame (global counter)
+//                     takes the candidate set Q and, when |Q| > 1 (or levels = 0, where
+//                     f_min is the coarse f), re-scores Q exactly: N = sum_D (a - b)^2 in
+//                     64-bit integers, straight from the level-0 frame.
+//
+// Transforms (N = N1 N2, n = n2 + N2 n1, k = k1 + N1 k2) run in place in shared memory with
+// the two index orders of one padded array, row r of N2+1 slots (the gap spreads the
+// stride-(N2+1) accesses over the banks):
+//     natural order   element n at ix(n)  = (N2+1) (n / N2) + n % N2
+//     k1-major order  element k at pos(k) = (N2+1) (k % N1) + k / N1
+// The forward transform takes natural order to k1-major order (pass 1: radix-N1 over n1 per
+// n2, twiddle; pass 2: radix-N2 over n2 per k1, both writing back to the addresses they
+// read); the inverse takes k1-major order back to natural order (the same passes
+// transposed).  No index arithmetic inside the passes beyond constant offsets, and no data
+// movement between them.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kernels_fft.cuh"
+#include "kernels_tc.cuh"
+
+namespace moco {
+
+constexpr int F2_THREADS = 288;
+constexpr int F2_WARPS = F2_THREADS / 32;
+
+template <int P>
+struct F2 {
+  static constexpr int N1 = Plan2p<P>::N1, N2 = Plan2p<P>::N2, N = N1 * N2, R = N2 + 1;
+  // transforms per block (one thread per (transform, n2) in the wider pass)
+  static constexpr int NF = F2_THREADS / (N1 > N2 ? N1 : N2) < 16 ? F2_THREADS / (N1 > N2 ? N1 : N2) : 16;
+  static constexpr int STRIDE = (N1 * R) | 1;   // slots per transform (odd: bank spread)
+  __device__ static __forceinline__ int ix(int n) { return n + n / N2; }
+  __device__ static __forceinline__ int pos(int k) { return R * (k % N1) + k / N1; }
+};
+
+// Forward: x natural -> X k1-major, X[k] = sum_n x[n] e^{-2 pi i n k / N}.  tw[m] =
+// e^{-2 pi i m / N}.  nfft <= NF transforms at x + q * STRIDE.  All threads; ends synced.
+template <int P>
+__device__ __forceinline__ void f2_fwd(float2 *x, const float2 *tw, int nfft) {
+  using G = F2<P>;
+  constexpr int N1 = G::N1, N2 = G::N2, R = G::R, S = G::STRIDE;
+  __syncthreads();
+  for (int task = threadIdx.x; task < nfft * N2; task += blockDim.x) {
+    const int q = task / N2, n2 = task - q * N2;
+    float2 *b = x + q * S + n2;
+    float2 v[N1];
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) v[n1] = b[R * n1];
+    Dft<N1, -1>::run(v);
+    b[0] = v[0];
+#pragma unroll
+    for (int k1 = 1; k1 < N1; ++k1) b[R * k1] = cmul(v[k1], tw[n2 * k1]);
+  }
+  __syncthreads();
+  for (int task = threadIdx.x; task < nfft * N1; task += blockDim.x) {
+    const int q = task / N1, k1 = task - q * N1;
+    float2 *b = x + q * S + R * k1;
+    float2 u[N2];
+#pragma unroll
+    for (int n2 = 0; n2 < N2; ++n2) u[n2] = b[n2];
+    Dft<N2, -1>::run(u);
+#pragma unroll
+    for (int k2 = 0; k2 < N2; ++k2) b[k2] = u[k2];
+  }
+  __syncthreads();
+}
+
+// Inverse: X k1-major -> x natural, x[n] = sum_k X[k] e^{+2 pi i n k / N} (unnormalised).
+template <int P>
+__device__ __forceinline__ void f2_inv(float2 *x, const float2 *tw, int nfft) {
+  using G = F2<P>;
+  constexpr int N1 = G::N1, N2 = G::N2, R = G::R, S = G::STRIDE;
+  __syncthreads();
+  for (int task = threadIdx.x; task < nfft * N1; task += blockDim.x) {
+    const int q = task / N1, k1 = task - q * N1;
+    float2 *b = x + q * S + R * k1;
+    float2 u[N2];
+#pragma unroll
+    for (int k2 = 0; k2 < N2; ++k2) u[k2] = b[k2];
+    Dft<N2, 1>::run(u);   // over k2 -> n2
+    b[0] = u[0];
+#pragma unroll
+    for (int n2 = 1; n2 < N2; ++n2) b[n2] = cmul(u[n2], conjf2(tw[k1 * n2]));
+  }
+  __syncthreads();
+  for (int task = threadIdx.x; task < nfft * N2; task += blockDim.x) {
+    const int q = task / N2, n2 = task - q * N2;
+    float2 *b = x + q * S + n2;
+    float2 v[N1];
+#pragma unroll
+    for (int k1 = 0; k1 < N1; ++k1) v[k1] = b[R * k1];
+    Dft<N1, 1>::run(v);   // over k1 -> n1
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) b[R * n1] = v[n1];
+  }
+  __syncthreads();
+}
+
+// inclusive warp scan of u64
+__device__ __forceinline__ u64 warp_scan_incl(u64 v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u64 t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// Per-frame energy scratch (u64), for a frame of coarse size mc x nc and hw = w - 1:
+//   [0]                       total sum of a^2                                    (atomic)
+//   [1, 1+hw)                 top rows i:           sum_j a^2[i][j]
+//   [1+hw, 1+2hw)             bottom rows (distance d from the last row)
+//   [1+2hw, 1+3hw)            left columns j:       sum_i a^2[i][j]               (atomic)
+//   [1+3hw, 1+4hw)            right columns (distance d from the last column)     (atomic)
+//   [1+4hw + (quad*hw + i)*hw + (a-1)]  corner row prefixes: sum of a^2 over the first a
+//                             columns from the quad's side of its i-th row from its edge
+//                             (quad = bottom*2 + right)
+// The atomic slots are zero on entry; the pick re-zeroes them.
+__host__ __device__ constexpr int f2_esz(int hw) { return 1 + 4 * hw + 4 * hw * hw; }
+
+struct F2RowsArgs {
+  const uint16_t *frames;   // level-0 frames (levels L) or coarse images (L = 0)
+  int64_t fstride;
+  int pitch;
+  int mc, nc, hw, Kc, mcp;
+  int per;                  // row pairs per block (<= NF)
+  const float2 *tw;         // [Mc]
+  float2 *S;                // [B][Kc][mcp]
+  u64 *E;                   // [B][esz] energy partials, or null (template)
+};
+
+// raw bytes a k_fft2_rows block stages: 2 per row pairs x 2^L raw rows of 2^L nc samples
+__host__ __device__ constexpr int f2_stage_bytes(int per, int L, int nc) { return 2 * per * (1 << L) * (1 << L) * nc * 2; }
+constexpr int F2_STAGE_MAX = 64 * 1024;
+
+template <int P, int L>
+__global__ void __launch_bounds__(F2_THREADS) k_fft2_rows(F2RowsArgs a) {
+  static_assert(L == 0 || L == 1, "2x2 block sums at most (levels = 2 runs on the level-1 image)");
+  using G = F2<P>;
+  constexpr int Mc = G::N, S = G::STRIDE, N2 = G::N2, D = 1 << L;
+  extern __shared__ __align__(128) unsigned char f2sm[];
+  __shared__ __align__(8) uint64_t bar;
+  const int hw = a.hw, nc = a.nc, mc = a.mc;
+  const int nrb = (a.mcp / 2 + a.per - 1) / a.per;
+  const int64_t f = blockIdx.x / nrb;
+  const int p0 = (blockIdx.x - (int)(f * nrb)) * a.per;
+  const int np = min(a.per, a.mcp / 2 - p0), nr = 2 * np;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // the block's raw rows (D per coarse row, D nc samples each), staged by bulk copies
+  uint16_t *stg = reinterpret_cast<uint16_t *>(f2sm);
+  float2 *tw = reinterpret_cast<float2 *>(f2sm + f2_stage_bytes(a.per, L, nc));
+  float2 *x = tw + Mc;
+  const int rawrow = D * nc;
+  const int nraw = D * max(0, min(nr, mc - 2 * p0));
+  const uint16_t *Fr = a.frames + f * a.fstride + (int64_t)(D * 2 * p0) * a.pitch;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if (lane == 0) mbar_arrive_expect_tx(&bar, (uint32_t)(nraw * rawrow * 2));
+    __syncwarp();
+    for (int r = lane; r < nraw; r += 32)
+      bulk_g2s(stg + (size_t)r * rawrow, Fr + (int64_t)r * a.pitch, (uint32_t)(rawrow * 2), &bar);
+  }
+  for (int k = threadIdx.x; k < Mc; k += blockDim.x) tw[k] = a.tw[k];
+  // zero columns [nc, Mc) of every transform of the block
+  const int tail = Mc - nc;
+  for (int e = threadIdx.x; e < np * tail; e += blockDim.x) {
+    const int q = e / tail, j = nc + (e - q * tail);
+    x[q * S + G::ix(j)] = make_float2(0.f, 0.f);
+  }
+  mbar_wait(&bar, 0);
+  // a warp per coarse row pair (one complex transform), a lane per 8 coarse columns; the
+  // lane's first and last chunks hold the edge columns (hw <= 256), whose squares it
+  // accumulates over its rows
+  const int nch = nc >> 3;
+  const int cl = lane, cr = lane + 32 * ((nch - 1 - lane) >> 5);
+  const bool hasL = a.E && lane < nch && 8 * cl < hw, hasR = a.E && lane < nch && 8 * cr + 8 > nc - hw;
+  u64 eL[8], eR[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) eL[k] = eR[k] = 0;
+  u64 wtot = 0;
+  u64 *E = a.E ? a.E + f * f2_esz(hw) : nullptr;
+  // 8 coarse values of coarse row rl (block-local), columns 8c .. 8c+7, from the staged rows
+  auto load8 = [&](int rl, int c, uint32_t (&v)[8]) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = 0;
+    if (2 * p0 + rl >= mc) return;
+    const uint16_t *Rr = stg + (size_t)(D * rl) * rawrow;
+    if constexpr (L == 0) {
+      const uint4 q4 = *reinterpret_cast<const uint4 *>(Rr + 8 * c);
+      const uint32_t wv[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) { v[2 * k] = wv[k] & 0xffffu; v[2 * k + 1] = wv[k] >> 16; }
+    } else {
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        const uint4 u0 = *reinterpret_cast<const uint4 *>(Rr + 16 * c + 8 * g);
+        const uint4 u1 = *reinterpret_cast<const uint4 *>(Rr + rawrow + 16 * c + 8 * g);
+        const uint32_t w0[4] = {u0.x, u0.y, u0.z, u0.w}, w1[4] = {u1.x, u1.y, u1.z, u1.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          v[4 * g + k] = (w0[k] & 0xffffu) + (w0[k] >> 16) + (w1[k] & 0xffffu) + (w1[k] >> 16);
+      }
+    }
+  };
+  for (int q = warp; q < np; q += F2_WARPS) {
+    float2 *xq = x + q * S;
+    u64 rs0 = 0, rs1 = 0;
+    for (int c = lane; c < nch; c += 32) {
+      uint32_t v0[8], v1[8];
+      load8(2 * q, c, v0);
+      load8(2 * q + 1, c, v1);
+      // natural-order slots of columns 8c .. 8c+7 (at most one row break of the padding)
+      const int j0 = 8 * c, q0 = j0 / N2, brk = (q0 + 1) * N2 - j0;
+      float2 *xc = xq + j0 + q0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) xc[k + (k >= brk ? 1 : 0)] = make_float2((float)v0[k], (float)v1[k]);
+      if (a.E) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t s0 = v0[k] * v0[k], s1 = v1[k] * v1[k];   // < 2^32 (coarse values < 2^16)
+          rs0 += s0;
+          rs1 += s1;
+          if (hasL && c == cl) eL[k] += (u64)s0 + s1;
+          if (hasR && c == cr) eR[k] += (u64)s0 + s1;
+        }
+      }
+    }
+    if (a.E) {
+      rs0 = warp_sum(rs0);
+      rs1 = warp_sum(rs1);
+      if (lane < 2) {
+        const int r = 2 * (p0 + q) + lane;
+        const u64 rs = lane ? rs1 : rs0;
+        if (r < mc) {
+          wtot += rs;
+          if (r < hw) E[1 + r] = rs;
+          if (r >= mc - hw) E[1 + hw + (mc - 1 - r)] = rs;
+        }
+      }
+    }
+  }
+  if (a.E) {
+    if (lane < 2 && wtot) atomicAdd(&E[0], wtot);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int jl = 8 * cl + k, jr = 8 * cr + k;
+      if (hasL && jl < hw && eL[k]) atomicAdd(&E[1 + 2 * hw + jl], eL[k]);
+      if (hasR && jr < nc && jr >= nc - hw && eR[k]) atomicAdd(&E[1 + 3 * hw + (nc - 1 - jr)], eR[k]);
+    }
+  }
+  __syncthreads();
+  if (a.E) {
+    // corner row prefixes: a warp per (corner row, side), scanning the hw columns
+    for (int t = warp; t < 2 * nr; t += F2_WARPS) {
+      const int rl = t >> 1, right = t & 1, r = 2 * p0 + rl;
+      if (r >= mc) continue;
+      const float *xr = reinterpret_cast<const float *>(x + (rl >> 1) * S) + (rl & 1);
+      for (int bot = 0; bot < 2; ++bot) {
+        const int i = bot ? mc - 1 - r : r;
+        if (i >= hw) continue;
+        u64 *o = E + 1 + 4 * hw + ((2 * bot + right) * hw + i) * hw;
+        u64 carry = 0;
+        for (int a0 = 0; a0 < hw; a0 += 32) {
+          const int aa = a0 + lane;
+          u64 v2 = 0;
+          if (aa < hw) {
+            const uint32_t v = (uint32_t)xr[2 * G::ix(right ? nc - 1 - aa : aa)];
+            v2 = (u64)(v * v);
+          }
+          const u64 sc = warp_scan_incl(v2) + carry;
+          if (aa < hw) o[aa] = sc;
+          carry = __shfl_sync(0xffffffffu, sc, 31);
+        }
+      }
+    }
+  }
+  f2_fwd<P>(x, tw, np);
+  // unpack the two real rows' spectra into S[f][k][row]: warps over k, lanes over rows
+  {
+    float2 *Sk = a.S + f * a.Kc * a.mcp + 2 * p0 + lane + (int64_t)warp * a.mcp;
+    const int q = lane >> 1;
+    const bool odd = lane & 1;
+    const float2 *xq = x + q * S;
+    const int64_t step = (int64_t)F2_WARPS * a.mcp;
+    for (int k = warp; k < a.Kc; k += F2_WARPS, Sk += step) {
+      if (lane >= nr) continue;
+      const unsigned uk = (unsigned)k, un = (unsigned)(k == 0 ? 0 : Mc - k);
+      const float2 zk = xq[G::R * (uk % G::N1) + uk / G::N1];
+      const float2 zn = xq[G::R * (un % G::N1) + un / G::N1];
+      // X0 = (Z[k] + conj Z[-k]) / 2, X1 = (Z[k] - conj Z[-k]) / 2i
+      *Sk = odd ? make_float2(0.5f * (zk.y + zn.y), -0.5f * (zk.x - zn.x))
+                : make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y - zn.y));
+    }
+  }
+}
+
+struct F2ColsArgs {
+  const float2 *S;          // [B][Kc][mcp]
+  int mc, Kc, mcp, W, hw;
+  int per;                  // column bins per block (<= NF)
+  const float2 *tw;         // [Mr]
+  const float2 *Bc;         // [Kc][Mr] conj(B^)/(Mr Mc)   (frames)
+  float2 *P;                // [B][W][Kc]                  (frames)
+  float2 *Bout;             // template mode: Bc out, or null
+  float scale;              // template mode: 1/(Mr Mc)
+};
+
+template <int P>
+__global__ void __launch_bounds__(F2_THREADS) k_fft2_cols(F2ColsArgs a) {
+  using G = F2<P>;
+  constexpr int Mr = G::N, S = G::STRIDE;
+  extern __shared__ __align__(128) unsigned char f2sm[];
+  float2 *tw = reinterpret_cast<float2 *>(f2sm);
+  float2 *x = tw + Mr;
+  const int ncb = (a.Kc + a.per - 1) / a.per;
+  const int64_t f = blockIdx.x / ncb;
+  const int k0 = (blockIdx.x - (int)(f * ncb)) * a.per;
+  const int nk = min(a.per, a.Kc - k0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = threadIdx.x; k < Mr; k += blockDim.x) tw[k] = a.tw[k];
+  // a warp per column bin: rows u (natural order), 4 loads in flight per lane
+  const float2 *Sf = a.S + (f * a.Kc + k0) * a.mcp;
+  for (int q = warp; q < nk; q += F2_WARPS) {
+    float2 *xq = x + q * S;
+    for (int u0 = 0; u0 < Mr; u0 += 128) {
+      float2 v[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int u = u0 + 32 * h + lane;
+        v[h] = u < a.mc ? __ldcg(Sf + (int64_t)q * a.mcp + u) : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int u = u0 + 32 * h + lane;
+        if (u < Mr) xq[G::ix(u)] = v[h];
+      }
+    }
+  }
+  f2_fwd<P>(x, tw, nk);
+  if (a.Bout) {
+    for (int q = warp; q < nk; q += F2_WARPS)
+      for (int u = lane; u < Mr; u += 32) {
+        const float2 v = x[q * S + G::pos(u)];
+        a.Bout[(int64_t)(k0 + q) * Mr + u] = make_float2(v.x * a.scale, -v.y * a.scale);
+      }
+    return;
+  }
+  for (int q = warp; q < nk; q += F2_WARPS) {
+    const float2 *Bk = a.Bc + (int64_t)(k0 + q) * Mr;
+    for (int u = lane; u < Mr; u += 32) {
+      float2 *c = x + q * S + G::pos(u);
+      *c = cmul(*c, __ldg(Bk + u));
+    }
+  }
+  f2_inv<P>(x, tw, nk);
+  float2 *Pf = a.P + f * a.W * a.Kc + k0;
+  for (int e = threadIdx.x; e < a.W * nk; e += blockDim.x) {
+    const int si = e / nk, q = e - si * nk;
+    int u = si - a.hw;
+    u += u < 0 ? Mr : 0;
+    Pf[(int64_t)si * a.Kc + q] = x[q * S + G::ix(u)];
+  }
+}
+
+struct F2ScoreArgs {
+  const float2 *P;          // [B][W][Kc]
+  const float2 *tw;         // [Mc]
+  int mc, nc, hw, W, Kc;
+  int per;                  // lag-row pairs per block (<= NF)
+  const u64 *E;             // [B][esz] energy partials (k_fft2_rows)
+  u64 *Ew;                  // the same, written: the pick re-zeroes the accumulated slots
+  const u64 *gb;            // [W*W] template energies
+  double scale;             // 16^L
+  double eps_rel;           // C u log2(Mr Mc)
+  const uint16_t *frames;   // level-0 frames (exact rescoring through block sums)
+  int64_t fstride;
+  int pitch;
+  int L;                    // block-sum levels from `frames` to the coarse level (0 or 1)
+  const uint16_t *tpl;      // coarse template
+  int tpitch;
+  float *lb;                // [B][W*W]
+  int *ub;                  // [B] float bits, FFT_UB_INIT between calls
+  int *cnt;                 // [B] finished blocks, 0 between calls
+  int32_t *shift_out;       // [B][2]
+  double *f_out;            // [B] or null (levels = 0: f_min is the coarse f)
+  uint8_t *flags;           // [B] or null
+  int *qcount;              // [B] or null
+  float *h_out;             // [B][W*W] or null (diagnostics)
+  int *qn;                  // [B] candidates left for k_fft2_rescore (0: resolved; -1: all lags)
+  int *ql;                  // [B][FFT_QCAP] their lags
+  u64 *nacc;                // [B][max(FFT_QCAP, W*W)] exact N partial sums, zero between calls
+  int *cnt2;                // [B] finished k_fft2_rescore blocks, 0 between calls
+  int rparts;               // k_fft2_rescore blocks per frame
+};
+
+// coarse value (2^L x 2^L block sum) at coarse column jj of the coarse row whose first raw
+// row is ar: D raw rows, D adjacent samples each (4- / 8-byte aligned loads)
+template <int L>
+__device__ __forceinline__ uint32_t f2_coarse_at(const uint16_t *ar, int pitch, int jj) {
+  if constexpr (L == 0) {
+    return __ldg(ar + jj);
+  } else if constexpr (L == 1) {
+    const uint32_t u0 = __ldg(reinterpret_cast<const uint32_t *>(ar + 2 * jj));
+    const uint32_t u1 = __ldg(reinterpret_cast<const uint32_t *>(ar + pitch + 2 * jj));
+    return (u0 & 0xffffu) + (u0 >> 16) + (u1 & 0xffffu) + (u1 >> 16);
+  } else {
+    uint32_t v = 0;
+#pragma unroll
+    for (int dy = 0; dy < 4; ++dy) {
+      const uint2 u = __ldg(reinterpret_cast<const uint2 *>(ar + (int64_t)dy * pitch + 4 * jj));
+      v += (u.x & 0xffffu) + (u.x >> 16) + (u.y & 0xffffu) + (u.y >> 16);
+    }
+    return v;
+  }
+}
+
+// partial exact N(s,t) = sum over the coarse rows [r0, r1) of D_{s,t} of
+// (a_c[i+s][j+t] - b_c[i][j])^2, a_c the 2^L x 2^L block sums of the level-0 frame,
+// in 64-bit integers; all threads of the block; result to thread 0.  Warps over rows (four
+// in flight), lanes over columns.
+template <int L>
+__device__ u64 f2_exact_N(const F2ScoreArgs &a, int64_t f, int s, int t, int r0, int r1, u64 *red) {
+  constexpr int D = 1 << L;
+  const int mc = a.mc, nc = a.nc;
+  const int i0 = max(r0, max(0, -s)), i1 = min(r1, mc - max(0, s)), j0 = max(0, -t), j1 = nc - max(0, t);
+  const uint16_t *Fr = a.frames + f * a.fstride;
+  const int nw = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  u64 acc = 0;
+  for (int i = i0 + 4 * wid; i < i1; i += 4 * nw) {
+    for (int j = j0 + lane; j < j1; j += 32) {
+      uint32_t av[4], bv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int ii = min(i + q, i1 - 1);
+        av[q] = f2_coarse_at<L>(Fr + (int64_t)(D * (ii + s)) * a.pitch, a.pitch, j + t);
+        bv[q] = __ldg(a.tpl + (int64_t)ii * a.tpitch + j);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int d = (int)av[q] - (int)bv[q];
+        if (i + q < i1) acc += (u64)((uint32_t)(d * d));   // |d| < 2^16
+      }
+    }
+  }
+  acc = warp_sum(acc);
+  __syncthreads();
+  if (lane == 0) red[wid] = acc;
+  __syncthreads();
+  u64 tot = 0;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < nw; ++k) tot += red[k];
+  return tot;
+}
+
+template <int P>
+__global__ void __launch_bounds__(F2_THREADS) k_fft2_score(F2ScoreArgs a) {
+  using G = F2<P>;
+  constexpr int Mc = G::N, S = G::STRIDE;
+  extern __shared__ __align__(128) unsigned char f2sm[];
+  const int W = a.W, hw = a.hw;
+  float2 *tw = reinterpret_cast<float2 *>(f2sm);
+  float2 *x = tw + Mc;
+  u64 *RX = reinterpret_cast<u64 *>(x + G::NF * S);   // [W] excluded-row energy per s
+  u64 *CX = RX + W;                                   // [W] excluded-column energy per t
+  u64 *CP = CX + W;                                   // [2 NF][2][hw] corner sums per block row
+  double *rinv = reinterpret_cast<double *>(CP + 2 * G::NF * 2 * hw);   // [W]
+  double *cinv = rinv + W;                                               // [W]
+  __shared__ float redf[32];
+  __shared__ int qn, qlist[FFT_QCAP], last;
+  const int npairs = (W + 1) / 2, npb = (npairs + a.per - 1) / a.per;
+  const int64_t f = blockIdx.x / npb;
+  const int p0 = (blockIdx.x - (int)(f * npb)) * a.per;
+  const int np = min(a.per, npairs - p0), s0 = 2 * p0, nr = min(2 * np, W - s0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const u64 *E = a.E + f * f2_esz(hw);
+  for (int k = threadIdx.x; k < Mc; k += blockDim.x) tw[k] = a.tw[k];
+  // packed lag rows, Hermitian extension of each half spectrum: x = row s1 + i row s2, in
+  // k1-major order for the inverse transform; a warp per pair
+  const float2 *Pf = a.P + (f * W + s0) * a.Kc;
+  for (int q = warp; q < np; q += F2_WARPS) {
+    const bool two = 2 * q + 1 < nr;
+    const float2 *P1 = Pf + (int64_t)(2 * q) * a.Kc, *P2 = P1 + a.Kc;
+    for (int k = lane; k < Mc; k += 32) {
+      const bool lo = k < a.Kc;
+      const int kk = lo ? k : Mc - k;
+      float2 v1 = __ldcg(P1 + kk);
+      float2 v2 = two ? __ldcg(P2 + kk) : make_float2(0.f, 0.f);
+      if (!lo) { v1.y = -v1.y; v2.y = -v2.y; }
+      x[q * S + G::pos(k)] = make_float2(v1.x - v2.y, v1.y + v2.x);
+    }
+  }
+  // energies: the excluded strips by warp scans of the edge row / column sums
+  if (warp < 4) {   // 0 top rows, 1 bottom rows, 2 left cols, 3 right cols
+    u64 *o = warp < 2 ? RX : CX;
+    const u64 *src = E + 1 + warp * hw;
+    if ((warp & 1) && lane == 0) o[hw] = 0;
+    u64 carry = 0;
+    for (int d0 = 0; d0 < hw; d0 += 32) {
+      const int d = d0 + lane;
+      const u64 sc = warp_scan_incl(d < hw ? src[d] : 0) + carry;
+      if (d < hw) o[(warp & 1) ? hw - d - 1 : hw + d + 1] = sc;   // s > 0 excludes the top rows
+      carry = __shfl_sync(0xffffffffu, sc, 31);
+    }
+  }
+  // corner sums CP[row][t<0][|t|-1] = sum_{i<|s|} (row prefix of corner row i at |t|): one
+  // thread per (sign of s, sign of t, |t|), running once over the excluded rows
+  for (int task = threadIdx.x; task < 4 * hw; task += blockDim.x) {
+    const int g = task / (2 * hw), r2 = task - g * 2 * hw, tneg = r2 / hw, aa = r2 - tneg * hw;
+    // rows of this block with s > 0 (g = 0) or s < 0 (g = 1): the largest |s| among them
+    const int smax = g == 0 ? s0 + nr - 1 - hw : hw - s0;
+    const u64 *rp = E + 1 + 4 * hw + (int64_t)((g ? 2 : 0) + tneg) * hw * hw + aa;
+    u64 acc = 0;
+#pragma unroll 4
+    for (int i = 0; i < smax; ++i) {
+      acc += __ldg(rp + (int64_t)i * hw);
+      const int rl = (g == 0 ? hw + i + 1 : hw - i - 1) - s0;
+      if (rl >= 0 && rl < nr) CP[(rl * 2 + tneg) * hw + aa] = acc;
+    }
+  }
+  for (int k = threadIdx.x; k < W; k += blockDim.x) {
+    rinv[k] = 1.0 / (a.scale * (double)(a.mc - abs(k - hw)));
+    cinv[k] = 1.0 / (double)(a.nc - abs(k - hw));
+  }
+  f2_inv<P>(x, tw, np);
+  const u64 tot = E[0];
+  const double eps2 = 2.0 * a.eps_rel * sqrt((double)tot) * sqrt((double)a.gb[hw * W + hw]);
+  float best = 3.0e38f;
+  float *lbf = a.lb + f * W * W;
+  for (int rl = warp; rl < nr; rl += F2_WARPS) {
+    const int si = s0 + rl, s = si - hw;
+    const float *xr = reinterpret_cast<const float *>(x + (rl >> 1) * S) + (rl & 1);
+    const double ri = rinv[si];
+    const u64 rx = RX[si];
+    for (int ti = lane; ti < W; ti += 32) {
+      const int t = ti - hw;
+      const int tt = t < 0 ? t + Mc : t;
+      const float h = xr[2 * G::ix(tt)];
+      const int lag = si * W + ti;
+      if (a.h_out) a.h_out[f * W * W + lag] = h;
+      u64 ga = tot - rx - CX[ti];
+      if (s != 0 && t != 0) ga += CP[(rl * 2 + (t < 0)) * hw + abs(t) - 1];
+      const double inv = ri * cinv[ti];
+      const double fa = ((double)ga + (double)a.gb[lag] - 2.0 * (double)h) * inv;
+      const double del = eps2 * inv;
+      best = fminf(best, (float)(fa + del) * (1.0f + 1e-6f));
+      lbf[lag] = (float)(fa - del) * (1.0f - 1e-6f);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) best = fminf(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if (lane == 0) redf[warp] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float b = 3.0e38f;
+    for (int k = 0; k < F2_WARPS; ++k) b = fminf(b, redf[k]);
+    atomicMin(a.ub + f, __float_as_int(fmaxf(b, 0.f)));
+    __threadfence();
+    last = atomicAdd(a.cnt + f, 1) == npb - 1;
+    qn = 0;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // the last block of the frame: candidate set Q = {lag : f~ - delta <= min(f~ + delta)}
+  const float thr = __int_as_float(atomicAdd(a.ub + f, 0));
+  for (int lag = threadIdx.x; lag < W * W; lag += blockDim.x) {
+    if (__ldcg(lbf + lag) <= thr) {
+      const int q = atomicAdd(&qn, 1);
+      if (q < FFT_QCAP) qlist[q] = lag;
+    }
+  }
+  __syncthreads();
+  const int nq = qn;
+  const bool all = nq > FFT_QCAP;
+  if (threadIdx.x == 0) {
+    if (nq == 1 && !a.f_out) {   // the one candidate is the exact argmin
+      const int s = qlist[0] / W - hw, t = qlist[0] % W - hw;
+      a.shift_out[2 * f] = s;
+      a.shift_out[2 * f + 1] = t;
+      if (a.flags) a.flags[f] = (uint8_t)((abs(s) == hw || abs(t) == hw) ? 1 : 0);
+      a.qn[f] = 0;
+    } else {
+      a.qn[f] = all ? -1 : nq;   // exact rescoring by k_fft2_rescore
+    }
+    if (a.qcount) a.qcount[f] = nq;
+    a.ub[f] = FFT_UB_INIT;
+    a.cnt[f] = 0;
+  }
+  if (!(nq == 1 && !a.f_out) && !all)
+    for (int k = threadIdx.x; k < nq; k += blockDim.x) a.ql[f * FFT_QCAP + k] = qlist[k];
+  // re-zero the accumulated energy slots (total, edge columns) for the next call
+  u64 *Ew = a.Ew + f * f2_esz(hw);
+  if (threadIdx.x == 0) Ew[0] = 0;
+  for (int k = threadIdx.x; k < 2 * hw; k += blockDim.x) Ew[1 + 2 * hw + k] = 0;
+}
+
+// Exact rescoring of the certified candidates (S4): blocks (frame, row part); frames whose
+// candidate set k_fft2_score resolved exit at once.  Partial N of every candidate over the
+// part's coarse rows -> 64-bit atomics; the last part of a frame takes the argmin of the
+// key (f, s, t) over the exact values and writes the outputs.
+template <int L>
+__global__ void __launch_bounds__(256) k_fft2_rescore(F2ScoreArgs a) {
+  __shared__ u64 red[32];
+  __shared__ int last;
+  const int64_t f = blockIdx.x / a.rparts;
+  const int part = blockIdx.x - (int)(f * a.rparts);
+  const int qn = a.qn[f];
+  if (qn == 0) return;
+  const int W = a.W, hw = a.hw;
+  const bool all = qn < 0;
+  const int ncand = all ? W * W : qn;
+  const int rows = (a.mc + a.rparts - 1) / a.rparts, r0 = part * rows, r1 = min(a.mc, r0 + rows);
+  u64 *acc = a.nacc + f * (int64_t)max(FFT_QCAP, W * W);
+  for (int c = 0; c < ncand; ++c) {
+    const int lag = all ? c : a.ql[f * FFT_QCAP + c];
+    const u64 part_n = f2_exact_N<L>(a, f, lag / W - hw, lag % W - hw, r0, r1, red);
+    if (threadIdx.x == 0 && part_n) atomicAdd(acc + c, part_n);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(a.cnt2 + f, 1) == a.rparts - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  Key bk{~0ull, ~0u};
+  for (int c = threadIdx.x; c < ncand; c += blockDim.x) {
+    const int lag = all ? c : a.ql[f * FFT_QCAP + c];
+    const int s = lag / W - hw, t = lag % W - hw;
+    const u64 N = atomicExch(acc + c, 0ull);   // read and re-zero
+    const double area = (double)((a.mc - abs(s)) * (a.nc - abs(t)));
+    const Key kk{(u64)__double_as_longlong((double)N / (a.scale * area)), (unsigned)lag};
+    if (key_less(kk, bk)) bk = kk;
+  }
+  __shared__ Key kred[32];
+  bk = block_min_key(bk, kred);
+  if (threadIdx.x == 0) {
+    const int s = (int)(bk.idx / W) - hw, t = (int)(bk.idx % W) - hw;
+    a.shift_out[2 * f] = s;
+    a.shift_out[2 * f + 1] = t;
+    if (a.f_out) a.f_out[f] = __longlong_as_double((long long)bk.f);
+    if (a.flags) a.flags[f] = (uint8_t)(((abs(s) == hw || abs(t) == hw) ? 1 : 0) | (all ? 2 : 0));
+    a.qn[f] = 0;
+    a.cnt2[f] = 0;
+  }
+}
+
+}  // namespace moco

@@ -22,6 +22,7 @@
 #include "kernels_refine.cuh"
 #include "kernels_rtc.cuh"
 #include "kernels_fft.cuh"
+#include "kernels_fft2.cuh"
 #include "kernels_fra.cuh"
 
 using namespace moco;
@@ -80,6 +81,7 @@ struct moco_plan {
                            // DESIGN.md section 11) instead of the tensor-core refine + pick
     int fra_min = 64;      // MOCO_FRA_MIN: smallest batch for k_refine_frame
     bool nofuse_ds = false, ga_inpick = false, nopipe = false;
+    bool fft_v1 = false;   // MOCO_FFT_V1=1: the generic FFT kernels (kernels_fft.cuh) for every length
   } knob;
   bool simple_refine;         // MOCO_REFINE=simple: unfused K6/K7 (cross-check in tests)
   int simple_level;           // MOCO_REFINE=simpleN: simple K6 at level N only (debug)
@@ -105,6 +107,18 @@ struct moco_plan {
     double eps_rel = 0;
     int smem_rows = 0, smem_cols = 0, smem_score = 0, smem_energy = 0;
     int pc = 0, pr = 0;         // register FFT plans of the row (Mc) and column (Mr) lengths
+    // kernels_fft2.cuh (both lengths with a register plan, n_c % 8 == 0): the frame-to-
+    // spectrum row kernel reads the level-0 frames itself (no downsample, no g_a kernel)
+    bool v2 = false;
+    u64 *E = nullptr;           // energy partials [cap][f2_esz(hw)], accumulated slots kept zero
+    int *cnt = nullptr;         // finished score blocks per frame [cap], kept zero
+    int *qn = nullptr, *ql = nullptr, *cnt2 = nullptr;   // k_fft2_rescore hand-over [cap], kept zero
+    u64 *nacc = nullptr;        // its exact N partial sums [cap][max(QCAP, W^2)], kept zero
+    int smem2_rows = 0, smem2_cols = 0, smem2_score = 0;
+    // sub-batches alternate between two streams and two scratch sets (S, P, E, lb, ub, cnt
+    // hold 2 x cap frames): one sub-batch's kernel tails overlap the other's work
+    cudaStream_t ss[2] = {nullptr, nullptr};
+    cudaEvent_t ev_j[2] = {nullptr, nullptr};
   } fft;
   // two-stream batch pipeline (align_tc_pipelined)
   bool pipe_ready;
@@ -304,6 +318,16 @@ static void plan_free(moco_plan *p) {
   if (p->racc2) cudaFree(p->racc2);
   for (int k = 0; k < 2; ++k)
     if (p->gbin[k]) cudaFree(p->gbin[k]);
+  for (int k = 0; k < 2; ++k) {
+    if (p->fft.ss[k]) cudaStreamDestroy(p->fft.ss[k]);
+    if (p->fft.ev_j[k]) cudaEventDestroy(p->fft.ev_j[k]);
+  }
+  if (p->fft.E) cudaFree(p->fft.E);
+  if (p->fft.cnt) cudaFree(p->fft.cnt);
+  if (p->fft.qn) cudaFree(p->fft.qn);
+  if (p->fft.ql) cudaFree(p->fft.ql);
+  if (p->fft.cnt2) cudaFree(p->fft.cnt2);
+  if (p->fft.nacc) cudaFree(p->fft.nacc);
   for (auto &r : p->prof_live) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : p->prof_pool) cudaEventDestroy(e);
   delete p;
@@ -330,6 +354,14 @@ static bool fft_supported(const moco_plan *p) {
   return fft_len_make(p->ml[L] + p->w - 1, &a) && fft_len_make(p->nl[L] + p->w - 1, &b);
 }
 
+// row pairs per k_fft2_rows block: at most NF transforms and F2_STAGE_MAX staged raw bytes
+static int fft2_rows_per_max(int NF, int L, int nc) {
+  return std::max(1, std::min(NF, F2_STAGE_MAX / f2_stage_bytes(1, L, nc)));
+}
+static int fft2_rows_smem(int P_N, int NF, int STRIDE, int per, int L, int nc, int hw) {
+  return f2_stage_bytes(per, L, nc) + (P_N + NF * STRIDE) * 8 + 2 * NF * 8 + 2 * hw * 8;
+}
+
 static int fft_init(moco_plan *p) {
   auto &F = p->fft;
   if (F.ready) return MOCO_OK;
@@ -339,22 +371,47 @@ static int fft_init(moco_plan *p) {
   if (!fft_len_make(g.mc + g.hw, &g.Lr) || !fft_len_make(g.nc + g.hw, &g.Lc)) return MOCO_EINVAL;
   g.Kc = g.Lc.N / 2 + 1;
   g.mcp = (g.mc + 1) / 2 * 2;
+  F.pc = fft_plan_of(g.Lc.N);
+  F.pr = fft_plan_of(g.Lr.N);
+  F.v2 = F.pc > 0 && F.pr > 0 && g.nc % 8 == 0 && !p->knob.fft_v1;
+  const size_t esz = (size_t)f2_esz(g.hw) * 8;
   // sub-batches sized so the spectra stay in L2 (about 80 MB)
-  const size_t per = (size_t)g.Kc * g.mcp * 8 + (size_t)g.W * g.Kc * 8 + (size_t)g.W * g.W * 8;
-  F.cap = std::max<int64_t>(1, std::min<int64_t>(p->cap, (int64_t)((80u << 20) / per)));
+  const size_t per = F.v2 ? (size_t)g.Kc * g.mcp * 8 + (size_t)g.W * g.Kc * 8 + (size_t)g.W * g.W * 4 + esz
+                          : (size_t)g.Kc * g.mcp * 8 + (size_t)g.W * g.Kc * 8 + (size_t)g.W * g.W * 8;
+  F.cap = std::max<int64_t>(1, std::min<int64_t>(p->cap, (int64_t)(((F.v2 ? 40u : 80u) << 20) / per)));
+  const int64_t nset = F.v2 ? 2 : 1;   // v2: two scratch sets (two streams)
   const int Mr = g.Lr.N, Mc = g.Lc.N;
   auto al = [&](void **q, size_t bytes) {
     if (cudaMalloc(q, bytes) != cudaSuccess) { cudaGetLastError(); return false; }
     return true;
   };
   if (!al((void **)&F.twr, Mr * 8) || !al((void **)&F.twc, Mc * 8) || !al((void **)&F.Bc, (size_t)g.Kc * Mr * 8) ||
-      !al((void **)&F.S, (size_t)F.cap * g.Kc * g.mcp * 8) || !al((void **)&F.P, (size_t)F.cap * g.W * g.Kc * 8) ||
+      !al((void **)&F.S, (size_t)nset * F.cap * g.Kc * g.mcp * 8) ||
+      !al((void **)&F.P, (size_t)nset * F.cap * g.W * g.Kc * 8) ||
       !al((void **)&F.ga, (size_t)F.cap * g.W * g.W * 8) || !al((void **)&F.qc, (size_t)p->cap * sizeof(int)) ||
-      !al((void **)&F.lb, (size_t)F.cap * g.W * g.W * 4) || !al((void **)&F.ub, (size_t)F.cap * sizeof(int)) ||
+      !al((void **)&F.lb, (size_t)nset * F.cap * g.W * g.W * 4) ||
+      !al((void **)&F.ub, (size_t)nset * F.cap * sizeof(int)) ||
       !al((void **)&F.epart, (size_t)F.cap * (4 * g.hw + 1) * 8))
     return MOCO_ENOMEM;
   CK(cudaMemset(F.epart, 0, (size_t)F.cap * (4 * g.hw + 1) * 8));
-  CK(cudaMemset(F.ub, 0x7f, (size_t)F.cap * sizeof(int)));   // FFT_UB_INIT
+  if (F.v2) {
+    if (!al((void **)&F.E, (size_t)2 * F.cap * esz) || !al((void **)&F.cnt, (size_t)2 * F.cap * sizeof(int)))
+      return MOCO_ENOMEM;
+    CK(cudaMemset(F.E, 0, (size_t)2 * F.cap * esz));
+    CK(cudaMemset(F.cnt, 0, (size_t)2 * F.cap * sizeof(int)));
+    const size_t nslots = (size_t)std::max(FFT_QCAP, g.W * g.W);
+    if (!al((void **)&F.qn, (size_t)2 * F.cap * sizeof(int)) || !al((void **)&F.cnt2, (size_t)2 * F.cap * sizeof(int)) ||
+        !al((void **)&F.ql, (size_t)2 * F.cap * FFT_QCAP * sizeof(int)) || !al((void **)&F.nacc, (size_t)2 * F.cap * nslots * 8))
+      return MOCO_ENOMEM;
+    CK(cudaMemset(F.qn, 0, (size_t)2 * F.cap * sizeof(int)));
+    CK(cudaMemset(F.cnt2, 0, (size_t)2 * F.cap * sizeof(int)));
+    CK(cudaMemset(F.nacc, 0, (size_t)2 * F.cap * nslots * 8));
+    for (int k = 0; k < 2; ++k) {
+      CK(cudaStreamCreateWithFlags(&F.ss[k], cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&F.ev_j[k], cudaEventDisableTiming));
+    }
+  }
+  CK(cudaMemset(F.ub, 0x7f, (size_t)nset * F.cap * sizeof(int)));   // FFT_UB_INIT
   CK(cudaStreamCreateWithFlags(&F.side, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&F.ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&F.ev_join, cudaEventDisableTiming));
@@ -366,9 +423,34 @@ static int fft_init(moco_plan *p) {
   F.smem_score = (Mc + FFT_ROWS_PAIRS * Mc + FFT_ROWS_PAIRS * (Mc + FFT_YPAD)) * 8 + ((g.W * g.W + 1) & ~1) * 4 + 2 * g.W * 8;
   F.smem_energy = (4 * g.hw + g.w * g.w + 1) * 8;
   if (F.smem_score > 227 * 1024 || F.smem_energy > 227 * 1024) return MOCO_EINVAL;
-  F.pc = fft_plan_of(Mc);
-  F.pr = fft_plan_of(Mr);
   int rc_attr = MOCO_OK;
+  if (F.v2) {
+    fft_dispatch(F.pc, [&](auto PC) {
+      constexpr int P = decltype(PC)::value;
+      if constexpr (P > 0) {
+        using G = F2<P>;
+        const int LK = std::min(L, 1);
+        const int stg = std::max(f2_stage_bytes(fft2_rows_per_max(G::NF, LK, g.nc), LK, g.nc),
+                                 f2_stage_bytes(fft2_rows_per_max(G::NF, 0, g.nc), 0, g.nc));
+        F.smem2_rows = stg + (G::N + G::NF * G::STRIDE) * 8 + 2 * G::NF * 8 + 2 * g.hw * 8;
+        F.smem2_score = (G::N + G::NF * G::STRIDE) * 8 + 2 * g.W * 8 + 2 * G::NF * 2 * g.hw * 8 + 2 * g.W * 8;
+        if (smem_attr(k_fft2_rows<P, 0>, F.smem2_rows) != cudaSuccess ||
+            smem_attr(k_fft2_rows<P, 1>, F.smem2_rows) != cudaSuccess ||
+            smem_attr(k_fft2_score<P>, F.smem2_score) != cudaSuccess)
+          rc_attr = set_cuda_err(cudaGetLastError(), "fft2 kernel attributes");
+      }
+    });
+    fft_dispatch(F.pr, [&](auto PR) {
+      constexpr int P = decltype(PR)::value;
+      if constexpr (P > 0) {
+        using G = F2<P>;
+        F.smem2_cols = (G::N + G::NF * G::STRIDE) * 8;
+        if (smem_attr(k_fft2_cols<P>, F.smem2_cols) != cudaSuccess)
+          rc_attr = set_cuda_err(cudaGetLastError(), "fft2 kernel attributes");
+      }
+    });
+    if (F.smem2_score > 227 * 1024) return MOCO_EINVAL;
+  }
   fft_dispatch(F.pc, [&](auto PC) {
     constexpr int P = decltype(PC)::value;
     if (smem_attr(k_fft_rows<P>, F.smem_rows) != cudaSuccess || smem_attr(k_fft_score_rows<P>, F.smem_rows) != cudaSuccess ||
@@ -389,9 +471,162 @@ static int fft_init(moco_plan *p) {
   return MOCO_OK;
 }
 
+// ---- kernels_fft2.cuh launches (F.v2)
+static F2RowsArgs fft2_rows_args(const moco_plan *p, const void *img, int64_t fstride, int pitch, int per, int set) {
+  const auto &F = p->fft;
+  const FftGeom &g = F.g;
+  F2RowsArgs a{};
+  a.frames = (const uint16_t *)img; a.fstride = fstride; a.pitch = pitch;
+  a.mc = g.mc; a.nc = g.nc; a.hw = g.hw; a.Kc = g.Kc; a.mcp = g.mcp;
+  a.per = per; a.tw = F.twc; a.S = F.S + (int64_t)set * F.cap * g.Kc * g.mcp;
+  a.E = nullptr;
+  return a;
+}
+template <int PC>
+static void fft2_rows_launch(const F2RowsArgs &a, int L, int64_t nblk, int hw, cudaStream_t st) {
+  using G = F2<PC>;
+  const int smem = fft2_rows_smem(G::N, G::NF, G::STRIDE, a.per, L, a.nc, hw);
+  if (L == 0) k_fft2_rows<PC, 0><<<(unsigned)nblk, F2_THREADS, smem, st>>>(a);
+  else k_fft2_rows<PC, 1><<<(unsigned)nblk, F2_THREADS, smem, st>>>(a);
+}
+
+static int fft2_set_template(moco_plan *p, cudaStream_t st) {
+  auto &F = p->fft;
+  const int L = p->levels;
+  const FftGeom &g = F.g;
+  fft_dispatch(F.pc, [&](auto PC) {
+    constexpr int P = decltype(PC)::value;
+    if constexpr (P > 0) {
+      const int per = fft2_rows_per_max(F2<P>::NF, 0, g.nc);
+      F2RowsArgs a = fft2_rows_args(p, p->tpl[L], 0, p->pitch[L], per, 0);
+      fft2_rows_launch<P>(a, 0, (g.mcp / 2 + per - 1) / per, g.hw, st);
+    }
+  });
+  fft_dispatch(F.pr, [&](auto PR) {
+    constexpr int P = decltype(PR)::value;
+    if constexpr (P > 0) {
+      F2ColsArgs c{};
+      c.S = F.S; c.mc = g.mc; c.Kc = g.Kc; c.mcp = g.mcp; c.W = g.W; c.hw = g.hw;
+      c.per = F2<P>::NF; c.tw = F.twr; c.Bc = nullptr; c.P = nullptr; c.Bout = F.Bc;
+      c.scale = 1.0f / ((float)g.Lr.N * (float)g.Lc.N);
+      k_fft2_cols<P><<<(unsigned)((g.Kc + c.per - 1) / c.per), F2_THREADS, F.smem2_cols, st>>>(c);
+    }
+  });
+  CKL("fft2_set_template");
+  F.tpl_ready = true;
+  return MOCO_OK;
+}
+
+// One sub-batch of nb level-0 frames through the three kernels of kernels_fft2.cuh, with
+// scratch set `set`, on stream st.
+// fr: the sub-batch's level-0 frames (levels <= 1) or level-1 images (levels = 2, LK = 1)
+static int fft2_sub(moco_plan *p, const char *fr, int64_t fstride, int pitch, int64_t nb, int set,
+                    int32_t *shift_out, double *f_out, uint8_t *flags, float *h_out, int *qcount,
+                    cudaStream_t st) {
+  auto &F = p->fft;
+  const FftGeom &g = F.g;
+  const int L = p->levels, LK = std::min(L, 1);
+  const int64_t so = (int64_t)set * F.cap;
+  float2 *Pset = F.P + so * g.W * g.Kc;
+  fft_dispatch(F.pc, [&](auto PC) {
+    constexpr int P = decltype(PC)::value;
+    if constexpr (P > 0) {
+      // transforms per block: as many as fit, fewer when the batch cannot fill the SMs
+      const int npair = g.mcp / 2;
+      const int per = (int)std::max<int64_t>(1, std::min<int64_t>(fft2_rows_per_max(F2<P>::NF, LK, g.nc),
+                                                                  nb * npair / p->nsm));
+      F2RowsArgs a = fft2_rows_args(p, fr, fstride, pitch, per, set);
+      a.E = F.E + so * f2_esz(g.hw);
+      ProfScope ps(p, MOCO_K_PREP, st);
+      fft2_rows_launch<P>(a, LK, nb * ((npair + per - 1) / per), g.hw, st);
+    }
+  });
+  CKL("k_fft2_rows");
+  fft_dispatch(F.pr, [&](auto PR) {
+    constexpr int P = decltype(PR)::value;
+    if constexpr (P > 0) {
+      constexpr int NF = F2<P>::NF;
+      // even split of the Kc bins over the fewest blocks of <= NF
+      int per = (int)std::max<int64_t>(1, std::min<int64_t>(NF, nb * g.Kc / p->nsm));
+      const int nblk = (g.Kc + per - 1) / per;
+      per = (g.Kc + nblk - 1) / nblk;
+      F2ColsArgs c{};
+      c.S = F.S + so * g.Kc * g.mcp; c.mc = g.mc; c.Kc = g.Kc; c.mcp = g.mcp; c.W = g.W; c.hw = g.hw;
+      c.per = per; c.tw = F.twr; c.Bc = F.Bc; c.P = Pset; c.Bout = nullptr; c.scale = 0.f;
+      ProfScope ps(p, MOCO_K_COARSE, st);
+      k_fft2_cols<P><<<(unsigned)(nb * nblk), F2_THREADS, F.smem2_cols, st>>>(c);
+    }
+  });
+  CKL("k_fft2_cols");
+  fft_dispatch(F.pc, [&](auto PC) {
+    constexpr int P = decltype(PC)::value;
+    if constexpr (P > 0) {
+      constexpr int NF = F2<P>::NF;
+      const int npairs = (g.W + 1) / 2;
+      // several blocks per SM: the per-block energy set-up is small, the transforms few
+      int per = (int)std::max<int64_t>(1, std::min<int64_t>(NF, nb * npairs / (4 * p->nsm)));
+      const int nblk = (npairs + per - 1) / per;
+      per = (npairs + nblk - 1) / nblk;
+      F2ScoreArgs a{};
+      a.P = Pset; a.tw = F.twc; a.mc = g.mc; a.nc = g.nc; a.hw = g.hw; a.W = g.W; a.Kc = g.Kc;
+      a.per = per; a.E = F.E + so * f2_esz(g.hw); a.Ew = F.E + so * f2_esz(g.hw); a.gb = (const u64 *)p->gb;
+      a.scale = (double)(1u << (4 * L)); a.eps_rel = F.eps_rel;
+      a.frames = (const uint16_t *)fr; a.fstride = fstride; a.pitch = pitch; a.L = LK;
+      a.tpl = (const uint16_t *)p->tpl[L]; a.tpitch = p->pitch[L];
+      a.lb = F.lb + so * g.W * g.W; a.ub = F.ub + so; a.cnt = F.cnt + so;
+      a.shift_out = shift_out; a.f_out = f_out; a.flags = flags; a.qcount = qcount; a.h_out = h_out;
+      a.qn = F.qn + so; a.ql = F.ql + so * FFT_QCAP; a.cnt2 = F.cnt2 + so;
+      a.nacc = F.nacc + so * (int64_t)std::max(FFT_QCAP, g.W * g.W);
+      a.rparts = std::max(1, std::min(16, g.mc / 16));
+      ProfScope ps(p, MOCO_K_SCORE, st);
+      k_fft2_score<P><<<(unsigned)(nb * nblk), F2_THREADS, F.smem2_score, st>>>(a);
+      const unsigned rg = (unsigned)(nb * a.rparts);
+      if (LK == 0) k_fft2_rescore<0><<<rg, 256, 0, st>>>(a);
+      else k_fft2_rescore<1><<<rg, 256, 0, st>>>(a);
+    }
+  });
+  CKL("k_fft2_score");
+  p->launches += 4;
+  return MOCO_OK;
+}
+
+// S1-S4 by FFT for B level-0 frames (kernels_fft2.cuh): rows (block sums, energies, row
+// FFTs), columns (times the template spectrum), score + certified pick, per sub-batch of
+// <= F.cap frames; several sub-batches alternate between two streams (fork/join with the
+// caller's stream, graph-capturable).  img1: levels = 2, the level-1 images out.
+static int launch_fft2(moco_plan *p, const void *frames, int64_t fstride, int pitch, int64_t B, int32_t *shift_out,
+                       double *f_out, uint8_t *flags, cudaStream_t st, float *h_out = nullptr,
+                       int *qcount = nullptr) {
+  auto &F = p->fft;
+  const FftGeom &g = F.g;
+  const int64_t nsub = (B + F.cap - 1) / F.cap;
+  const bool two = nsub > 1;
+  if (two) {
+    CK(cudaEventRecord(F.ev_fork, st));
+    for (int k = 0; k < 2; ++k) CK(cudaStreamWaitEvent(F.ss[k], F.ev_fork, 0));
+  }
+  for (int64_t k = 0; k < nsub; ++k) {
+    const int64_t b0 = k * F.cap, nb = std::min<int64_t>(F.cap, B - b0);
+    const int set = two ? (int)(k & 1) : 0;
+    const int rc = fft2_sub(p, (const char *)frames + b0 * fstride * 2, fstride, pitch, nb, set, shift_out + 2 * b0,
+                            f_out ? f_out + b0 : nullptr, flags ? flags + b0 : nullptr,
+                            h_out ? h_out + b0 * g.W * g.W : nullptr, qcount ? qcount + b0 : nullptr,
+                            two ? F.ss[set] : st);
+    if (rc) return rc;
+  }
+  if (two) {
+    for (int k = 0; k < 2; ++k) {
+      CK(cudaEventRecord(F.ev_j[k], F.ss[k]));
+      CK(cudaStreamWaitEvent(st, F.ev_j[k], 0));
+    }
+  }
+  return MOCO_OK;
+}
+
 // template spectrum conj(B^)/(Mr Mc), column-major [k][u] (once per template)
 static int fft_set_template(moco_plan *p, cudaStream_t st) {
   auto &F = p->fft;
+  if (F.v2) return fft2_set_template(p, st);
   const int L = p->levels;
   const FftGeom &g = F.g;
   const int nrb = (g.mcp / 2 + FFT_ROWS_PAIRS - 1) / FFT_ROWS_PAIRS;
@@ -536,6 +771,7 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
     p->knob.nofuse_ds = getenv("MOCO_NOFUSE_DS") != nullptr;
     p->knob.ga_inpick = getenv("MOCO_GA_INPICK") != nullptr;
     p->knob.nopipe = getenv("MOCO_NOPIPE") != nullptr;
+    p->knob.fft_v1 = getenv("MOCO_FFT_V1") != nullptr;
     if (const char *v = getenv("MOCO_FRA")) p->knob.fra = atoi(v);
     if (const char *v = getenv("MOCO_FRA_MIN")) p->knob.fra_min = std::max(1, atoi(v));
   }
@@ -1174,6 +1410,19 @@ static int run_batch(moco_plan *p, const void *frames_b, int64_t B, int32_t *shi
     fstride[l] = (int64_t)p->ml[l] * p->pitch[l];
   }
   const bool tc = p->algo == MOCO_ALGO_TC;
+  // the FFT row kernel of kernels_fft2.cuh reads the level-0 frames (and writes level 1)
+  const bool fft2 = p->algo == MOCO_ALGO_FFT && p->fft.v2 && !grid_b && p->dtype == MOCO_U16;
+  if (fft2) {
+    // levels = 2: the level-1 images (the level-1 refine reads them) feed the FFT rows
+    if (L == 2) {
+      int rc = launch_downsample(p, 0, frames_b, fstride[0], p->scratch[1], B, st);
+      if (rc) return rc;
+    }
+    int rc = launch_fft2(p, img[L == 2 ? 1 : 0], fstride[L == 2 ? 1 : 0], p->pitch[L == 2 ? 1 : 0], B,
+                         L == 0 ? shifts_b : p->sh[L], L == 0 ? fmin_b : nullptr, flags_b, st);
+    if (rc) return rc;
+    return refine_levels(p, img, fstride, B, shifts_b, fmin_b, corr_b, st);
+  }
   // the tensor-core search block-sums the level-0 frames itself; only the levels the
   // refine steps read (1..L-1) are materialised
   const bool emit1 = tc && !grid_b && prep_emits_l1(p);   // level 1 written by the operand prep
@@ -1390,6 +1639,20 @@ int moco_fft_cross(moco_plan *p, const void *d_frames, int64_t T, float *d_h, in
     const void *img = stage_frames(p, (const char *)d_frames + f0 * fbytes, B, st, &rc);
     if (rc) return rc;
     int64_t fs = (int64_t)p->m * p->pitch[0];
+    if (p->fft.v2) {
+      int lin = 0;
+      if (L == 2) {
+        rc = launch_downsample(p, 0, img, fs, p->scratch[1], B, st);
+        if (rc) return rc;
+        img = p->scratch[1];
+        fs = (int64_t)p->ml[1] * p->pitch[1];
+        lin = 1;
+      }
+      rc = launch_fft2(p, img, fs, p->pitch[lin], B, d_shifts + 2 * f0, nullptr, nullptr, st, d_h + f0 * WW,
+                       d_qcount ? d_qcount + f0 : nullptr);
+      if (rc) return rc;
+      continue;
+    }
     for (int l = 0; l < L; ++l) {
       rc = launch_downsample(p, l, img, fs, p->scratch[l + 1], B, st);
       if (rc) return rc;

@@ -214,3 +214,51 @@ def test_fft_paper_default_window_w_over_64():
     sh, fm = _np(sh), _np(fm)
     for k in range(2):
         check_frame(st.frames[k].numpy(), st.template.numpy(), 85, 1, sh[k], fm[k], _np(co[k]))
+
+
+@pytest.mark.parametrize("c,T,extra", [(1, 300, {}), (2, 400, {}), (3, 300, {}), (4, 40, {}),
+                                       (2, 64, {"m": 512, "n": 512, "w": 85, "n_blobs": 400, "shift_bound": 150})])
+def test_fft_v2_equals_generic_fft(c, T, extra, monkeypatch):
+    """The register-plan FFT path (kernels_fft2.cuh: fused frame-to-spectrum rows, energy
+    partials, in-block certified pick) against the generic FFT kernels (kernels_fft.cuh,
+    MOCO_FFT_V1=1) and against the oracle on sampled frames: shifts, f_min, corrected
+    frames and edge flags identical (both are exact by certification)."""
+    spec = config_spec(c, T=T, **extra)
+    st = make_stack(spec, 0, T, device=DEV)
+    out = {}
+    for v1 in (False, True):
+        if v1:
+            monkeypatch.setenv("MOCO_FFT_V1", "1")
+        p = Plan(spec.m, spec.n, spec.w, spec.levels, "u16", 12, device=0, algo="fft")
+        p.set_template(st.template)
+        sh, fm, co, fl = p.align(st.frames, corrected=True, flags=True)
+        out[v1] = (sh, fm, co.view(torch.int16), fl & 1)
+        h, shc, q = p.fft_cross(st.frames[:4].contiguous())
+        out[(v1, "h")] = h
+        monkeypatch.delenv("MOCO_FFT_V1", raising=False)
+    for a, b in zip(out[False], out[True]):
+        assert torch.equal(a, b)
+    # the two fp32 cross terms differ only by rounding (different transform order)
+    scale = torch.clamp(out[(True, "h")].abs().amax(), min=1.0)
+    assert float((out[(False, "h")] - out[(True, "h")]).abs().amax() / scale) < 1e-5
+    sh, fm, co = _np(out[False][0]), _np(out[False][1]), _np(out[False][2].view(torch.uint16))
+    fr, tp = _np(st.frames), _np(st.template)
+    for k in ((0,) if spec.w > 64 else (0, T // 2, T - 1)):
+        check_frame(fr[k], tp, spec.w, spec.levels, sh[k], fm[k], co[k], exact=True)
+
+
+@pytest.mark.parametrize("c", [1, 2, 3])
+def test_fft_v2_single_frame_calls(c):
+    """Closed-loop sizes (1, 2, 5 frames per call) on the register-plan FFT path: the same
+    results as one whole-stack call."""
+    spec = config_spec(c, T=8)
+    st = make_stack(spec, 0, 8, device=DEV)
+    p = Plan(spec.m, spec.n, spec.w, spec.levels, "u16", 12, device=0, algo="fft")
+    p.set_template(st.template)
+    ref = p.align(st.frames, corrected=True)
+    k = 0
+    for T in (1, 2, 5):
+        sh, fm, co, _ = p.align(st.frames[k:k + T].contiguous(), corrected=True)
+        assert torch.equal(sh, ref[0][k:k + T]) and torch.equal(fm, ref[1][k:k + T])
+        assert torch.equal(co.view(torch.int16), ref[2][k:k + T].view(torch.int16))
+        k += T
