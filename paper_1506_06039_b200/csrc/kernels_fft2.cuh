@@ -53,6 +53,124 @@ struct F2 {
   __device__ static __forceinline__ int pos(int k) { return R * (k % N1) + k / N1; }
 };
 
+// ------------------------------------------------ packed-fp32 complex arithmetic (sm_100)
+// A complex value is one 64-bit register pair (re, im); add/sub/mul/fma.rn.f32x2 do both
+// halves in one instruction (FADD2/FMUL2/FFMA2), and ptxas folds the operand swaps and
+// broadcasts below into the instructions' swizzle modifiers.
+struct c2 { unsigned long long v; };
+__device__ __forceinline__ c2 c2of(float2 z) { c2 r; asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(z.x), "f"(z.y)); return r; }
+__device__ __forceinline__ float2 f2of(c2 a) { float2 z; asm("mov.b64 {%0, %1}, %2;" : "=f"(z.x), "=f"(z.y) : "l"(a.v)); return z; }
+__device__ __forceinline__ c2 c2mk(float x, float y) { return c2of(make_float2(x, y)); }
+__device__ __forceinline__ c2 operator+(c2 a, c2 b) { c2 r; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v)); return r; }
+__device__ __forceinline__ c2 operator-(c2 a, c2 b) { c2 r; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v)); return r; }
+__device__ __forceinline__ c2 mul2(c2 a, c2 b) { c2 r; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v)); return r; }
+__device__ __forceinline__ c2 fma2(c2 a, c2 b, c2 c) {
+  c2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+  return r;
+}
+__device__ __forceinline__ c2 swp(c2 a) { const float2 z = f2of(a); return c2mk(z.y, z.x); }
+// z * (c + i s) = z c + (i s) z, (i s) z = (-s z.y, s z.x) = swap(z) * (-s, s)
+__device__ __forceinline__ c2 cmul2(c2 z, float c, float s) { return fma2(z, c2mk(c, c), mul2(swp(z), c2mk(-s, s))); }
+// m + (i s) u
+__device__ __forceinline__ c2 addi(c2 m, c2 u, float s) { return fma2(swp(u), c2mk(-s, s), m); }
+
+// z e^{SIGN 2 pi i m / N} with m a compile-time constant after unrolling: the quarter
+// turns are swaps and sign changes, the rest two packed instructions
+template <int N, int SIGN>
+__device__ __forceinline__ c2 rotc(c2 z, int m) {
+  if (m == 0) return z;
+  if (N % 4 == 0 && m == N / 4) return mul2(swp(z), c2mk(-(float)SIGN, (float)SIGN));
+  if (N % 2 == 0 && m == N / 2) return mul2(z, c2mk(-1.f, -1.f));
+  if (N % 4 == 0 && m == 3 * N / 4) return mul2(swp(z), c2mk((float)SIGN, -(float)SIGN));
+  const float2 cs = twk<N>(m);
+  return cmul2(z, cs.x, (float)SIGN * cs.y);
+}
+
+template <int N, int SIGN>
+struct D2;
+template <int SIGN>
+struct D2<2, SIGN> {
+  static __device__ __forceinline__ void run(c2 (&v)[2]) {
+    const c2 a = v[0], b = v[1];
+    v[0] = a + b;
+    v[1] = a - b;
+  }
+};
+template <int SIGN>
+struct D2<3, SIGN> {
+  static __device__ __forceinline__ void run(c2 (&v)[3]) {
+    const float s1 = (float)SIGN * 0.86602540378443865f;
+    const c2 t = v[1] + v[2], u = v[1] - v[2];
+    const c2 m = fma2(t, c2mk(-0.5f, -0.5f), v[0]);
+    v[0] = v[0] + t;
+    v[1] = addi(m, u, s1);
+    v[2] = addi(m, u, -s1);
+  }
+};
+template <int SIGN>
+struct D2<4, SIGN> {
+  static __device__ __forceinline__ void run(c2 (&v)[4]) {
+    const c2 t0 = v[0] + v[2], t1 = v[0] - v[2], t2 = v[1] + v[3], d = v[1] - v[3];
+    v[0] = t0 + t2;
+    v[2] = t0 - t2;
+    v[1] = addi(t1, d, (float)SIGN);
+    v[3] = addi(t1, d, -(float)SIGN);
+  }
+};
+template <int SIGN>
+struct D2<5, SIGN> {
+  static __device__ __forceinline__ void run(c2 (&v)[5]) {
+    const float c1 = 0.30901699437494742f, c2_ = -0.80901699437494742f;
+    const float s1 = (float)SIGN * 0.95105651629515357f, s2 = (float)SIGN * 0.58778525229247313f;
+    const c2 a = v[0];
+    const c2 t1 = v[1] + v[4], u1 = v[1] - v[4];
+    const c2 t2 = v[2] + v[3], u2 = v[2] - v[3];
+    v[0] = a + (t1 + t2);
+    const c2 m1 = fma2(t2, c2mk(c2_, c2_), fma2(t1, c2mk(c1, c1), a));
+    const c2 m2 = fma2(t2, c2mk(c1, c1), fma2(t1, c2mk(c2_, c2_), a));
+    // r1 = i (s1 u1 + s2 u2), r2 = i (s2 u1 - s1 u2)
+    const c2 r1 = fma2(swp(u2), c2mk(-s2, s2), mul2(swp(u1), c2mk(-s1, s1)));
+    const c2 r2 = fma2(swp(u2), c2mk(s1, -s1), mul2(swp(u1), c2mk(-s2, s2)));
+    v[1] = m1 + r1;
+    v[4] = m1 - r1;
+    v[2] = m2 + r2;
+    v[3] = m2 - r2;
+  }
+};
+template <int N1, int N2, int SIGN>
+struct D2CT {
+  static __device__ __forceinline__ void run(c2 (&v)[N1 * N2]) {
+    constexpr int N = N1 * N2;
+    c2 t[N1][N2];
+#pragma unroll
+    for (int n2 = 0; n2 < N2; ++n2) {
+      c2 u[N1];
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) u[n1] = v[N2 * n1 + n2];
+      D2<N1, SIGN>::run(u);
+#pragma unroll
+      for (int k1 = 0; k1 < N1; ++k1) t[k1][n2] = rotc<N, SIGN>(u[k1], (n2 * k1) % N);
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < N1; ++k1) {
+      D2<N2, SIGN>::run(t[k1]);
+#pragma unroll
+      for (int k2 = 0; k2 < N2; ++k2) v[k1 + N1 * k2] = t[k1][k2];
+    }
+  }
+};
+template <int SIGN> struct D2<8, SIGN> : D2CT<2, 4, SIGN> {};
+template <int SIGN> struct D2<9, SIGN> : D2CT<3, 3, SIGN> {};
+template <int SIGN> struct D2<12, SIGN> : D2CT<3, 4, SIGN> {};
+template <int SIGN> struct D2<15, SIGN> : D2CT<3, 5, SIGN> {};
+template <int SIGN> struct D2<16, SIGN> : D2CT<4, 4, SIGN> {};
+template <int SIGN> struct D2<18, SIGN> : D2CT<2, 9, SIGN> {};
+template <int SIGN> struct D2<20, SIGN> : D2CT<4, 5, SIGN> {};
+
+__device__ __forceinline__ c2 lds2(const float2 *p) { return c2of(*p); }
+__device__ __forceinline__ void sts2(float2 *p, c2 a) { *p = f2of(a); }
+
 // Forward: x natural -> X k1-major, X[k] = sum_n x[n] e^{-2 pi i n k / N}.  tw[m] =
 // e^{-2 pi i m / N}.  nfft <= NF transforms at x + q * STRIDE.  All threads; ends synced.
 template <int P>
@@ -63,24 +181,27 @@ __device__ __forceinline__ void f2_fwd(float2 *x, const float2 *tw, int nfft) {
   for (int task = threadIdx.x; task < nfft * N2; task += blockDim.x) {
     const int q = task / N2, n2 = task - q * N2;
     float2 *b = x + q * S + n2;
-    float2 v[N1];
+    c2 v[N1];
 #pragma unroll
-    for (int n1 = 0; n1 < N1; ++n1) v[n1] = b[R * n1];
-    Dft<N1, -1>::run(v);
-    b[0] = v[0];
+    for (int n1 = 0; n1 < N1; ++n1) v[n1] = lds2(b + R * n1);
+    D2<N1, -1>::run(v);
+    sts2(b, v[0]);
 #pragma unroll
-    for (int k1 = 1; k1 < N1; ++k1) b[R * k1] = cmul(v[k1], tw[n2 * k1]);
+    for (int k1 = 1; k1 < N1; ++k1) {
+      const float2 t = tw[n2 * k1];
+      sts2(b + R * k1, cmul2(v[k1], t.x, t.y));
+    }
   }
   __syncthreads();
   for (int task = threadIdx.x; task < nfft * N1; task += blockDim.x) {
     const int q = task / N1, k1 = task - q * N1;
     float2 *b = x + q * S + R * k1;
-    float2 u[N2];
+    c2 u[N2];
 #pragma unroll
-    for (int n2 = 0; n2 < N2; ++n2) u[n2] = b[n2];
-    Dft<N2, -1>::run(u);
+    for (int n2 = 0; n2 < N2; ++n2) u[n2] = lds2(b + n2);
+    D2<N2, -1>::run(u);
 #pragma unroll
-    for (int k2 = 0; k2 < N2; ++k2) b[k2] = u[k2];
+    for (int k2 = 0; k2 < N2; ++k2) sts2(b + k2, u[k2]);
   }
   __syncthreads();
 }
@@ -94,24 +215,27 @@ __device__ __forceinline__ void f2_inv(float2 *x, const float2 *tw, int nfft) {
   for (int task = threadIdx.x; task < nfft * N1; task += blockDim.x) {
     const int q = task / N1, k1 = task - q * N1;
     float2 *b = x + q * S + R * k1;
-    float2 u[N2];
+    c2 u[N2];
 #pragma unroll
-    for (int k2 = 0; k2 < N2; ++k2) u[k2] = b[k2];
-    Dft<N2, 1>::run(u);   // over k2 -> n2
-    b[0] = u[0];
+    for (int k2 = 0; k2 < N2; ++k2) u[k2] = lds2(b + k2);
+    D2<N2, 1>::run(u);   // over k2 -> n2
+    sts2(b, u[0]);
 #pragma unroll
-    for (int n2 = 1; n2 < N2; ++n2) b[n2] = cmul(u[n2], conjf2(tw[k1 * n2]));
+    for (int n2 = 1; n2 < N2; ++n2) {
+      const float2 t = tw[k1 * n2];
+      sts2(b + n2, cmul2(u[n2], t.x, -t.y));
+    }
   }
   __syncthreads();
   for (int task = threadIdx.x; task < nfft * N2; task += blockDim.x) {
     const int q = task / N2, n2 = task - q * N2;
     float2 *b = x + q * S + n2;
-    float2 v[N1];
+    c2 v[N1];
 #pragma unroll
-    for (int k1 = 0; k1 < N1; ++k1) v[k1] = b[R * k1];
-    Dft<N1, 1>::run(v);   // over k1 -> n1
+    for (int k1 = 0; k1 < N1; ++k1) v[k1] = lds2(b + R * k1);
+    D2<N1, 1>::run(v);   // over k1 -> n1
 #pragma unroll
-    for (int n1 = 0; n1 < N1; ++n1) b[R * n1] = v[n1];
+    for (int n1 = 0; n1 < N1; ++n1) sts2(b + R * n1, v[n1]);
   }
   __syncthreads();
 }
