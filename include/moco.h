@@ -169,6 +169,15 @@ int moco_fft_cross(moco_plan *p, const void *d_frames, int64_t T, float *d_h, in
                    int32_t *d_qcount, moco_stream_t stream);
 
 /*
+ * moco_fft_bound -- the constants of the FFT path's certified error bound
+ *     |h~(s,t) - h(s,t)| <= u ||a_c||_2 (Cf ||b_c||_2 + Ci ||b_c||_1),  u = 2^-24,
+ * for every coarse lag (DESIGN.md §5 derives them from the transforms' stage structure:
+ * per-stage and twiddle rounding, the fp64 template spectrum rounded once to fp32, the
+ * spectrum product).  Cf, Ci: host outputs.  MOCO_EINVAL if the plan has no FFT path.
+ */
+int moco_fft_bound(const moco_plan *p, double *Cf, double *Ci);
+
+/*
  * moco_mean_image -- report helper (Fig. 2 caption:
  * "the mean of every image"): d_mean[i*n + j] = (1/T) sum_k frames[k][i][j] for T device
  * frames of m x n samples (dtype MOCO_U16 or MOCO_F32, rows of n samples, no padding).

@@ -37,6 +37,7 @@ SIGNATURES = [
     ("moco_align_host", _I, [_P, _P, _I64, _P, _P, _P, _P]),
     ("moco_score_grid", _I, [_P, _P, _I64, _P, _P]),
     ("moco_fft_cross", _I, [_P, _P, _I64, _P, _P, _P, _P]),
+    ("moco_fft_bound", _I, [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
     ("moco_probe_peaks", _I, [_I, ctypes.POINTER(ctypes.c_double), _I]),
     ("moco_mean_image", _I, [_P, _I64, _I, _I, _I, _P, _P]),
     ("moco_last_launch_count", _I64, [_P]),
@@ -205,6 +206,13 @@ class Plan:
         _check(load().moco_fft_cross(self._h, _ptr(frames), T, _ptr(h), _ptr(sh), _ptr(q), self._stream()),
                "moco_fft_cross")
         return h, sh, q
+
+    def fft_bound(self):
+        """(Cf, Ci) of the FFT path's certified bound |h~ - h| <= u ||a||_2 (Cf ||b||_2 +
+        Ci ||b||_1)."""
+        cf, ci = ctypes.c_double(), ctypes.c_double()
+        _check(load().moco_fft_bound(self._h, ctypes.byref(cf), ctypes.byref(ci)), "moco_fft_bound")
+        return cf.value, ci.value
 
     def align_host(self, frames: torch.Tensor, shifts=None, fmin=None, corrected=None, flags=None):
         """End-to-end moco_align_host on HOST tensors (pinned for full speed)."""

@@ -18,22 +18,52 @@
 //   k_fft_score   per frame: two lag rows packed -> IFFT_Mc -> h~(s,t); then the
 //                 certified search of S4 (below) and exact rescoring
 //
-// fp32 certification (S4): with |h~ - h| <= eps_h = C u log2(Mr Mc) ||a||_2 ||b||_2
-// (u = 2^-24; C = RS_FFT_C, validated against exact h in the GPU tests), the score
-// f~ = (g_a + g_b - 2 h~) / (16^L A) is within delta = 2 eps_h / (16^L A) of the exact
-// f.  Every lag whose interval [f~ - delta, f~ + delta] reaches below min(f~ + delta)
-// is re-scored EXACTLY (64-bit integer direct sum of P:31) and the argmin of the key
-// (f, s, t) is taken over those exact values -- the result is the exact method's,
-// bit for bit.  More than FFT_QCAP candidates: every lag is re-scored (flag bit 1).
+// fp32 certification (S4): with |h~ - h| <= eps_h = u ||a||_2 (Cf ||b||_2 + Ci ||b||_1)
+// (u = 2^-24; Cf, Ci derived from the transforms' stage structure), the
+// score f~ = (g_a + g_b - 2 h~) / (16^L A) is within delta = 2 eps_h / (16^L A) of the
+// exact f.  Every lag whose interval [f~ - delta, f~ + delta] reaches below
+// min(f~ + delta) is re-scored EXACTLY (64-bit integer direct sum of P:31) and the argmin
+// of the key (f, s, t) is taken over those exact values -- the result is the exact
+// method's, bit for bit.  More than FFT_QCAP candidates: every lag is re-scored (flag
+// bit 1).  The template spectrum is computed in fp64 (direct separable DFT) and rounded
+// once to fp32.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <cmath>
 
 #include "kernels_direct.cuh"
 
 namespace moco {
 
-constexpr double RS_FFT_C = 8.0;   // error-bound constant (measured max ~0.5)
+// ---------------------------------------------------------------- error bound
+// First-order bound on the fp32 cross term, DESIGN.md §5.  A transform is a product of
+// stages; a stage whose outputs are computed with |fl(y_k) - y_k| <= rho u sum_j |z_j|
+// over its radix-r block has ||fl(Az) - Az||_2 <= mu ||A||_2 ||z||_2 with mu = sqrt(r) rho
+// u, and a diagonal twiddle stage (rounded constant, two roundings per component) mu = 3u.
+// Summed over the stages (the unnormalised stages multiply to ||F||_2 = sqrt(N)):
+//   ||fl(F x) - F x||_2 <= kappa u sqrt(N) ||x||_2.
+// rho per butterfly as written (kernels_fft.cuh dft_small / Dft, kernels_fft2.cuh D2):
+// radix 2: 1, radix 4 (two add layers, +-i exact): 2, radix 3 (depth 3 and one rounded
+// constant): 4, radix 5 (depth 4 and rounded constants): 8.
+inline double fft_mu(int r) {
+  return r == 2 ? std::sqrt(2.0) * 1 : r == 4 ? 2.0 * 2 : r == 3 ? std::sqrt(3.0) * 4 : std::sqrt(5.0) * 8;
+}
+// kappa of a codelet of length n (kernels_fft.cuh DftCT splits, innermost radices 2-5)
+inline double fft_kappa_codelet(int n) {
+  switch (n) {
+    case 2: case 3: case 4: case 5: return fft_mu(n);
+    case 8: return fft_mu(2) + 3 + fft_mu(4);
+    case 9: return fft_mu(3) + 3 + fft_mu(3);
+    case 12: return fft_mu(3) + 3 + fft_mu(4);
+    case 15: return fft_mu(3) + 3 + fft_mu(5);
+    case 16: return fft_mu(4) + 3 + fft_mu(4);
+    case 18: return fft_mu(2) + 3 + fft_kappa_codelet(9);
+    case 20: return fft_mu(4) + 3 + fft_mu(5);
+    default: return 1e30;
+  }
+}
 constexpr int FFT_QCAP = 64;
 constexpr int FFT_UB_INIT = 0x7f7f7f7f;   // ~3.4e38f: a.ub between calls
 constexpr int FFT_MAXST = 10;
@@ -371,6 +401,67 @@ __global__ void k_fft_twiddles(float2 *tw, int N) {
   }
 }
 
+// Template spectrum in fp64 (once per template), separable direct DFT:
+//   R[i][k] = sum_j b[i][j] e^{-2 pi i j k / Mc}                (k < Kc)
+//   Bc[k][u] = conj(sum_i R[i][k] e^{-2 pi i i u / Mr}) / (Mr Mc), rounded once to fp32
+// twiddles by sincospi in double; |rounding error| ~ 1e-16 relative to ||b||_1, far
+// below the fp32 rounding of the result.
+__global__ void k_tpl_dft_rows(const uint16_t *__restrict__ b, int pitch, int nc, int Mc, int Kc,
+                               double2 *__restrict__ R) {
+  extern __shared__ double2 tw64[];
+  for (int m = threadIdx.x; m < Mc; m += blockDim.x) {
+    double s_, c_;
+    sincospi(-2.0 * m / Mc, &s_, &c_);
+    tw64[m] = make_double2(c_, s_);
+  }
+  __syncthreads();
+  const int i = blockIdx.x;
+  const uint16_t *br = b + (int64_t)i * pitch;
+  for (int k = threadIdx.x; k < Kc; k += blockDim.x) {
+    double re = 0, im = 0;
+    int m = 0;
+    for (int j = 0; j < nc; ++j) {
+      const double v = (double)br[j];
+      re += v * tw64[m].x;
+      im += v * tw64[m].y;
+      m += k;
+      if (m >= Mc) m -= Mc;
+    }
+    R[(int64_t)i * Kc + k] = make_double2(re, im);
+  }
+}
+__global__ void k_tpl_dft_cols(const double2 *__restrict__ R, int mc, int Mr, int Mc, int Kc, float2 *__restrict__ Bc,
+                               unsigned long long *__restrict__ b1, const uint16_t *__restrict__ b, int pitch, int nc) {
+  extern __shared__ double2 tw64[];
+  for (int m = threadIdx.x; m < Mr; m += blockDim.x) {
+    double s_, c_;
+    sincospi(-2.0 * m / Mr, &s_, &c_);
+    tw64[m] = make_double2(c_, s_);
+  }
+  __syncthreads();
+  const int k = blockIdx.x;
+  const double scale = 1.0 / ((double)Mr * (double)Mc);
+  for (int u = threadIdx.x; u < Mr; u += blockDim.x) {
+    double re = 0, im = 0;
+    int m = 0;
+    for (int i = 0; i < mc; ++i) {
+      const double2 r = R[(int64_t)i * Kc + k];
+      const double2 t = tw64[m];
+      re += r.x * t.x - r.y * t.y;
+      im += r.x * t.y + r.y * t.x;
+      m += u;
+      if (m >= Mr) m -= Mr;
+    }
+    Bc[(int64_t)k * Mr + u] = make_float2((float)(re * scale), (float)(-im * scale));
+  }
+  if (k == 0 && b1) {   // ||b||_1 of the coarse template (non-negative samples): sum b
+    unsigned long long acc = 0;
+    for (int e = threadIdx.x; e < mc * nc; e += blockDim.x) acc += b[(int64_t)(e / nc) * pitch + e % nc];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(b1, acc);
+  }
+}
+
 struct FftGeom {
   int mc, nc, w, hw, W;
   FftLen Lr, Lc;   // column length Mr (over rows), row length Mc (over columns)
@@ -483,7 +574,8 @@ struct FftScoreArgs {
   const u64 *gb;            // [W*W]
   FftGeom g;
   double scale;             // 16^L
-  double eps_rel;           // C u log2(Mr Mc): eps_h = eps_rel ||a|| ||b||
+  double eps_f, eps_i;      // Cf u, Ci u: eps_h = ||a||_2 (eps_f ||b||_2 + eps_i ||b||_1)
+  const unsigned long long *b1;   // ||b||_1 of the coarse template (device)
   int B;
   int32_t *shift_out;       // [B][2]
   double *f_out;            // [B] or null
@@ -622,8 +714,8 @@ __global__ void __launch_bounds__(1024) k_fft_score(FftScoreArgs a) {
   }
   __syncthreads();
   const u64 *gaf = a.ga + f * W * W;
-  const double na = sqrt((double)gaf[hw * W + hw]), nb = sqrt((double)a.gb[hw * W + hw]);
-  const double eps2 = 2.0 * a.eps_rel * na * nb;
+  const double na = sqrt((double)gaf[hw * W + hw]) * (1.0 + 1e-12);
+  const double eps2 = 2.0 * na * (a.eps_f * sqrt((double)a.gb[hw * W + hw]) * (1.0 + 1e-12) + a.eps_i * (double)*a.b1);
   float best = 3.0e38f;
   for (int lag = threadIdx.x; lag < W * W; lag += blockDim.x) {
     const int si = lag / W, ti = lag - si * W;
@@ -677,8 +769,8 @@ __global__ void __launch_bounds__(FFT_THREADS) k_fft_score_rows(FftScoreArgs a, 
   __syncthreads();
   const float2 *Hr = fft_batch<P>(x, y, tw, g.Lc, np, +1.f);
   const u64 *gaf = a.ga + f * W * W;
-  const double na = sqrt((double)gaf[hw * W + hw]), nb = sqrt((double)a.gb[hw * W + hw]);
-  const double eps2 = 2.0 * a.eps_rel * na * nb;
+  const double na = sqrt((double)gaf[hw * W + hw]) * (1.0 + 1e-12);
+  const double eps2 = 2.0 * na * (a.eps_f * sqrt((double)a.gb[hw * W + hw]) * (1.0 + 1e-12) + a.eps_i * (double)*a.b1);
   float best = 3.0e38f;
   for (int e = threadIdx.x; e < np * 2 * W; e += blockDim.x) {
     const int q = e / (2 * W), r = e - q * 2 * W, half = r / W, ti = r - half * W;

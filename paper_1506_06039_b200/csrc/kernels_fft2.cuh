@@ -520,7 +520,8 @@ struct F2ScoreArgs {
   u64 *Ew;                  // the same, written: the pick re-zeroes the accumulated slots
   const u64 *gb;            // [W*W] template energies
   double scale;             // 16^L
-  double eps_rel;           // C u log2(Mr Mc)
+  double eps_f, eps_i;      // eps_h = ||a||_2 (eps_f ||b||_2 + eps_i ||b||_1) (kernels_fft.cuh)
+  const unsigned long long *b1;   // ||b||_1 of the coarse template (device)
   const uint16_t *frames;   // level-0 frames (exact rescoring through block sums)
   int64_t fstride;
   int pitch;
@@ -601,6 +602,46 @@ __device__ u64 f2_exact_N(const F2ScoreArgs &a, int64_t f, int s, int t, int r0,
   return tot;
 }
 
+// Partial exact N over the coarse rows [r0, r1) for EVERY lag of a box s in [s0, s0+ns),
+// t in [t0, t0+nt) (ns, nt <= 3) in one pass: the template value b_c[i][j] is loaded once
+// per pixel, each box row's frame values once per lane (two words) and shifted to the box
+// columns with warp shuffles.  acc[ds*3+dt] per thread (u64), not yet reduced.
+template <int L>
+__device__ __forceinline__ void f2_exact_box(const F2ScoreArgs &a, int64_t f, int s0, int ns, int t0, int nt, int r0,
+                                             int r1, u64 (&acc)[9]) {
+  constexpr int D = 1 << L;
+  const int mc = a.mc, nc = a.nc;
+  const uint16_t *Fr = a.frames + f * a.fstride;
+  const int nw = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = r0 + wid; i < r1; i += nw) {
+    const uint16_t *br = a.tpl + (int64_t)i * a.tpitch;
+    for (int jb = 0; jb < nc; jb += 32) {
+      const int j = jb + lane;
+      const int bv = j < nc ? (int)__ldg(br + j) : 0;
+#pragma unroll
+      for (int ds = 0; ds < 3; ++ds) {
+        if (ds >= ns) break;
+        const int fr = i + s0 + ds;   // frame row (warp-uniform)
+        if (fr < 0 || fr >= mc) continue;
+        const uint16_t *ar = Fr + (int64_t)(D * fr) * a.pitch;
+        const int c0 = j + t0, c1 = c0 + 32;
+        const uint32_t v0 = (c0 >= 0 && c0 < nc) ? f2_coarse_at<L>(ar, a.pitch, c0) : 0u;
+        const uint32_t v1 = (c1 >= 0 && c1 < nc) ? f2_coarse_at<L>(ar, a.pitch, c1) : 0u;
+#pragma unroll
+        for (int dt = 0; dt < 3; ++dt) {
+          const uint32_t x0 = __shfl_sync(0xffffffffu, v0, (lane + dt) & 31);
+          const uint32_t x1 = __shfl_sync(0xffffffffu, v1, (lane + dt) & 31);
+          if (dt >= nt) continue;
+          const int fc = j + t0 + dt;   // frame column of this lane's pixel at lag t0 + dt
+          if (j >= nc || fc < 0 || fc >= nc) continue;
+          const int d = (int)(lane + dt < 32 ? x0 : x1) - bv;
+          acc[ds * 3 + dt] += (u64)((uint32_t)(d * d));   // |d| < 2^16
+        }
+      }
+    }
+  }
+}
+
 template <int P>
 __global__ void __launch_bounds__(F2_THREADS) k_fft2_score(F2ScoreArgs a) {
   using G = F2<P>;
@@ -672,7 +713,8 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_score(F2ScoreArgs a) {
   }
   f2_inv<P>(x, tw, np);
   const u64 tot = E[0];
-  const double eps2 = 2.0 * a.eps_rel * sqrt((double)tot) * sqrt((double)a.gb[hw * W + hw]);
+  const double eps2 = 2.0 * (sqrt((double)tot) * (1.0 + 1e-12)) *
+                      (a.eps_f * sqrt((double)a.gb[hw * W + hw]) * (1.0 + 1e-12) + a.eps_i * (double)*a.b1);
   float best = 3.0e38f;
   float *lbf = a.lb + f * W * W;
   for (int rl = warp; rl < nr; rl += F2_WARPS) {
@@ -743,13 +785,15 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_score(F2ScoreArgs a) {
 }
 
 // Exact rescoring of the certified candidates (S4): blocks (frame, row part); frames whose
-// candidate set k_fft2_score resolved exit at once.  Partial N of every candidate over the
-// part's coarse rows -> 64-bit atomics; the last part of a frame takes the argmin of the
-// key (f, s, t) over the exact values and writes the outputs.
+// candidate set k_fft2_score resolved exit at once.  Candidates inside a 3 x 3 box of lags
+// (the usual case: the neighbours of the optimum) are scored in one pass over the part's
+// rows; others one lag at a time.  Partial N -> 64-bit atomics; the last part of a frame
+// takes the argmin of the key (f, s, t) over the exact values and writes the outputs.
 template <int L>
 __global__ void __launch_bounds__(256) k_fft2_rescore(F2ScoreArgs a) {
   __shared__ u64 red[32];
-  __shared__ int last;
+  __shared__ u64 bred[8][9];
+  __shared__ int last, box[4];
   const int64_t f = blockIdx.x / a.rparts;
   const int part = blockIdx.x - (int)(f * a.rparts);
   const int qn = a.qn[f];
@@ -758,11 +802,42 @@ __global__ void __launch_bounds__(256) k_fft2_rescore(F2ScoreArgs a) {
   const bool all = qn < 0;
   const int ncand = all ? W * W : qn;
   const int rows = (a.mc + a.rparts - 1) / a.rparts, r0 = part * rows, r1 = min(a.mc, r0 + rows);
+  const int *ql = a.ql + f * FFT_QCAP;
   u64 *acc = a.nacc + f * (int64_t)max(FFT_QCAP, W * W);
-  for (int c = 0; c < ncand; ++c) {
-    const int lag = all ? c : a.ql[f * FFT_QCAP + c];
-    const u64 part_n = f2_exact_N<L>(a, f, lag / W - hw, lag % W - hw, r0, r1, red);
-    if (threadIdx.x == 0 && part_n) atomicAdd(acc + c, part_n);
+  if (threadIdx.x == 0) {
+    int smin = 1 << 30, smax = -(1 << 30), tmin = 1 << 30, tmax = -(1 << 30);
+    for (int c = 0; c < (all ? 0 : ncand); ++c) {
+      const int s = ql[c] / W - hw, t = ql[c] % W - hw;
+      smin = min(smin, s); smax = max(smax, s); tmin = min(tmin, t); tmax = max(tmax, t);
+    }
+    box[0] = smin; box[1] = smax - smin + 1; box[2] = tmin; box[3] = tmax - tmin + 1;
+  }
+  __syncthreads();
+  const bool boxed = !all && box[1] <= 3 && box[3] <= 3;
+  if (boxed) {
+    // slots of the box lags: acc[ds * 3 + dt]; the last block maps candidates to them
+    u64 v[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) v[k] = 0;
+    f2_exact_box<L>(a, f, box[0], box[1], box[2], box[3], r0, r1, v);
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const u64 x = warp_sum(v[k]);
+      if (lane == 0) bred[wid][k] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x < 9) {
+      u64 x = 0;
+      for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) x += bred[w2][threadIdx.x];
+      if (x) atomicAdd(acc + threadIdx.x, x);
+    }
+  } else {
+    for (int c = 0; c < ncand; ++c) {
+      const int lag = all ? c : ql[c];
+      const u64 part_n = f2_exact_N<L>(a, f, lag / W - hw, lag % W - hw, r0, r1, red);
+      if (threadIdx.x == 0 && part_n) atomicAdd(acc + c, part_n);
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -774,15 +849,18 @@ __global__ void __launch_bounds__(256) k_fft2_rescore(F2ScoreArgs a) {
   __threadfence();
   Key bk{~0ull, ~0u};
   for (int c = threadIdx.x; c < ncand; c += blockDim.x) {
-    const int lag = all ? c : a.ql[f * FFT_QCAP + c];
+    const int lag = all ? c : ql[c];
     const int s = lag / W - hw, t = lag % W - hw;
-    const u64 N = atomicExch(acc + c, 0ull);   // read and re-zero
+    const int slot = boxed ? (s - box[0]) * 3 + (t - box[2]) : c;
+    const u64 N = __ldcg(acc + slot);
     const double area = (double)((a.mc - abs(s)) * (a.nc - abs(t)));
     const Key kk{(u64)__double_as_longlong((double)N / (a.scale * area)), (unsigned)lag};
     if (key_less(kk, bk)) bk = kk;
   }
   __shared__ Key kred[32];
   bk = block_min_key(bk, kred);
+  // re-zero the accumulators for the next call
+  for (int k = threadIdx.x; k < (boxed ? 9 : ncand); k += blockDim.x) acc[k] = 0;
   if (threadIdx.x == 0) {
     const int s = (int)(bk.idx / W) - hw, t = (int)(bk.idx % W) - hw;
     a.shift_out[2 * f] = s;

@@ -104,7 +104,9 @@ struct moco_plan {
     cudaStream_t side = nullptr;   // small batches: frame energies beside the FFT
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int64_t cap = 0;
-    double eps_rel = 0;
+    double bound_Cf = 0, bound_Ci = 0;   // eps_h = u ||a||_2 (Cf ||b||_2 + Ci ||b||_1)
+    double2 *R64 = nullptr;     // template spectrum rows in fp64 [mc][Kc] (k_tpl_dft_rows)
+    unsigned long long *b1 = nullptr;   // ||b||_1 of the coarse template
     int smem_rows = 0, smem_cols = 0, smem_score = 0, smem_energy = 0;
     int pc = 0, pr = 0;         // register FFT plans of the row (Mc) and column (Mr) lengths
     // kernels_fft2.cuh (both lengths with a register plan, n_c % 8 == 0): the frame-to-
@@ -322,6 +324,8 @@ static void plan_free(moco_plan *p) {
     if (p->fft.ss[k]) cudaStreamDestroy(p->fft.ss[k]);
     if (p->fft.ev_j[k]) cudaEventDestroy(p->fft.ev_j[k]);
   }
+  if (p->fft.R64) cudaFree(p->fft.R64);
+  if (p->fft.b1) cudaFree(p->fft.b1);
   if (p->fft.E) cudaFree(p->fft.E);
   if (p->fft.cnt) cudaFree(p->fft.cnt);
   if (p->fft.qn) cudaFree(p->fft.qn);
@@ -362,6 +366,38 @@ static int fft2_rows_smem(int P_N, int NF, int STRIDE, int per, int L, int nc, i
   return f2_stage_bytes(per, L, nc) + (P_N + NF * STRIDE) * 8 + 2 * NF * 8 + 2 * hw * 8;
 }
 
+// kappa of one 1-D transform of length L.N as the kernels compute it: a two-pass register
+// plan (N1 codelet, twiddle stage, N2 codelet) or the generic radix-2/3/4/5 Stockham stages
+static double fft_kappa_len(const FftLen &L, int plan) {
+  int n1 = 0, n2 = 0;
+  switch (plan) {
+    case 1: n1 = Plan2p<1>::N1; n2 = Plan2p<1>::N2; break;
+    case 2: n1 = Plan2p<2>::N1; n2 = Plan2p<2>::N2; break;
+    case 3: n1 = Plan2p<3>::N1; n2 = Plan2p<3>::N2; break;
+    case 4: n1 = Plan2p<4>::N1; n2 = Plan2p<4>::N2; break;
+    case 5: n1 = Plan2p<5>::N1; n2 = Plan2p<5>::N2; break;
+    case 6: n1 = Plan2p<6>::N1; n2 = Plan2p<6>::N2; break;
+    default: break;
+  }
+  if (n1) return fft_kappa_codelet(n1) + 3 + fft_kappa_codelet(n2);
+  double k = 0;
+  for (int st = 0; st < L.nst; ++st) k += fft_mu(L.rad[st]) + 3;
+  return k;
+}
+// Constants of eps_h = u ||a||_2 (Cf ||b||_2 + Ci ||b||_1), DESIGN.md §5.  Per lag, the
+// errors made before the inverse transform -- the forward 2-D transform of a (row
+// transforms, unpack of the packed real rows, column transforms), the fp32 rounding of the
+// fp64 template spectrum (1) and of the spectrum product (2 sqrt 2) -- reach h(s,t) as a
+// correlation with b, so Cauchy-Schwarz bounds them by ||.||_2 ||b||_2; the inverse
+// transform's own rounding (columns, packing of two lag rows, rows) is bounded through
+// ||Y||_2 <= ||a||_2 ||b||_1 / sqrt(N).  x 1.1 for the second-order terms (each first-order
+// term is ~ kappa u ~ 1e-5 relative).
+static void fft_bound_C(const FftLen &Lr, int pr, const FftLen &Lc, int pc, double *Cf, double *Ci) {
+  const double kr = fft_kappa_len(Lr, pr), kc = fft_kappa_len(Lc, pc);
+  *Cf = 1.1 * ((kc + 1 + kr) + 1 + 2 * std::sqrt(2.0));
+  *Ci = 1.1 * (kr + 1 + kc);
+}
+
 static int fft_init(moco_plan *p) {
   auto &F = p->fft;
   if (F.ready) return MOCO_OK;
@@ -385,6 +421,7 @@ static int fft_init(moco_plan *p) {
     if (cudaMalloc(q, bytes) != cudaSuccess) { cudaGetLastError(); return false; }
     return true;
   };
+  if (!al((void **)&F.R64, (size_t)g.mc * g.Kc * 16) || !al((void **)&F.b1, 8)) return MOCO_ENOMEM;
   if (!al((void **)&F.twr, Mr * 8) || !al((void **)&F.twc, Mc * 8) || !al((void **)&F.Bc, (size_t)g.Kc * Mr * 8) ||
       !al((void **)&F.S, (size_t)nset * F.cap * g.Kc * g.mcp * 8) ||
       !al((void **)&F.P, (size_t)nset * F.cap * g.W * g.Kc * 8) ||
@@ -415,7 +452,8 @@ static int fft_init(moco_plan *p) {
   CK(cudaStreamCreateWithFlags(&F.side, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&F.ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&F.ev_join, cudaEventDisableTiming));
-  F.eps_rel = RS_FFT_C * std::ldexp(1.0, -24) * std::log2((double)Mr * (double)Mc);
+  // derived first-order bound |h~ - h| <= C u ||a||_2 ||b||_1 (kernels_fft.cuh)
+  fft_bound_C(g.Lr, F.pr, g.Lc, F.pc, &F.bound_Cf, &F.bound_Ci);
   // (the scratch half of each transform buffer carries FFT_YPAD extra elements per
   // transform: the padded rows of the two-pass register plans, kernels_fft.cuh fft2p)
   F.smem_rows = (Mc + FFT_ROWS_PAIRS * Mc + FFT_ROWS_PAIRS * (Mc + FFT_YPAD)) * 8;
@@ -490,32 +528,6 @@ static void fft2_rows_launch(const F2RowsArgs &a, int L, int64_t nblk, int hw, c
   else k_fft2_rows<PC, 1><<<(unsigned)nblk, F2_THREADS, smem, st>>>(a);
 }
 
-static int fft2_set_template(moco_plan *p, cudaStream_t st) {
-  auto &F = p->fft;
-  const int L = p->levels;
-  const FftGeom &g = F.g;
-  fft_dispatch(F.pc, [&](auto PC) {
-    constexpr int P = decltype(PC)::value;
-    if constexpr (P > 0) {
-      const int per = fft2_rows_per_max(F2<P>::NF, 0, g.nc);
-      F2RowsArgs a = fft2_rows_args(p, p->tpl[L], 0, p->pitch[L], per, 0);
-      fft2_rows_launch<P>(a, 0, (g.mcp / 2 + per - 1) / per, g.hw, st);
-    }
-  });
-  fft_dispatch(F.pr, [&](auto PR) {
-    constexpr int P = decltype(PR)::value;
-    if constexpr (P > 0) {
-      F2ColsArgs c{};
-      c.S = F.S; c.mc = g.mc; c.Kc = g.Kc; c.mcp = g.mcp; c.W = g.W; c.hw = g.hw;
-      c.per = F2<P>::NF; c.tw = F.twr; c.Bc = nullptr; c.P = nullptr; c.Bout = F.Bc;
-      c.scale = 1.0f / ((float)g.Lr.N * (float)g.Lc.N);
-      k_fft2_cols<P><<<(unsigned)((g.Kc + c.per - 1) / c.per), F2_THREADS, F.smem2_cols, st>>>(c);
-    }
-  });
-  CKL("fft2_set_template");
-  F.tpl_ready = true;
-  return MOCO_OK;
-}
 
 // One sub-batch of nb level-0 frames through the three kernels of kernels_fft2.cuh, with
 // scratch set `set`, on stream st.
@@ -570,7 +582,7 @@ static int fft2_sub(moco_plan *p, const char *fr, int64_t fstride, int pitch, in
       F2ScoreArgs a{};
       a.P = Pset; a.tw = F.twc; a.mc = g.mc; a.nc = g.nc; a.hw = g.hw; a.W = g.W; a.Kc = g.Kc;
       a.per = per; a.E = F.E + so * f2_esz(g.hw); a.Ew = F.E + so * f2_esz(g.hw); a.gb = (const u64 *)p->gb;
-      a.scale = (double)(1u << (4 * L)); a.eps_rel = F.eps_rel;
+      a.scale = (double)(1u << (4 * L)); a.eps_f = std::ldexp(F.bound_Cf, -24); a.eps_i = std::ldexp(F.bound_Ci, -24); a.b1 = F.b1;
       a.frames = (const uint16_t *)fr; a.fstride = fstride; a.pitch = pitch; a.L = LK;
       a.tpl = (const uint16_t *)p->tpl[L]; a.tpitch = p->pitch[L];
       a.lb = F.lb + so * g.W * g.W; a.ub = F.ub + so; a.cnt = F.cnt + so;
@@ -623,10 +635,25 @@ static int launch_fft2(moco_plan *p, const void *frames, int64_t fstride, int pi
   return MOCO_OK;
 }
 
-// template spectrum conj(B^)/(Mr Mc), column-major [k][u] (once per template)
+// template spectrum conj(B^)/(Mr Mc), column-major [k][u] (once per template), computed
+// in fp64 by a direct separable DFT and rounded once (the error bound of kernels_fft.cuh
+// counts that single rounding), and ||b||_1
 static int fft_set_template(moco_plan *p, cudaStream_t st) {
   auto &F = p->fft;
-  if (F.v2) return fft2_set_template(p, st);
+  const int L = p->levels;
+  const FftGeom &g = F.g;
+  const int Mr = g.Lr.N, Mc = g.Lc.N;
+  CK(cudaMemsetAsync(F.b1, 0, 8, st));
+  k_tpl_dft_rows<<<g.mc, 256, Mc * 16, st>>>((const uint16_t *)p->tpl[L], p->pitch[L], g.nc, Mc, g.Kc, F.R64);
+  k_tpl_dft_cols<<<g.Kc, 256, Mr * 16, st>>>(F.R64, g.mc, Mr, Mc, g.Kc, F.Bc, F.b1, (const uint16_t *)p->tpl[L],
+                                            p->pitch[L], g.nc);
+  CKL("fft template spectrum");
+  F.tpl_ready = true;
+  return MOCO_OK;
+}
+
+[[maybe_unused]] static int fft_set_template_fp32(moco_plan *p, cudaStream_t st) {
+  auto &F = p->fft;
   const int L = p->levels;
   const FftGeom &g = F.g;
   const int nrb = (g.mcp / 2 + FFT_ROWS_PAIRS - 1) / FFT_ROWS_PAIRS;
@@ -697,7 +724,7 @@ static int launch_fft(moco_plan *p, const void *img, int64_t fstride, int pitch,
     a.P = F.P; a.twc = F.twc; a.img = im; a.fstride = fstride; a.pitch = pitch;
     a.tpl = (const uint16_t *)p->tpl[L]; a.tpitch = p->pitch[L];
     a.ga = F.ga; a.gb = (const u64 *)p->gb; a.g = g;
-    a.scale = (double)(1u << (4 * L)); a.eps_rel = F.eps_rel; a.B = (int)nb;
+    a.scale = (double)(1u << (4 * L)); a.eps_f = std::ldexp(F.bound_Cf, -24); a.eps_i = std::ldexp(F.bound_Ci, -24); a.b1 = F.b1; a.B = (int)nb;
     a.shift_out = shift_out + 2 * b0; a.f_out = f_out ? f_out + b0 : nullptr;
     a.flags = flags ? flags + b0 : nullptr;
     a.qcount = qcount ? qcount + b0 : F.qc + b0;
@@ -1613,6 +1640,13 @@ int moco_score_grid(moco_plan *p, const void *d_frames, int64_t T, double *d_f,
                    d_f + f0 * WW, (cudaStream_t)stream);
     if (rc) return rc;
   }
+  return MOCO_OK;
+}
+
+int moco_fft_bound(const moco_plan *p, double *Cf, double *Ci) {
+  if (!p || !Cf || !Ci || !p->fft.ready) return MOCO_EINVAL;
+  *Cf = p->fft.bound_Cf;
+  *Ci = p->fft.bound_Ci;
   return MOCO_OK;
 }
 
