@@ -452,6 +452,8 @@ struct F2ColsArgs {
   float2 *P;                // [B][W][Kc]                  (frames)
   float2 *Bout;             // template mode: Bc out, or null
   float scale;              // template mode: 1/(Mr Mc)
+  u64 *E;                   // [B][esz] energy partials: the corner row prefixes become 2-D
+                            // corner sums here (split over the frame's blocks)
 };
 
 template <int P>
@@ -482,6 +484,26 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_cols(F2ColsArgs a) {
       for (int h = 0; h < 4; ++h) {
         const int u = u0 + 32 * h + lane;
         if (u < Mr) xq[G::ix(u)] = v[h];
+      }
+    }
+  }
+  if (a.E) {
+    // corner tables of the DP: the row prefixes RP[quad][i][a] of k_fft2_rows become
+    // CP[quad][p-1][a] = sum_{i<p} RP[quad][i][a], in place; this block scans its share of
+    // the 4 hw columns (quad, a), the column held in registers while it is loaded
+    const int hw = a.hw, ncol = 4 * hw;
+    const int cpb = (ncol + ncb - 1) / ncb, c0 = (blockIdx.x - (int)(f * ncb)) * cpb, c1 = min(ncol, c0 + cpb);
+    u64 *RP = a.E + f * f2_esz(hw) + 1 + 4 * hw;
+    for (int c = c0 + warp; c < c1; c += F2_WARPS) {
+      const int quad = c / hw, aa = c - quad * hw;
+      u64 *col = RP + (int64_t)quad * hw * hw + aa;
+      u64 carry = 0;
+      for (int i0 = 0; i0 < hw; i0 += 32) {
+        const int i = i0 + lane;
+        const u64 v = i < hw ? col[(int64_t)i * hw] : 0;
+        const u64 sc = warp_scan_incl(v) + carry;
+        if (i < hw) col[(int64_t)i * hw] = sc;
+        carry = __shfl_sync(0xffffffffu, sc, 31);
       }
     }
   }
@@ -652,8 +674,7 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_score(F2ScoreArgs a) {
   float2 *x = tw + Mc;
   u64 *RX = reinterpret_cast<u64 *>(x + G::NF * S);   // [W] excluded-row energy per s
   u64 *CX = RX + W;                                   // [W] excluded-column energy per t
-  u64 *CP = CX + W;                                   // [2 NF][2][hw] corner sums per block row
-  double *rinv = reinterpret_cast<double *>(CP + 2 * G::NF * 2 * hw);   // [W]
+  double *rinv = reinterpret_cast<double *>(CX + W);                    // [W]
   double *cinv = rinv + W;                                               // [W]
   __shared__ float redf[32];
   __shared__ int qn, qlist[FFT_QCAP], last;
@@ -692,21 +713,6 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_score(F2ScoreArgs a) {
       carry = __shfl_sync(0xffffffffu, sc, 31);
     }
   }
-  // corner sums CP[row][t<0][|t|-1] = sum_{i<|s|} (row prefix of corner row i at |t|): one
-  // thread per (sign of s, sign of t, |t|), running once over the excluded rows
-  for (int task = threadIdx.x; task < 4 * hw; task += blockDim.x) {
-    const int g = task / (2 * hw), r2 = task - g * 2 * hw, tneg = r2 / hw, aa = r2 - tneg * hw;
-    // rows of this block with s > 0 (g = 0) or s < 0 (g = 1): the largest |s| among them
-    const int smax = g == 0 ? s0 + nr - 1 - hw : hw - s0;
-    const u64 *rp = E + 1 + 4 * hw + (int64_t)((g ? 2 : 0) + tneg) * hw * hw + aa;
-    u64 acc = 0;
-#pragma unroll 4
-    for (int i = 0; i < smax; ++i) {
-      acc += __ldg(rp + (int64_t)i * hw);
-      const int rl = (g == 0 ? hw + i + 1 : hw - i - 1) - s0;
-      if (rl >= 0 && rl < nr) CP[(rl * 2 + tneg) * hw + aa] = acc;
-    }
-  }
   for (int k = threadIdx.x; k < W; k += blockDim.x) {
     rinv[k] = 1.0 / (a.scale * (double)(a.mc - abs(k - hw)));
     cinv[k] = 1.0 / (double)(a.nc - abs(k - hw));
@@ -722,6 +728,7 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_score(F2ScoreArgs a) {
     const float *xr = reinterpret_cast<const float *>(x + (rl >> 1) * S) + (rl & 1);
     const double ri = rinv[si];
     const u64 rx = RX[si];
+    const u64 *CPq = E + 1 + 4 * hw + (int64_t)(s < 0 ? 2 : 0) * hw * hw;
     for (int ti = lane; ti < W; ti += 32) {
       const int t = ti - hw;
       const int tt = t < 0 ? t + Mc : t;
@@ -729,7 +736,8 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_score(F2ScoreArgs a) {
       const int lag = si * W + ti;
       if (a.h_out) a.h_out[f * W * W + lag] = h;
       u64 ga = tot - rx - CX[ti];
-      if (s != 0 && t != 0) ga += CP[(rl * 2 + (t < 0)) * hw + abs(t) - 1];
+      if (s != 0 && t != 0)   // 2-D corner sum of the excluded |s| x |t| corner (k_fft2_cols)
+        ga += __ldg(CPq + (t < 0 ? hw * hw : 0) + (int64_t)(abs(s) - 1) * hw + abs(t) - 1);
       const double inv = ri * cinv[ti];
       const double fa = ((double)ga + (double)a.gb[lag] - 2.0 * (double)h) * inv;
       const double del = eps2 * inv;

@@ -414,7 +414,9 @@ static int fft_init(moco_plan *p) {
   // sub-batches sized so the spectra stay in L2 (about 80 MB)
   const size_t per = F.v2 ? (size_t)g.Kc * g.mcp * 8 + (size_t)g.W * g.Kc * 8 + (size_t)g.W * g.W * 4 + esz
                           : (size_t)g.Kc * g.mcp * 8 + (size_t)g.W * g.Kc * 8 + (size_t)g.W * g.W * 8;
-  F.cap = std::max<int64_t>(1, std::min<int64_t>(p->cap, (int64_t)(((F.v2 ? 40u : 80u) << 20) / per)));
+  size_t budget = (size_t)(F.v2 ? 160u : 80u) << 20;   // per set (v2: two sets); measured: 40 -> 160 MB per set C3 595 -> 628 k, w = 85 306 -> 348 k frames/s
+  if (const char *mb = getenv("MOCO_FFT_MB")) budget = (size_t)std::max(4, atoi(mb)) << 20;   // tuning (plan creation)
+  F.cap = std::max<int64_t>(1, std::min<int64_t>(p->cap, (int64_t)(budget / per)));
   const int64_t nset = F.v2 ? 2 : 1;   // v2: two scratch sets (two streams)
   const int Mr = g.Lr.N, Mc = g.Lc.N;
   auto al = [&](void **q, size_t bytes) {
@@ -471,7 +473,7 @@ static int fft_init(moco_plan *p) {
         const int stg = std::max(f2_stage_bytes(fft2_rows_per_max(G::NF, LK, g.nc), LK, g.nc),
                                  f2_stage_bytes(fft2_rows_per_max(G::NF, 0, g.nc), 0, g.nc));
         F.smem2_rows = stg + (G::N + G::NF * G::STRIDE) * 8 + 2 * G::NF * 8 + 2 * g.hw * 8;
-        F.smem2_score = (G::N + G::NF * G::STRIDE) * 8 + 2 * g.W * 8 + 2 * G::NF * 2 * g.hw * 8 + 2 * g.W * 8;
+        F.smem2_score = (G::N + G::NF * G::STRIDE) * 8 + 2 * g.W * 8 + 2 * g.W * 8;
         if (smem_attr(k_fft2_rows<P, 0>, F.smem2_rows) != cudaSuccess ||
             smem_attr(k_fft2_rows<P, 1>, F.smem2_rows) != cudaSuccess ||
             smem_attr(k_fft2_score<P>, F.smem2_score) != cudaSuccess)
@@ -565,6 +567,7 @@ static int fft2_sub(moco_plan *p, const char *fr, int64_t fstride, int pitch, in
       F2ColsArgs c{};
       c.S = F.S + so * g.Kc * g.mcp; c.mc = g.mc; c.Kc = g.Kc; c.mcp = g.mcp; c.W = g.W; c.hw = g.hw;
       c.per = per; c.tw = F.twr; c.Bc = F.Bc; c.P = Pset; c.Bout = nullptr; c.scale = 0.f;
+      c.E = F.E + so * f2_esz(g.hw);
       ProfScope ps(p, MOCO_K_COARSE, st);
       k_fft2_cols<P><<<(unsigned)(nb * nblk), F2_THREADS, F.smem2_cols, st>>>(c);
     }
