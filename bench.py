@@ -79,8 +79,14 @@ def kernel_models(spec, esz, algo):
         coarse = ("tensor_i8", 2.0 * 4 * W * W * mc * nc, "op")
         prep = ("hbm", m * n * esz + 2 * (mc + 64) * nc, "B")
     elif algo == "fft":
-        coarse = ("alu", fm["coarse"], "flop")
-        prep = ("hbm", mc * nc * 2, "B")        # k_energy_u16 reads the coarse image
+        # kernels_fft2.cuh: rows (block sums, energies, forward row FFTs) = MOCO_K_PREP, columns
+        # (forward column FFTs, spectrum product, inverse column FFTs) = MOCO_K_COARSE, score
+        # (inverse row FFTs of the lag rows, certified intervals) = MOCO_K_SCORE; the
+        # SURVEY §8(d) FFT flops split 1/4 : 1/2 + product : 1/4
+        P_ = (mc + spec.w) * (nc + spec.w)
+        half = 2.5 * P_ * math.log2(P_)
+        coarse = ("alu", half + 3 * P_, "flop")
+        prep = ("alu", 0.5 * half + 2 * mc * nc, "flop")
     else:
         coarse = ("alu", 2.0 * W * W * mc * nc, "op")
         prep = ("hbm", mc * nc * 2, "B")
@@ -88,7 +94,8 @@ def kernel_models(spec, esz, algo):
         "downsample": ("hbm", down_bytes, "B"),
         "coarse": coarse,
         "tc_prep": prep,
-        "tc_score": ("alu", 6 * W * W, "flop"),
+        "tc_score": ("alu", (0.5 * 2.5 * (mc + spec.w) * (nc + spec.w) * math.log2((mc + spec.w) * (nc + spec.w))
+                             if algo == "fft" else 0) + 6 * W * W, "flop"),
         # tensor-core refine sums (kernels_rtc.cuh): one read of each refine level's frame;
         # the MMAs need < 10 % of the tensor pipe, so the bound is the read
         "refine": ("hbm", sum((m >> l) * (n >> l) * 2 for l in range(L)), "B") if esz == 2
