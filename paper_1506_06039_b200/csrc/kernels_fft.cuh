@@ -416,12 +416,14 @@ __global__ void k_tpl_dft_rows(const uint16_t *__restrict__ b, int pitch, int nc
   }
   __syncthreads();
   const int i = blockIdx.x;
-  const uint16_t *br = b + (int64_t)i * pitch;
+  double *row = reinterpret_cast<double *>(tw64 + Mc);   // the template row, staged once
+  for (int j = threadIdx.x; j < nc; j += blockDim.x) row[j] = (double)b[(int64_t)i * pitch + j];
+  __syncthreads();
   for (int k = threadIdx.x; k < Kc; k += blockDim.x) {
     double re = 0, im = 0;
     int m = 0;
     for (int j = 0; j < nc; ++j) {
-      const double v = (double)br[j];
+      const double v = row[j];
       re += v * tw64[m].x;
       im += v * tw64[m].y;
       m += k;
@@ -440,12 +442,15 @@ __global__ void k_tpl_dft_cols(const double2 *__restrict__ R, int mc, int Mr, in
   }
   __syncthreads();
   const int k = blockIdx.x;
+  double2 *col = tw64 + Mr;   // the column R[.][k], staged once
+  for (int i = threadIdx.x; i < mc; i += blockDim.x) col[i] = R[(int64_t)i * Kc + k];
+  __syncthreads();
   const double scale = 1.0 / ((double)Mr * (double)Mc);
   for (int u = threadIdx.x; u < Mr; u += blockDim.x) {
     double re = 0, im = 0;
     int m = 0;
     for (int i = 0; i < mc; ++i) {
-      const double2 r = R[(int64_t)i * Kc + k];
+      const double2 r = col[i];
       const double2 t = tw64[m];
       re += r.x * t.x - r.y * t.y;
       im += r.x * t.y + r.y * t.x;

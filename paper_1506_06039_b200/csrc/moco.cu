@@ -592,7 +592,9 @@ static int fft2_sub(moco_plan *p, const char *fr, int64_t fstride, int pitch, in
       a.shift_out = shift_out; a.f_out = f_out; a.flags = flags; a.qcount = qcount; a.h_out = h_out;
       a.qn = F.qn + so; a.ql = F.ql + so * FFT_QCAP; a.cnt2 = F.cnt2 + so;
       a.nacc = F.nacc + so * (int64_t)std::max(FFT_QCAP, g.W * g.W);
-      a.rparts = std::max(1, std::min(16, g.mc / 16));
+      // row parts per frame: 16 rows each for full batches, down to 2 rows when few frames
+      // (the closed-loop call: the exact sums are latency-bound, one block per part)
+      a.rparts = (int)std::max<int64_t>(1, std::min<int64_t>(g.mc / 2, std::max<int64_t>(g.mc / 16, 4 * p->nsm / nb)));
       ProfScope ps(p, MOCO_K_SCORE, st);
       k_fft2_score<P><<<(unsigned)(nb * nblk), F2_THREADS, F.smem2_score, st>>>(a);
       const unsigned rg = (unsigned)(nb * a.rparts);
@@ -647,8 +649,9 @@ static int fft_set_template(moco_plan *p, cudaStream_t st) {
   const FftGeom &g = F.g;
   const int Mr = g.Lr.N, Mc = g.Lc.N;
   CK(cudaMemsetAsync(F.b1, 0, 8, st));
-  k_tpl_dft_rows<<<g.mc, 256, Mc * 16, st>>>((const uint16_t *)p->tpl[L], p->pitch[L], g.nc, Mc, g.Kc, F.R64);
-  k_tpl_dft_cols<<<g.Kc, 256, Mr * 16, st>>>(F.R64, g.mc, Mr, Mc, g.Kc, F.Bc, F.b1, (const uint16_t *)p->tpl[L],
+  k_tpl_dft_rows<<<g.mc, 256, Mc * 16 + g.nc * 8, st>>>((const uint16_t *)p->tpl[L], p->pitch[L], g.nc, Mc, g.Kc,
+                                                          F.R64);
+  k_tpl_dft_cols<<<g.Kc, 256, (Mr + g.mc) * 16, st>>>(F.R64, g.mc, Mr, Mc, g.Kc, F.Bc, F.b1, (const uint16_t *)p->tpl[L],
                                             p->pitch[L], g.nc);
   CKL("fft template spectrum");
   F.tpl_ready = true;
