@@ -78,6 +78,10 @@ struct TcPlan {
   u64 *ga2 = nullptr;
   uint8_t *T8 = nullptr;    // template parts [2][mc][nc]
   uint8_t *Btab = nullptr;  // the B tiles of every (strip, pair), built once per template (or null)
+  // fused search (kernels_tcf.cuh, levels <= 1): layout and the corner-square scratch
+  bool fused = false;
+  int f_smem = 0, f_offE = 0, f_offBars = 0, f_nch = 0;
+  u64 *corner = nullptr;    // [cap][4][w][w]
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -1117,6 +1121,8 @@ inline void tc_free(TcPlan *tc) {
   tc->G2 = nullptr; tc->ga2 = nullptr;
   if (tc->T8) cudaFree(tc->T8);
   if (tc->Btab) cudaFree(tc->Btab);
+  if (tc->corner) cudaFree(tc->corner);
+  tc->corner = nullptr;
   tc->G = nullptr; tc->ga = nullptr; tc->T8 = nullptr; tc->Btab = nullptr;
   tc->ready = tc->tpl_ready = false;
 }

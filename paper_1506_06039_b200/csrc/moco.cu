@@ -23,6 +23,7 @@
 #include "kernels_rtc.cuh"
 #include "kernels_fft.cuh"
 #include "kernels_fft2.cuh"
+#include "kernels_tcf.cuh"
 #include "kernels_fra.cuh"
 
 using namespace moco;
@@ -82,6 +83,8 @@ struct moco_plan {
     int fra_min = 64;      // MOCO_FRA_MIN: smallest batch for k_refine_frame
     bool nofuse_ds = false, ga_inpick = false, nopipe = false;
     bool fft_v1 = false;   // MOCO_FFT_V1=1: the generic FFT kernels (kernels_fft.cuh) for every length
+    int tc_fused = 0;      // MOCO_TC_FUSED=1: k_tc_fused (operand strips built in the search kernel,
+                           // kernels_tcf.cuh; measured slower: C2 1.38 vs 1.83 M frames/s)
   } knob;
   bool simple_refine;         // MOCO_REFINE=simple: unfused K6/K7 (cross-check in tests)
   int simple_level;           // MOCO_REFINE=simpleN: simple K6 at level N only (debug)
@@ -755,6 +758,26 @@ static int launch_fft(moco_plan *p, const void *img, int64_t fstride, int pitch,
   return MOCO_OK;
 }
 
+// Fused tensor-core search (kernels_tcf.cuh): levels <= 1, B tiles from the table, the
+// layout fits; needs the corner-square scratch for a batch.  Failure just leaves the
+// two-kernel path (k_tc_prep + k_tc_coarse).
+static void tcf_setup(moco_plan *p) {
+  TcPlan &tc = p->tc;
+  const TcGeom &g = tc.g;
+  if (p->levels > 1 || g.stg || !p->knob.tc_fused) return;
+  if (!tcf_layout(g, &tc.f_smem, &tc.f_offE, &tc.f_offBars, &tc.f_nch)) return;
+  if (cudaMalloc(&tc.corner, (size_t)p->cap * 4 * g.w * g.w * sizeof(u64)) != cudaSuccess) {
+    cudaGetLastError();
+    tc.corner = nullptr;
+    return;
+  }
+  if (smem_attr(k_tc_fused<0>, tc.f_smem) != cudaSuccess || smem_attr(k_tc_fused<1>, tc.f_smem) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  tc.fused = true;
+}
+
 static int pipe_create(moco_plan *p) {
   for (int k = 0; k < 3; ++k) CK(cudaStreamCreateWithFlags(&p->ps[k], cudaStreamNonBlocking));
   for (int k = 0; k < 2; ++k) {
@@ -805,6 +828,7 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
     p->knob.ga_inpick = getenv("MOCO_GA_INPICK") != nullptr;
     p->knob.nopipe = getenv("MOCO_NOPIPE") != nullptr;
     p->knob.fft_v1 = getenv("MOCO_FFT_V1") != nullptr;
+    if (const char *v = getenv("MOCO_TC_FUSED")) p->knob.tc_fused = atoi(v);
     if (const char *v = getenv("MOCO_FRA")) p->knob.fra = atoi(v);
     if (const char *v = getenv("MOCO_FRA_MIN")) p->knob.fra_min = std::max(1, atoi(v));
   }
@@ -935,6 +959,7 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
   if (tc_ok && tc_auto_prefers(p->w)) {
     if (tc_init(&p->tc, p->w, p->ml[levels], p->nl[levels], levels, p->bits + 2 * levels, p->cap) == 0) {
       p->algo = MOCO_ALGO_TC;
+      tcf_setup(p);
       // whole waves of the tensor-core search per internal batch (CTAs/SM x GG*F frames)
       const int64_t wave = (int64_t)nsm * p->tc.g.ctas * p->tc.g.GG * p->tc.g.F;
       // one wave per internal batch when the search is short and the batches pipeline
@@ -1367,8 +1392,32 @@ static int launch_tc_coarse(moco_plan *p, int64_t B, const uint8_t *G, const u64
   return MOCO_OK;
 }
 
+// The fused search (k_tc_fused) on B level-0 frames with row pitch n.
+static int launch_tc_fused(moco_plan *p, const void *frames_b, int64_t B, int32_t *shift_out, double *f_out,
+                           uint8_t *flags, double *grid_out, cudaStream_t st) {
+  const TcPlan &tc = p->tc;
+  const TcGeom &g = tc.g;
+  const int64_t groups = (B + g.F - 1) / g.F;
+  TcfArgs fa;
+  fa.t.G = nullptr; fa.t.T8 = tc.T8; fa.t.Btab = tc.Btab; fa.t.ga = nullptr; fa.t.gb = (const u64 *)p->gb;
+  fa.t.g = g; fa.t.scale = (double)(1u << (4 * p->levels)); fa.t.B = (int)B;
+  fa.t.shift_out = shift_out; fa.t.f_out = f_out; fa.t.flags = flags; fa.t.grid_out = grid_out;
+  fa.frames = (const uint16_t *)frames_b; fa.fstride = (int64_t)p->m * p->n; fa.n = p->n;
+  fa.corner = tc.corner; fa.offE = tc.f_offE; fa.offBars = tc.f_offBars; fa.nch = tc.f_nch;
+  {
+    ProfScope ps(p, MOCO_K_COARSE, st);
+    const unsigned grid = (unsigned)((groups + g.GG - 1) / g.GG);
+    if (p->levels == 0) k_tc_fused<0><<<grid, TC_THREADS, tc.f_smem, st>>>(fa);
+    else k_tc_fused<1><<<grid, TC_THREADS, tc.f_smem, st>>>(fa);
+  }
+  p->launches++;
+  CKL("k_tc_fused");
+  return MOCO_OK;
+}
+
 static int launch_tc(moco_plan *p, const void *frames_b, int64_t B, int32_t *shift_out, double *f_out,
                      uint8_t *flags, double *grid_out, cudaStream_t st, void *img1 = nullptr) {
+  if (p->tc.fused && !img1) return launch_tc_fused(p, frames_b, B, shift_out, f_out, flags, grid_out, st);
   int rc = launch_tc_prep(p, frames_b, B, p->tc.G, p->tc.ga, st, img1);
   if (rc) return rc;
   return launch_tc_coarse(p, B, p->tc.G, p->tc.ga, shift_out, f_out, flags, grid_out, st);
@@ -1545,19 +1594,24 @@ static int align_tc_pipelined(moco_plan *p, const void *d_frames, int64_t T, int
     const int64_t B = std::min<int64_t>(p->cap, T - f0);
     const int buf = (int)(k & 1);
     const char *fr = (const char *)d_frames + f0 * fbytes;
-    if (k >= 2) CK(cudaStreamWaitEvent(sp, p->pe_free[buf], 0));
+    const bool fused = p->tc.fused && !two;
     const bool emit1 = two && prep_emits_l1(p);
-    int rc = launch_tc_prep(p, fr, B, G[buf], ga[buf], sp, emit1 ? img1[buf] : nullptr);
-    if (rc) return rc;
-    if (two && !emit1) {
-      rc = launch_downsample(p, 0, fr, (int64_t)p->m * p->n, img1[buf], B, sp);
+    int rc = MOCO_OK;
+    if (!fused) {
+      if (k >= 2) CK(cudaStreamWaitEvent(sp, p->pe_free[buf], 0));
+      rc = launch_tc_prep(p, fr, B, G[buf], ga[buf], sp, emit1 ? img1[buf] : nullptr);
       if (rc) return rc;
+      if (two && !emit1) {
+        rc = launch_downsample(p, 0, fr, (int64_t)p->m * p->n, img1[buf], B, sp);
+        if (rc) return rc;
+      }
+      CK(cudaEventRecord(p->pe_prep[buf], sp));
+      CK(cudaStreamWaitEvent(sm, p->pe_prep[buf], 0));
     }
-    CK(cudaEventRecord(p->pe_prep[buf], sp));
-    CK(cudaStreamWaitEvent(sm, p->pe_prep[buf], 0));
     if (k >= 2) CK(cudaStreamWaitEvent(sm, p->pe_pick[buf], 0));   // sh1/racc of batch k-2 consumed
     int32_t *sc = two ? p->sh2b[buf] : sh1[buf];
-    rc = launch_tc_coarse(p, B, G[buf], ga[buf], sc, nullptr, d_flags ? d_flags + f0 : nullptr, nullptr, sm);
+    rc = fused ? launch_tc_fused(p, fr, B, sc, nullptr, d_flags ? d_flags + f0 : nullptr, nullptr, sm)
+               : launch_tc_coarse(p, B, G[buf], ga[buf], sc, nullptr, d_flags ? d_flags + f0 : nullptr, nullptr, sm);
     if (rc) return rc;
     if (two) {
       rc = launch_refine_h(p, 1, img1[buf], fs1, B, sc, sh1[buf], nullptr, nullptr, sm, racc[buf]);

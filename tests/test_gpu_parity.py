@@ -126,6 +126,26 @@ def test_tc_btile_table_equals_in_cta_build(c, T, monkeypatch):
         assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("c,T", [(1, 1000), (2, 2500), (3, 2600), (2, 37)])
+def test_tc_fused_search_equals_two_kernel_search(c, T, monkeypatch):
+    """The search with the operand preparation fused in (k_tc_fused: strips built from the
+    raw frames while the tensor cores run, energies in the kernel) and the two-kernel
+    search (k_tc_prep planes through HBM + k_tc_coarse, the default): identical shifts,
+    f_min, corrected frames and edge flags -- whole stacks through the pipelined batches
+    (C2, C3), levels = 0 (C1) and a ragged batch (37 frames)."""
+    spec = config_spec(c, T=T)
+    st = make_stack(spec, 0, T, device=DEV)
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("MOCO_TC_FUSED", mode)
+        p = _plan_for(spec, "tc")
+        p.set_template(st.template)
+        sh, fm, co, fl = p.align(st.frames, corrected=True, flags=True)
+        out[mode] = (sh, fm, co.view(torch.int16), fl)
+    for a, b in zip(out["1"], out["0"]):
+        assert torch.equal(a, b)
+
+
 @pytest.mark.parametrize("c,T", [(2, 2100), (4, 24)])
 def test_fused_refine_equals_simple_refine(c, T, monkeypatch):
     """The fused, register-blocked refine+apply kernel and the simple one-candidate-
