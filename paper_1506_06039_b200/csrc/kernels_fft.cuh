@@ -406,8 +406,71 @@ __global__ void k_fft_twiddles(float2 *tw, int N) {
 //   Bc[k][u] = conj(sum_i R[i][k] e^{-2 pi i i u / Mr}) / (Mr Mc), rounded once to fp32
 // twiddles by sincospi in double; |rounding error| ~ 1e-16 relative to ||b||_1, far
 // below the fp32 rounding of the result.
+// Template statistics for the mean-removed FFT path (kernels_fft2.cuh): with `mean` set,
+// mu = round(sum b / (mc nc)) (else 0), then ||b - mu||_1 and ||b - mu||_2^2 over the
+// template's support.  st[0] = mu, st[1] = ||b'||_1, st[2] = ||b'||_2^2.  One block.
+__global__ void k_tpl_stats(const uint16_t *__restrict__ b, int pitch, int mc, int nc, int mean,
+                            long long *__restrict__ st) {
+  __shared__ unsigned long long red[32];
+  __shared__ long long mu_s;
+  unsigned long long acc = 0;
+  for (int e = threadIdx.x; e < mc * nc; e += blockDim.x) acc += b[(int64_t)(e / nc) * pitch + e % nc];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += red[k];
+    const unsigned long long n = (unsigned long long)mc * nc;
+    mu_s = mean ? (long long)((t + n / 2) / n) : 0;
+  }
+  __syncthreads();
+  const long long mu = mu_s;
+  unsigned long long a1 = 0, a2 = 0;
+  for (int e = threadIdx.x; e < mc * nc; e += blockDim.x) {
+    const long long d = (long long)b[(int64_t)(e / nc) * pitch + e % nc] - mu;
+    a1 += (unsigned long long)(d < 0 ? -d : d);
+    a2 += (unsigned long long)(d * d);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+  }
+  __syncthreads();
+  __shared__ unsigned long long r1[32], r2[32];
+  if ((threadIdx.x & 31) == 0) { r1[threadIdx.x >> 5] = a1; r2[threadIdx.x >> 5] = a2; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t1 = 0, t2 = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) { t1 += r1[k]; t2 += r2[k]; }
+    st[0] = mu;
+    st[1] = (long long)t1;
+    st[2] = (long long)t2;
+  }
+}
+// gl[s][t] = sum over the template rectangle of D_{s,t} of b (the linear analogue of g_b,
+// k_template_energy): one block per lag, once per template.
+__global__ void k_template_lin(const uint16_t *__restrict__ b, int pitch, int mc, int nc, int w,
+                               long long *__restrict__ gl) {
+  const int W = 2 * w - 1;
+  const int s = (int)(blockIdx.x / W) - (w - 1), t = (int)(blockIdx.x % W) - (w - 1);
+  const int i0 = max(0, -s), i1 = mc - max(0, s), j0 = max(0, -t), j1 = nc - max(0, t);
+  unsigned long long acc = 0;
+  for (int i = i0; i < i1; ++i)
+    for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) acc += b[(int64_t)i * pitch + j];
+  __shared__ unsigned long long red[32];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t2 = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t2 += red[k];
+    gl[blockIdx.x] = (long long)t2;
+  }
+}
+
 __global__ void k_tpl_dft_rows(const uint16_t *__restrict__ b, int pitch, int nc, int Mc, int Kc,
-                               double2 *__restrict__ R) {
+                               double2 *__restrict__ R, const long long *__restrict__ mu) {
   extern __shared__ double2 tw64[];
   for (int m = threadIdx.x; m < Mc; m += blockDim.x) {
     double s_, c_;
@@ -416,8 +479,9 @@ __global__ void k_tpl_dft_rows(const uint16_t *__restrict__ b, int pitch, int nc
   }
   __syncthreads();
   const int i = blockIdx.x;
-  double *row = reinterpret_cast<double *>(tw64 + Mc);   // the template row, staged once
-  for (int j = threadIdx.x; j < nc; j += blockDim.x) row[j] = (double)b[(int64_t)i * pitch + j];
+  double *row = reinterpret_cast<double *>(tw64 + Mc);   // the template row (minus mu), staged once
+  const double m0 = mu ? (double)mu[0] : 0.0;
+  for (int j = threadIdx.x; j < nc; j += blockDim.x) row[j] = (double)b[(int64_t)i * pitch + j] - m0;
   __syncthreads();
   for (int k = threadIdx.x; k < Kc; k += blockDim.x) {
     double re = 0, im = 0;

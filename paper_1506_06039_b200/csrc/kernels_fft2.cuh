@@ -260,8 +260,10 @@ __device__ __forceinline__ u64 warp_scan_incl(u64 v) {
 //   [1+4hw + (quad*hw + i)*hw + (a-1)]  corner row prefixes: sum of a^2 over the first a
 //                             columns from the quad's side of its i-th row from its edge
 //                             (quad = bottom*2 + right)
-// The atomic slots are zero on entry; the pick re-zeroes them.
+// The atomic slots are zero on entry; the pick re-zeroes them.  Each frame holds two such
+// sets: the squares a^2 (g_a) and the values a themselves (S_a, for the mean removal).
 __host__ __device__ constexpr int f2_esz(int hw) { return 1 + 4 * hw + 4 * hw * hw; }
+__host__ __device__ constexpr int f2_esz2(int hw) { return 2 * f2_esz(hw); }
 
 struct F2RowsArgs {
   const uint16_t *frames;   // level-0 frames (levels L) or coarse images (L = 0)
@@ -271,7 +273,8 @@ struct F2RowsArgs {
   int per;                  // row pairs per block (<= NF)
   const float2 *tw;         // [Mc]
   float2 *S;                // [B][Kc][mcp]
-  u64 *E;                   // [B][esz] energy partials, or null (template)
+  u64 *E;                   // [B][2 esz] energy and linear partials
+  const long long *mu;      // [0]: the integer mean removed from the frames (k_tpl_stats)
 };
 
 // raw bytes a k_fft2_rows block stages: 2 per row pairs x 2^L raw rows of 2^L nc samples
@@ -322,12 +325,17 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_rows(F2RowsArgs a) {
   // accumulates over its rows
   const int nch = nc >> 3;
   const int cl = lane, cr = lane + 32 * ((nch - 1 - lane) >> 5);
-  const bool hasL = a.E && lane < nch && 8 * cl < hw, hasR = a.E && lane < nch && 8 * cr + 8 > nc - hw;
+  const bool hasL = lane < nch && 8 * cl < hw, hasR = lane < nch && 8 * cr + 8 > nc - hw;
+  // squares (g_a) and values (S_a) of the edge columns, per lane
+  // (values: 32-bit, < 2^16 x 2 rows x 2 NF rows per block)
   u64 eL[8], eR[8];
+  uint32_t lL[8], lR[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) eL[k] = eR[k] = 0;
-  u64 wtot = 0;
-  u64 *E = a.E ? a.E + f * f2_esz(hw) : nullptr;
+  for (int k = 0; k < 8; ++k) { eL[k] = eR[k] = 0; lL[k] = lR[k] = 0; }
+  u64 wtot = 0, wlin = 0;
+  u64 *E = a.E + f * f2_esz2(hw), *EL = E + f2_esz(hw);
+  const int mu = (int)a.mu[0];
+  const bool lin = mu != 0;   // mean removal on: the linear partials (S_a) are needed
   // 8 coarse values of coarse row rl (block-local), columns 8c .. 8c+7, from the staged rows
   auto load8 = [&](int rl, int c, uint32_t (&v)[8]) {
 #pragma unroll
@@ -353,72 +361,91 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_rows(F2RowsArgs a) {
   };
   for (int q = warp; q < np; q += F2_WARPS) {
     float2 *xq = x + q * S;
+    const int r0 = 2 * (p0 + q);
+    const float m0 = r0 < mc ? (float)mu : 0.f, m1 = r0 + 1 < mc ? (float)mu : 0.f;
     u64 rs0 = 0, rs1 = 0;
+    uint32_t ls0 = 0, ls1 = 0;   // < 2^16 x nc / 32 per lane
     for (int c = lane; c < nch; c += 32) {
       uint32_t v0[8], v1[8];
       load8(2 * q, c, v0);
       load8(2 * q + 1, c, v1);
-      // natural-order slots of columns 8c .. 8c+7 (at most one row break of the padding)
+      // natural-order slots of columns 8c .. 8c+7 (at most one row break of the padding);
+      // the transforms see a - mu on the support (exact in fp32), 0 outside
       const int j0 = 8 * c, q0 = j0 / N2, brk = (q0 + 1) * N2 - j0;
       float2 *xc = xq + j0 + q0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) xc[k + (k >= brk ? 1 : 0)] = make_float2((float)v0[k], (float)v1[k]);
-      if (a.E) {
+      for (int k = 0; k < 8; ++k)
+        xc[k + (k >= brk ? 1 : 0)] = make_float2((float)v0[k] - m0, (float)v1[k] - m1);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t s0 = v0[k] * v0[k], s1 = v1[k] * v1[k];   // < 2^32 (coarse values < 2^16)
-          rs0 += s0;
-          rs1 += s1;
-          if (hasL && c == cl) eL[k] += (u64)s0 + s1;
-          if (hasR && c == cr) eR[k] += (u64)s0 + s1;
-        }
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t s0 = v0[k] * v0[k], s1 = v1[k] * v1[k];   // < 2^32 (coarse values < 2^16)
+        rs0 += s0;
+        rs1 += s1;
+        ls0 += v0[k];
+        ls1 += v1[k];
+        if (hasL && c == cl) { eL[k] += (u64)s0 + s1; lL[k] += v0[k] + v1[k]; }
+        if (hasR && c == cr) { eR[k] += (u64)s0 + s1; lR[k] += v0[k] + v1[k]; }
       }
     }
-    if (a.E) {
-      rs0 = warp_sum(rs0);
-      rs1 = warp_sum(rs1);
-      if (lane < 2) {
-        const int r = 2 * (p0 + q) + lane;
-        const u64 rs = lane ? rs1 : rs0;
-        if (r < mc) {
-          wtot += rs;
-          if (r < hw) E[1 + r] = rs;
-          if (r >= mc - hw) E[1 + hw + (mc - 1 - r)] = rs;
-        }
+    rs0 = warp_sum(rs0);
+    rs1 = warp_sum(rs1);
+    if (lin) {
+      ls0 = warp_sum(ls0);
+      ls1 = warp_sum(ls1);
+    }
+    if (lane < 2) {
+      const int r = r0 + lane;
+      const u64 rs = lane ? rs1 : rs0, ls = lane ? ls1 : ls0;
+      if (r < mc) {
+        wtot += rs;
+        wlin += ls;
+        if (r < hw) { E[1 + r] = rs; EL[1 + r] = ls; }
+        if (r >= mc - hw) { E[1 + hw + (mc - 1 - r)] = rs; EL[1 + hw + (mc - 1 - r)] = ls; }
       }
     }
   }
-  if (a.E) {
-    if (lane < 2 && wtot) atomicAdd(&E[0], wtot);
+  if (lane < 2 && wtot) atomicAdd(&E[0], wtot);
+  if (lane < 2 && wlin) atomicAdd(&EL[0], wlin);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int jl = 8 * cl + k, jr = 8 * cr + k;
-      if (hasL && jl < hw && eL[k]) atomicAdd(&E[1 + 2 * hw + jl], eL[k]);
-      if (hasR && jr < nc && jr >= nc - hw && eR[k]) atomicAdd(&E[1 + 3 * hw + (nc - 1 - jr)], eR[k]);
+  for (int k = 0; k < 8; ++k) {
+    const int jl = 8 * cl + k, jr = 8 * cr + k;
+    if (hasL && jl < hw) {
+      if (eL[k]) atomicAdd(&E[1 + 2 * hw + jl], eL[k]);
+      if (lin && lL[k]) atomicAdd(&EL[1 + 2 * hw + jl], (u64)lL[k]);
+    }
+    if (hasR && jr < nc && jr >= nc - hw) {
+      if (eR[k]) atomicAdd(&E[1 + 3 * hw + (nc - 1 - jr)], eR[k]);
+      if (lin && lR[k]) atomicAdd(&EL[1 + 3 * hw + (nc - 1 - jr)], (u64)lR[k]);
     }
   }
   __syncthreads();
-  if (a.E) {
-    // corner row prefixes: a warp per (corner row, side), scanning the hw columns
-    for (int t = warp; t < 2 * nr; t += F2_WARPS) {
-      const int rl = t >> 1, right = t & 1, r = 2 * p0 + rl;
-      if (r >= mc) continue;
-      const float *xr = reinterpret_cast<const float *>(x + (rl >> 1) * S) + (rl & 1);
-      for (int bot = 0; bot < 2; ++bot) {
-        const int i = bot ? mc - 1 - r : r;
-        if (i >= hw) continue;
-        u64 *o = E + 1 + 4 * hw + ((2 * bot + right) * hw + i) * hw;
-        u64 carry = 0;
-        for (int a0 = 0; a0 < hw; a0 += 32) {
-          const int aa = a0 + lane;
-          u64 v2 = 0;
-          if (aa < hw) {
-            const uint32_t v = (uint32_t)xr[2 * G::ix(right ? nc - 1 - aa : aa)];
-            v2 = (u64)(v * v);
-          }
-          const u64 sc = warp_scan_incl(v2) + carry;
-          if (aa < hw) o[aa] = sc;
-          carry = __shfl_sync(0xffffffffu, sc, 31);
+  // corner row prefixes (squares and values): a warp per (corner row, side), scanning the
+  // hw columns (the frame value is the transform input plus mu)
+  for (int t = warp; t < 2 * nr; t += F2_WARPS) {
+    const int rl = t >> 1, right = t & 1, r = 2 * p0 + rl;
+    if (r >= mc) continue;
+    const float *xr = reinterpret_cast<const float *>(x + (rl >> 1) * S) + (rl & 1);
+    for (int bot = 0; bot < 2; ++bot) {
+      const int i = bot ? mc - 1 - r : r;
+      if (i >= hw) continue;
+      u64 *o = E + 1 + 4 * hw + ((2 * bot + right) * hw + i) * hw;
+      u64 *ol = EL + 1 + 4 * hw + ((2 * bot + right) * hw + i) * hw;
+      u64 carry = 0, carryl = 0;
+      for (int a0 = 0; a0 < hw; a0 += 32) {
+        const int aa = a0 + lane;
+        u64 v2 = 0, v1 = 0;
+        if (aa < hw) {
+          const uint32_t v = (uint32_t)((int)xr[2 * G::ix(right ? nc - 1 - aa : aa)] + mu);
+          v2 = (u64)(v * v);
+          v1 = v;
+        }
+        const u64 sc = warp_scan_incl(v2) + carry;
+        if (aa < hw) o[aa] = sc;
+        carry = __shfl_sync(0xffffffffu, sc, 31);
+        if (lin) {
+          const u64 scl = warp_scan_incl(v1) + carryl;
+          if (aa < hw) ol[aa] = scl;
+          carryl = __shfl_sync(0xffffffffu, scl, 31);
         }
       }
     }
@@ -446,6 +473,8 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_rows(F2RowsArgs a) {
 struct F2ColsArgs {
   const float2 *S;          // [B][Kc][mcp]
   int mc, Kc, mcp, W, hw;
+  int Mc;                   // row transform length (Hermitian weights of the stored bins)
+  int lin;                  // mean removal on: also the values' corner tables
   int per;                  // column bins per block (<= NF)
   const float2 *tw;         // [Mr]
   const float2 *Bc;         // [Kc][Mr] conj(B^)/(Mr Mc)   (frames)
@@ -454,6 +483,8 @@ struct F2ColsArgs {
   float scale;              // template mode: 1/(Mr Mc)
   u64 *E;                   // [B][esz] energy partials: the corner row prefixes become 2-D
                             // corner sums here (split over the frame's blocks)
+  double *ynorm;            // [B] sum over the full spectrum of |Y|^2, Y the product the
+                            // inverse transform gets (the certification bound's inverse term)
 };
 
 template <int P>
@@ -491,12 +522,14 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_cols(F2ColsArgs a) {
     // corner tables of the DP: the row prefixes RP[quad][i][a] of k_fft2_rows become
     // CP[quad][p-1][a] = sum_{i<p} RP[quad][i][a], in place; this block scans its share of
     // the 4 hw columns (quad, a), the column held in registers while it is loaded
-    const int hw = a.hw, ncol = 4 * hw;
+    // (both sets -- squares and values -- when the mean is removed)
+    const int hw = a.hw, ncol = (a.lin ? 8 : 4) * hw;
     const int cpb = (ncol + ncb - 1) / ncb, c0 = (blockIdx.x - (int)(f * ncb)) * cpb, c1 = min(ncol, c0 + cpb);
-    u64 *RP = a.E + f * f2_esz(hw) + 1 + 4 * hw;
+    u64 *RP = a.E + f * f2_esz2(hw) + 1 + 4 * hw;
     for (int c = c0 + warp; c < c1; c += F2_WARPS) {
-      const int quad = c / hw, aa = c - quad * hw;
-      u64 *col = RP + (int64_t)quad * hw * hw + aa;
+      const int set = c / (4 * hw), cq = c - set * 4 * hw;
+      const int quad = cq / hw, aa = cq - quad * hw;
+      u64 *col = RP + (int64_t)set * f2_esz(hw) + (int64_t)quad * hw * hw + aa;
       u64 carry = 0;
       for (int i0 = 0; i0 < hw; i0 += 32) {
         const int i = i0 + lane;
@@ -516,12 +549,24 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_cols(F2ColsArgs a) {
       }
     return;
   }
+  double ysq = 0.0;
   for (int q = warp; q < nk; q += F2_WARPS) {
     const float2 *Bk = a.Bc + (int64_t)(k0 + q) * Mr;
+    // a stored bin k stands for k and Mc - k of the Hermitian full spectrum
+    const int kk = k0 + q;
+    const double wk = (kk == 0 || 2 * kk == a.Mc) ? 1.0 : 2.0;
+    double yq = 0.0;
     for (int u = lane; u < Mr; u += 32) {
       float2 *c = x + q * S + G::pos(u);
-      *c = cmul(*c, __ldg(Bk + u));
+      const float2 y = cmul(*c, __ldg(Bk + u));
+      *c = y;
+      yq += (double)y.x * y.x + (double)y.y * y.y;
     }
+    ysq += wk * yq;
+  }
+  if (a.ynorm) {
+    ysq = warp_sum(ysq);
+    if (lane == 0 && ysq > 0) atomicAdd(a.ynorm + f, ysq);
   }
   f2_inv<P>(x, tw, nk);
   float2 *Pf = a.P + f * a.W * a.Kc + k0;
@@ -542,8 +587,12 @@ struct F2ScoreArgs {
   u64 *Ew;                  // the same, written: the pick re-zeroes the accumulated slots
   const u64 *gb;            // [W*W] template energies
   double scale;             // 16^L
-  double eps_f, eps_i;      // eps_h = ||a||_2 (eps_f ||b||_2 + eps_i ||b||_1) (kernels_fft.cuh)
-  const unsigned long long *b1;   // ||b||_1 of the coarse template (device)
+  double eps_f, eps_i;      // eps_h = ||a'||_2 (eps_f ||b'||_2 + eps_i ||b'||_1) (kernels_fft.cuh)
+  const unsigned long long *b1;   // (unused by k_fft2_score: the mean-removed norms come from tst)
+  const long long *tst;     // [3] mu, ||b - mu||_1, ||b - mu||_2^2 (k_tpl_stats)
+  const long long *gl;      // [W*W] template linear sums per lag (k_template_lin)
+  double *ynorm;            // [B] |Y|^2 summed over the full spectrum (k_fft2_cols), re-zeroed by the pick
+  double sqrtN;             // sqrt(Mr Mc)
   const uint16_t *frames;   // level-0 frames (exact rescoring through block sums)
   int64_t fstride;
   int pitch;
@@ -674,7 +723,8 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_score(F2ScoreArgs a) {
   float2 *x = tw + Mc;
   u64 *RX = reinterpret_cast<u64 *>(x + G::NF * S);   // [W] excluded-row energy per s
   u64 *CX = RX + W;                                   // [W] excluded-column energy per t
-  double *rinv = reinterpret_cast<double *>(CX + W);                    // [W]
+  u64 *RXl = CX + W, *CXl = RXl + W;                  // [W] the same for the values (S_a)
+  double *rinv = reinterpret_cast<double *>(CXl + W);                   // [W]
   double *cinv = rinv + W;                                               // [W]
   __shared__ float redf[32];
   __shared__ int qn, qlist[FFT_QCAP], last;
@@ -683,7 +733,7 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_score(F2ScoreArgs a) {
   const int p0 = (blockIdx.x - (int)(f * npb)) * a.per;
   const int np = min(a.per, npairs - p0), s0 = 2 * p0, nr = min(2 * np, W - s0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const u64 *E = a.E + f * f2_esz(hw);
+  const u64 *E = a.E + f * f2_esz2(hw), *EL = E + f2_esz(hw);
   for (int k = threadIdx.x; k < Mc; k += blockDim.x) tw[k] = a.tw[k];
   // packed lag rows, Hermitian extension of each half spectrum: x = row s1 + i row s2, in
   // k1-major order for the inverse transform; a warp per pair
@@ -700,16 +750,19 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_score(F2ScoreArgs a) {
       x[q * S + G::pos(k)] = make_float2(v1.x - v2.y, v1.y + v2.x);
     }
   }
-  // energies: the excluded strips by warp scans of the edge row / column sums
-  if (warp < 4) {   // 0 top rows, 1 bottom rows, 2 left cols, 3 right cols
-    u64 *o = warp < 2 ? RX : CX;
-    const u64 *src = E + 1 + warp * hw;
-    if ((warp & 1) && lane == 0) o[hw] = 0;
+  // energies and linear sums: the excluded strips by warp scans of the edge row /
+  // column sums
+  const bool lin = a.tst[0] != 0;
+  if (warp < (lin ? 8 : 4)) {   // (warp & 3): 0 top rows, 1 bottom rows, 2 left cols, 3 right cols; warp >= 4: values
+    const int side = warp & 3;
+    u64 *o = warp < 4 ? (side < 2 ? RX : CX) : (side < 2 ? RXl : CXl);
+    const u64 *src = (warp < 4 ? E : EL) + 1 + side * hw;
+    if ((side & 1) && lane == 0) o[hw] = 0;
     u64 carry = 0;
     for (int d0 = 0; d0 < hw; d0 += 32) {
       const int d = d0 + lane;
       const u64 sc = warp_scan_incl(d < hw ? src[d] : 0) + carry;
-      if (d < hw) o[(warp & 1) ? hw - d - 1 : hw + d + 1] = sc;   // s > 0 excludes the top rows
+      if (d < hw) o[(side & 1) ? hw - d - 1 : hw + d + 1] = sc;   // s > 0 excludes the top rows
       carry = __shfl_sync(0xffffffffu, sc, 31);
     }
   }
@@ -718,29 +771,49 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_score(F2ScoreArgs a) {
     cinv[k] = 1.0 / (double)(a.nc - abs(k - hw));
   }
   f2_inv<P>(x, tw, np);
-  const u64 tot = E[0];
-  const double eps2 = 2.0 * (sqrt((double)tot) * (1.0 + 1e-12)) *
-                      (a.eps_f * sqrt((double)a.gb[hw * W + hw]) * (1.0 + 1e-12) + a.eps_i * (double)*a.b1);
+  // The transforms saw a' = a - mu and b' = b - mu on the supports, so
+  //   h~' ~ h' = sum_D a' b' = h - mu (S_a + S_b) + mu^2 A          (exact integers aside h')
+  // with S_a, S_b the frame / template sums over D's two rectangles.  Error of h~ = h~' +
+  // [mu (S_a + S_b) - mu^2 A]: the derived bound with the mean-removed norms, plus the
+  // rounding of the fp64 sum; the fp64 evaluation of N~ = g_a + g_b - 2 h~ adds its own.
+  const u64 tot = E[0], totl = EL[0];
+  const long long mu = a.tst[0];
+  const long long n_sup = (long long)a.mc * a.nc;
+  const double a2p = (double)((long long)tot - 2 * mu * (long long)totl + mu * mu * n_sup);   // ||a - mu||_2^2
+  // forward terms through Cauchy-Schwarz with ||b'||_2; the inverse transform's term from
+  // the computed spectrum norm: ||E_inv||_2 <= Ci u sqrt(N) ||Y~||_2
+  const double epsh = (sqrt(a2p) * (1.0 + 1e-12)) * a.eps_f * sqrt((double)a.tst[2]) * (1.0 + 1e-12) +
+                      a.eps_i * a.sqrtN * sqrt(a.ynorm[f]) * (1.0 + 1e-9);
+  constexpr double U53 = 1.1102230246251565e-16;   // 2^-53
   float best = 3.0e38f;
   float *lbf = a.lb + f * W * W;
   for (int rl = warp; rl < nr; rl += F2_WARPS) {
     const int si = s0 + rl, s = si - hw;
     const float *xr = reinterpret_cast<const float *>(x + (rl >> 1) * S) + (rl & 1);
     const double ri = rinv[si];
-    const u64 rx = RX[si];
-    const u64 *CPq = E + 1 + 4 * hw + (int64_t)(s < 0 ? 2 : 0) * hw * hw;
+    const u64 rx = RX[si], rxl = lin ? RXl[si] : 0;
+    const int64_t cq = (int64_t)(s < 0 ? 2 : 0) * hw * hw;
+    const u64 *CPq = E + 1 + 4 * hw + cq, *CPl = EL + 1 + 4 * hw + cq;
     for (int ti = lane; ti < W; ti += 32) {
       const int t = ti - hw;
       const int tt = t < 0 ? t + Mc : t;
-      const float h = xr[2 * G::ix(tt)];
+      const float hp = xr[2 * G::ix(tt)];
       const int lag = si * W + ti;
-      if (a.h_out) a.h_out[f * W * W + lag] = h;
-      u64 ga = tot - rx - CX[ti];
-      if (s != 0 && t != 0)   // 2-D corner sum of the excluded |s| x |t| corner (k_fft2_cols)
-        ga += __ldg(CPq + (t < 0 ? hw * hw : 0) + (int64_t)(abs(s) - 1) * hw + abs(t) - 1);
+      u64 ga = tot - rx - CX[ti], sa = lin ? totl - rxl - CXl[ti] : 0;
+      if (s != 0 && t != 0) {   // 2-D corner sums of the excluded |s| x |t| corner (k_fft2_cols)
+        const int64_t o = (t < 0 ? hw * hw : 0) + (int64_t)(abs(s) - 1) * hw + abs(t) - 1;
+        ga += __ldg(CPq + o);
+        if (lin) sa += __ldg(CPl + o);
+      }
+      const long long area = (long long)(a.mc - abs(s)) * (a.nc - abs(t));
+      const long long corr = lin ? mu * ((long long)sa + a.gl[lag]) - mu * mu * area : 0;
+      const double h = (double)hp + (double)corr;
+      if (a.h_out) a.h_out[f * W * W + lag] = (float)h;
+      const double gsum = (double)ga + (double)a.gb[lag];
+      const double hdev = epsh + 2 * U53 * (fabs((double)hp) + fabs((double)corr));   // |h~ - h|
       const double inv = ri * cinv[ti];
-      const double fa = ((double)ga + (double)a.gb[lag] - 2.0 * (double)h) * inv;
-      const double del = eps2 * inv;
+      const double fa = (gsum - 2.0 * h) * inv;
+      const double del = (2.0 * hdev + 4 * U53 * (gsum + 2.0 * fabs(h))) * inv;
       best = fminf(best, (float)(fa + del) * (1.0f + 1e-6f));
       lbf[lag] = (float)(fa - del) * (1.0f - 1e-6f);
     }
@@ -787,9 +860,13 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_score(F2ScoreArgs a) {
   if (!(nq == 1 && !a.f_out) && !all)
     for (int k = threadIdx.x; k < nq; k += blockDim.x) a.ql[f * FFT_QCAP + k] = qlist[k];
   // re-zero the accumulated energy slots (total, edge columns) for the next call
-  u64 *Ew = a.Ew + f * f2_esz(hw);
-  if (threadIdx.x == 0) Ew[0] = 0;
-  for (int k = threadIdx.x; k < 2 * hw; k += blockDim.x) Ew[1 + 2 * hw + k] = 0;
+  if (threadIdx.x == 0) a.ynorm[f] = 0.0;
+  u64 *Ew = a.Ew + f * f2_esz2(hw);
+  for (int st2 = 0; st2 < 2; ++st2) {
+    u64 *e = Ew + st2 * f2_esz(hw);
+    if (threadIdx.x == 0) e[0] = 0;
+    for (int k = threadIdx.x; k < 2 * hw; k += blockDim.x) e[1 + 2 * hw + k] = 0;
+  }
 }
 
 // Exact rescoring of the certified candidates (S4): blocks (frame, row part); frames whose

@@ -83,6 +83,8 @@ struct moco_plan {
     int fra_min = 64;      // MOCO_FRA_MIN: smallest batch for k_refine_frame
     bool nofuse_ds = false, ga_inpick = false, nopipe = false;
     bool fft_v1 = false;   // MOCO_FFT_V1=1: the generic FFT kernels (kernels_fft.cuh) for every length
+    int fft_mean = -1;     // MOCO_FFT_MEAN=0/1: mean removal on the FFT path off / on (default: on
+                           // for levels >= 1 and w <= 32, where it pays)
     int tc_fused = 0;      // MOCO_TC_FUSED=1: k_tc_fused (operand strips built in the search kernel,
                            // kernels_tcf.cuh; measured slower: C2 1.38 vs 1.83 M frames/s)
   } knob;
@@ -110,6 +112,11 @@ struct moco_plan {
     double bound_Cf = 0, bound_Ci = 0;   // eps_h = u ||a||_2 (Cf ||b||_2 + Ci ||b||_1)
     double2 *R64 = nullptr;     // template spectrum rows in fp64 [mc][Kc] (k_tpl_dft_rows)
     unsigned long long *b1 = nullptr;   // ||b||_1 of the coarse template
+    // mean removal (v2): the transforms see a - mu and b - mu on the supports, the score adds
+    // back mu (S_a + S_b) - mu^2 A exactly (kernels_fft2.cuh)
+    long long *tst = nullptr;   // [3] mu, ||b - mu||_1, ||b - mu||_2^2 (k_tpl_stats)
+    long long *gl = nullptr;    // [W*W] template linear sums per lag (k_template_lin)
+    double *ynorm = nullptr;    // [2 cap] spectrum norms (k_fft2_cols), kept zero
     int smem_rows = 0, smem_cols = 0, smem_score = 0, smem_energy = 0;
     int pc = 0, pr = 0;         // register FFT plans of the row (Mc) and column (Mr) lengths
     // kernels_fft2.cuh (both lengths with a register plan, n_c % 8 == 0): the frame-to-
@@ -328,6 +335,9 @@ static void plan_free(moco_plan *p) {
     if (p->fft.ev_j[k]) cudaEventDestroy(p->fft.ev_j[k]);
   }
   if (p->fft.R64) cudaFree(p->fft.R64);
+  if (p->fft.tst) cudaFree(p->fft.tst);
+  if (p->fft.gl) cudaFree(p->fft.gl);
+  if (p->fft.ynorm) cudaFree(p->fft.ynorm);
   if (p->fft.b1) cudaFree(p->fft.b1);
   if (p->fft.E) cudaFree(p->fft.E);
   if (p->fft.cnt) cudaFree(p->fft.cnt);
@@ -413,7 +423,7 @@ static int fft_init(moco_plan *p) {
   F.pc = fft_plan_of(g.Lc.N);
   F.pr = fft_plan_of(g.Lr.N);
   F.v2 = F.pc > 0 && F.pr > 0 && g.nc % 8 == 0 && !p->knob.fft_v1;
-  const size_t esz = (size_t)f2_esz(g.hw) * 8;
+  const size_t esz = (size_t)f2_esz2(g.hw) * 8;
   // sub-batches sized so the spectra stay in L2 (about 80 MB)
   const size_t per = F.v2 ? (size_t)g.Kc * g.mcp * 8 + (size_t)g.W * g.Kc * 8 + (size_t)g.W * g.W * 4 + esz
                           : (size_t)g.Kc * g.mcp * 8 + (size_t)g.W * g.Kc * 8 + (size_t)g.W * g.W * 8;
@@ -426,7 +436,9 @@ static int fft_init(moco_plan *p) {
     if (cudaMalloc(q, bytes) != cudaSuccess) { cudaGetLastError(); return false; }
     return true;
   };
-  if (!al((void **)&F.R64, (size_t)g.mc * g.Kc * 16) || !al((void **)&F.b1, 8)) return MOCO_ENOMEM;
+  if (!al((void **)&F.R64, (size_t)g.mc * g.Kc * 16) || !al((void **)&F.b1, 8) || !al((void **)&F.tst, 3 * 8) ||
+      !al((void **)&F.gl, (size_t)g.W * g.W * 8))
+    return MOCO_ENOMEM;
   if (!al((void **)&F.twr, Mr * 8) || !al((void **)&F.twc, Mc * 8) || !al((void **)&F.Bc, (size_t)g.Kc * Mr * 8) ||
       !al((void **)&F.S, (size_t)nset * F.cap * g.Kc * g.mcp * 8) ||
       !al((void **)&F.P, (size_t)nset * F.cap * g.W * g.Kc * 8) ||
@@ -448,6 +460,8 @@ static int fft_init(moco_plan *p) {
     CK(cudaMemset(F.qn, 0, (size_t)2 * F.cap * sizeof(int)));
     CK(cudaMemset(F.cnt2, 0, (size_t)2 * F.cap * sizeof(int)));
     CK(cudaMemset(F.nacc, 0, (size_t)2 * F.cap * nslots * 8));
+    if (!al((void **)&F.ynorm, (size_t)2 * F.cap * 8)) return MOCO_ENOMEM;
+    CK(cudaMemset(F.ynorm, 0, (size_t)2 * F.cap * 8));
     for (int k = 0; k < 2; ++k) {
       CK(cudaStreamCreateWithFlags(&F.ss[k], cudaStreamNonBlocking));
       CK(cudaEventCreateWithFlags(&F.ev_j[k], cudaEventDisableTiming));
@@ -476,7 +490,7 @@ static int fft_init(moco_plan *p) {
         const int stg = std::max(f2_stage_bytes(fft2_rows_per_max(G::NF, LK, g.nc), LK, g.nc),
                                  f2_stage_bytes(fft2_rows_per_max(G::NF, 0, g.nc), 0, g.nc));
         F.smem2_rows = stg + (G::N + G::NF * G::STRIDE) * 8 + 2 * G::NF * 8 + 2 * g.hw * 8;
-        F.smem2_score = (G::N + G::NF * G::STRIDE) * 8 + 2 * g.W * 8 + 2 * g.W * 8;
+        F.smem2_score = (G::N + G::NF * G::STRIDE) * 8 + 4 * g.W * 8 + 2 * g.W * 8;
         if (smem_attr(k_fft2_rows<P, 0>, F.smem2_rows) != cudaSuccess ||
             smem_attr(k_fft2_rows<P, 1>, F.smem2_rows) != cudaSuccess ||
             smem_attr(k_fft2_score<P>, F.smem2_score) != cudaSuccess)
@@ -515,6 +529,16 @@ static int fft_init(moco_plan *p) {
 }
 
 // ---- kernels_fft2.cuh launches (F.v2)
+// mean removal on the register-plan FFT path (kernels_fft2.cuh): default for levels >= 1
+// and w <= 32 (C2 648 -> 734 k, C3 632 -> 668 k frames/s); off for levels = 0 (every frame
+// re-scores its winner for f_min anyway) and large w (the values' corner tables cost more
+// than the rescoring they save: w = 85 347 vs 297 k)
+static bool fft_mean_on(const moco_plan *p) {
+  if (!p->fft.v2) return false;
+  if (p->knob.fft_mean >= 0) return p->knob.fft_mean == 1;
+  return p->levels >= 1 && p->w <= 32;
+}
+
 static F2RowsArgs fft2_rows_args(const moco_plan *p, const void *img, int64_t fstride, int pitch, int per, int set) {
   const auto &F = p->fft;
   const FftGeom &g = F.g;
@@ -553,7 +577,8 @@ static int fft2_sub(moco_plan *p, const char *fr, int64_t fstride, int pitch, in
       const int per = (int)std::max<int64_t>(1, std::min<int64_t>(fft2_rows_per_max(F2<P>::NF, LK, g.nc),
                                                                   nb * npair / p->nsm));
       F2RowsArgs a = fft2_rows_args(p, fr, fstride, pitch, per, set);
-      a.E = F.E + so * f2_esz(g.hw);
+      a.E = F.E + so * f2_esz2(g.hw);
+      a.mu = F.tst;
       ProfScope ps(p, MOCO_K_PREP, st);
       fft2_rows_launch<P>(a, LK, nb * ((npair + per - 1) / per), g.hw, st);
     }
@@ -570,7 +595,10 @@ static int fft2_sub(moco_plan *p, const char *fr, int64_t fstride, int pitch, in
       F2ColsArgs c{};
       c.S = F.S + so * g.Kc * g.mcp; c.mc = g.mc; c.Kc = g.Kc; c.mcp = g.mcp; c.W = g.W; c.hw = g.hw;
       c.per = per; c.tw = F.twr; c.Bc = F.Bc; c.P = Pset; c.Bout = nullptr; c.scale = 0.f;
-      c.E = F.E + so * f2_esz(g.hw);
+      c.E = F.E + so * f2_esz2(g.hw);
+      c.Mc = g.Lc.N;
+      c.lin = fft_mean_on(p) ? 1 : 0;
+      c.ynorm = F.ynorm + so;
       ProfScope ps(p, MOCO_K_COARSE, st);
       k_fft2_cols<P><<<(unsigned)(nb * nblk), F2_THREADS, F.smem2_cols, st>>>(c);
     }
@@ -587,7 +615,8 @@ static int fft2_sub(moco_plan *p, const char *fr, int64_t fstride, int pitch, in
       per = (npairs + nblk - 1) / nblk;
       F2ScoreArgs a{};
       a.P = Pset; a.tw = F.twc; a.mc = g.mc; a.nc = g.nc; a.hw = g.hw; a.W = g.W; a.Kc = g.Kc;
-      a.per = per; a.E = F.E + so * f2_esz(g.hw); a.Ew = F.E + so * f2_esz(g.hw); a.gb = (const u64 *)p->gb;
+      a.per = per; a.E = F.E + so * f2_esz2(g.hw); a.Ew = F.E + so * f2_esz2(g.hw); a.gb = (const u64 *)p->gb;
+      a.tst = F.tst; a.gl = F.gl; a.ynorm = F.ynorm + so; a.sqrtN = std::sqrt((double)g.Lr.N * (double)g.Lc.N);
       a.scale = (double)(1u << (4 * L)); a.eps_f = std::ldexp(F.bound_Cf, -24); a.eps_i = std::ldexp(F.bound_Ci, -24); a.b1 = F.b1;
       a.frames = (const uint16_t *)fr; a.fstride = fstride; a.pitch = pitch; a.L = LK;
       a.tpl = (const uint16_t *)p->tpl[L]; a.tpitch = p->pitch[L];
@@ -652,8 +681,13 @@ static int fft_set_template(moco_plan *p, cudaStream_t st) {
   const FftGeom &g = F.g;
   const int Mr = g.Lr.N, Mc = g.Lc.N;
   CK(cudaMemsetAsync(F.b1, 0, 8, st));
+  // v2: the spectrum of b - mu (mean removal); the generic kernels use b itself (mu = 0)
+  const bool mean = fft_mean_on(p);
+  k_tpl_stats<<<1, 1024, 0, st>>>((const uint16_t *)p->tpl[L], p->pitch[L], g.mc, g.nc, mean ? 1 : 0, F.tst);
+  if (mean)
+    k_template_lin<<<g.W * g.W, 256, 0, st>>>((const uint16_t *)p->tpl[L], p->pitch[L], g.mc, g.nc, g.w, F.gl);
   k_tpl_dft_rows<<<g.mc, 256, Mc * 16 + g.nc * 8, st>>>((const uint16_t *)p->tpl[L], p->pitch[L], g.nc, Mc, g.Kc,
-                                                          F.R64);
+                                                          F.R64, F.tst);
   k_tpl_dft_cols<<<g.Kc, 256, (Mr + g.mc) * 16, st>>>(F.R64, g.mc, Mr, Mc, g.Kc, F.Bc, F.b1, (const uint16_t *)p->tpl[L],
                                             p->pitch[L], g.nc);
   CKL("fft template spectrum");
@@ -829,6 +863,7 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
     p->knob.nopipe = getenv("MOCO_NOPIPE") != nullptr;
     p->knob.fft_v1 = getenv("MOCO_FFT_V1") != nullptr;
     if (const char *v = getenv("MOCO_TC_FUSED")) p->knob.tc_fused = atoi(v);
+    if (const char *v = getenv("MOCO_FFT_MEAN")) p->knob.fft_mean = atoi(v) ? 1 : 0;
     if (const char *v = getenv("MOCO_FRA")) p->knob.fra = atoi(v);
     if (const char *v = getenv("MOCO_FRA_MIN")) p->knob.fra_min = std::max(1, atoi(v));
   }

@@ -58,23 +58,32 @@ def _block_sums(x, L):
 
 
 def _worst_ratio(p, spec, frames_dev, template_dev):
-    """max |h~ - h| / eps_h over the frames, eps_h = u ||a||_2 (Cf ||b||_2 + Ci ||b||_1) the
-    plan's derived certification bound (moco_fft_bound); h exact."""
+    """max |h~ - h| / eps_h over the frames, with h exact (int64) and eps_h the derived
+    certification bound of the register-plan FFT path, recomputed
+    here from its definition: the transforms see a' = a - mu and b' = b - mu on the
+    supports (mu = the template's rounded mean), and
+        eps_h = u (Cf ||a'||_2 ||b'||_2 + Ci sqrt(Mr Mc) ||Y||_2),  Y = FFT2(a') conj(FFT2(b')) / (Mr Mc)
+    (Cf, Ci from moco_fft_bound; Y in fp64 here).  h~ comes back as float32 (moco_fft_cross),
+    so its own rounding, 2^-24 |h|, is allowed on top."""
     h, _, _ = p.fft_cross(frames_dev)
     h = _np(h).astype(np.float64)
     Bs = _block_sums(_np(template_dev), spec.levels)
     Cf, Ci = p.fft_bound()
-    b1, b2 = float(np.abs(Bs).sum()), math.sqrt(float((Bs * Bs).sum()))
+    mc, nc = Bs.shape
+    Mr, Mc = _fft_len(mc + spec.w - 1), _fft_len(nc + spec.w - 1)
+    mu = int(np.floor(Bs.sum() / Bs.size + 0.5))
+    bp = Bs - mu
+    Bf = np.fft.fft2(bp, (Mr, Mc))
     worst = 0.0
     for k in range(frames_dev.shape[0]):
         A = _block_sums(_np(frames_dev[k]), spec.levels)
         ex = _exact_h(A, Bs, spec.w)
-        eps = 2.0 ** -24 * math.sqrt(float((A * A).sum())) * (Cf * b2 + Ci * b1)
-        err = float(np.abs(h[k] - ex).max())
-        if eps == 0:
-            assert err == 0.0
-            continue
-        worst = max(worst, err / eps)
+        ap = A - mu
+        Y = np.fft.fft2(ap, (Mr, Mc)) * np.conj(Bf) / (Mr * Mc)
+        eps = 2.0 ** -24 * (Cf * np.sqrt(float((ap * ap).sum())) * np.sqrt(float((bp * bp).sum())) +
+                            Ci * math.sqrt(Mr * Mc) * float(np.sqrt((np.abs(Y) ** 2).sum())))
+        err = np.abs(h[k] - ex) - 2.0 ** -24 * np.abs(ex)
+        worst = max(worst, float(err.max()) / eps)
     return worst
 
 
