@@ -18,7 +18,9 @@ MOCO_BATCH_WAVES=1 timeout 120 python tools/profile_run.py --frames 4736 --iters
   timeout 900 ncu --set full --clock-control none --import-source on \
     -k regex:"k_tc_prep|k_tc_coarse|k_refine_tc|k_refine_pick|k_ga_pieces" -c 5 -o $O/prof_c2 -f \
     env MOCO_BATCH_WAVES=1 python tools/profile_run.py --frames 4736 --iters 1 > $O/ncu_c2.log 2>&1
+# FFT path at C3: one 256-frame call (a single sub-batch), second of two (warm L2): its four launches
 timeout 900 ncu --set full --cache-control none --clock-control none --import-source on -k regex:"k_fft2" \
-  --launch-skip 30 -c 4 -o $O/prof_fft2_c3 -f python tools/profile_run.py --config 3 --frames 1184 --iters 2 --algo fft > $O/ncu_fft.log 2>&1
+  --launch-skip 4 -c 4 -o $O/prof_fft2_c3 -f python tools/profile_run.py --config 3 --frames 256 --iters 2 --algo fft > $O/ncu_fft.log 2>&1
+python tools/ncu_traffic.py $O/prof_c2.ncu-rep 1184 $O/prof_fft2_c3.ncu-rep 256 > $O/ncu_traffic.json
 timeout 300 python bench.py --impl reference --steps 2 --warmup 1 2>/dev/null | tail -1 > $O/bench_reference.json
 ls -la $O
