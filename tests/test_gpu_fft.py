@@ -288,3 +288,35 @@ def test_fft_bound_constant_and_candidate_cost(c):
     _, _, q = p.fft_cross(st.frames)
     q = _np(q)
     assert q.min() >= 1 and q.max() <= 64 and q.mean() < 4.0, np.bincount(q)
+
+
+@pytest.mark.parametrize("kind", ["constant", "offset_blobs", "full_range", "one_bright_row"])
+def test_fft_mean_removal_adversarial_templates(kind):
+    """Templates that stress the mean removal of the certified FFT path (b' = b - mu on the
+    support): constant (b' = 0: the transform carries nothing, h is the exact correction
+    alone), blobs on a large offset (mu >> the structure), full-range noise (|b'| ~ mu) and
+    one saturated row; frames: the config's, a few adversarial ones and the template itself.
+    Shifts, f_min, corrected frames and edge flags equal the exact tensor-core path's."""
+    spec = config_spec(2, T=10)
+    rng = np.random.default_rng(7)
+    m, n = spec.m, spec.n
+    if kind == "constant":
+        tp = np.full((m, n), 2000, np.uint16)
+    elif kind == "offset_blobs":
+        tp = np.clip(_np(make_stack(spec, 0, 1).template).astype(np.int64) // 8 + 3500, 0, 4095).astype(np.uint16)
+    elif kind == "full_range":
+        tp = rng.integers(0, 4096, (m, n)).astype(np.uint16)
+    else:
+        tp = np.full((m, n), 100, np.uint16)
+        tp[m // 3, :] = 4095
+    fr = np.concatenate([_np(make_stack(spec, 0, 4).frames), _adversarial(spec, rng)[:5], tp[None]], axis=0)
+    frames = torch.from_numpy(np.ascontiguousarray(fr)).to(DEV)
+    t = torch.from_numpy(tp).to(DEV)
+    out = {}
+    for algo in ("fft", "tc"):
+        p = Plan(m, n, spec.w, spec.levels, "u16", 12, device=0, algo=algo)
+        p.set_template(t)
+        sh, fm, co, fl = p.align(frames, corrected=True, flags=True)
+        out[algo] = (sh, fm, co.view(torch.int16), fl & 1)
+    for a, b in zip(out["fft"], out["tc"]):
+        assert torch.equal(a, b)
