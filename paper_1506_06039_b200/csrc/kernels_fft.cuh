@@ -918,9 +918,15 @@ __global__ void __launch_bounds__(256) k_energy_rows(const uint16_t *__restrict_
   if (lane == 0 && mytot) atomicAdd(reinterpret_cast<unsigned long long *>(tot), (unsigned long long)mytot);
 }
 
-__global__ void __launch_bounds__(1024) k_energy_u16(const uint16_t *__restrict__ img, int64_t fstride, int pitch,
-                                                    int mc, int nc, int w, u64 *__restrict__ ga,
-                                                    u64 *__restrict__ part) {
+// SQ = true: g(s,t) = sum over the frame-side rectangle of D_{s,t} of a^2 (the energies);
+// SQ = false: the same sums of a itself (the template's linear lag sums of the mean
+// removal, kernels_fft2.cuh).  One block per image.
+// flip = 1 stores g(-s,-t) at lag (s,t): the TEMPLATE-side rectangle of D_{s,t} (g_b and the
+// template's linear sums).
+template <bool SQ>
+__global__ void __launch_bounds__(1024) k_energy_u16_t(const uint16_t *__restrict__ img, int64_t fstride, int pitch,
+                                                      int mc, int nc, int w, u64 *__restrict__ ga,
+                                                      u64 *__restrict__ part, int flip = 0) {
   extern __shared__ __align__(16) u64 esm[];
   const int hw = w - 1, W = 2 * w - 1, CS = w * w;
   u64 *rowE = esm;                 // [2 hw]: top rows, bottom rows (from the bottom)
@@ -960,7 +966,7 @@ __global__ void __launch_bounds__(1024) k_energy_u16(const uint16_t *__restrict_
 #pragma unroll
         for (int x = 0; x < 8; ++x) {
           const uint32_t v = (x & 1) ? (wv[x >> 1] >> 16) : (wv[x >> 1] & 0xffffu);
-          sq[x] = 8 * c + x < nc ? v * v : 0u;   // < 2^32
+          sq[x] = 8 * c + x < nc ? (SQ ? v * v : v) : 0u;   // < 2^32
           rs += sq[x];
         }
         if (c == cl && hasL)
@@ -997,7 +1003,7 @@ __global__ void __launch_bounds__(1024) k_energy_u16(const uint16_t *__restrict_
     const int s = lag / W - hw, t = lag % W - hw;
     const u64 rex = s > 0 ? rowE[s - 1] : (s < 0 ? rowE[hw + (-s) - 1] : 0);
     const u64 cex = t > 0 ? colE[t - 1] : (t < 0 ? colE[hw + (-t) - 1] : 0);
-    gf[lag] = *tot - rex - cex;
+    gf[flip ? W * W - 1 - lag : lag] = *tot - rex - cex;
   }
   // corners: quadrant (s<0 ? 2 : 0) | (t<0 ? 1 : 0) -- s > 0 excludes the TOP rows, t > 0
   // the LEFT columns; table[p][q] = sum of a^2 over the p x q corner block
@@ -1010,7 +1016,7 @@ __global__ void __launch_bounds__(1024) k_energy_u16(const uint16_t *__restrict_
       if (pp > 0 && qq > 0) {
         const int r = bot ? mc - pp : pp - 1, c = rt ? nc - qq : qq - 1;
         const u64 v = A[(int64_t)r * pitch + c];
-        v2 = v * v;
+        v2 = SQ ? v * v : v;
       }
       cor[e] = v2;
     }
@@ -1024,9 +1030,11 @@ __global__ void __launch_bounds__(1024) k_energy_u16(const uint16_t *__restrict_
     for (int e = threadIdx.x; e < hw * hw; e += blockDim.x) {
       const int as = e / hw + 1, at = e % hw + 1;
       const int s = bot ? -as : as, t = rt ? -at : at;
-      gf[(s + hw) * W + (t + hw)] += cor[as * w + at];
+      const int lg = (s + hw) * W + (t + hw);
+      gf[flip ? W * W - 1 - lg : lg] += cor[as * w + at];
     }
   }
 }
+#define k_energy_u16 k_energy_u16_t<true>
 
 }  // namespace moco

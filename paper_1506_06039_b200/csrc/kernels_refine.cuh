@@ -38,30 +38,55 @@ namespace moco {
 
 // 2-D prefix of b^2: P[i][j] = sum_{i' < i, j' < j} b[i'][j']^2, (m+1) x (n+1), once per plan.
 // Pass 1 (rows) then pass 2 (columns), one thread per row / column.
+// 2-D prefix of b^2, P[i][j] = sum_{i'<i, j'<j} b[i'][j']^2, (m+1) x (n+1): a warp per row
+// (warp scans over 32-column chunks, coalesced), then the column pass in row segments
+// (each thread scans a segment of its column, the segment totals are prefixed, a second
+// pass adds them): independent loads in flight instead of one dependent chain per column.
 __global__ void k_prefix2d_rows(const uint16_t *__restrict__ b, int pitch, int m, int n, u64 *__restrict__ P) {
-  const int n1 = n + 1;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= m; i += gridDim.x * blockDim.x) {
+  const int n1 = n + 1, lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i <= m; i += nw) {
     u64 *row = P + (int64_t)i * n1;
-    row[0] = 0;
-    u64 acc = 0;
-    for (int j = 0; j < n; ++j) {
-      if (i > 0) {
-        const u64 v = b[(int64_t)(i - 1) * pitch + j];
-        acc += v * v;
+    if (lane == 0) row[0] = 0;
+    u64 carry = 0;
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      const int j = j0 + lane;
+      u64 v = 0;
+      if (i > 0 && j < n) {
+        const u64 x = b[(int64_t)(i - 1) * pitch + j];
+        v = x * x;
       }
-      row[j + 1] = acc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u64 t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+      }
+      v += carry;
+      if (j < n) row[j + 1] = v;
+      carry = __shfl_sync(0xffffffffu, v, 31);
     }
   }
 }
+constexpr int PF_SEG = 16;   // row segments of the column pass
 __global__ void k_prefix2d_cols(int m, int n, u64 *__restrict__ P) {
-  const int n1 = n + 1;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= n; j += gridDim.x * blockDim.x) {
-    u64 acc = 0;
-    for (int i = 0; i <= m; ++i) {
-      acc += P[(int64_t)i * n1 + j];
-      P[(int64_t)i * n1 + j] = acc;
+  // block: 32 columns x PF_SEG segments
+  __shared__ u64 seg[PF_SEG][33];
+  const int n1 = n + 1, m1 = m + 1;
+  const int c = threadIdx.x & 31, sg = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + c;
+  const int rows = (m1 + PF_SEG - 1) / PF_SEG, r0 = sg * rows, r1 = min(m1, r0 + rows);
+  u64 acc = 0;
+  if (j <= n)
+    for (int i = r0; i < r1; ++i) acc += P[(int64_t)i * n1 + j];
+  seg[sg][c] = acc;
+  __syncthreads();
+  u64 off = 0;
+  for (int k = 0; k < sg; ++k) off += seg[k][c];
+  if (j <= n)
+    for (int i = r0; i < r1; ++i) {
+      off += P[(int64_t)i * n1 + j];
+      P[(int64_t)i * n1 + j] = off;
     }
-  }
 }
 
 struct RefineSumArgs {

@@ -520,6 +520,7 @@ static int fft_init(moco_plan *p) {
   });
   if (rc_attr) return rc_attr;
   CK(smem_attr(k_energy_u16, F.smem_energy));
+  CK(smem_attr(k_energy_u16_t<false>, F.smem_energy));
   k_fft_twiddles<<<(Mr + 255) / 256, 256>>>(F.twr, Mr);
   k_fft_twiddles<<<(Mc + 255) / 256, 256>>>(F.twc, Mc);
   CKL("k_fft_twiddles");
@@ -685,7 +686,8 @@ static int fft_set_template(moco_plan *p, cudaStream_t st) {
   const bool mean = fft_mean_on(p);
   k_tpl_stats<<<1, 1024, 0, st>>>((const uint16_t *)p->tpl[L], p->pitch[L], g.mc, g.nc, mean ? 1 : 0, F.tst);
   if (mean)
-    k_template_lin<<<g.W * g.W, 256, 0, st>>>((const uint16_t *)p->tpl[L], p->pitch[L], g.mc, g.nc, g.w, F.gl);
+    k_energy_u16_t<false><<<1, 1024, (4 * g.hw + g.w * g.w + 1) * 8, st>>>(   // (w - 1 <= 248: fft_supported)
+        (const uint16_t *)p->tpl[L], 0, p->pitch[L], g.mc, g.nc, g.w, (u64 *)F.gl, nullptr, 1);
   k_tpl_dft_rows<<<g.mc, 256, Mc * 16 + g.nc * 8, st>>>((const uint16_t *)p->tpl[L], p->pitch[L], g.nc, Mc, g.Kc,
                                                           F.R64, F.tst);
   k_tpl_dft_cols<<<g.Kc, 256, (Mr + g.mc) * 16, st>>>(F.R64, g.mc, Mr, Mc, g.Kc, F.Bc, F.b1, (const uint16_t *)p->tpl[L],
@@ -1330,7 +1332,13 @@ int moco_set_template(moco_plan *p, const void *d_template, moco_stream_t stream
     if (rc) return rc;
   }
   const int L = p->levels;
-  if (p->dtype == MOCO_U16)
+  const int esm = (4 * (p->w - 1) + p->w * p->w + 1) * 8;   // k_energy_u16_t shared memory
+  if (p->dtype == MOCO_U16 && p->w - 1 <= 248) {   // g_b by the strip/corner DP of P:33-35, one block
+    CK(smem_attr(k_energy_u16_t<true>, esm));
+    CK(smem_attr(k_energy_u16_t<false>, esm));
+    k_energy_u16_t<true><<<1, 1024, esm, st>>>((const uint16_t *)p->tpl[L], 0, p->pitch[L], p->ml[L], p->nl[L], p->w,
+                                               (u64 *)p->gb, nullptr, 1);
+  } else if (p->dtype == MOCO_U16)
     k_template_energy<uint16_t><<<p->W * p->W, 256, 0, st>>>(
         (const uint16_t *)p->tpl[L], p->pitch[L], p->ml[L], p->nl[L], p->w, (u64 *)p->gb);
   else if (L == 0)
@@ -1342,9 +1350,9 @@ int moco_set_template(moco_plan *p, const void *d_template, moco_stream_t stream
   CKL("k_template_energy");
   if (p->dtype == MOCO_U16)
     for (int l = 0; l < L; ++l) {
-      k_prefix2d_rows<<<(p->ml[l] + 128) / 128, 128, 0, st>>>((const uint16_t *)p->tpl[l], p->pitch[l],
+      k_prefix2d_rows<<<(p->ml[l] + 8) / 8, 256, 0, st>>>((const uint16_t *)p->tpl[l], p->pitch[l],
                                                                p->ml[l], p->nl[l], p->pb2[l]);
-      k_prefix2d_cols<<<(p->nl[l] + 128) / 128, 128, 0, st>>>(p->ml[l], p->nl[l], p->pb2[l]);
+      k_prefix2d_cols<<<(p->nl[l] + 32) / 32, 32 * PF_SEG, 0, st>>>(p->ml[l], p->nl[l], p->pb2[l]);
       CKL("k_prefix2d");
       if (p->rtab[l]) {
         k_rtc_table<<<1024, 256, 0, st>>>((const uint16_t *)p->tpl[l], p->pitch[l], p->ml[l], p->nl[l],
