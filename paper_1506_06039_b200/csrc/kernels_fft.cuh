@@ -448,27 +448,6 @@ __global__ void k_tpl_stats(const uint16_t *__restrict__ b, int pitch, int mc, i
     st[2] = (long long)t2;
   }
 }
-// gl[s][t] = sum over the template rectangle of D_{s,t} of b (the linear analogue of g_b,
-// k_template_energy): one block per lag, once per template.
-__global__ void k_template_lin(const uint16_t *__restrict__ b, int pitch, int mc, int nc, int w,
-                               long long *__restrict__ gl) {
-  const int W = 2 * w - 1;
-  const int s = (int)(blockIdx.x / W) - (w - 1), t = (int)(blockIdx.x % W) - (w - 1);
-  const int i0 = max(0, -s), i1 = mc - max(0, s), j0 = max(0, -t), j1 = nc - max(0, t);
-  unsigned long long acc = 0;
-  for (int i = i0; i < i1; ++i)
-    for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) acc += b[(int64_t)i * pitch + j];
-  __shared__ unsigned long long red[32];
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long t2 = 0;
-    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t2 += red[k];
-    gl[blockIdx.x] = (long long)t2;
-  }
-}
-
 __global__ void k_tpl_dft_rows(const uint16_t *__restrict__ b, int pitch, int nc, int Mc, int Kc,
                                double2 *__restrict__ R, const long long *__restrict__ mu) {
   extern __shared__ double2 tw64[];

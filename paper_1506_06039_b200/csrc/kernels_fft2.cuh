@@ -590,7 +590,7 @@ struct F2ScoreArgs {
   double eps_f, eps_i;      // eps_h = ||a'||_2 (eps_f ||b'||_2 + eps_i ||b'||_1) (kernels_fft.cuh)
   const unsigned long long *b1;   // (unused by k_fft2_score: the mean-removed norms come from tst)
   const long long *tst;     // [3] mu, ||b - mu||_1, ||b - mu||_2^2 (k_tpl_stats)
-  const long long *gl;      // [W*W] template linear sums per lag (k_template_lin)
+  const long long *gl;      // [W*W] template linear sums per lag (k_energy_u16_t<false> on the template)
   double *ynorm;            // [B] |Y|^2 summed over the full spectrum (k_fft2_cols), re-zeroed by the pick
   double sqrtN;             // sqrt(Mr Mc)
   const uint16_t *frames;   // level-0 frames (exact rescoring through block sums)

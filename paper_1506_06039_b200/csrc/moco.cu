@@ -115,7 +115,7 @@ struct moco_plan {
     // mean removal (v2): the transforms see a - mu and b - mu on the supports, the score adds
     // back mu (S_a + S_b) - mu^2 A exactly (kernels_fft2.cuh)
     long long *tst = nullptr;   // [3] mu, ||b - mu||_1, ||b - mu||_2^2 (k_tpl_stats)
-    long long *gl = nullptr;    // [W*W] template linear sums per lag (k_template_lin)
+    long long *gl = nullptr;    // [W*W] template linear sums per lag (k_energy_u16_t<false>, flipped)
     double *ynorm = nullptr;    // [2 cap] spectrum norms (k_fft2_cols), kept zero
     int smem_rows = 0, smem_cols = 0, smem_score = 0, smem_energy = 0;
     int pc = 0, pr = 0;         // register FFT plans of the row (Mc) and column (Mr) lengths
