@@ -169,13 +169,25 @@ int moco_fft_cross(moco_plan *p, const void *d_frames, int64_t T, float *d_h, in
                    int32_t *d_qcount, moco_stream_t stream);
 
 /*
- * moco_fft_bound -- the constants of the FFT path's certified error bound
- *     |h~(s,t) - h(s,t)| <= u ||a_c||_2 (Cf ||b_c||_2 + Ci ||b_c||_1),  u = 2^-24,
- * for every coarse lag (DESIGN.md §5 derives them from the transforms' stage structure:
- * per-stage and twiddle rounding, the fp64 template spectrum rounded once to fp32, the
- * spectrum product).  Cf, Ci: host outputs.  MOCO_EINVAL if the plan has no FFT path.
+ * moco_fft_bound -- the constants of the FFT path's certified error bound (DESIGN.md §5,
+ * SURVEY.md §8(c)-O6): for every coarse lag
+ *     |h~(s,t) - h(s,t)| <= u (Cf ||a'||_2 ||b'||_2 + Ci sqrt(Mr Mc) ||Y~||_2),  u = 2^-24,
+ * a' = a - mu_a, b' = b - mu_b on the supports (moco_fft_means), Y~ the computed spectrum
+ * product the inverse transform receives.  Cf covers the forward transforms (per-stage and
+ * twiddle rounding, the fp64 template spectrum rounded once to fp32, the product), Ci the
+ * inverse.  Cf, Ci: host outputs.  MOCO_EINVAL if the plan has no FFT path.
  */
 int moco_fft_bound(const moco_plan *p, double *Cf, double *Ci);
+
+/*
+ * moco_fft_means -- the mean removal of the FFT path: the transforms see
+ * a - mu_a (frames) and b - mu_b (template) on the supports, and the exact integer
+ * correction h = h' + mu_b S_a + mu_a S_b - mu_a mu_b A restores the cross term.  mu_a is
+ * the coarse template's rounded mean (0 when mean removal is off); mu_b = mu_a (two-sided)
+ * or 0 (frames only).  Host outputs; reads the plan's device copy (synchronises the plan's
+ * device).  MOCO_EINVAL if the plan has no FFT path or no template yet.
+ */
+int moco_fft_means(const moco_plan *p, int64_t *mu_a, int64_t *mu_b);
 
 /*
  * moco_mean_image -- report helper (Fig. 2 caption:

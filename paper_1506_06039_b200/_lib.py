@@ -38,6 +38,7 @@ SIGNATURES = [
     ("moco_score_grid", _I, [_P, _P, _I64, _P, _P]),
     ("moco_fft_cross", _I, [_P, _P, _I64, _P, _P, _P, _P]),
     ("moco_fft_bound", _I, [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
+    ("moco_fft_means", _I, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     ("moco_probe_peaks", _I, [_I, ctypes.POINTER(ctypes.c_double), _I]),
     ("moco_mean_image", _I, [_P, _I64, _I, _I, _I, _P, _P]),
     ("moco_last_launch_count", _I64, [_P]),
@@ -208,11 +209,17 @@ class Plan:
         return h, sh, q
 
     def fft_bound(self):
-        """(Cf, Ci) of the FFT path's certified bound |h~ - h| <= u ||a||_2 (Cf ||b||_2 +
-        Ci ||b||_1)."""
+        """(Cf, Ci) of the FFT path's certified bound |h~ - h| <= u (Cf ||a'||_2 ||b'||_2 +
+        Ci sqrt(Mr Mc) ||Y~||_2) (include/moco.h)."""
         cf, ci = ctypes.c_double(), ctypes.c_double()
         _check(load().moco_fft_bound(self._h, ctypes.byref(cf), ctypes.byref(ci)), "moco_fft_bound")
         return cf.value, ci.value
+
+    def fft_means(self):
+        """(mu_a, mu_b): the shifts of frames and template on the FFT path (moco_fft_means)."""
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        _check(load().moco_fft_means(self._h, ctypes.byref(a), ctypes.byref(b)), "moco_fft_means")
+        return a.value, b.value
 
     def align_host(self, frames: torch.Tensor, shifts=None, fmin=None, corrected=None, flags=None):
         """End-to-end moco_align_host on HOST tensors (pinned for full speed)."""

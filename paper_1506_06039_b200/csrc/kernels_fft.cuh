@@ -425,7 +425,8 @@ __global__ void k_tpl_stats(const uint16_t *__restrict__ b, int pitch, int mc, i
     mu_s = mean ? (long long)((t + n / 2) / n) : 0;
   }
   __syncthreads();
-  const long long mu = mu_s;
+  // mean 1: both sides shifted by mu (b' = b - mu); mean 2: the frames only (b' = b)
+  const long long mu = mean == 1 ? mu_s : 0;
   unsigned long long a1 = 0, a2 = 0;
   for (int e = threadIdx.x; e < mc * nc; e += blockDim.x) {
     const long long d = (long long)b[(int64_t)(e / nc) * pitch + e % nc] - mu;
@@ -443,9 +444,10 @@ __global__ void k_tpl_stats(const uint16_t *__restrict__ b, int pitch, int mc, i
   if (threadIdx.x == 0) {
     unsigned long long t1 = 0, t2 = 0;
     for (int k = 0; k < (int)(blockDim.x >> 5); ++k) { t1 += r1[k]; t2 += r2[k]; }
-    st[0] = mu;
+    st[0] = mu_s;   // the frames' shift
     st[1] = (long long)t1;
     st[2] = (long long)t2;
+    st[3] = mu;     // the template's shift
   }
 }
 __global__ void k_tpl_dft_rows(const uint16_t *__restrict__ b, int pitch, int nc, int Mc, int Kc,
@@ -459,7 +461,7 @@ __global__ void k_tpl_dft_rows(const uint16_t *__restrict__ b, int pitch, int nc
   __syncthreads();
   const int i = blockIdx.x;
   double *row = reinterpret_cast<double *>(tw64 + Mc);   // the template row (minus mu), staged once
-  const double m0 = mu ? (double)mu[0] : 0.0;
+  const double m0 = mu ? (double)mu[3] : 0.0;   // k_tpl_stats: the template's shift
   for (int j = threadIdx.x; j < nc; j += blockDim.x) row[j] = (double)b[(int64_t)i * pitch + j] - m0;
   __syncthreads();
   for (int k = threadIdx.x; k < Kc; k += blockDim.x) {

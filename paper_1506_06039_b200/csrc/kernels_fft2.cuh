@@ -335,7 +335,9 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_rows(F2RowsArgs a) {
   u64 wtot = 0, wlin = 0;
   u64 *E = a.E + f * f2_esz2(hw), *EL = E + f2_esz(hw);
   const int mu = (int)a.mu[0];
-  const bool lin = mu != 0;   // mean removal on: the linear partials (S_a) are needed
+  // two-sided mean removal (the template shifted too): the linear partials (S_a) per lag
+  // are needed; one-sided: only the frame total (for ||a - mu||_2)
+  const bool lin = a.mu[3] != 0;
   // 8 coarse values of coarse row rl (block-local), columns 8c .. 8c+7, from the staged rows
   auto load8 = [&](int rl, int c, uint32_t (&v)[8]) {
 #pragma unroll
@@ -389,7 +391,7 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_rows(F2RowsArgs a) {
     }
     rs0 = warp_sum(rs0);
     rs1 = warp_sum(rs1);
-    if (lin) {
+    if (mu) {
       ls0 = warp_sum(ls0);
       ls1 = warp_sum(ls1);
     }
@@ -399,8 +401,8 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_rows(F2RowsArgs a) {
       if (r < mc) {
         wtot += rs;
         wlin += ls;
-        if (r < hw) { E[1 + r] = rs; EL[1 + r] = ls; }
-        if (r >= mc - hw) { E[1 + hw + (mc - 1 - r)] = rs; EL[1 + hw + (mc - 1 - r)] = ls; }
+        if (r < hw) { E[1 + r] = rs; if (lin) EL[1 + r] = ls; }
+        if (r >= mc - hw) { E[1 + hw + (mc - 1 - r)] = rs; if (lin) EL[1 + hw + (mc - 1 - r)] = ls; }
       }
     }
   }
@@ -752,7 +754,7 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_score(F2ScoreArgs a) {
   }
   // energies and linear sums: the excluded strips by warp scans of the edge row /
   // column sums
-  const bool lin = a.tst[0] != 0;
+  const bool lin = a.tst[3] != 0;   // two-sided mean removal: S_a per lag
   if (warp < (lin ? 8 : 4)) {   // (warp & 3): 0 top rows, 1 bottom rows, 2 left cols, 3 right cols; warp >= 4: values
     const int side = warp & 3;
     u64 *o = warp < 4 ? (side < 2 ? RX : CX) : (side < 2 ? RXl : CXl);
@@ -771,13 +773,14 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_score(F2ScoreArgs a) {
     cinv[k] = 1.0 / (double)(a.nc - abs(k - hw));
   }
   f2_inv<P>(x, tw, np);
-  // The transforms saw a' = a - mu and b' = b - mu on the supports, so
-  //   h~' ~ h' = sum_D a' b' = h - mu (S_a + S_b) + mu^2 A          (exact integers aside h')
-  // with S_a, S_b the frame / template sums over D's two rectangles.  Error of h~ = h~' +
-  // [mu (S_a + S_b) - mu^2 A]: the derived bound with the mean-removed norms, plus the
-  // rounding of the fp64 sum; the fp64 evaluation of N~ = g_a + g_b - 2 h~ adds its own.
+  // The transforms saw a' = a - mu_a and b' = b - mu_b on the supports, so
+  //   h = sum_D a b = h' + mu_b S_a + mu_a S_b - mu_a mu_b A         (exact integers aside h')
+  // with S_a, S_b the frame / template sums over D's two rectangles (two-sided: mu_a = mu_b
+  // = mu; one-sided: mu_b = 0, no S_a).  Error of h~ = h~' + [correction]: the derived
+  // bound with the shifted norms, plus the rounding of the fp64 sum; the fp64 evaluation of
+  // N~ = g_a + g_b - 2 h~ adds its own.
   const u64 tot = E[0], totl = EL[0];
-  const long long mu = a.tst[0];
+  const long long mu = a.tst[0], mub = a.tst[3];
   const long long n_sup = (long long)a.mc * a.nc;
   const double a2p = (double)((long long)tot - 2 * mu * (long long)totl + mu * mu * n_sup);   // ||a - mu||_2^2
   // forward terms through Cauchy-Schwarz with ||b'||_2; the inverse transform's term from
@@ -806,7 +809,7 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_score(F2ScoreArgs a) {
         if (lin) sa += __ldg(CPl + o);
       }
       const long long area = (long long)(a.mc - abs(s)) * (a.nc - abs(t));
-      const long long corr = lin ? mu * ((long long)sa + a.gl[lag]) - mu * mu * area : 0;
+      const long long corr = mu ? mub * (long long)sa + mu * ((long long)a.gl[lag] - mub * area) : 0;
       const double h = (double)hp + (double)corr;
       if (a.h_out) a.h_out[f * W * W + lag] = (float)h;
       const double gsum = (double)ga + (double)a.gb[lag];

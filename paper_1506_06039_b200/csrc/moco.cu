@@ -83,8 +83,8 @@ struct moco_plan {
     int fra_min = 64;      // MOCO_FRA_MIN: smallest batch for k_refine_frame
     bool nofuse_ds = false, ga_inpick = false, nopipe = false;
     bool fft_v1 = false;   // MOCO_FFT_V1=1: the generic FFT kernels (kernels_fft.cuh) for every length
-    int fft_mean = -1;     // MOCO_FFT_MEAN=0/1: mean removal on the FFT path off / on (default: on
-                           // for levels >= 1 and w <= 32, where it pays)
+    int fft_mean = -1;     // MOCO_FFT_MEAN=0/1/2: mean removal on the FFT path off / two-sided /
+                           // frames only (default: fft_mean_mode)
     int tc_fused = 0;      // MOCO_TC_FUSED=1: k_tc_fused (operand strips built in the search kernel,
                            // kernels_tcf.cuh; measured slower: C2 1.38 vs 1.83 M frames/s)
   } knob;
@@ -114,7 +114,7 @@ struct moco_plan {
     unsigned long long *b1 = nullptr;   // ||b||_1 of the coarse template
     // mean removal (v2): the transforms see a - mu and b - mu on the supports, the score adds
     // back mu (S_a + S_b) - mu^2 A exactly (kernels_fft2.cuh)
-    long long *tst = nullptr;   // [3] mu, ||b - mu||_1, ||b - mu||_2^2 (k_tpl_stats)
+    long long *tst = nullptr;   // [4] mu_a, ||b - mu_b||_1, ||b - mu_b||_2^2, mu_b (k_tpl_stats)
     long long *gl = nullptr;    // [W*W] template linear sums per lag (k_energy_u16_t<false>, flipped)
     double *ynorm = nullptr;    // [2 cap] spectrum norms (k_fft2_cols), kept zero
     int smem_rows = 0, smem_cols = 0, smem_score = 0, smem_energy = 0;
@@ -436,7 +436,7 @@ static int fft_init(moco_plan *p) {
     if (cudaMalloc(q, bytes) != cudaSuccess) { cudaGetLastError(); return false; }
     return true;
   };
-  if (!al((void **)&F.R64, (size_t)g.mc * g.Kc * 16) || !al((void **)&F.b1, 8) || !al((void **)&F.tst, 3 * 8) ||
+  if (!al((void **)&F.R64, (size_t)g.mc * g.Kc * 16) || !al((void **)&F.b1, 8) || !al((void **)&F.tst, 4 * 8) ||
       !al((void **)&F.gl, (size_t)g.W * g.W * 8))
     return MOCO_ENOMEM;
   if (!al((void **)&F.twr, Mr * 8) || !al((void **)&F.twc, Mc * 8) || !al((void **)&F.Bc, (size_t)g.Kc * Mr * 8) ||
@@ -530,14 +530,16 @@ static int fft_init(moco_plan *p) {
 }
 
 // ---- kernels_fft2.cuh launches (F.v2)
-// mean removal on the register-plan FFT path (kernels_fft2.cuh): default for levels >= 1
-// and w <= 32 (C2 648 -> 734 k, C3 632 -> 668 k frames/s); off for levels = 0 (every frame
-// re-scores its winner for f_min anyway) and large w (the values' corner tables cost more
-// than the rescoring they save: w = 85 347 vs 297 k)
-static bool fft_mean_on(const moco_plan *p) {
-  if (!p->fft.v2) return false;
-  if (p->knob.fft_mean >= 0) return p->knob.fft_mean == 1;
-  return p->levels >= 1 && p->w <= 32;
+// mean removal on the register-plan FFT path (kernels_fft2.cuh): 0 off, 1 two-sided (frames
+// and template shifted by the template's mean mu; the frames' value strips and corner
+// tables cost a second set of scans), 2 one-sided (the frames only: h = h' + mu S_b, S_b per
+// plan; one frame total).  Measured (B200, u16 frames/s, modes 0 / 1 / 2): C2 602 / 749 /
+// 757 k, C4 294 / 303 / 309 k, w = 85 320 / 290 / 342 k, C1 (levels = 0, every frame
+// re-scores its winner anyway) 798 / 764 / 788 k.  Default: 2 for levels >= 1, else 0.
+static int fft_mean_mode(const moco_plan *p) {
+  if (!p->fft.v2) return 0;
+  if (p->knob.fft_mean >= 0) return p->knob.fft_mean;
+  return p->levels >= 1 ? 2 : 0;
 }
 
 static F2RowsArgs fft2_rows_args(const moco_plan *p, const void *img, int64_t fstride, int pitch, int per, int set) {
@@ -598,7 +600,7 @@ static int fft2_sub(moco_plan *p, const char *fr, int64_t fstride, int pitch, in
       c.per = per; c.tw = F.twr; c.Bc = F.Bc; c.P = Pset; c.Bout = nullptr; c.scale = 0.f;
       c.E = F.E + so * f2_esz2(g.hw);
       c.Mc = g.Lc.N;
-      c.lin = fft_mean_on(p) ? 1 : 0;
+      c.lin = fft_mean_mode(p) == 1 ? 1 : 0;
       c.ynorm = F.ynorm + so;
       ProfScope ps(p, MOCO_K_COARSE, st);
       k_fft2_cols<P><<<(unsigned)(nb * nblk), F2_THREADS, F.smem2_cols, st>>>(c);
@@ -683,8 +685,8 @@ static int fft_set_template(moco_plan *p, cudaStream_t st) {
   const int Mr = g.Lr.N, Mc = g.Lc.N;
   CK(cudaMemsetAsync(F.b1, 0, 8, st));
   // v2: the spectrum of b - mu (mean removal); the generic kernels use b itself (mu = 0)
-  const bool mean = fft_mean_on(p);
-  k_tpl_stats<<<1, 1024, 0, st>>>((const uint16_t *)p->tpl[L], p->pitch[L], g.mc, g.nc, mean ? 1 : 0, F.tst);
+  const int mean = fft_mean_mode(p);
+  k_tpl_stats<<<1, 1024, 0, st>>>((const uint16_t *)p->tpl[L], p->pitch[L], g.mc, g.nc, mean, F.tst);
   if (mean)
     k_energy_u16_t<false><<<1, 1024, (4 * g.hw + g.w * g.w + 1) * 8, st>>>(   // (w - 1 <= 248: fft_supported)
         (const uint16_t *)p->tpl[L], 0, p->pitch[L], g.mc, g.nc, g.w, (u64 *)F.gl, nullptr, 1);
@@ -865,7 +867,7 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
     p->knob.nopipe = getenv("MOCO_NOPIPE") != nullptr;
     p->knob.fft_v1 = getenv("MOCO_FFT_V1") != nullptr;
     if (const char *v = getenv("MOCO_TC_FUSED")) p->knob.tc_fused = atoi(v);
-    if (const char *v = getenv("MOCO_FFT_MEAN")) p->knob.fft_mean = atoi(v) ? 1 : 0;
+    if (const char *v = getenv("MOCO_FFT_MEAN")) p->knob.fft_mean = std::min(2, std::max(0, atoi(v)));
     if (const char *v = getenv("MOCO_FRA")) p->knob.fra = atoi(v);
     if (const char *v = getenv("MOCO_FRA_MIN")) p->knob.fra_min = std::max(1, atoi(v));
   }
@@ -1750,6 +1752,16 @@ int moco_fft_bound(const moco_plan *p, double *Cf, double *Ci) {
   if (!p || !Cf || !Ci || !p->fft.ready) return MOCO_EINVAL;
   *Cf = p->fft.bound_Cf;
   *Ci = p->fft.bound_Ci;
+  return MOCO_OK;
+}
+
+int moco_fft_means(const moco_plan *p, int64_t *mu_a, int64_t *mu_b) {
+  if (!p || !mu_a || !mu_b || !p->fft.ready || !p->fft.tpl_ready || !p->fft.tst) return MOCO_EINVAL;
+  CK(cudaSetDevice(p->device));
+  long long t[4];
+  CK(cudaMemcpy(t, p->fft.tst, sizeof t, cudaMemcpyDeviceToHost));
+  *mu_a = t[0];
+  *mu_b = t[3];
   return MOCO_OK;
 }
 

@@ -60,8 +60,8 @@ def _block_sums(x, L):
 def _worst_ratio(p, spec, frames_dev, template_dev):
     """max |h~ - h| / eps_h over the frames, with h exact (int64) and eps_h the derived
     certification bound of the register-plan FFT path, recomputed
-    here from its definition: the transforms see a' = a - mu and b' = b - mu on the
-    supports (mu = the template's rounded mean), and
+    here from its definition: the transforms see a' = a - mu_a and b' = b - mu_b on the
+    supports (moco_fft_means: mu_a the template's rounded mean or 0, mu_b = mu_a or 0), and
         eps_h = u (Cf ||a'||_2 ||b'||_2 + Ci sqrt(Mr Mc) ||Y||_2),  Y = FFT2(a') conj(FFT2(b')) / (Mr Mc)
     (Cf, Ci from moco_fft_bound; Y in fp64 here).  h~ comes back as float32 (moco_fft_cross),
     so its own rounding, 2^-24 |h|, is allowed on top."""
@@ -71,14 +71,16 @@ def _worst_ratio(p, spec, frames_dev, template_dev):
     Cf, Ci = p.fft_bound()
     mc, nc = Bs.shape
     Mr, Mc = _fft_len(mc + spec.w - 1), _fft_len(nc + spec.w - 1)
-    mu = int(np.floor(Bs.sum() / Bs.size + 0.5))
-    bp = Bs - mu
+    mu_a, mu_b = p.fft_means()
+    if mu_a:   # the template's rounded mean (moco_fft_means); mu_b: mu_a or 0
+        assert mu_a == int(np.floor(Bs.sum() / Bs.size + 0.5)) and mu_b in (0, mu_a)
+    bp = Bs - mu_b
     Bf = np.fft.fft2(bp, (Mr, Mc))
     worst = 0.0
     for k in range(frames_dev.shape[0]):
         A = _block_sums(_np(frames_dev[k]), spec.levels)
         ex = _exact_h(A, Bs, spec.w)
-        ap = A - mu
+        ap = A - mu_a
         Y = np.fft.fft2(ap, (Mr, Mc)) * np.conj(Bf) / (Mr * Mc)
         eps = 2.0 ** -24 * (Cf * np.sqrt(float((ap * ap).sum())) * np.sqrt(float((bp * bp).sum())) +
                             Ci * math.sqrt(Mr * Mc) * float(np.sqrt((np.abs(Y) ** 2).sum())))
@@ -87,11 +89,14 @@ def _worst_ratio(p, spec, frames_dev, template_dev):
     return worst
 
 
+@pytest.mark.parametrize("mode", [None, "0", "1", "2"])
 @pytest.mark.parametrize("c", [1, 2, 3, 4])
-def test_fft_cross_term_error_within_bound(c):
+def test_fft_cross_term_error_within_bound(c, mode, monkeypatch):
     """The measured fp32 error |h~ - h| on the configs' own data (stripes included for C3)
-    stays at most 1/8 of the derived certification bound eps_h = C u ||a||_2 ||b||_1
-    (DESIGN.md section 5)."""
+    stays at most 1/8 of the derived certification bound eps_h (SURVEY.md section 8(c)-O6,
+    DESIGN.md section 5), for the default and every mean-removal mode (MOCO_FFT_MEAN)."""
+    if mode is not None:
+        monkeypatch.setenv("MOCO_FFT_MEAN", mode)
     T = 3
     spec = config_spec(c, T=T)
     st = make_stack(spec, 0, T, device=DEV)
@@ -290,10 +295,11 @@ def test_fft_bound_constant_and_candidate_cost(c):
     assert q.min() >= 1 and q.max() <= 64 and q.mean() < 4.0, np.bincount(q)
 
 
+@pytest.mark.parametrize("mode", ["1", "2"])
 @pytest.mark.parametrize("kind", ["constant", "offset_blobs", "full_range", "one_bright_row"])
-def test_fft_mean_removal_adversarial_templates(kind):
-    """Templates that stress the mean removal of the certified FFT path (b' = b - mu on the
-    support): constant (b' = 0: the transform carries nothing, h is the exact correction
+def test_fft_mean_removal_adversarial_templates(kind, mode, monkeypatch):
+    """Templates that stress the mean removal of the certified FFT path (mode 1: a' = a - mu,
+    b' = b - mu on the supports; mode 2: the frames only, MOCO_FFT_MEAN): constant (b' = 0: the transform carries nothing, h is the exact correction
     alone), blobs on a large offset (mu >> the structure), full-range noise (|b'| ~ mu) and
     one saturated row; frames: the config's, a few adversarial ones and the template itself.
     Shifts, f_min, corrected frames and edge flags equal the exact tensor-core path's."""
@@ -314,9 +320,14 @@ def test_fft_mean_removal_adversarial_templates(kind):
     t = torch.from_numpy(tp).to(DEV)
     out = {}
     for algo in ("fft", "tc"):
+        monkeypatch.setenv("MOCO_FFT_MEAN", mode)
         p = Plan(m, n, spec.w, spec.levels, "u16", 12, device=0, algo=algo)
+        monkeypatch.delenv("MOCO_FFT_MEAN")
         p.set_template(t)
         sh, fm, co, fl = p.align(frames, corrected=True, flags=True)
+        if algo == "fft":
+            mu_a, mu_b = p.fft_means()
+            assert mu_a > 0 and mu_b == (mu_a if mode == "1" else 0), (mu_a, mu_b)
         out[algo] = (sh, fm, co.view(torch.int16), fl & 1)
     for a, b in zip(out["fft"], out["tc"]):
         assert torch.equal(a, b)
