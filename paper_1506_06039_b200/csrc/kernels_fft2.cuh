@@ -281,8 +281,11 @@ struct F2RowsArgs {
 __host__ __device__ constexpr int f2_stage_bytes(int per, int L, int nc) { return 2 * per * (1 << L) * (1 << L) * nc * 2; }
 constexpr int F2_STAGE_MAX = 64 * 1024;
 
+// two blocks per SM (<= 113 registers, 36 B of spills): one block's bulk copy overlaps the
+// other's transforms (126 registers and one block per SM before: C3 161 -> 106 us per
+// 256 frames, the whole FFT path 723 -> 825 k frames/s)
 template <int P, int L>
-__global__ void __launch_bounds__(F2_THREADS) k_fft2_rows(F2RowsArgs a) {
+__global__ void __launch_bounds__(F2_THREADS, 2) k_fft2_rows(F2RowsArgs a) {
   static_assert(L == 0 || L == 1, "2x2 block sums at most (levels = 2 runs on the level-1 image)");
   using G = F2<P>;
   constexpr int Mc = G::N, S = G::STRIDE, N2 = G::N2, D = 1 << L;
@@ -715,8 +718,10 @@ __device__ __forceinline__ void f2_exact_box(const F2ScoreArgs &a, int64_t f, in
   }
 }
 
+// four blocks per SM (<= 56 registers, no spills; 68 and three blocks before: w = 85
+// 370 -> 381 k frames/s).  Five for k_fft2_cols spills its radix-20 codelets and is slower.
 template <int P>
-__global__ void __launch_bounds__(F2_THREADS) k_fft2_score(F2ScoreArgs a) {
+__global__ void __launch_bounds__(F2_THREADS, 4) k_fft2_score(F2ScoreArgs a) {
   using G = F2<P>;
   constexpr int Mc = G::N, S = G::STRIDE;
   extern __shared__ __align__(128) unsigned char f2sm[];

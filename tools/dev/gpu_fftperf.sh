@@ -1,0 +1,2 @@
+for c in 1 2 3 4; do python tools/align_probe.py --config $c --frames 4096 --algo fft 2>&1 | grep "corrected=True"; done
+python tools/align_probe.py --config 2 --w 85 --frames 4096 --algo fft 2>&1 | grep "corrected=True"
