@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(F2_THREADS, 2) k_fft2_rows(F2RowsArgs a) {
   using G = F2<P>;
   constexpr int Mc = G::N, S = G::STRIDE, N2 = G::N2, D = 1 << L;
   extern __shared__ __align__(128) unsigned char f2sm[];
-  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bar[2];
   const int hw = a.hw, nc = a.nc, mc = a.mc;
   const int nrb = (a.mcp / 2 + a.per - 1) / a.per;
   const int64_t f = blockIdx.x / nrb;
@@ -304,16 +304,23 @@ __global__ void __launch_bounds__(F2_THREADS, 2) k_fft2_rows(F2RowsArgs a) {
   const int rawrow = D * nc;
   const int nraw = D * max(0, min(nr, mc - 2 * p0));
   const uint16_t *Fr = a.frames + f * a.fstride + (int64_t)(D * 2 * p0) * a.pitch;
+  // two barriers: the raw rows of the first round of row pairs (one per warp) and the
+  // rest, so that the first round starts while the second is still in flight
+  const int n0 = min(nraw, 2 * D * F2_WARPS), n1 = nraw - n0;
   if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
     fence_mbar_init();
   }
   __syncthreads();
   if (warp == 0) {
-    if (lane == 0) mbar_arrive_expect_tx(&bar, (uint32_t)(nraw * rawrow * 2));
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&bar[0], (uint32_t)(n0 * rawrow * 2));
+      if (n1 > 0) mbar_arrive_expect_tx(&bar[1], (uint32_t)(n1 * rawrow * 2));
+    }
     __syncwarp();
     for (int r = lane; r < nraw; r += 32)
-      bulk_g2s(stg + (size_t)r * rawrow, Fr + (int64_t)r * a.pitch, (uint32_t)(rawrow * 2), &bar);
+      bulk_g2s(stg + (size_t)r * rawrow, Fr + (int64_t)r * a.pitch, (uint32_t)(rawrow * 2), &bar[r < n0 ? 0 : 1]);
   }
   for (int k = threadIdx.x; k < Mc; k += blockDim.x) tw[k] = a.tw[k];
   // zero columns [nc, Mc) of every transform of the block
@@ -322,7 +329,6 @@ __global__ void __launch_bounds__(F2_THREADS, 2) k_fft2_rows(F2RowsArgs a) {
     const int q = e / tail, j = nc + (e - q * tail);
     x[q * S + G::ix(j)] = make_float2(0.f, 0.f);
   }
-  mbar_wait(&bar, 0);
   // a warp per coarse row pair (one complex transform), a lane per 8 coarse columns; the
   // lane's first and last chunks hold the edge columns (hw <= 256), whose squares it
   // accumulates over its rows
@@ -365,6 +371,8 @@ __global__ void __launch_bounds__(F2_THREADS, 2) k_fft2_rows(F2RowsArgs a) {
     }
   };
   for (int q = warp; q < np; q += F2_WARPS) {
+    if (q < F2_WARPS) mbar_wait(&bar[0], 0);
+    else if (q < 2 * F2_WARPS && n1 > 0) mbar_wait(&bar[1], 0);
     float2 *xq = x + q * S;
     const int r0 = 2 * (p0 + q);
     const float m0 = r0 < mc ? (float)mu : 0.f, m1 = r0 + 1 < mc ? (float)mu : 0.f;
