@@ -500,8 +500,10 @@ struct F2ColsArgs {
                             // inverse transform gets (the certification bound's inverse term)
 };
 
+// four blocks per SM (<= 56 registers; the 360-point instantiation needs 66 and ran three
+// blocks: w = 85 435 -> 457 k frames/s)
 template <int P>
-__global__ void __launch_bounds__(F2_THREADS) k_fft2_cols(F2ColsArgs a) {
+__global__ void __launch_bounds__(F2_THREADS, 4) k_fft2_cols(F2ColsArgs a) {
   using G = F2<P>;
   constexpr int Mr = G::N, S = G::STRIDE;
   extern __shared__ __align__(128) unsigned char f2sm[];
@@ -534,22 +536,45 @@ __global__ void __launch_bounds__(F2_THREADS) k_fft2_cols(F2ColsArgs a) {
   if (a.E) {
     // corner tables of the DP: the row prefixes RP[quad][i][a] of k_fft2_rows become
     // CP[quad][p-1][a] = sum_{i<p} RP[quad][i][a], in place; this block scans its share of
-    // the 4 hw columns (quad, a), the column held in registers while it is loaded
-    // (both sets -- squares and values -- when the mean is removed)
+    // the 4 hw columns (quad, a) (both sets -- squares and values -- when the mean is
+    // removed from both sides).  hw >= 24: lanes over columns (adjacent a: coalesced), warps over segments of the hw
+    // rows -- each warp sums its segment, the segment sums are scanned through shared
+    // memory, a second pass writes the prefixes (w = 85 382 -> 434 k, C3 844 -> 876 k
+    // frames/s); smaller hw: a warp scan per column (one 32-row chunk; C2 897 vs 889 k)
+    __shared__ u64 segsum[F2_WARPS][32];
     const int hw = a.hw, ncol = (a.lin ? 8 : 4) * hw;
     const int cpb = (ncol + ncb - 1) / ncb, c0 = (blockIdx.x - (int)(f * ncb)) * cpb, c1 = min(ncol, c0 + cpb);
     u64 *RP = a.E + f * f2_esz2(hw) + 1 + 4 * hw;
-    for (int c = c0 + warp; c < c1; c += F2_WARPS) {
+    auto colp = [&](int c) {
       const int set = c / (4 * hw), cq = c - set * 4 * hw;
       const int quad = cq / hw, aa = cq - quad * hw;
-      u64 *col = RP + (int64_t)set * f2_esz(hw) + (int64_t)quad * hw * hw + aa;
-      u64 carry = 0;
-      for (int i0 = 0; i0 < hw; i0 += 32) {
-        const int i = i0 + lane;
-        const u64 v = i < hw ? col[(int64_t)i * hw] : 0;
-        const u64 sc = warp_scan_incl(v) + carry;
-        if (i < hw) col[(int64_t)i * hw] = sc;
-        carry = __shfl_sync(0xffffffffu, sc, 31);
+      return RP + (int64_t)set * f2_esz(hw) + (int64_t)quad * hw * hw + aa;
+    };
+    if (hw < 24) {
+      for (int c = c0 + warp; c < c1; c += F2_WARPS) {
+        u64 *col = colp(c);
+        const u64 v = lane < hw ? col[(int64_t)lane * hw] : 0;
+        const u64 sc = warp_scan_incl(v);
+        if (lane < hw) col[(int64_t)lane * hw] = sc;
+      }
+    } else {
+      const int seg = (hw + F2_WARPS - 1) / F2_WARPS, i0 = min(hw, warp * seg), i1 = min(hw, i0 + seg);
+      for (int cg = c0; cg < c1; cg += 32) {
+        const int c = cg + lane;
+        u64 *col = c < c1 ? colp(c) : RP;
+        u64 sum = 0;
+        if (c < c1)
+          for (int i = i0; i < i1; ++i) sum += col[(int64_t)i * hw];
+        segsum[warp][lane] = sum;
+        __syncthreads();
+        u64 carry = 0;
+        for (int w2 = 0; w2 < warp; ++w2) carry += segsum[w2][lane];
+        if (c < c1)
+          for (int i = i0; i < i1; ++i) {
+            carry += col[(int64_t)i * hw];
+            col[(int64_t)i * hw] = carry;
+          }
+        __syncthreads();
       }
     }
   }

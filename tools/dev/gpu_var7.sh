@@ -1,0 +1,6 @@
+for v in cscan2 cscan2c4 cscan2 cscan2c4; do echo "== $v"; cp dev_so/$v.so paper_1506_06039_b200/libmoco.so
+for c in 1 2 3 4; do python tools/align_probe.py --config $c --frames 4096 --algo fft 2>&1 | grep "corrected=True"; done
+python tools/align_probe.py --config 2 --w 85 --frames 4096 --algo fft 2>&1 | grep "corrected=True"
+done
+cp dev_so/cscan2.so paper_1506_06039_b200/libmoco.so
+python -m pytest tests/test_gpu_fft.py -x -q 2>&1 | tail -2
