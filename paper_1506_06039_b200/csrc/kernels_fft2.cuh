@@ -638,6 +638,7 @@ struct F2ScoreArgs {
   const uint16_t *tpl;      // coarse template
   int tpitch;
   float *lb;                // [B][W*W]
+  float *rmin;              // [B][W] per lag row: the minimum of its lb values
   int *ub;                  // [B] float bits, FFT_UB_INIT between calls
   int *cnt;                 // [B] finished blocks, 0 between calls
   int32_t *shift_out;       // [B][2]
@@ -835,6 +836,7 @@ __global__ void __launch_bounds__(F2_THREADS, 4) k_fft2_score(F2ScoreArgs a) {
     const u64 rx = RX[si], rxl = lin ? RXl[si] : 0;
     const int64_t cq = (int64_t)(s < 0 ? 2 : 0) * hw * hw;
     const u64 *CPq = E + 1 + 4 * hw + cq, *CPl = EL + 1 + 4 * hw + cq;
+    float rowlb = 3.0e38f;
     for (int ti = lane; ti < W; ti += 32) {
       const int t = ti - hw;
       const int tt = t < 0 ? t + Mc : t;
@@ -856,8 +858,12 @@ __global__ void __launch_bounds__(F2_THREADS, 4) k_fft2_score(F2ScoreArgs a) {
       const double fa = (gsum - 2.0 * h) * inv;
       const double del = (2.0 * hdev + 4 * U53 * (gsum + 2.0 * fabs(h))) * inv;
       best = fminf(best, (float)(fa + del) * (1.0f + 1e-6f));
-      lbf[lag] = (float)(fa - del) * (1.0f - 1e-6f);
+      const float lbv = (float)(fa - del) * (1.0f - 1e-6f);
+      lbf[lag] = lbv;
+      rowlb = fminf(rowlb, lbv);
     }
+    for (int o = 16; o > 0; o >>= 1) rowlb = fminf(rowlb, __shfl_xor_sync(0xffffffffu, rowlb, o));
+    if (lane == 0) a.rmin[f * W + si] = rowlb;
   }
   for (int o = 16; o > 0; o >>= 1) best = fminf(best, __shfl_xor_sync(0xffffffffu, best, o));
   if (lane == 0) redf[warp] = best;
@@ -874,14 +880,25 @@ __global__ void __launch_bounds__(F2_THREADS, 4) k_fft2_score(F2ScoreArgs a) {
   if (!last) return;
   __threadfence();
   // the last block of the frame: candidate set Q = {lag : f~ - delta <= min(f~ + delta)}
+  // (only the lag rows whose minimum lower bound reaches thr are scanned: the same set)
   const float thr = __int_as_float(atomicAdd(a.ub + f, 0));
-  for (int lag = threadIdx.x; lag < W * W; lag += blockDim.x) {
-    if (__ldcg(lbf + lag) <= thr) {
-      const int q = atomicAdd(&qn, 1);
-      if (q < FFT_QCAP) qlist[q] = lag;
+  __shared__ int nrows, rlist[F2_THREADS];
+  for (int r0 = 0; r0 < W; r0 += F2_THREADS) {
+    if (threadIdx.x == 0) nrows = 0;
+    __syncthreads();
+    const int si = r0 + threadIdx.x;
+    if (si < W && __ldcg(a.rmin + f * W + si) <= thr) rlist[atomicAdd(&nrows, 1)] = si;
+    __syncthreads();
+    for (int k = warp; k < nrows; k += F2_WARPS) {
+      const int base = rlist[k] * W;
+      for (int ti = lane; ti < W; ti += 32)
+        if (__ldcg(lbf + base + ti) <= thr) {
+          const int q = atomicAdd(&qn, 1);
+          if (q < FFT_QCAP) qlist[q] = base + ti;
+        }
     }
+    __syncthreads();
   }
-  __syncthreads();
   const int nq = qn;
   const bool all = nq > FFT_QCAP;
   if (threadIdx.x == 0) {

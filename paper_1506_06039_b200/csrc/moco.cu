@@ -105,6 +105,7 @@ struct moco_plan {
     int *qc = nullptr;
     u64 *epart = nullptr;       // small batches: row-pass energy partials [cap][4 hw + 1], kept zero
     float *lb = nullptr;        // small-batch split score: lower bounds [cap][W*W]
+    float *rmin = nullptr;      // kernels_fft2.cuh: per lag row, the minimum lower bound [2][cap][W]
     int *ub = nullptr;          // and min upper bound per frame [cap]
     cudaStream_t side = nullptr;   // small batches: frame energies beside the FFT
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -299,7 +300,7 @@ static void plan_free(moco_plan *p) {
   if (p->rmeta) cudaFree(p->rmeta);
   tc_free(&p->tc);
   for (void *q : {(void *)p->fft.twr, (void *)p->fft.twc, (void *)p->fft.Bc, (void *)p->fft.S, (void *)p->fft.P,
-                  (void *)p->fft.ga, (void *)p->fft.qc, (void *)p->fft.lb, (void *)p->fft.ub, (void *)p->fft.epart})
+                  (void *)p->fft.ga, (void *)p->fft.qc, (void *)p->fft.lb, (void *)p->fft.rmin, (void *)p->fft.ub, (void *)p->fft.epart})
     if (q) cudaFree(q);
   if (p->fft.side) cudaStreamDestroy(p->fft.side);
   if (p->fft.ev_fork) cudaEventDestroy(p->fft.ev_fork);
@@ -443,7 +444,7 @@ static int fft_init(moco_plan *p) {
       !al((void **)&F.S, (size_t)nset * F.cap * g.Kc * g.mcp * 8) ||
       !al((void **)&F.P, (size_t)nset * F.cap * g.W * g.Kc * 8) ||
       !al((void **)&F.ga, (size_t)F.cap * g.W * g.W * 8) || !al((void **)&F.qc, (size_t)p->cap * sizeof(int)) ||
-      !al((void **)&F.lb, (size_t)nset * F.cap * g.W * g.W * 4) ||
+      !al((void **)&F.lb, (size_t)nset * F.cap * g.W * g.W * 4) || !al((void **)&F.rmin, (size_t)nset * F.cap * g.W * 4) ||
       !al((void **)&F.ub, (size_t)nset * F.cap * sizeof(int)) ||
       !al((void **)&F.epart, (size_t)F.cap * (4 * g.hw + 1) * 8))
     return MOCO_ENOMEM;
@@ -623,7 +624,7 @@ static int fft2_sub(moco_plan *p, const char *fr, int64_t fstride, int pitch, in
       a.scale = (double)(1u << (4 * L)); a.eps_f = std::ldexp(F.bound_Cf, -24); a.eps_i = std::ldexp(F.bound_Ci, -24); a.b1 = F.b1;
       a.frames = (const uint16_t *)fr; a.fstride = fstride; a.pitch = pitch; a.L = LK;
       a.tpl = (const uint16_t *)p->tpl[L]; a.tpitch = p->pitch[L];
-      a.lb = F.lb + so * g.W * g.W; a.ub = F.ub + so; a.cnt = F.cnt + so;
+      a.lb = F.lb + so * g.W * g.W; a.rmin = F.rmin + so * g.W; a.ub = F.ub + so; a.cnt = F.cnt + so;
       a.shift_out = shift_out; a.f_out = f_out; a.flags = flags; a.qcount = qcount; a.h_out = h_out;
       a.qn = F.qn + so; a.ql = F.ql + so * FFT_QCAP; a.cnt2 = F.cnt2 + so;
       a.nacc = F.nacc + so * (int64_t)std::max(FFT_QCAP, g.W * g.W);
