@@ -282,6 +282,53 @@ def reference_arm(args, spec, rank, world):
     print(json.dumps(out), flush=True)
 
 
+def gpu_local_cpus(dev):
+    """The host CPUs NVML reports as local to `dev` (its NUMA node), or None."""
+    try:
+        import pynvml
+        pr = torch.cuda.get_device_properties(dev)
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByPciBusId(f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0")
+        n = os.cpu_count() or 1
+        mask = pynvml.nvmlDeviceGetCpuAffinity(h, (n + 63) // 64)
+        cpus = {i for i in range(n) if (mask[i // 64] >> (i % 64)) & 1} & os.sched_getaffinity(0)
+        return cpus or None
+    except Exception:
+        return None
+
+
+def pinned_ceiling(hf, hc, dev, nbytes=256 << 20):
+    """Frames/s the PCIe link allows through THESE pinned buffers: H2D from hf and D2H into
+    hc at once on two streams (frame in + corrected out per frame), timed with events."""
+    try:
+        a8, c8 = hf.view(-1).view(torch.uint8), hc.view(-1).view(torch.uint8)
+        n = min(nbytes, a8.numel(), c8.numel())
+        d_in = torch.empty(n, dtype=torch.uint8, device=dev)
+        d_out = torch.empty(n, dtype=torch.uint8, device=dev)
+        s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        cur = torch.cuda.current_stream(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for it in range(2):
+            e0.record(cur)
+            s1.wait_stream(cur)
+            s2.wait_stream(cur)
+            for _ in range(4):
+                with torch.cuda.stream(s1):
+                    d_in.copy_(a8[:n], non_blocking=True)
+                with torch.cuda.stream(s2):
+                    c8[:n].copy_(d_out, non_blocking=True)
+            cur.wait_stream(s1)
+            cur.wait_stream(s2)
+            e1.record(cur)
+        torch.cuda.synchronize(dev)
+        dt = e0.elapsed_time(e1) / 1e3 / 4
+        gbs = n / dt / 1e9
+        fbytes = hf[0].numel() * hf.element_size()
+        return {"bidir_each_GBps": gbs, "ceiling_fps": gbs * 1e9 / fbytes}
+    except Exception as e:
+        return {"error": str(e)[:120]}
+
+
 def workload_config(spec, world, algo):
     L = spec.levels
     return {"workload": f"C{spec.index}: {spec.T} frames/rank of {spec.m}x{spec.n} "
@@ -581,14 +628,24 @@ def main():
     # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
+        # pinned buffers on the GPU's own NUMA node (allocated from its local CPUs; the
+        # affinity is restored after the measurement)
+        aff0 = os.sched_getaffinity(0)
+        local_cpus = gpu_local_cpus(dev)
+        if local_cpus:
+            os.sched_setaffinity(0, local_cpus)
         hf = frames.cpu().pin_memory()
         hc = torch.empty_like(hf).pin_memory()
         hs = torch.empty((Tl, 2), dtype=torch.int32).pin_memory()
         hfm = torch.empty((Tl,), dtype=torch.float64).pin_memory()
         plan.align_host(hf, hs, hfm, hc)
+        # the copy ceiling of these very buffers (host pages of a pinned allocation land on
+        # either of the host's memory nodes: the same binary measures ~57 k or ~87 k
+        # frames/s from one process to the next, stable within a process)
+        ceil = pinned_ceiling(hf, hc, dev)
         if world > 1:
             dist.barrier()
-        ksteps = 2
+        ksteps = 4
         t0 = time.perf_counter()
         for _ in range(ksteps):
             plan.align_host(hf, hs, hfm, hc)
@@ -598,8 +655,13 @@ def main():
         e2e = {"value": world * Tl / float(dt.item()), "unit": UNIT,
                "h2d_bytes_per_step": int(hf.numel() * esz * world),
                "d2h_bytes_per_step": int((hc.numel() * esz + hs.numel() * 4 + hfm.numel() * 8) * world),
-               "api": "moco_align_host (pinned host frames in, shifts/f_min/corrected out)"}
+               "api": "moco_align_host (pinned host frames in, shifts/f_min/corrected out)",
+               "host_cpus": len(local_cpus) if local_cpus else None,
+               "pcie_same_buffers": ceil}
+        if "ceiling_fps" in ceil:
+            e2e["frac_of_pcie_ceiling"] = e2e["value"] / (world * ceil["ceiling_fps"])
         del hf, hc
+        os.sched_setaffinity(0, aff0)
 
     # ---- parity on a bounded sample of the timed workload + the CPU oracle baseline
     # (rank 0, N=1 only): the same oracle run gives both

@@ -21,6 +21,13 @@ MOCO_BATCH_WAVES=1 timeout 120 python tools/profile_run.py --frames 4736 --iters
 # FFT path at C3: one 256-frame call (a single sub-batch), second of two (warm L2): its four launches
 timeout 900 ncu --set full --cache-control none --clock-control none --import-source on -k regex:"k_fft2" \
   --launch-skip 4 -c 4 -o $O/prof_fft2_c3 -f python tools/profile_run.py --config 3 --frames 256 --iters 2 --algo fft > $O/ncu_fft.log 2>&1
+# FFT path at the paper setting (512^2, w = 85 at 256^2): the second of two 1024-frame calls
+timeout 900 ncu --set full --cache-control none --clock-control none --import-source on -k regex:"k_fft2" \
+  --launch-skip 5 -c 5 -o $O/prof_fft2_w85 -f python tools/profile_run.py --config 2 --w 85 --frames 1024 --iters 2 --algo fft > $O/ncu_w85.log 2>&1
 python tools/ncu_traffic.py $O/prof_c2.ncu-rep 1184 $O/prof_fft2_c3.ncu-rep 256 > $O/ncu_traffic.json
+for r in prof_c2 prof_fft2_c3 prof_fft2_w85; do python tools/ncu_summary.py $O/$r.ncu-rep > $O/sum_$r.txt 2>&1; done
 timeout 300 python bench.py --impl reference --steps 2 --warmup 1 2>/dev/null | tail -1 > $O/bench_reference.json
+timeout 1200 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1
+# the reports themselves stay on the box (gpurun returns at most 64 MiB)
 ls -la $O
+rm -f $O/*.ncu-rep
