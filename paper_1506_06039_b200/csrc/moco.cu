@@ -60,6 +60,7 @@ struct moco_plan {
   RtcGeom rtc[3];             // tensor-core refine geometry per level (kernels_rtc.cuh)
   FraGeom fra;                // frame-resident refine + pick + apply at level 0 (kernels_fra.cuh)
   bool fra_ok;
+  uint32_t *fra_tc = nullptr; // its shifted, pre-split template copies (k_fra_tcopy)
   uint8_t *rtab[3];           // its template candidate tiles, or null: CUDA-core refine
   int *rperm, *rmeta;         // its per-batch alignment-class bucketing
   int nsm;                    // multiprocessors of the plan's device
@@ -290,6 +291,7 @@ static void plan_free(moco_plan *p) {
   }
   if (p->gb) cudaFree(p->gb);
   if (p->racc) cudaFree(p->racc);
+  if (p->fra_tc) cudaFree(p->fra_tc);
   for (int l = 0; l < 3; ++l) {
     if (p->pb2[l]) cudaFree(p->pb2[l]);
     if (p->rtab[l]) cudaFree(p->rtab[l]);
@@ -975,13 +977,14 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
   // frame-resident level-0 refine + apply (kernels_fra.cuh): clusters of Q CTAs, as many
   // as can be co-resident (occupancy query with the cluster launch configuration)
   if (dtype == MOCO_U16 && levels > 0 && !p->stage && p->knob.fra &&
-      fra_make(&p->fra, p->ml[0], p->nl[0], p->pitch[0], p->pitch[0], bits)) {
-    if (smem_attr(k_refine_frame, p->fra.smem) == cudaSuccess) {
+      fra_make(&p->fra, p->ml[0], p->nl[0], p->pitch[0], bits, 2 * (levels == 1 ? w - 1 : 2 * w - 1))) {
+    if (smem_attr(k_refine_frame, p->fra.smem) == cudaSuccess &&
+        cudaMalloc((void **)&p->fra_tc, fra_tcopy_bytes(p->fra, p->ml[0])) == cudaSuccess) {
       cudaLaunchConfig_t cfg = {};
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeClusterDimension;
       at[0].val.clusterDim.x = p->fra.Q; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-      cfg.gridDim = dim3(p->fra.Q * nsm / p->fra.Q);
+      cfg.gridDim = dim3(p->fra.Q * (nsm / p->fra.Q));
       cfg.blockDim = dim3(FRA_THREADS);
       cfg.dynamicSmemBytes = p->fra.smem;
       cfg.attrs = at;
@@ -1363,6 +1366,11 @@ int moco_set_template(moco_plan *p, const void *d_template, moco_stream_t stream
         CKL("k_rtc_table");
       }
     }
+  if (p->fra_ok) {
+    k_fra_tcopy<<<1024, 256, 0, st>>>((const uint16_t *)p->tpl[0], p->pitch[0], p->ml[0], p->nl[0], p->fra.m,
+                                      p->fra.WT, p->fra_tc);
+    CKL("k_fra_tcopy");
+  }
   if (p->tc.ready) {
     if (tc_set_template(&p->tc, (const uint16_t *)p->tpl[L], p->pitch[L], st) != 0)
       return set_cuda_err(cudaGetLastError(), "tc_set_template");
@@ -1478,7 +1486,7 @@ static int launch_fra(moco_plan *p, const void *img, int64_t fstride, int64_t B,
                       double *fout, void *corr, cudaStream_t st) {
   FraArgs a;
   a.frames = (const uint16_t *)img; a.fstride = fstride; a.pitch = p->pitch[0];
-  a.tpl = (const uint16_t *)p->tpl[0]; a.tpitch = p->pitch[0];
+  a.tcopy = p->fra_tc;
   a.pb2 = p->pb2[0]; a.ml = p->ml[0]; a.nl = p->nl[0]; a.scale = 1.0;
   a.B = (int)B; a.shift_in = sin; a.shift_out = sout; a.f_out = fout;
   a.corrected = (uint16_t *)corr;

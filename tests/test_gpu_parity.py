@@ -456,16 +456,19 @@ def test_frame_resident_refine_equals_tc_refine(c, T, monkeypatch):
     (MOCO_FRA=0, the default), through the pipelined multi-batch path."""
     spec = config_spec(c, T=T)
     st = make_stack(spec, 0, T, device=DEV)
-    out = {}
+    out, nl = {}, {}
     for mode in ("1", "0"):
         monkeypatch.setenv("MOCO_FRA", mode)
         monkeypatch.setenv("MOCO_BATCH_MB", "128")
         p = _plan_for(spec)
         p.set_template(st.template)
         sh, fm, co, _ = p.align(st.frames, corrected=True)
+        nl[mode] = p.launches
         sh2, fm2, _, _ = p.align(st.frames, corrected=False)
         assert torch.equal(sh, sh2) and torch.equal(fm, fm2)
         out[mode] = (sh, fm, co.view(torch.int16))
+    # the cluster kernel replaces four launches per batch (bucket, refine sums, GA pieces, pick)
+    assert nl["1"] < nl["0"], nl
     for a, b in zip(out["1"], out["0"]):
         assert torch.equal(a, b)
 
@@ -487,6 +490,12 @@ def test_frame_resident_refine_ragged_vs_oracle(m, n, w, T, monkeypatch):
     p = Plan(m, n, w, 1, "u16", 12, device=0)
     p.set_template(torch.from_numpy(tp).to(DEV))
     sh, fm, co, _ = p.align(torch.from_numpy(fr).to(DEV), corrected=True)
+    n_fra = p.launches
+    monkeypatch.setenv("MOCO_FRA", "0")
+    p0 = Plan(m, n, w, 1, "u16", 12, device=0)
+    p0.set_template(torch.from_numpy(tp).to(DEV))
+    p0.align(torch.from_numpy(fr).to(DEV), corrected=True)
+    assert n_fra < p0.launches, "the frame-resident kernel did not run"
     torch.cuda.synchronize()
     sh, fm = _np(sh), _np(fm)
     for k in list(range(0, T, 3)):
