@@ -820,7 +820,14 @@ static void tcf_setup(moco_plan *p) {
 }
 
 static int pipe_create(moco_plan *p) {
-  for (int k = 0; k < 3; ++k) CK(cudaStreamCreateWithFlags(&p->ps[k], cudaStreamNonBlocking));
+  // MOCO_PRIO="xyz": stream priorities of (prep, main, pick), 1 = highest, 0 = lowest (tuning)
+  int lo = 0, hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  const char *pr = getenv("MOCO_PRIO");
+  for (int k = 0; k < 3; ++k) {
+    const int pv = (pr && (int)strlen(pr) > k && pr[k] == '1') ? hi : lo;
+    CK(cudaStreamCreateWithPriority(&p->ps[k], cudaStreamNonBlocking, pv));
+  }
   for (int k = 0; k < 2; ++k) {
     CK(cudaEventCreateWithFlags(&p->pe_prep[k], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&p->pe_free[k], cudaEventDisableTiming));
@@ -1255,6 +1262,7 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
     ProfScope ps(p, MOCO_K_REFINE, st);
     k_rtc_bucket<<<1, 1024, 0, st>>>(sin, (int)B, p->rperm, p->rmeta);
     RtcArgs r;
+    r.img = (const uint16_t *)img; r.fstride = fstride; r.pitch = p->pitch[l];
     r.tab = p->rtab[l]; r.acc = racc; r.shift_in = sin; r.perm = p->rperm; r.meta = p->rmeta;
     r.B = (int)B; r.g = p->rtc[l];
     b.ga_total = RTC_GA_TOTAL;   // the pick completes GA from the staged-pixel total
