@@ -286,6 +286,7 @@ constexpr int F2_STAGE_MAX = 64 * 1024;
 // 256 frames, the whole FFT path 723 -> 825 k frames/s)
 template <int P, int L>
 __global__ void __launch_bounds__(F2_THREADS, 2) k_fft2_rows(F2RowsArgs a) {
+  pdl_enter();
   static_assert(L == 0 || L == 1, "2x2 block sums at most (levels = 2 runs on the level-1 image)");
   using G = F2<P>;
   constexpr int Mc = G::N, S = G::STRIDE, N2 = G::N2, D = 1 << L;
@@ -504,6 +505,7 @@ struct F2ColsArgs {
 // blocks: w = 85 435 -> 457 k frames/s)
 template <int P>
 __global__ void __launch_bounds__(F2_THREADS, 4) k_fft2_cols(F2ColsArgs a) {
+  pdl_enter();
   using G = F2<P>;
   constexpr int Mr = G::N, S = G::STRIDE;
   extern __shared__ __align__(128) unsigned char f2sm[];
@@ -756,6 +758,7 @@ __device__ __forceinline__ void f2_exact_box(const F2ScoreArgs &a, int64_t f, in
 // 370 -> 381 k frames/s).  Five for k_fft2_cols spills its radix-20 codelets and is slower.
 template <int P>
 __global__ void __launch_bounds__(F2_THREADS, 4) k_fft2_score(F2ScoreArgs a) {
+  pdl_enter();
   using G = F2<P>;
   constexpr int Mc = G::N, S = G::STRIDE;
   extern __shared__ __align__(128) unsigned char f2sm[];
@@ -937,6 +940,7 @@ __global__ void __launch_bounds__(256) k_fft2_rescore(F2ScoreArgs a) {
   __shared__ u64 red[32];
   __shared__ u64 bred[8][9];
   __shared__ int last, box[4];
+  pdl_enter();
   const int64_t f = blockIdx.x / a.rparts;
   const int part = blockIdx.x - (int)(f * a.rparts);
   const int qn = a.qn[f];

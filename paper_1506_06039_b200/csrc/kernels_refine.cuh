@@ -281,6 +281,7 @@ __device__ __forceinline__ void rs_frame(const uint16_t *Tt, const uint16_t *Fs,
 template <bool WIDE>
 __global__ void __launch_bounds__(RS_THREADS, 1)
     k_refine_sums(const __grid_constant__ CUtensorMap tmF, RefineSumArgs a) {
+  pdl_enter();
   extern __shared__ __align__(1024) unsigned char rs_smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(rs_smem);   // [32]
   uint64_t *empty = full + 32;                               // [32], then int[32] stage misalignments
@@ -593,6 +594,7 @@ __device__ __forceinline__ void pick_apply_rows(const uint16_t *A, uint16_t *O, 
 __global__ void __launch_bounds__(256) k_refine_pick(RefinePickArgs a) {
   __shared__ int res[2];
   __shared__ u64 gbins[26];
+  pdl_enter();
   const int parts = a.parts;
   const int64_t f = blockIdx.x / parts;
   const int part = blockIdx.x % parts;

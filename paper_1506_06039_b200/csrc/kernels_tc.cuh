@@ -128,6 +128,13 @@ __device__ __forceinline__ void cp_async16_zfill(void *dst, const void *src, uin
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+// Programmatic dependent launch (the closed-loop chain): let the next kernel of the stream
+// be scheduled now, then wait until the previous one has completed and its writes are
+// visible.  Both are no-ops for a kernel launched without the PDL attribute.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

@@ -28,6 +28,25 @@
 
 using namespace moco;
 
+// Kernel launch, optionally with programmatic dependent launch (PDL): the kernel may be
+// scheduled while the stream's previous kernel finishes; it calls pdl_enter() first
+// (griddepcontrol.wait), so it still sees every write of its predecessor.
+template <typename... KArgs, typename... Args>
+static cudaError_t launchk(bool pdl, void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                           Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 static thread_local char g_err[512] = "";
 
 static int set_cuda_err(cudaError_t e, const char *what) {
@@ -58,6 +77,7 @@ struct moco_plan {
   int rrt[3], rnrt[3];        // refine levels: template rows per tile, row tiles
   u64 *racc;                  // refine accumulators [cap][18] (kept zero between calls)
   RtcGeom rtc[3];             // tensor-core refine geometry per level (kernels_rtc.cuh)
+  bool pdl_now = false;       // inside a closed-loop (latency-route) call: kernels chained by PDL
   FraGeom fra;                // frame-resident refine + pick + apply at level 0 (kernels_fra.cuh)
   bool fra_ok;
   uint32_t *fra_tc = nullptr; // its shifted, pre-split template copies (k_fra_tcopy)
@@ -77,6 +97,7 @@ struct moco_plan {
   struct {
     int rtc = -1;          // MOCO_RTC: -1 default, 0 CUDA-core refine sums, 1 force tensor cores
     int rtc_parts = 0;     // MOCO_RTC_PARTS (0: cost model)
+    int pdl = 1;           // MOCO_PDL=0: no programmatic dependent launch on the closed-loop route
     int fra = 0;           // MOCO_FRA=1: level-0 refine + pick + apply by the frame-resident
                            // cluster kernel k_refine_frame (one HBM read per frame, but CUDA-core
                            // bound: 0.68 us/frame alone vs 0.30 for k_refine_tc + k_refine_pick,
@@ -556,11 +577,11 @@ static F2RowsArgs fft2_rows_args(const moco_plan *p, const void *img, int64_t fs
   return a;
 }
 template <int PC>
-static void fft2_rows_launch(const F2RowsArgs &a, int L, int64_t nblk, int hw, cudaStream_t st) {
+static void fft2_rows_launch(const F2RowsArgs &a, int L, int64_t nblk, int hw, cudaStream_t st, bool pdl = false) {
   using G = F2<PC>;
   const int smem = fft2_rows_smem(G::N, G::NF, G::STRIDE, a.per, L, a.nc, hw);
-  if (L == 0) k_fft2_rows<PC, 0><<<(unsigned)nblk, F2_THREADS, smem, st>>>(a);
-  else k_fft2_rows<PC, 1><<<(unsigned)nblk, F2_THREADS, smem, st>>>(a);
+  if (L == 0) launchk(pdl, k_fft2_rows<PC, 0>, (unsigned)nblk, F2_THREADS, smem, st, a);
+  else launchk(pdl, k_fft2_rows<PC, 1>, (unsigned)nblk, F2_THREADS, smem, st, a);
 }
 
 
@@ -586,7 +607,7 @@ static int fft2_sub(moco_plan *p, const char *fr, int64_t fstride, int pitch, in
       a.E = F.E + so * f2_esz2(g.hw);
       a.mu = F.tst;
       ProfScope ps(p, MOCO_K_PREP, st);
-      fft2_rows_launch<P>(a, LK, nb * ((npair + per - 1) / per), g.hw, st);
+      fft2_rows_launch<P>(a, LK, nb * ((npair + per - 1) / per), g.hw, st, p->pdl_now);
     }
   });
   CKL("k_fft2_rows");
@@ -606,7 +627,7 @@ static int fft2_sub(moco_plan *p, const char *fr, int64_t fstride, int pitch, in
       c.lin = fft_mean_mode(p) == 1 ? 1 : 0;
       c.ynorm = F.ynorm + so;
       ProfScope ps(p, MOCO_K_COARSE, st);
-      k_fft2_cols<P><<<(unsigned)(nb * nblk), F2_THREADS, F.smem2_cols, st>>>(c);
+      launchk(p->pdl_now, k_fft2_cols<P>, (unsigned)(nb * nblk), F2_THREADS, F.smem2_cols, st, c);
     }
   });
   CKL("k_fft2_cols");
@@ -634,10 +655,10 @@ static int fft2_sub(moco_plan *p, const char *fr, int64_t fstride, int pitch, in
       // (the closed-loop call: the exact sums are latency-bound, one block per part)
       a.rparts = (int)std::max<int64_t>(1, std::min<int64_t>(g.mc / 2, std::max<int64_t>(g.mc / 16, 4 * p->nsm / nb)));
       ProfScope ps(p, MOCO_K_SCORE, st);
-      k_fft2_score<P><<<(unsigned)(nb * nblk), F2_THREADS, F.smem2_score, st>>>(a);
+      launchk(p->pdl_now, k_fft2_score<P>, (unsigned)(nb * nblk), F2_THREADS, F.smem2_score, st, a);
       const unsigned rg = (unsigned)(nb * a.rparts);
-      if (LK == 0) k_fft2_rescore<0><<<rg, 256, 0, st>>>(a);
-      else k_fft2_rescore<1><<<rg, 256, 0, st>>>(a);
+      if (LK == 0) launchk(p->pdl_now, k_fft2_rescore<0>, rg, 256, 0, st, a);
+      else launchk(p->pdl_now, k_fft2_rescore<1>, rg, 256, 0, st, a);
     }
   });
   CKL("k_fft2_score");
@@ -879,6 +900,7 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
     if (const char *v = getenv("MOCO_TC_FUSED")) p->knob.tc_fused = atoi(v);
     if (const char *v = getenv("MOCO_FFT_MEAN")) p->knob.fft_mean = std::min(2, std::max(0, atoi(v)));
     if (const char *v = getenv("MOCO_FRA")) p->knob.fra = atoi(v);
+    if (const char *v = getenv("MOCO_PDL")) p->knob.pdl = atoi(v);
     if (const char *v = getenv("MOCO_FRA_MIN")) p->knob.fra_min = std::max(1, atoi(v));
   }
   for (int l = 0; l <= levels; ++l) {
@@ -1253,7 +1275,7 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
   b.corrected = (uint16_t *)corr;
   // small batches: several CTAs per frame for the apply (the accumulators are then
   // cleared by a memset after the pick instead of by the single CTA)
-  b.parts = (int)std::max<int64_t>(1, std::min<int64_t>(16, p->nsm / std::max<int64_t>(1, B)));
+  b.parts = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(16, p->ml[l] / 4), p->nsm / std::max<int64_t>(1, B)));
   if (!corr) b.parts = 1;
   b.ga_total = 0;
   b.kw = 0;
@@ -1289,8 +1311,8 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
     ProfScope ps(p, MOCO_K_REFINE, st);
     const int smem = rs_smem_bytes(a.rt, a.stages);
     const int nct = (a.nl + RS_CT - 1) / RS_CT;
-    if (a.wide) k_refine_sums<true><<<(unsigned)(a.nrt * nct), RS_THREADS, smem, st>>>(tmF, a);
-    else k_refine_sums<false><<<(unsigned)(a.nrt * nct), RS_THREADS, smem, st>>>(tmF, a);
+    if (a.wide) launchk(p->pdl_now, k_refine_sums<true>, (unsigned)(a.nrt * nct), RS_THREADS, smem, st, tmF, a);
+    else launchk(p->pdl_now, k_refine_sums<false>, (unsigned)(a.nrt * nct), RS_THREADS, smem, st, tmF, a);
   }
   p->launches++;
   CKL(rtc ? "k_refine_tc" : "k_refine_sums");
@@ -1301,7 +1323,7 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
   }
   {
     ProfScope ps(p, MOCO_K_APPLY, st);
-    k_refine_pick<<<(unsigned)(B * b.parts), 256, 0, st>>>(b);
+    launchk(p->pdl_now && !st_pick, k_refine_pick, (unsigned)(B * b.parts), 256, 0, st, b);
   }
   p->launches++;
   CKL("k_refine_pick");
@@ -1725,6 +1747,7 @@ int moco_align_batch(moco_plan *p, const void *d_frames, int64_t T, int32_t *d_s
   // closed-loop sizes: the FFT path spreads one frame over many SMs (DESIGN.md §8 latency)
   if (p->algo == MOCO_ALGO_TC && T <= LAT_T && p->fft.ready && p->fft.tpl_ready && !p->algo_forced) {
     p->algo = MOCO_ALGO_FFT;
+    p->pdl_now = p->knob.pdl != 0 && !p->prof_on;   // (profiling events between kernels: plain launches)
     for (int64_t f0 = 0; f0 < T && rc == MOCO_OK; f0 += p->cap) {
       const int64_t B = std::min<int64_t>(p->cap, T - f0);
       rc = run_batch_user(p, (const char *)d_frames + f0 * fbytes, B, d_shifts + 2 * f0, d_fmin + f0,
@@ -1732,6 +1755,7 @@ int moco_align_batch(moco_plan *p, const void *d_frames, int64_t T, int32_t *d_s
                      d_flags ? d_flags + f0 : nullptr, nullptr, (cudaStream_t)stream);
     }
     p->algo = MOCO_ALGO_TC;
+    p->pdl_now = false;
     return rc;
   }
   if (p->algo == MOCO_ALGO_TC && T > p->cap && p->tc.G2 && p->racc2 && p->sh1b && fused_ok(p, 0) &&
