@@ -97,7 +97,8 @@ struct moco_plan {
   struct {
     int rtc = -1;          // MOCO_RTC: -1 default, 0 CUDA-core refine sums, 1 force tensor cores
     int rtc_parts = 0;     // MOCO_RTC_PARTS (0: cost model)
-    int pdl = 1;           // MOCO_PDL=0: no programmatic dependent launch on the closed-loop route
+    int pdl = 2;           // MOCO_PDL: programmatic dependent launch 0 off, 1 closed-loop route only,
+                           // 2 also every FFT sub-batch chain (w = 85 467 -> 470 k frames/s)
     int fra = 0;           // MOCO_FRA=1: level-0 refine + pick + apply by the frame-resident
                            // cluster kernel k_refine_frame (one HBM read per frame, but CUDA-core
                            // bound: 0.68 us/frame alone vs 0.30 for k_refine_tc + k_refine_pick,
@@ -595,6 +596,9 @@ static int fft2_sub(moco_plan *p, const char *fr, int64_t fstride, int pitch, in
   const FftGeom &g = F.g;
   const int L = p->levels, LK = std::min(L, 1);
   const int64_t so = (int64_t)set * F.cap;
+  // PDL through the sub-batch's chain (rows -> cols -> score -> rescore): the closed-loop
+  // route, and (MOCO_PDL=2, the default) every sub-batch
+  const bool pdl = p->pdl_now || (p->knob.pdl >= 2 && !p->prof_on);
   float2 *Pset = F.P + so * g.W * g.Kc;
   fft_dispatch(F.pc, [&](auto PC) {
     constexpr int P = decltype(PC)::value;
@@ -607,7 +611,7 @@ static int fft2_sub(moco_plan *p, const char *fr, int64_t fstride, int pitch, in
       a.E = F.E + so * f2_esz2(g.hw);
       a.mu = F.tst;
       ProfScope ps(p, MOCO_K_PREP, st);
-      fft2_rows_launch<P>(a, LK, nb * ((npair + per - 1) / per), g.hw, st, p->pdl_now);
+      fft2_rows_launch<P>(a, LK, nb * ((npair + per - 1) / per), g.hw, st, pdl);
     }
   });
   CKL("k_fft2_rows");
@@ -627,7 +631,7 @@ static int fft2_sub(moco_plan *p, const char *fr, int64_t fstride, int pitch, in
       c.lin = fft_mean_mode(p) == 1 ? 1 : 0;
       c.ynorm = F.ynorm + so;
       ProfScope ps(p, MOCO_K_COARSE, st);
-      launchk(p->pdl_now, k_fft2_cols<P>, (unsigned)(nb * nblk), F2_THREADS, F.smem2_cols, st, c);
+      launchk(pdl, k_fft2_cols<P>, (unsigned)(nb * nblk), F2_THREADS, F.smem2_cols, st, c);
     }
   });
   CKL("k_fft2_cols");
@@ -655,10 +659,10 @@ static int fft2_sub(moco_plan *p, const char *fr, int64_t fstride, int pitch, in
       // (the closed-loop call: the exact sums are latency-bound, one block per part)
       a.rparts = (int)std::max<int64_t>(1, std::min<int64_t>(g.mc / 2, std::max<int64_t>(g.mc / 16, 4 * p->nsm / nb)));
       ProfScope ps(p, MOCO_K_SCORE, st);
-      launchk(p->pdl_now, k_fft2_score<P>, (unsigned)(nb * nblk), F2_THREADS, F.smem2_score, st, a);
+      launchk(pdl, k_fft2_score<P>, (unsigned)(nb * nblk), F2_THREADS, F.smem2_score, st, a);
       const unsigned rg = (unsigned)(nb * a.rparts);
-      if (LK == 0) launchk(p->pdl_now, k_fft2_rescore<0>, rg, 256, 0, st, a);
-      else launchk(p->pdl_now, k_fft2_rescore<1>, rg, 256, 0, st, a);
+      if (LK == 0) launchk(pdl, k_fft2_rescore<0>, rg, 256, 0, st, a);
+      else launchk(pdl, k_fft2_rescore<1>, rg, 256, 0, st, a);
     }
   });
   CKL("k_fft2_score");
