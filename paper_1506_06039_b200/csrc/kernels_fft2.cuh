@@ -840,22 +840,35 @@ __global__ void __launch_bounds__(F2_THREADS, 4) k_fft2_score(F2ScoreArgs a) {
     const int64_t cq = (int64_t)(s < 0 ? 2 : 0) * hw * hw;
     const u64 *CPq = E + 1 + 4 * hw + cq, *CPl = EL + 1 + 4 * hw + cq;
     float rowlb = 3.0e38f;
+    // the lag's global operands (2-D corner sum of the frame, template energy and sum),
+    // loaded one lane iteration ahead so their latency overlaps the previous lag's math
+    auto ldlag = [&](int ti, u64 &cv, u64 &gbv, long long &glv) {
+      const int t = ti - hw, lag = si * W + ti;
+      cv = 0;
+      if (s != 0 && t != 0)   // 2-D corner sums of the excluded |s| x |t| corner (k_fft2_cols)
+        cv = __ldg(CPq + (t < 0 ? hw * hw : 0) + (int64_t)(abs(s) - 1) * hw + abs(t) - 1);
+      gbv = __ldg(a.gb + lag);
+      glv = mu ? __ldg(a.gl + lag) : 0;
+    };
+    u64 cv_n = 0, gb_n = 0;
+    long long gl_n = 0;
+    if (lane < W) ldlag(lane, cv_n, gb_n, gl_n);
     for (int ti = lane; ti < W; ti += 32) {
+      const u64 cv = cv_n, gbv = gb_n;
+      const long long glv = gl_n;
+      if (ti + 32 < W) ldlag(ti + 32, cv_n, gb_n, gl_n);
       const int t = ti - hw;
       const int tt = t < 0 ? t + Mc : t;
       const float hp = xr[2 * G::ix(tt)];
       const int lag = si * W + ti;
-      u64 ga = tot - rx - CX[ti], sa = lin ? totl - rxl - CXl[ti] : 0;
-      if (s != 0 && t != 0) {   // 2-D corner sums of the excluded |s| x |t| corner (k_fft2_cols)
-        const int64_t o = (t < 0 ? hw * hw : 0) + (int64_t)(abs(s) - 1) * hw + abs(t) - 1;
-        ga += __ldg(CPq + o);
-        if (lin) sa += __ldg(CPl + o);
-      }
+      u64 ga = tot - rx - CX[ti] + cv, sa = lin ? totl - rxl - CXl[ti] : 0;
+      if (lin && s != 0 && t != 0)
+        sa += __ldg(CPl + (t < 0 ? hw * hw : 0) + (int64_t)(abs(s) - 1) * hw + abs(t) - 1);
       const long long area = (long long)(a.mc - abs(s)) * (a.nc - abs(t));
-      const long long corr = mu ? mub * (long long)sa + mu * ((long long)a.gl[lag] - mub * area) : 0;
+      const long long corr = mu ? mub * (long long)sa + mu * (glv - mub * area) : 0;
       const double h = (double)hp + (double)corr;
       if (a.h_out) a.h_out[f * W * W + lag] = (float)h;
-      const double gsum = (double)ga + (double)a.gb[lag];
+      const double gsum = (double)ga + (double)gbv;
       const double hdev = epsh + 2 * U53 * (fabs((double)hp) + fabs((double)corr));   // |h~ - h|
       const double inv = ri * cinv[ti];
       const double fa = (gsum - 2.0 * h) * inv;
