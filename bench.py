@@ -10,9 +10,11 @@ corrected frames written.  A step = one moco_align_batch over the whole
 
 N>1 is launched by torch.distributed.run (one rank per GPU, NCCL): weak
 scaling -- every rank aligns its own contiguous 10,000-frame block of an
-N*10,000-frame stack, the template is broadcast from rank 0 (setup), and each
-timed step ends with an NCCL all_gather of the per-frame results (shifts,
-f_min) to every rank; timing is the max over ranks of CUDA-event time.
+N*10,000-frame stack, the template is broadcast from rank 0 (setup), and in each
+timed step the library's kernels store every frame's (shifts, f_min) record straight
+into rank 0's memory over NVLink (CUDA symmetric memory; one device-side barrier per
+step -- ``--gather nccl``: an NCCL all_gather instead); timing is the max over ranks of
+CUDA-event time.
 
 Rank 0 prints ONE JSON line (contract in the task statement / DESIGN.md §8).
 """
@@ -349,6 +351,9 @@ def main():
     ap.add_argument("--frames", type=int, default=None, help="override frames per rank")
     ap.add_argument("--impl", default="moco", choices=["moco", "reference"])
     ap.add_argument("--algo", default="auto", choices=["auto", "direct", "tc", "fft"])
+    ap.add_argument("--gather", default="peer", choices=["peer", "nccl"],
+                    help="N>1: per-frame results into rank 0's memory by the kernels over peer "
+                         "memory (fused) or an NCCL all-gather")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-paper", action="store_true", help="skip the paper-default (w=85) context line")
@@ -390,9 +395,23 @@ def main():
     shifts = torch.empty((Tl, 2), dtype=torch.int32, device=dev)
     fmin = torch.empty((Tl,), dtype=torch.float64, device=dev)
     corrected = torch.empty_like(frames)
-    from paper_1506_06039_b200.dist import gather_results
+    from paper_1506_06039_b200.dist import PeerResults, gather_results
+    peer = None
+    gather_mode = None
+    if world > 1:
+        gather_mode = args.gather
+        if args.gather == "peer":
+            try:   # fused: the kernels store each frame's record into rank 0's memory
+                peer = PeerResults(Tl, dev)
+            except Exception as e:   # (no symmetric memory on this node: the NCCL all-gather)
+                print(f"[bench] peer-memory gather unavailable ({str(e)[:120]}); NCCL all-gather", file=sys.stderr)
+                gather_mode = "nccl"
 
     def step():
+        if peer is not None:
+            plan.align_into(frames, peer.shifts, peer.fmin, corrected)
+            peer.barrier()
+            return
         plan.align_into(frames, shifts, fmin, corrected)
         if world > 1:   # per-frame results of every rank to every rank (16 B/frame)
             gather_results(shifts, fmin, world * Tl)
@@ -682,7 +701,8 @@ def main():
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
                "vs_baseline": None, "dtype": "u16" if spec.dtype == "u16" else "f32", "data": "synthetic",
-               "config": workload_config(spec, world, plan.algo),
+               "config": dict(workload_config(spec, world, plan.algo),
+                              **({"results_gather": gather_mode} if world > 1 else {})),
                "roofline": roofline,
                "step_roofline": {"fps": step_roof, "frac": value / world / step_roof,
                                  "hbm_fps": hbm_roof_fps, "alu_fps": alu_roof_fps,

@@ -9,7 +9,11 @@ rank (one process per GPU).  The only exchanges are at the two ends:
     every rank -- in particular rank 0 -- holds the whole trajectory
     (16 bytes per frame).
 
-Corrected frames stay on the rank that produced them.  ``align_fn`` is the
+Corrected frames stay on the rank that produced them.  The results exchange is a
+compute step followed by a collective, so it also comes fused (``PeerResults``): the
+kernels that produce the per-frame records (the level-0 pick's epilogue) store them
+straight into rank 0's memory through a CUDA symmetric-memory peer mapping (NVLink P2P
+stores), and one device-side barrier per step replaces the all-gather.  ``align_fn`` is the
 per-rank aligner: ``Plan.align`` on GPUs; the CPU tests pass a stand-in so the
 sharding and gather logic is exercised under the gloo backend without a GPU.
 """
@@ -68,3 +72,34 @@ def align_sharded(frames_local: torch.Tensor, T: int, align_fn: Callable, group=
     sh, fm, co = align_fn(frames_local)[:3]
     full_sh, full_fm = gather_results(sh, fm, T, group=group)
     return full_sh, full_fm, co
+
+
+class PeerResults:
+    """Fused results gather over peer memory.
+
+    Rank 0 owns symmetric buffers of ``world * per`` records; every rank gets views of
+    rank 0's buffers at its own block (``shifts``, ``fmin``), which it passes to
+    ``Plan.align_into`` as the output pointers: the library's kernels then write each
+    frame's (s, t, f_min) over NVLink into rank 0's memory as they produce it (the
+    C-ABI takes any device-accessible pointer).  ``barrier()`` (device-side, stream
+    ordered, release/acquire across ranks) makes them visible to rank 0."""
+
+    def __init__(self, per: int, device, group=None):
+        import torch.distributed._symmetric_memory as symm
+        g = group if group is not None else dist.group.WORLD
+        world, rank = dist.get_world_size(g), dist.get_rank(g)
+        self.per, self.world, self.rank = per, world, rank
+        self._sh = symm.empty((world * per, 2), dtype=torch.int32, device=device)
+        self._fm = symm.empty((world * per,), dtype=torch.float64, device=device)
+        self._hs = symm.rendezvous(self._sh, g)
+        self._hf = symm.rendezvous(self._fm, g)
+        lo, hi = rank * per, (rank + 1) * per
+        self.shifts = self._hs.get_buffer(0, (world * per, 2), torch.int32)[lo:hi]
+        self.fmin = self._hf.get_buffer(0, (world * per,), torch.float64)[lo:hi]
+
+    def barrier(self) -> None:
+        self._hs.barrier()
+
+    def gathered(self, T: int):
+        """(shifts [T,2], fmin [T]) on rank 0 after ``barrier()`` (frame order)."""
+        return self._sh[:T], self._fm[:T]
