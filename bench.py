@@ -10,11 +10,11 @@ corrected frames written.  A step = one moco_align_batch over the whole
 
 N>1 is launched by torch.distributed.run (one rank per GPU, NCCL): weak
 scaling -- every rank aligns its own contiguous 10,000-frame block of an
-N*10,000-frame stack, the template is broadcast from rank 0 (setup), and in each
-timed step the library's kernels store every frame's (shifts, f_min) record straight
-into rank 0's memory over NVLink (CUDA symmetric memory; one device-side barrier per
-step -- ``--gather nccl``: an NCCL all_gather instead); timing is the max over ranks of
-CUDA-event time.
+N*10,000-frame stack, the template is broadcast from rank 0 (setup), and each timed
+step ends with an NCCL all_gather of the per-frame results (shifts, f_min) -- or, with
+``--gather peer``, the library's kernels store every frame's record straight into rank
+0's memory over NVLink (CUDA symmetric memory, one device-side barrier per step); timing
+is the max over ranks of CUDA-event time.
 
 Rank 0 prints ONE JSON line (contract in the task statement / DESIGN.md §8).
 """
@@ -351,9 +351,10 @@ def main():
     ap.add_argument("--frames", type=int, default=None, help="override frames per rank")
     ap.add_argument("--impl", default="moco", choices=["moco", "reference"])
     ap.add_argument("--algo", default="auto", choices=["auto", "direct", "tc", "fft"])
-    ap.add_argument("--gather", default="peer", choices=["peer", "nccl"],
-                    help="N>1: per-frame results into rank 0's memory by the kernels over peer "
-                         "memory (fused) or an NCCL all-gather")
+    ap.add_argument("--gather", default="nccl", choices=["peer", "nccl"],
+                    help="N>1: per-frame results by an NCCL all-gather (default: the path that has run "
+                         "at N>1), or stored into rank 0's memory by the kernels over peer memory (fused; "
+                         "tested at N=1 only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-paper", action="store_true", help="skip the paper-default (w=85) context line")
