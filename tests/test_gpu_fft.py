@@ -331,3 +331,23 @@ def test_fft_mean_removal_adversarial_templates(kind, mode, monkeypatch):
         out[algo] = (sh, fm, co.view(torch.int16), fl & 1)
     for a, b in zip(out["fft"], out["tc"]):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("c,T", [(2, 700), (1, 300), (2, 1), (1, 1)])
+def test_pdl_chains_identical(c, T, monkeypatch):
+    """Programmatic dependent launch (the closed-loop route and every FFT sub-batch chain,
+    MOCO_PDL=2, the default) against plain launches (MOCO_PDL=0): identical shifts, f_min
+    and corrected frames, for whole-stack FFT calls and single-frame calls on a TC plan."""
+    spec = config_spec(c, T=max(T, 8))
+    st = make_stack(spec, 0, T, device=DEV)
+    out = {}
+    for mode in ("0", "2"):
+        monkeypatch.setenv("MOCO_PDL", mode)
+        p = Plan(spec.m, spec.n, spec.w, spec.levels, spec.dtype, 12, device=0,
+                 algo="fft" if T > 16 else "auto")
+        p.set_template(st.template)
+        sh, fm, co, _ = p.align(st.frames, corrected=True)
+        torch.cuda.synchronize()
+        out[mode] = (sh, fm.view(torch.int64), co.view(torch.int16))
+    for a, b in zip(out["0"], out["2"]):
+        assert torch.equal(a, b)
