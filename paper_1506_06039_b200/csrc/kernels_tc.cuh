@@ -64,7 +64,7 @@ struct TcGeom {
   int GG;       // operand groups per CTA
   int tmem_cols;
   int smem;     // dynamic shared memory bytes
-  int prep_smem;
+  int prep_smem, prep_smem1;   // k_tc_prep dynamic shared memory: F frames / one frame per CTA
 };
 
 struct TcPlan {
@@ -263,6 +263,7 @@ struct TcPrepArgs {
   TcGeom g;
   uint8_t *G;               // [groups][nstrips][2][R][F][2][16]
   u64 *ga;                  // [B][W*W]
+  int fp;                   // frames per CTA: g.F, or 1 (the CTA then fits beside the search)
   uint16_t *img1;           // L = 2: also write the level-1 image (2x2 sums) here, or null
   int64_t fs1;              // its frame stride and row pitch (elements)
   int p1;
@@ -356,30 +357,32 @@ template <int L>
 __global__ void __launch_bounds__(256, TC_PREP_MINB) k_tc_prep(TcPrepArgs a) {
   const TcGeom &g = a.g;
   extern __shared__ __align__(16) unsigned char smem[];
-  const int F = g.F, hw = g.hw, w = g.w, mc = g.mc, nc = g.nc, W = g.W;
+  const int F = g.F, FP = a.fp, hw = g.hw, w = g.w, mc = g.mc, nc = g.nc, W = g.W;
   const int CS = w * w;                       // corner table size per quad (index 0 = empty)
-  u64 *rowE = reinterpret_cast<u64 *>(smem);  // [F][2*hw]  top rows 0..hw-1, bottom rows from the bottom
-  u64 *colE = rowE + F * 2 * hw;              // [F][2*hw]
-  u64 *cor = colE + F * 2 * hw;               // [F][4][w][w]
-  u64 *tot = cor + F * 4 * CS;                // [F]
+  u64 *rowE = reinterpret_cast<u64 *>(smem);  // [FP][2*hw]  top rows 0..hw-1, bottom rows from the bottom
+  u64 *colE = rowE + FP * 2 * hw;             // [FP][2*hw]
+  u64 *cor = colE + FP * 2 * hw;              // [FP][4][w][w]
+  u64 *tot = cor + FP * 4 * CS;               // [FP]
   const int tid = threadIdx.x, nth = blockDim.x;
-  for (int k = tid; k < F * (4 * hw + 4 * CS + 1); k += nth) rowE[k] = 0;
+  for (int k = tid; k < FP * (4 * hw + 4 * CS + 1); k += nth) rowE[k] = 0;
   __syncthreads();
-  const int grp = blockIdx.x;
   // warp = one (frame, plane row) item at a time, lanes = 8-column chunks of the coarse
   // row: every load instruction reads 512 contiguous bytes of a raw row (L >= 1 folds
   // 2^L raw rows); energies: row sums by warp reduction, edge columns by atomics on
   // distinct addresses, corner tables by plain stores
   const int warp = tid >> 5, lane = tid & 31, nwarp = nth >> 5;
   const int nchunk = nc >> 3;
-  // F divides the warp count, so a warp always works on the same frame f = warp % F;
-  // edge-column energies accumulate in registers (a lane owns at most one left-edge
-  // and one right-edge chunk) and are added to shared memory once at the end
-  const int f = warp % F;
-  const int fi = grp * F + f;
+  // FP (frames per CTA: F, or 1 so that a CTA fits beside the search kernel) divides the
+  // warp count, so a warp always works on the same frame fl = warp % FP; edge-column
+  // energies accumulate in registers (a lane owns at most one left-edge and one
+  // right-edge chunk) and are added to shared memory once at the end.  The operand
+  // planes keep the search's layout: group grp = fi / F, slot f = fi % F.
+  const int fl = warp % FP;
+  const int fi = (int)blockIdx.x * FP + fl;
+  const int grp = fi / F, f = fi - grp * F;
   const uint16_t *frame = a.frames + (int64_t)(fi < a.B ? fi : 0) * a.fstride;
   // this warp's edge-column sums (left hw, right hw), owned by the warp: no atomics
-  u64 *ce = tot + F + warp * 2 * hw;
+  u64 *ce = tot + FP + warp * 2 * hw;
   for (int k = lane; k < 2 * hw; k += 32) ce[k] = 0;
   __syncwarp();
   u64 ftot = 0;
@@ -455,7 +458,7 @@ __global__ void __launch_bounds__(256, TC_PREP_MINB) k_tc_prep(TcPrepArgs a) {
         for (int qr = 0; qr < 2; ++qr) {
           if (!(qr ? rt : lf)) continue;
           const int qq = qr ? nc - c : c + 1;
-          cor[((f * 4) + (qb * 2 + qr)) * CS + pp * w + qq] = v2;
+          cor[((fl * 4) + (qb * 2 + qr)) * CS + pp * w + qq] = v2;
         }
       }
     }
@@ -466,14 +469,14 @@ __global__ void __launch_bounds__(256, TC_PREP_MINB) k_tc_prep(TcPrepArgs a) {
     rs = warp_sum(rs);
     if (lane == 0) {
       ftot += rs;
-      if (cr < hw) rowE[f * 2 * hw + cr] = rs;
-      if (cr >= mc - hw) rowE[f * 2 * hw + hw + (mc - 1 - cr)] = rs;
+      if (cr < hw) rowE[fl * 2 * hw + cr] = rs;
+      if (cr >= mc - hw) rowE[fl * 2 * hw + hw + (mc - 1 - cr)] = rs;
     }
   };
   // plane rows pr = warp / F, + nwarp / F, ...; TC_PREP_RPP rows per pass (loads first)
-  const int pstep = nwarp / F;
+  const int pstep = nwarp / FP;
   int nrows = 0;
-  for (int pr0 = warp / F; pr0 < g.R; pr0 += TC_PREP_RPP * pstep) {
+  for (int pr0 = warp / FP; pr0 < g.R; pr0 += TC_PREP_RPP * pstep) {
     if (one_chunk && nrows + TC_PREP_RPP > 16) {   // <= 16 rows of squares per flush
       flush_edges();
       nrows = 0;
@@ -520,28 +523,28 @@ __global__ void __launch_bounds__(256, TC_PREP_MINB) k_tc_prep(TcPrepArgs a) {
   // flush this warp's edge-column and total energies
   if (one_chunk) flush_edges();
   __syncwarp();
-  for (int k = lane; k < 2 * hw; k += 32) atomicAdd(&colE[f * 2 * hw + k], ce[k]);
-  if (lane == 0) atomicAdd(&tot[f], ftot);
+  for (int k = lane; k < 2 * hw; k += 32) atomicAdd(&colE[fl * 2 * hw + k], ce[k]);
+  if (lane == 0) atomicAdd(&tot[fl], ftot);
   __syncthreads();
   // prefix sums: edge strips (1-D), corners (2-D, the DP of P:35 in each corner)
-  for (int k = tid; k < F * 4; k += nth) {
+  for (int k = tid; k < FP * 4; k += nth) {
     u64 *e = (k & 2) ? colE : rowE;
     u64 *p = e + (k >> 2) * 2 * hw + (k & 1) * hw;
     for (int q = 1; q < hw; ++q) p[q] += p[q - 1];
   }
-  for (int k = tid; k < F * 4 * w; k += nth) {
+  for (int k = tid; k < FP * 4 * w; k += nth) {
     u64 *c = cor + (k / w) * CS + (k % w) * w;
     for (int q = 1; q < w; ++q) c[q] += c[q - 1];
   }
   __syncthreads();
-  for (int k = tid; k < F * 4 * w; k += nth) {
+  for (int k = tid; k < FP * 4 * w; k += nth) {
     u64 *c = cor + (k / w) * CS + (k % w);
     for (int p = 1; p < w; ++p) c[p * w] += c[(p - 1) * w];
   }
   __syncthreads();
-  for (int k = tid; k < F * W * W; k += nth) {
+  for (int k = tid; k < FP * W * W; k += nth) {
     const int f = k / (W * W), lag = k % (W * W);
-    const int fi = grp * F + f;
+    const int fi = (int)blockIdx.x * FP + f;
     if (fi >= a.B) continue;
     const int s = lag / W - hw, t = lag % W - hw;
     const u64 *re = rowE + f * 2 * hw, *ce = colE + f * 2 * hw;
@@ -1064,6 +1067,7 @@ inline bool tc_make_geom(TcGeom *gp, int w, int mc, int nc, int L, int vb) {
   g.tmem_cols = cols;
   g.smem = smem_for(g.GG, g.ICH);
   g.prep_smem = (g.F * (4 * g.hw + 4 * w * w + 1) + 8 * 2 * g.hw) * 8;   // + per-warp edge-column sums
+  g.prep_smem1 = ((4 * g.hw + 4 * w * w + 1) + 8 * 2 * g.hw) * 8;        // one frame per CTA
   *gp = g;
   return true;
 }
@@ -1113,6 +1117,13 @@ inline int tc_init(TcPlan *tc, int w, int mc, int nc, int L, int vb, int64_t cap
       smem_attr(k_tc_prep<1>, g.prep_smem) != cudaSuccess ||
       smem_attr(k_tc_prep<2>, g.prep_smem) != cudaSuccess)
     return -1;
+  if (const char *cv = getenv("MOCO_PREP_CARVE")) {   // tuning: the prep's shared-memory carveout (%)
+    const int pc = atoi(cv);
+    cudaFuncSetAttribute((const void *)k_tc_prep<0>, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
+    cudaFuncSetAttribute((const void *)k_tc_prep<1>, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
+    cudaFuncSetAttribute((const void *)k_tc_prep<2>, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
+    cudaGetLastError();
+  }
   tc->ready = true;
   return 0;
 }

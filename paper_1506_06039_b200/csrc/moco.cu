@@ -97,6 +97,7 @@ struct moco_plan {
   struct {
     int rtc = -1;          // MOCO_RTC: -1 default, 0 CUDA-core refine sums, 1 force tensor cores
     int rtc_parts = 0;     // MOCO_RTC_PARTS (0: cost model)
+    int prep_fp = 0;       // MOCO_PREP_FP=1: k_tc_prep one frame per CTA (co-resides with the search)
     int pdl = 2;           // MOCO_PDL: programmatic dependent launch 0 off, 1 closed-loop route only,
                            // 2 also every FFT sub-batch chain (w = 85 467 -> 470 k frames/s)
     int fra = 0;           // MOCO_FRA=1: level-0 refine + pick + apply by the frame-resident
@@ -905,6 +906,7 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
     if (const char *v = getenv("MOCO_FFT_MEAN")) p->knob.fft_mean = std::min(2, std::max(0, atoi(v)));
     if (const char *v = getenv("MOCO_FRA")) p->knob.fra = atoi(v);
     if (const char *v = getenv("MOCO_PDL")) p->knob.pdl = atoi(v);
+    if (const char *v = getenv("MOCO_PREP_FP")) p->knob.prep_fp = atoi(v);
     if (const char *v = getenv("MOCO_FRA_MIN")) p->knob.fra_min = std::max(1, atoi(v));
   }
   for (int l = 0; l <= levels; ++l) {
@@ -1441,12 +1443,17 @@ static int launch_tc_prep(moco_plan *p, const void *frames_b, int64_t B, uint8_t
   TcPrepArgs pa;
   pa.frames = (const uint16_t *)frames_b; pa.fstride = (int64_t)p->m * p->n; pa.n = p->n;
   pa.B = (int)B; pa.g = g; pa.G = G; pa.ga = ga;
+  // one frame per CTA (MOCO_PREP_FP=1): the CTA's shared memory then fits in what the
+  // search kernel leaves free on its SM, so the prep of the next batch can co-run with it
+  pa.fp = p->knob.prep_fp == 1 ? 1 : g.F;
+  const int psm = pa.fp == 1 ? g.prep_smem1 : g.prep_smem;
+  const unsigned pgrid = (unsigned)(groups * g.F / pa.fp);
   pa.img1 = (uint16_t *)img1; pa.fs1 = (int64_t)p->ml[1] * p->pitch[1]; pa.p1 = p->pitch[1];
   {
     ProfScope ps(p, MOCO_K_PREP, st);
-    if (p->levels == 0) k_tc_prep<0><<<(unsigned)groups, 256, g.prep_smem, st>>>(pa);
-    else if (p->levels == 1) k_tc_prep<1><<<(unsigned)groups, 256, g.prep_smem, st>>>(pa);
-    else k_tc_prep<2><<<(unsigned)groups, 256, g.prep_smem, st>>>(pa);
+    if (p->levels == 0) k_tc_prep<0><<<pgrid, 256, psm, st>>>(pa);
+    else if (p->levels == 1) k_tc_prep<1><<<pgrid, 256, psm, st>>>(pa);
+    else k_tc_prep<2><<<pgrid, 256, psm, st>>>(pa);
   }
   p->launches++;
   CKL("k_tc_prep");
