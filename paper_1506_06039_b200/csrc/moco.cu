@@ -101,8 +101,9 @@ struct moco_plan {
     int pdl = 2;           // MOCO_PDL: programmatic dependent launch 0 off, 1 closed-loop route only,
                            // 2 also every FFT sub-batch chain (w = 85 467 -> 470 k frames/s)
     int fra = 0;           // MOCO_FRA=1: level-0 refine + pick + apply by the frame-resident
-                           // cluster kernel k_refine_frame (one HBM read per frame, but CUDA-core
-                           // bound: 0.68 us/frame alone vs 0.30 for k_refine_tc + k_refine_pick,
+                           // cluster kernel k_refine_frame (one HBM read per frame, but bound by
+                           // CUDA-core dot products and cluster synchronisation: 0.66 us/frame
+                           // alone vs 0.34 for k_refine_tc + k_ga_pieces + k_refine_pick,
                            // DESIGN.md section 11) instead of the tensor-core refine + pick
     int fra_min = 64;      // MOCO_FRA_MIN: smallest batch for k_refine_frame
     bool nofuse_ds = false, ga_inpick = false, nopipe = false;
