@@ -345,7 +345,7 @@ def workload_config(spec, world, algo):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=40)   # ~0.22 s timed: several 50-ms clock samples
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--frames", type=int, default=None, help="override frames per rank")
