@@ -1045,7 +1045,12 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
       // (levels > 0, N <= 192: C2 1.70 -> 1.77 M,
       // C4 399 -> 412 k; the finer batches keep the three streams busier), whole waves up
       // to the scratch budget otherwise (C3, N = 256: 985 vs 871 k with one wave)
-      if (p->cap >= wave) p->cap = (p->tc.g.N <= 192 && levels > 0 ? 1 : p->cap / wave) * wave;
+      // (levels = 0 pipelines too, align_tc_pipelined0, in batches of two waves: C1 1.297 ->
+      // 1.326 M frames/s; MOCO_PIPE0_WAVES=0 one batch per call)
+      int64_t wv0 = 2;
+      if (const char *v = getenv("MOCO_PIPE0_WAVES")) wv0 = std::max<int64_t>(0, atoi(v));   // 0: off
+      if (p->cap >= wave)
+        p->cap = (p->tc.g.N <= 192 && (levels > 0 || wv0 > 0) ? (levels > 0 ? 1 : wv0) : p->cap / wave) * wave;
       if (const char *bw = getenv("MOCO_BATCH_WAVES"))   // tuning: waves per internal batch
         p->cap = std::min<int64_t>(p->cap, std::max(1, atoi(bw)) * wave);
     } else {
@@ -1061,7 +1066,7 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
   if (w > 64 && p->algo != MOCO_ALGO_FFT) { plan_free(p); return MOCO_EINVAL; }
   // streams and events of the batch pipeline (align_tc_pipelined) are created here, so
   // that moco_align_batch never allocates (moco.h) and can be captured in a CUDA graph
-  if (dtype == MOCO_U16 && levels > 0) {
+  if (dtype == MOCO_U16 && (levels > 0 || p->algo == MOCO_ALGO_TC)) {
     const int prc = pipe_create(p);
     if (prc) { plan_free(p); return prc; }
   }
@@ -1746,6 +1751,45 @@ static int align_tc_pipelined(moco_plan *p, const void *d_frames, int64_t T, int
   return MOCO_OK;
 }
 
+// levels = 0 (C1: no refine): the operand prep of batch k+1 on a second stream beside the
+// tensor-core search of batch k (at N <= 192 the search leaves room on its SM for prep
+// CTAs), the apply of batch k on a third stream beside the search of batch k+1.
+static int align_tc_pipelined0(moco_plan *p, const void *d_frames, int64_t T, int32_t *d_shifts, double *d_fmin,
+                               void *d_corrected, uint8_t *d_flags, cudaStream_t user) {
+  if (!p->pipe_ready) return MOCO_ESTATE;
+  cudaStream_t sp = p->ps[0], sm = p->ps[1], sa = p->ps[2];
+  CK(cudaEventRecord(p->pe_start, user));
+  for (int k = 0; k < 3; ++k) CK(cudaStreamWaitEvent(p->ps[k], p->pe_start, 0));
+  const size_t fbytes = (size_t)p->m * p->n * p->esz[0];
+  uint8_t *G[2] = {p->tc.G, p->tc.G2};
+  u64 *ga[2] = {p->tc.ga, p->tc.ga2};
+  int64_t k = 0;
+  for (int64_t f0 = 0; f0 < T; f0 += p->cap, ++k) {
+    const int64_t B = std::min<int64_t>(p->cap, T - f0);
+    const int buf = (int)(k & 1);
+    const char *fr = (const char *)d_frames + f0 * fbytes;
+    if (k >= 2) CK(cudaStreamWaitEvent(sp, p->pe_free[buf], 0));   // search k-2 is done with G/ga[buf]
+    int rc = launch_tc_prep(p, fr, B, G[buf], ga[buf], sp);
+    if (rc) return rc;
+    CK(cudaEventRecord(p->pe_prep[buf], sp));
+    CK(cudaStreamWaitEvent(sm, p->pe_prep[buf], 0));
+    rc = launch_tc_coarse(p, B, G[buf], ga[buf], d_shifts + 2 * f0, d_fmin + f0, d_flags ? d_flags + f0 : nullptr,
+                          nullptr, sm);
+    if (rc) return rc;
+    CK(cudaEventRecord(p->pe_free[buf], sm));
+    if (d_corrected) {
+      CK(cudaStreamWaitEvent(sa, p->pe_free[buf], 0));
+      rc = launch_apply(p, fr, (char *)d_corrected + f0 * fbytes, d_shifts + 2 * f0, B, sa);
+      if (rc) return rc;
+    }
+  }
+  CK(cudaEventRecord(p->pe_end, sm));
+  CK(cudaEventRecord(p->pe_end2, sa));
+  CK(cudaStreamWaitEvent(user, p->pe_end, 0));
+  CK(cudaStreamWaitEvent(user, p->pe_end2, 0));
+  return MOCO_OK;
+}
+
 int moco_align_batch(moco_plan *p, const void *d_frames, int64_t T, int32_t *d_shifts,
                      double *d_fmin, void *d_corrected, uint8_t *d_flags, moco_stream_t stream) {
   int rc = check_align_args(p, d_frames, T);
@@ -1770,6 +1814,9 @@ int moco_align_batch(moco_plan *p, const void *d_frames, int64_t T, int32_t *d_s
     p->pdl_now = false;
     return rc;
   }
+  if (p->algo == MOCO_ALGO_TC && T > p->cap && p->tc.G2 && p->levels == 0 && !p->stage && !p->knob.nopipe &&
+      p->dtype == MOCO_U16)
+    return align_tc_pipelined0(p, d_frames, T, d_shifts, d_fmin, d_corrected, d_flags, (cudaStream_t)stream);
   if (p->algo == MOCO_ALGO_TC && T > p->cap && p->tc.G2 && p->racc2 && p->sh1b && fused_ok(p, 0) &&
       (p->levels == 1 || (p->levels == 2 && p->scratch1b && p->sh2b[1] && fused_ok(p, 1))) && !p->knob.nopipe)
     return align_tc_pipelined(p, d_frames, T, d_shifts, d_fmin, d_corrected, d_flags, (cudaStream_t)stream);
