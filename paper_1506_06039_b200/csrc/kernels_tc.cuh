@@ -45,7 +45,7 @@ struct TcGeom {
   int F;        // frames per operand group (1, 2, 4): core matrix = 4/F rows x (F frames x 2 parts)
   int ST;       // lag rows s per 128-row M tile = 64 / F
   int NT;       // M tiles
-  int Wt;       // t lags padded to a multiple of 16
+  int Wt;       // t lags padded to a multiple of 8 (16 with MOCO_TC_WT16=1)
   int N1;       // columns per template row = 2 * Wt (parts x lags)
   int N;        // 2 * N1: a template-row pair
   int R;        // rows per operand plane = mc + NT*ST (plane row = frame row + hw)
@@ -1001,7 +1001,11 @@ inline bool tc_make_geom(TcGeom *gp, int w, int mc, int nc, int L, int vb) {
   TcGeom g{};
   g.mc = mc; g.nc = nc; g.w = w; g.hw = w - 1; g.W = 2 * w - 1; g.L = L;
   g.sb = vb <= 14 ? 7 : 8;
-  g.Wt = (g.W + 15) / 16 * 16;
+  // t lags padded to a multiple of 8 (N = 4 Wt: a multiple of 32, so N/16 producer chunks
+  // per lane is one of the even instantiations); the epilogue reads 16-column chunks past
+  // Wt, inside the TMEM allocation and ignored.  MOCO_TC_WT16=1: pad to 16 (round 1)
+  const char *w16 = getenv("MOCO_TC_WT16");
+  g.Wt = (w16 && atoi(w16)) ? (g.W + 15) / 16 * 16 : (g.W + 7) / 8 * 8;
   g.N1 = 2 * g.Wt;
   g.N = 2 * g.N1;
   if (g.N > 256) return false;
