@@ -1045,9 +1045,10 @@ int moco_plan_create(moco_plan **out, int m, int n, int w, int levels, int dtype
       // (levels > 0, N <= 192: C2 1.70 -> 1.77 M,
       // C4 399 -> 412 k; the finer batches keep the three streams busier), whole waves up
       // to the scratch budget otherwise (C3, N = 256: 985 vs 871 k with one wave)
-      // (levels = 0 pipelines too, align_tc_pipelined0, in batches of two waves: C1 1.297 ->
-      // 1.326 M frames/s; MOCO_PIPE0_WAVES=0 one batch per call)
-      int64_t wv0 = 2;
+      // (levels = 0 pipelines too, align_tc_pipelined0, in batches of one wave -- 592 frames
+      // at C1 with four frames per CTA: 1.503 -> 1.524 M frames/s; with the round-1 lag
+      // padding two waves of 296 frames, 1.297 -> 1.326 M; MOCO_PIPE0_WAVES=0 one batch per call)
+      int64_t wv0 = 1;
       if (const char *v = getenv("MOCO_PIPE0_WAVES")) wv0 = std::max<int64_t>(0, atoi(v));   // 0: off
       if (p->cap >= wave)
         p->cap = (p->tc.g.N <= 192 && (levels > 0 || wv0 > 0) ? (levels > 0 ? 1 : wv0) : p->cap / wave) * wave;
