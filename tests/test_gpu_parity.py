@@ -306,6 +306,18 @@ def test_config2_full_stack_sampled():
     assert (sh == st.shifts).mean() > 0.95
 
 
+def test_config1_full_stack_sampled():
+    """C1 as bench.py runs it: all 1,000 frames of 256x256 (levels = 0) in one call -- the
+    levels-0 batch pipeline (prep of batch k+1 beside the search of batch k, one-wave
+    batches of 592 frames with the four-frame geometry of the lag padding to 8), frames on
+    both sides of the batch boundary checked bit-exactly against the oracle."""
+    spec = config_spec(1)
+    sample = [0, 1, 295, 296, 591, 592, 593, 887, 888, 999]
+    spec, st, sh, fm, fl, kinds, p = _run_config(1, spec.T, sample)
+    assert kinds == ["exact"] * len(sample)
+    assert (sh == st.shifts).mean() > 0.9
+
+
 def test_config4_full_stack_sampled():
     """C4 as bench.py runs it: all 2,000 frames of 1024x1024 in one moco_align_batch call
     (two pyramid levels: TC search on the 16-bit level-2 sums, the level-1 image written
