@@ -130,7 +130,13 @@ int moco_set_template(moco_plan *p, const void *d_template, moco_stream_t stream
  *   d_flags      out or NULL: uint8 [T], MOCO_FLAG_* bits.
  * T == 0 is a no-op; T < 0, NULL required pointers or misalignment -> EINVAL;
  * ESTATE before moco_set_template.  Never allocates; loops over internal
- * batches sized to the plan's workspace.
+ * batches sized to the plan's workspace.  The outputs may be any memory the
+ * device can store to -- including another GPU's buffer mapped into this
+ * device's address space (CUDA symmetric memory / peer mappings): the kernels
+ * that produce each frame's record store it there directly, which is how the
+ * multi-GPU results gather is fused into the hot path (dist.PeerResults,
+ * SURVEY.md 8(e)); at levels = 0 the apply reads d_shifts back (over the same
+ * mapping).
  */
 int moco_align_batch(moco_plan *p, const void *d_frames, int64_t T, int32_t *d_shifts,
                      double *d_fmin, void *d_corrected, uint8_t *d_flags,
