@@ -128,13 +128,6 @@ __device__ __forceinline__ void tma_load3(void *dst, const CUtensorMap *tm, int 
       "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
       : "memory");
 }
-// L2 prefetch of a 3-D tensor box (no shared-memory destination, no barrier)
-__device__ __forceinline__ void tma_prefetch3(const CUtensorMap *tm, int x, int y, int z) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
-                   reinterpret_cast<uint64_t>(tm)),
-               "r"(x), "r"(y), "r"(z)
-               : "memory");
-}
 __device__ __forceinline__ void tma_store3(const CUtensorMap *tm, int x, int y, int z, const void *src) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
                    reinterpret_cast<uint64_t>(tm)),

@@ -74,12 +74,6 @@ constexpr int RTC_R = (6 * RTC_RG + 2 + 7) / 8 * 8;  // grid rows per stage box 
 constexpr int RTC_KS = 4;                  // K-steps (16 pixels) per stage: one 128-byte row
 constexpr int RTC_NST = RTC_NSTAGE;        // ring depth
 constexpr int RTC_CH = 2 * RTC_KS;         // 8-pixel chunks per stage box
-#ifndef RTC_LSU_A
-#define RTC_LSU_A 0                // 1: A boxes by cp.async from the GA warps (measured slower: C2 refine 236 vs 168 us)
-#endif
-#ifndef RTC_PREFETCH
-#define RTC_PREFETCH 0             // stages ahead prefetched into L2 (0: off)
-#endif
 #ifndef RTC_GA_WARPS
 #define RTC_GA_WARPS 16
 #endif
@@ -235,9 +229,6 @@ __device__ __forceinline__ void mma_i8_k4_elect(uint32_t d, uint32_t a0, uint32_
 }
 
 struct RtcArgs {
-  const uint16_t *img;      // level-l images of the batch (cp.async A loads): frame stride, row pitch
-  int64_t fstride;
-  int pitch;
   const uint8_t *tab;       // rtc_table_bytes
   u64 *acc;                 // [B][18]: H for the nine candidates, then GA (atomically added)
   const int32_t *shift_in;  // [B][2] at level l+1
@@ -291,7 +282,7 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
   if (warp == 1) tmem_alloc(holder, tcols);
   if (tid == 0) {
     for (int s = 0; s < RTC_NST; ++s) {
-      mbar_init(&full[s], RTC_LSU_A ? 1 + RTC_CW : 1);   // (+ the GA warps' A loads)
+      mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1 + RTC_CW);
     }
     mbar_init(done, 1);
@@ -312,26 +303,16 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
       if (rnd > 0) mbar_wait(&empty[s], (rnd - 1) & 1);
       RT_T(w_a += gtimer() - t0;)
 #ifdef RTC_DIAG_NOB   // (diagnostic builds, results wrong: no B tiles loaded)
-      if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)(RTC_LSU_A ? 0 : nf * RTC_SLOT));
+      if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)(nf * RTC_SLOT));
 #else
       if (lane == 0)
-        mbar_arrive_expect_tx(&full[s], (uint32_t)((RTC_LSU_A ? 0 : nf * RTC_SLOT) + ngr * kc * RTC_BT));
+        mbar_arrive_expect_tx(&full[s], (uint32_t)(nf * RTC_SLOT + ngr * kc * RTC_BT));
 #endif
       __syncwarp();
       unsigned char *st = stg + s * RTC_STAGE;
-      if (!RTC_LSU_A && lane < nf) {
+      if (lane < nf) {
         const int x0 = (Tsh[lane] - 1) - ((Tsh[lane] - 1) & 7) + 16 * j0;   // 8-aligned column below T-1
         tma_load3(st + lane * RTC_SLOT, &tmF, x0, 6 * gb + Ssh[lane] - 1, Fid[lane], &full[s]);
-#if RTC_PREFETCH
-        // the frame boxes RTC_PREFETCH stages ahead into L2: more bytes in flight than the
-        // two-stage ring holds, so the ring's loads meet L2 latency instead of HBM's
-        const int ip = i + RTC_PREFETCH;
-        if (ip < nstage) {
-          const int gp = G0 + (ip / g.nstrips) * RTC_RG, jp = (ip % g.nstrips) * RTC_KS;
-          const int xp = (Tsh[lane] - 1) - ((Tsh[lane] - 1) & 7) + 16 * jp;
-          tma_prefetch3(&tmF, xp, 6 * gp + Ssh[lane] - 1, Fid[lane]);
-        }
-#endif
       }
 #ifndef RTC_DIAG_NOB
       if (lane == 0)
@@ -396,42 +377,10 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
     u64 tot[FPW], e0[FPW], e1[FPW], e2[FPW], e3[FPW];   // interior rows, per frame of this warp
 #pragma unroll
     for (int k = 0; k < FPW; ++k) tot[k] = e0[k] = e1[k] = e2[k] = e3[k] = 0;
-#if RTC_LSU_A
-    static_assert(RTC_CW == RTC_F, "one GA warp per frame loads that frame's A boxes");
-    // this warp's frame box of stage i (the TMA box of the other mode, 128-byte swizzle
-    // written by hand: row r's 16-byte chunk c at c ^ (r & 7); zero outside the frame),
-    // one cp.async group per stage
-    auto issue_a = [&](int i) {
-      if (i < nstage && cw < nf) {
-        const int gb = G0 + (i / g.nstrips) * RTC_RG, j0 = (i % g.nstrips) * RTC_KS;
-        unsigned char *dst = stg + (i % RTC_NST) * RTC_STAGE + cw * RTC_SLOT;
-        const int x = (Tsh[cw] - 1) - ((Tsh[cw] - 1) & 7) + 16 * j0 + 8 * (lane & 7);
-        const int y0 = 6 * gb + Ssh[cw] - 1;
-        const uint16_t *fb = a.img + (int64_t)Fid[cw] * a.fstride;
-        const bool xok = x >= 0 && x < g.nl;
-#pragma unroll
-        for (int k = 0; k < RTC_R / 4; ++k) {
-          const int r = (lane >> 3) + 4 * k, y = y0 + r;
-          const bool ok = xok && y >= 0 && y < g.ml;
-          cp_async16_zfill(dst + r * 128 + (((lane & 7) ^ (r & 7)) << 4), ok ? fb + (int64_t)y * a.pitch + x : fb,
-                           ok ? 16u : 0u);
-        }
-      }
-      cp_async_commit();
-    };
-#pragma unroll
-    for (int k = 0; k < RTC_NST; ++k) issue_a(k);
-#endif
     for (int i = 0; i < nstage; ++i) {
       const int s = i % RTC_NST, rnd = i / RTC_NST;
       const int gb = G0 + (i / g.nstrips) * RTC_RG, j0 = (i % g.nstrips) * RTC_KS;
       const int ngr = min(RTC_RG, G1 - gb), kc = min(RTC_KS, g.nk - j0);
-#if RTC_LSU_A
-      cp_async_wait<RTC_NST - 1>();   // this warp's box of stage i has landed
-      fence_proxy_async();            // (generic-proxy writes, read by the tensor cores)
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&full[s]);
-#endif
       // grid rows of this stage's row groups: [6gb, 6(gb+ngr)); the last group also owns
       // rows ml, ml+1 (the two below the template)
       const int r_lo = 6 * gb, r_hi = (gb + ngr == g.ng) ? g.ml + 2 : min(g.ml, 6 * (gb + ngr));
@@ -579,10 +528,6 @@ __global__ void __launch_bounds__(RTC_THREADS, 1) k_refine_tc(const __grid_const
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
-#if RTC_LSU_A
-      if (i + RTC_NST < nstage) mbar_wait(&empty[s], rnd & 1);   // the MMAs of stage i are done with slot s
-      issue_a(i + RTC_NST);
-#endif
     }
 #if RTC_GA_TOTAL
 #pragma unroll

@@ -121,10 +121,6 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes
 __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
-// the same with zero fill: n < 16 source bytes (0: the 16 bytes are zeroed, src not read)
-__device__ __forceinline__ void cp_async16_zfill(void *dst, const void *src, uint32_t n) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(n) : "memory");
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -1121,13 +1117,6 @@ inline int tc_init(TcPlan *tc, int w, int mc, int nc, int L, int vb, int64_t cap
       smem_attr(k_tc_prep<1>, g.prep_smem) != cudaSuccess ||
       smem_attr(k_tc_prep<2>, g.prep_smem) != cudaSuccess)
     return -1;
-  if (const char *cv = getenv("MOCO_PREP_CARVE")) {   // tuning: the prep's shared-memory carveout (%)
-    const int pc = atoi(cv);
-    cudaFuncSetAttribute((const void *)k_tc_prep<0>, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
-    cudaFuncSetAttribute((const void *)k_tc_prep<1>, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
-    cudaFuncSetAttribute((const void *)k_tc_prep<2>, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
-    cudaGetLastError();
-  }
   tc->ready = true;
   return 0;
 }

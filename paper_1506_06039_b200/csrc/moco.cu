@@ -1297,7 +1297,6 @@ static int launch_refine_h(moco_plan *p, int l, const void *img, int64_t fstride
     ProfScope ps(p, MOCO_K_REFINE, st);
     k_rtc_bucket<<<1, 1024, 0, st>>>(sin, (int)B, p->rperm, p->rmeta);
     RtcArgs r;
-    r.img = (const uint16_t *)img; r.fstride = fstride; r.pitch = p->pitch[l];
     r.tab = p->rtab[l]; r.acc = racc; r.shift_in = sin; r.perm = p->rperm; r.meta = p->rmeta;
     r.B = (int)B; r.g = p->rtc[l];
     b.ga_total = RTC_GA_TOTAL;   // the pick completes GA from the staged-pixel total
