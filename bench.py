@@ -407,6 +407,10 @@ def main():
             except Exception as e:   # (no symmetric memory on this node: the NCCL all-gather)
                 print(f"[bench] peer-memory gather unavailable ({str(e)[:120]}); NCCL all-gather", file=sys.stderr)
                 gather_mode = "nccl"
+            ok = torch.tensor([1 if peer is not None else 0], dtype=torch.int32, device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)   # every rank takes the same path
+            if int(ok.item()) == 0:
+                peer, gather_mode = None, "nccl"
 
     def step():
         if peer is not None:
